@@ -1,0 +1,368 @@
+#!/usr/bin/env python
+"""Benchmark: OpEvo tuning of an sm_100a kernel family on B200.
+
+A *step* is one OpEvo generation of the reference loop (ask rho=8 configs ->
+evaluate them on the GPUs -> tell), i.e. the hot path of ``run``
+(reference ``pkg/src/topotune/engine.py:293-310``) with the trial evaluator
+replaced by compile + verify + CUDA-event timing of a tcgen05/TMA kernel.
+
+``value`` = trials/s over the K timed generations (whole job, all ranks);
+the best-found TFLOP/s, its fraction of the measured tensor-core peak,
+trials-to-95 % and wall-clock-to-95 % of the best ride along.  Default
+workload: BASELINE configs[1], MatMul 1024x1024x1024 bf16.
+
+N > 1: launched by torchrun, one process per GPU; every rank runs an
+identical engine replica and evaluates the ask indices i = rank (mod N); one
+all_reduce of the result rows per generation (scheduler.ShardedEvaluator).
+
+``--impl reference``: the reference's own CPU path (OpEvo + its synthetic CPU
+evaluator, restated in oracle/opevo_port.py because the reference tree does
+not exist on the GPU box), rank 0 only, on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+RHO = 8
+DEFAULT_OP = "matmul:1024,1024,1024"
+METRIC = "best-found TFLOP/s (% of tensor peak) vs trials; trials/sec at 1/2/4/8 B200"
+
+
+def peaks() -> dict:
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return {"tflops": p["bf16_tflops"], "tflops_sustained": p.get("bf16_tflops_sustained"),
+                "hbm_gbs": p["hbm_gbs"], "source": "measured"}
+    except (OSError, KeyError, ValueError):
+        return {"tflops": 1590.0, "tflops_sustained": 1400.0, "hbm_gbs": 6650.0,
+                "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self) -> dict:
+        rows = []
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        util = [float(r[3]) for r in rows if r[3].replace(".", "").isdigit()]
+        loaded = [s for s, u in zip(sm, util) if u > 0] or sm
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v == "Active"})
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_reference_arm(op: str, steps: int, warmup: int, seed: int) -> dict:
+    """The reference's CPU search + synthetic evaluator, timed on this host."""
+    from oracle import opevo_port
+
+    budget = RHO * (steps + warmup)
+    reps, total_s, trials = 0, 0.0, 0
+    t_end = time.perf_counter() + 10.0
+    while True:
+        t0 = time.perf_counter()
+        _, log = opevo_port.opevo_run(op, seed=seed + reps, budget=budget)
+        total_s += time.perf_counter() - t0
+        trials += len(log)
+        reps += 1
+        if time.perf_counter() > t_end or reps >= 200:
+            break
+    return {"value": trials / total_s, "unit": "trials/s", "cores": 1, "kind": "port",
+            "sample": f"{reps} OpEvo runs x {budget} trials of {op} with the reference's "
+                      f"synthetic CPU evaluator (oracle/opevo_port.py), 1 thread, "
+                      f"{total_s:.1f} s of CPU work",
+            "cpu": _cpu_model(), "host_cpus": os.cpu_count()}
+
+
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args) -> None:
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cb = cpu_reference_arm(args.op, args.steps, args.warmup, args.seed)
+    ms = 1e3 * RHO / cb["value"]
+    line = {"metric": METRIC, "value": cb["value"], "unit": "trials/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"OpEvo search, {args.op}, reference synthetic CPU evaluator",
+                       "rho": RHO, "seed": args.seed},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "trials/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "note": "the reference's evaluator is a synthetic cost model (no device meaning, "
+                    "SPEC.md:13); its fitness is not TFLOP/s"}
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=60)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--op", default=DEFAULT_OP)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--reps", type=int, default=20, help="timed launches per trial")
+    ap.add_argument("--l2", default="warm", choices=("warm", "cold"))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--log", default="")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    args.warmup = max(args.warmup, 3)
+
+    world, rank, local = dist_env()
+    import torch
+    import torch.distributed as dist
+
+    from paper_2006_05664_b200 import EngineConfig, OpEvo, parse_operator
+    from paper_2006_05664_b200.evaluator import EvalSettings, GpuEvaluator
+    from paper_2006_05664_b200.logs import TrialRecorder
+    from paper_2006_05664_b200.mapping import config_to_knobs, gpu_operator_space
+    from paper_2006_05664_b200.reporting import trials_to_fraction, wallclock_to_fraction
+    from paper_2006_05664_b200.scheduler import ShardedEvaluator
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    spec = parse_operator(args.op)
+    space = gpu_operator_space(spec)
+    settings = EvalSettings(reps=args.reps, flush_l2=(args.l2 == "cold"))
+    local_ev = GpuEvaluator(spec, space, local, settings)
+    if world > 1:
+        evaluator = ShardedEvaluator(local_ev, rank, world, device=torch.device("cuda", local))
+    else:
+        evaluator = local_ev.evaluate
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def launches_of(extras) -> int:
+        # per verified trial: check launch + compare + warm-up + graph warm-up + timed graph
+        per = 1 + 1 + settings.warmup + 2 * settings.reps
+        return sum(per for e in extras if e.get("status") == "ok")
+
+    budget = RHO * (args.steps + args.warmup)
+    engine = OpEvo(space, EngineConfig(seed=args.seed, budget=budget, parents=RHO, offspring=RHO))
+    recorder = TrialRecorder(space)
+
+    def generation(upload=None) -> tuple[int, int]:
+        if upload is not None:
+            upload()
+        asked = engine.ask()
+        if not asked.configs:
+            return 0, 0
+        fits = evaluator(asked.configs)
+        engine.tell(list(zip(asked.configs, fits)))
+        owner = getattr(evaluator, "__self__", evaluator)
+        extras = owner.last_extras
+        for c, f, e in zip(asked.configs, fits, extras):
+            recorder.record(c, f, e)
+        return len(asked.configs), launches_of(extras[rank::world] if world > 1 else extras)
+
+    for _ in range(args.warmup):
+        generation()
+
+    # ---------------- timed region: K generations, device-timed, max over ranks
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    trials = launches = 0
+    with ClockSampler(local) as clocks:
+        e0.record()
+        t_wall0 = time.perf_counter()
+        for _ in range(args.steps):
+            n, nl = generation()
+            trials += n
+            launches += nl
+        barrier()
+        e1.record()
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t_wall0
+    sec = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+    trials_per_s = trials / sec if sec > 0 else 0.0
+
+    # ---------------- e2e: same loop through the public API, operands from
+    # pinned host memory uploaded every generation, results read back
+    e2e = None
+    if not args.no_e2e:
+        from paper_2006_05664_b200 import capi
+
+        op = local_ev.op
+        pa, pb = capi.PinnedBuffer(op.a_bytes), capi.PinnedBuffer(op.b_bytes)
+        # stage the device operands in pinned host memory once (untimed); every
+        # timed generation re-uploads them, so the kernel reference stays valid
+        op.read_inputs(pa.ptr, pb.ptr)
+        e2e_steps = max(1, min(args.steps, 20))
+        engine.config.budget += RHO * e2e_steps
+
+        def upload():
+            op.upload(pa.ptr, pb.ptr)
+
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        e2e_trials = 0
+        for _ in range(e2e_steps):
+            n, _ = generation(upload)
+            e2e_trials += n
+        barrier()
+        f1.record()
+        torch.cuda.synchronize()
+        e_sec = max_over_ranks(f0.elapsed_time(f1) / 1e3)
+        e2e = {"value": e2e_trials / e_sec if e_sec > 0 else 0.0, "unit": "trials/s",
+               "h2d_bytes_per_step": (op.a_bytes + op.b_bytes) * world,
+               "d2h_bytes_per_step": 12 * RHO, "steps": e2e_steps}
+        pa.close()
+        pb.close()
+
+    # ---------------- best kernel: re-time live (roofline.achieved)
+    best = engine.best()
+    records = recorder.records
+    pk = peaks()
+    roof = None
+    best_knobs = None
+    best_cold = None
+    if best.fitness > 0:
+        mapped = config_to_knobs(spec, space, best.config)
+        best_knobs = mapped.knobs.as_tuple()
+        k = local_ev.dev.kernel(local_ev.op, best_knobs)
+        ms = k.time(warmup=5, reps=100, flush_l2=False)
+        best_cold = spec.flops() / (k.time(warmup=2, reps=20, flush_l2=True) * 1e-3) / 1e12
+        k.close()
+        ach = spec.flops() / (ms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": ach, "peak": pk["tflops"], "unit": "TFLOP/s",
+                "frac": ach / pk["tflops"], "traffic": _ncu_traffic(best_knobs),
+                "peak_source": f"{pk['source']} burst bf16 (MEASURED_PEAKS.json)",
+                "kernel_ms": ms, "per_launch_flops": spec.flops()}
+
+    if rank == 0:
+        cpu = None if (args.no_cpu or world > 1) else cpu_reference_arm(
+            args.op, args.steps, args.warmup, args.seed)
+        if args.log:
+            from paper_2006_05664_b200.logs import write_trial_log
+
+            write_trial_log(args.log, records)
+        line = {
+            "metric": METRIC, "value": trials_per_s, "unit": "trials/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"OpEvo tuning of the sm_100a tcgen05 kernel family on "
+                                   f"{args.op} bf16 (BASELINE configs[1])",
+                       "operator": args.op, "rho": RHO, "lambda": RHO, "q": 0.5,
+                       "seed": args.seed, "trials_timed": trials,
+                       "space": "reference matmul_space + stages (mapping.py)",
+                       "fitness_timing": f"{settings.reps} back-to-back launches in one CUDA "
+                                         f"graph after {settings.warmup} warm-up, L2 "
+                                         f"{args.l2} (operands fit in L2)",
+                       "l2_between_steps": "inputs < L2; each step re-verifies every kernel "
+                                           "(output poisoned, recomputed, compared)",
+                       "parallelism": f"trial sharding x{world}"},
+            "best_tflops": best.fitness, "best_frac_of_peak": best.fitness / pk["tflops"],
+            "best_knobs": best_knobs, "best_config": space.config_to_json(best.config),
+            "best_tflops_cold_l2": best_cold,
+            "trials_to_95pct": trials_to_fraction(records),
+            "wallclock_to_95pct_s": wallclock_to_fraction(records) / 1e3,
+            "valid_fraction": sum(r.fitness > 0 for r in records) / len(records),
+            "trials_total": len(records), "wall_s_timed": wall,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches * world,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    local_ev.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _ncu_traffic(knobs) -> float | None:
+    """dram read+write bytes per launch from the committed ncu summary, if any."""
+    path = os.path.join(REPO, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        entry = d.get("kernels", {}).get(",".join(map(str, knobs)))
+        return entry.get("dram_bytes") if entry else d.get("best_dram_bytes")
+    except (OSError, ValueError):
+        return None
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,155 @@
+/*
+ * libopevo -- C ABI of the B200 trial evaluator for OpEvo.
+ *
+ * This library replaces the reference tuner's evaluation seam: the objective
+ * callable `Callable[[tuple], float]` consumed by `evaluate_batch` / `run`
+ * (reference pkg/src/topotune/engine.py:264-310), whose CPU implementation is
+ * the synthetic cost model `synthetic_cost` (benchmarks.py:278-291), and the
+ * subprocess protocol `ExternalEvaluator` (external.py:29-75).  A trial is:
+ * canonical kernel knobs -> JIT-compiled sm_100a kernel (NVRTC, cubin cache)
+ * -> verified against an independent reference on the same synthetic inputs
+ * -> timed with CUDA events -> fitness in TFLOP/s.
+ *
+ * Conventions (mirroring the reference's error semantics, engine.py:276-285):
+ *   status  0          ok
+ *   status  > 0        this configuration is invalid -> fitness 0
+ *                      (infeasible knobs, compile error, launch failure,
+ *                       result mismatch)
+ *   status  < 0        fatal for the worker (no device / driver / NVRTC, a
+ *                      sticky CUDA context error) -> FatalEvaluationError or
+ *                      worker respawn
+ * Error text is written to the caller's `err` buffer (may be NULL).  No C++
+ * exception crosses this boundary.  All pointers are plain; no torch types.
+ * Threading: one opevo_ctx per device, used by one thread at a time;
+ * opevo_compile() is thread-safe and needs no device (host NVRTC pool).
+ */
+#ifndef OPEVO_H
+#define OPEVO_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OPEVO_ABI_VERSION 1
+
+enum opevo_status {
+    OPEVO_OK = 0,
+    OPEVO_INVALID_CONFIG = 1,   /* knobs infeasible for this operator */
+    OPEVO_COMPILE_ERROR = 2,    /* NVRTC rejected the instance        */
+    OPEVO_LAUNCH_ERROR = 3,     /* launch refused (non-sticky)        */
+    OPEVO_VERIFY_FAILED = 4,    /* output differs from the reference  */
+    OPEVO_ERR_NO_DEVICE = -1,   /* libcuda / device unavailable       */
+    OPEVO_ERR_NO_NVRTC = -2,    /* libnvrtc unavailable               */
+    OPEVO_ERR_STICKY = -3,      /* context poisoned: restart worker   */
+    OPEVO_ERR_ARG = -4,         /* caller error                       */
+    OPEVO_ERR_CUDA = -5         /* other driver error                 */
+};
+
+/* operator kinds (reference benchmarks.py:36-107) */
+enum opevo_op_kind { OPEVO_MATMUL = 0, OPEVO_BATCHMATMUL = 1, OPEVO_CONV2D = 2 };
+enum opevo_dtype { OPEVO_BF16 = 0, OPEVO_F32 = 1 };
+
+/*
+ * Operator descriptor.  MatMul / BatchMatMul use GEMM naming:
+ *   rows = reference `n`, cols = reference `m`, depth = reference `k`,
+ *   batch = reference `b` (1 for MatMul).
+ * Conv2d uses conv[] = {batch, cin, h, w, cout, kh, kw, stride, pad}
+ * (reference Conv2dSpec field order, benchmarks.py:69-81).
+ */
+typedef struct opevo_op_desc {
+    int32_t kind;
+    int32_t dtype;
+    int64_t batch, rows, cols, depth;
+    int32_t conv[9];
+    uint64_t seed;            /* synthetic-input seed */
+} opevo_op_desc;
+
+/* Kernel knob vector: fixed order, OPEVO_NUM_KNOBS entries. */
+enum opevo_knob {
+    OPEVO_KNOB_BM = 0,        /* CTA tile rows (UMMA M / atoms)          */
+    OPEVO_KNOB_BN = 1,        /* CTA tile cols (UMMA N)                  */
+    OPEVO_KNOB_BK = 2,        /* K per pipeline stage                    */
+    OPEVO_KNOB_STAGES = 3,    /* smem ring depth                          */
+    OPEVO_KNOB_SPLIT = 4,     /* split-K factor (runtime)                 */
+    OPEVO_KNOB_CLUSTER = 5,   /* CTAs per cluster sharing A (multicast)   */
+    OPEVO_KNOB_TILE_H = 6,    /* conv: output rows per CTA tile           */
+    OPEVO_KNOB_TILE_W = 7,    /* conv: output cols per CTA tile           */
+    OPEVO_NUM_KNOBS = 8
+};
+
+/* Result of one trial (opevo_trial). */
+typedef struct opevo_trial_result {
+    double tflops;            /* fitness: algorithmic FLOPs / device time */
+    double ms;                /* device ms per launch                     */
+    double rel_err;           /* max|C-R| / max|R| vs the reference       */
+    double compile_ms;        /* NVRTC (0 on cache hit)                   */
+    double load_ms;           /* module load + launch setup               */
+    int32_t cache_hit;        /* 1: memory, 2: disk, 0: compiled          */
+    int32_t grid_ctas;
+    int32_t smem_bytes;
+} opevo_trial_result;
+
+typedef struct opevo_ctx opevo_ctx;
+typedef struct opevo_op opevo_op;
+typedef struct opevo_kernel opevo_kernel;
+
+int opevo_abi_version(void);
+
+/* NVRTC compile of one instance into the on-disk cubin cache; no device
+ * needed.  family: 0 = GEMM, 1 = implicit-GEMM conv.  Thread-safe. */
+int opevo_compile(int family, const int32_t* knobs, int nknobs, int batched, int out_f32,
+                  const char* cache_dir, double* compile_ms, char* err, size_t errlen);
+
+/* Canonical cache key of an instance (writes a NUL-terminated string). */
+int opevo_kernel_key(int family, const int32_t* knobs, int nknobs, int batched, int out_f32,
+                     char* key, size_t keylen);
+
+int opevo_ctx_create(int device, const char* cache_dir, opevo_ctx** out, char* err, size_t errlen);
+void opevo_ctx_destroy(opevo_ctx* ctx);
+int opevo_ctx_info(opevo_ctx* ctx, int* sm_count, int* max_smem_optin, int* cc_major, int* cc_minor);
+
+/* Allocate operands, fill them from desc->seed, compute the fp32 reference. */
+int opevo_op_prepare(opevo_ctx* ctx, const opevo_op_desc* desc, opevo_op** out,
+                     char* err, size_t errlen);
+void opevo_op_destroy(opevo_op* op);
+/* Operand sizes in bytes (A, B in the kernel layout, C output). */
+int opevo_op_sizes(const opevo_op* op, size_t* a_bytes, size_t* b_bytes, size_t* c_bytes);
+/* Host <-> device copies for the end-to-end path (inputs in kernel layout). */
+int opevo_op_upload(opevo_op* op, const void* a_host, const void* b_host, char* err, size_t errlen);
+int opevo_op_download(opevo_op* op, void* c_host, size_t bytes, char* err, size_t errlen);
+/* Device operands (kernel layout) to host, e.g. to stage them in pinned memory. */
+int opevo_op_read_inputs(opevo_op* op, void* a_host, void* b_host, char* err, size_t errlen);
+/* Reference output (fp32, kernel output layout) to host. */
+int opevo_op_reference(opevo_op* op, float* host, size_t count, char* err, size_t errlen);
+/* Recompute the reference (after opevo_op_upload). */
+int opevo_op_refresh_reference(opevo_op* op, char* err, size_t errlen);
+
+/* Bind knobs to an operator: validate, fetch/compile the module, build the
+ * TMA descriptors and launch plan. */
+int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nknobs,
+                     opevo_kernel** out, opevo_trial_result* info, char* err, size_t errlen);
+void opevo_kernel_release(opevo_kernel* k);
+int opevo_kernel_run(opevo_kernel* k, char* err, size_t errlen);
+/* Output vs reference; *rel_err = max|C-R|/max|R| (inf if non-finite). */
+int opevo_kernel_check(opevo_kernel* k, double tol, double* rel_err, char* err, size_t errlen);
+/* flush_l2 = 0: `reps` back-to-back launches in one CUDA graph (L2 warm);
+ * flush_l2 = 1: an L2-sized write before every launch, each launch timed. */
+int opevo_kernel_time(opevo_kernel* k, int warmup, int reps, int flush_l2, double* ms_per_launch,
+                      char* err, size_t errlen);
+
+/* One complete trial: get + check (tol) + time.  Fitness in res->tflops. */
+int opevo_trial(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nknobs, int warmup,
+                int reps, int flush_l2, double tol, opevo_trial_result* res, char* err,
+                size_t errlen);
+
+/* Pinned host memory for honest end-to-end copies. */
+void* opevo_host_alloc(size_t bytes);
+void opevo_host_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OPEVO_H */

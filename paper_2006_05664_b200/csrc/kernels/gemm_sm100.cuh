@@ -1,0 +1,556 @@
+// OpEvo B200 GEMM family (sm_100a): C = A . B^T, bf16 in, fp32 accumulate.
+//
+// JIT-instantiated by libopevo (NVRTC) once per canonical knob tuple; the
+// knobs arrive as -D macros (see kernel_source.cpp / mapping.py):
+//   OPEVO_BM      CTA rows: 64 (UMMA M=64), 128 (M=128), 256 (two M=128 atoms)
+//   OPEVO_BN      CTA cols = UMMA N (16..256, multiple of 16)
+//   OPEVO_BK      K elements staged per pipeline stage (16..256)
+//   OPEVO_STAGES  depth of the TMA -> MMA shared-memory ring
+//   OPEVO_BATCHED 1: 3-D tensor maps {K, rows, batch} (BatchMatMul)
+//   OPEVO_OUT_F32 1: fp32 output (else bf16)
+//   OPEVO_CLUSTER CTAs per cluster along the column-tile axis; the A tile is
+//                 TMA-multicast to all of them (1 = no cluster)
+//   OPEVO_CONV    1: implicit-GEMM Conv2d. A is the NHWC activation read by a
+//                 4-D TMA box {C, TILE_W, TILE_H, TILE_N} shifted per filter
+//                 tap; padding comes from TMA out-of-bounds zero fill.  B is
+//                 the O(HW)I weight matrix [Cout][Kh*Kw*Cin].
+//   OPEVO_TILE_H / OPEVO_TILE_W  conv output tile (BM = TILE_N*TILE_H*TILE_W)
+// Runtime: gridDim = (col tiles, row tiles, batch * split); split-K partials
+// are reduced in-kernel by the last-arriving CTA of each tile (deterministic
+// order z = 0..split-1).
+//
+// Layout: A [batch][rows][K], B [batch][cols][K] (both K-major, the natural
+// UMMA operand order, "NT"), C [batch][rows][cols] row-major.
+//
+// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM owner + MMA
+// issuer, warps 2..5 = epilogue (TMEM -> registers -> global).  Shared memory
+// operands use the canonical K-major swizzled layout (SW128/64/32 by BK) that
+// TMA writes and the UMMA descriptors read.
+//
+// The paper's thread-level tiling knobs have no tcgen05
+// counterpart -- a single thread issues each MMA -- so they do not reach this
+// file; see mapping.py for how a configuration becomes these macros.
+
+#ifndef OPEVO_BM
+#define OPEVO_BM 128
+#endif
+#ifndef OPEVO_BN
+#define OPEVO_BN 128
+#endif
+#ifndef OPEVO_BK
+#define OPEVO_BK 64
+#endif
+#ifndef OPEVO_STAGES
+#define OPEVO_STAGES 4
+#endif
+#ifndef OPEVO_BATCHED
+#define OPEVO_BATCHED 0
+#endif
+#ifndef OPEVO_OUT_F32
+#define OPEVO_OUT_F32 0
+#endif
+#ifndef OPEVO_CLUSTER
+#define OPEVO_CLUSTER 1
+#endif
+#ifndef OPEVO_CONV
+#define OPEVO_CONV 0
+#endif
+#ifndef OPEVO_TILE_H
+#define OPEVO_TILE_H 1
+#endif
+#ifndef OPEVO_TILE_W
+#define OPEVO_TILE_W 1
+#endif
+
+#pragma nv_diag_suppress 177
+typedef unsigned int u32;
+typedef unsigned long long u64;
+typedef unsigned short u16;
+
+namespace opevo {
+
+constexpr int BM = OPEVO_BM;
+constexpr int BN = OPEVO_BN;
+constexpr int BK = OPEVO_BK;
+constexpr int STAGES = OPEVO_STAGES;
+constexpr int CLUSTER = OPEVO_CLUSTER;
+
+constexpr int SWZ = (BK * 2 >= 128) ? 128 : BK * 2;     // swizzle span in bytes
+constexpr int ATOM_K = SWZ / 2;                          // K elements per swizzle row
+constexpr int KATOMS = BK / ATOM_K;                      // swizzle atoms along K
+constexpr int MATOMS = (BM == 256) ? 2 : 1;              // M=128 MMAs per k-step
+constexpr int UMMA_M = (BM == 256) ? 128 : BM;
+constexpr int A_TILE = BM * BK * 2;
+constexpr int B_TILE = BN * BK * 2;
+constexpr int STAGE_BYTES = A_TILE + B_TILE;
+constexpr int A_SLICE_ROWS = BM / CLUSTER;                // rows of A each cluster CTA fetches
+constexpr int TMEM_USED = MATOMS * BN;
+constexpr int TMEM_COLS = TMEM_USED <= 32 ? 32 : TMEM_USED <= 64 ? 64 :
+                          TMEM_USED <= 128 ? 128 : TMEM_USED <= 256 ? 256 : 512;
+constexpr u32 LAYOUT = SWZ == 128 ? 2u : SWZ == 64 ? 4u : 6u;
+constexpr int EPI_COLS = (BN % 32 == 0) ? 32 : 16;
+constexpr int NUM_THREADS = 192;
+constexpr int SMEM_ALIGN = 1024;
+constexpr int TILE_H = OPEVO_TILE_H;
+constexpr int TILE_W = OPEVO_TILE_W;
+constexpr int TILE_N = BM / (TILE_H * TILE_W);
+
+static_assert(BM == 64 || BM == 128 || BM == 256, "BM must be 64, 128 or 256");
+static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "BN must be a multiple of 16 in [16, 256]");
+static_assert(BK % 16 == 0 && BK >= 16 && BK <= 256, "BK must be a multiple of 16 in [16, 256]");
+static_assert(BK % ATOM_K == 0, "BK must tile the swizzle atom");
+static_assert(TMEM_USED <= 512, "accumulator exceeds TMEM");
+static_assert(BM % (8 * CLUSTER) == 0, "multicast slice must be whole 8-row groups");
+static_assert(!OPEVO_CONV || (TILE_N * TILE_H * TILE_W == BM && CLUSTER == 1),
+              "conv tile must cover BM pixels, no multicast");
+
+// UMMA instruction descriptor, kind::f16: D=f32, A=B=bf16, both K-major.
+constexpr u32 IDESC = (1u << 4) | (1u << 7) | (1u << 10) |
+                      ((u32)(BN >> 3) << 17) | ((u32)(UMMA_M >> 4) << 24);
+
+// Shared-memory matrix descriptor minus the start address.
+constexpr u64 DESC_HI = ((u64)1 << 16)                          // LBO (unused for swizzled K-major)
+                      | ((u64)((8 * SWZ) >> 4) << 32)            // SBO: next 8-row group
+                      | ((u64)1 << 46)                           // descriptor version (sm_100)
+                      | ((u64)LAYOUT << 61);
+
+struct __align__(64) TmaDesc { u64 raw[16]; };
+
+// Conv geometry (unused by the GEMM instances).
+struct ConvGeom {
+    int cin, ho, wo, kw, pad;
+    int taps_cchunks;      // (Cin / BK): K blocks per filter tap
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ u32 smem_u32(const void* p) {
+    return (u32)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(u32 bar, u32 count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(u32 bar, u32 bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 :: "r"(bar), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ u64 global_ns() {
+    u64 t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Parity wait with a watchdog: a configuration that deadlocks traps after
+// ~4 s instead of hanging the device (the evaluator scores it 0).
+__device__ __forceinline__ void mbar_wait(u32 bar, u32 parity) {
+    u32 done;
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+                 "selp.u32 %0, 1, 0, p; }" : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+    if (done) return;
+    const u64 t0 = global_ns();
+    while (true) {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+                     "selp.u32 %0, 1, 0, p; }" : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+        if (done) return;
+        if (global_ns() - t0 > 4000000000ull) asm volatile("trap;");
+    }
+}
+
+__device__ __forceinline__ void tma_prefetch(const TmaDesc* d) {
+    asm volatile("prefetch.tensormap [%0];" :: "l"(d) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(u32 dst, const TmaDesc* d, u32 bar, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+                 "[%0], [%1, {%3, %4}], [%2];"
+                 :: "r"(dst), "l"(d), "r"(bar), "r"(c0), "r"(c1) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(u32 dst, const TmaDesc* d, u32 bar, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+                 "[%0], [%1, {%3, %4, %5}], [%2];"
+                 :: "r"(dst), "l"(d), "r"(bar), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d(u32 dst, const TmaDesc* d, u32 bar, int c0, int c1, int c2,
+                                            int c3) {
+    asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes "
+                 "[%0], [%1, {%3, %4, %5, %6}], [%2];"
+                 :: "r"(dst), "l"(d), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d_mc(u32 dst, const TmaDesc* d, u32 bar, int c0, int c1,
+                                               u16 mask) {
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                 ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;"
+                 :: "r"(dst), "l"(d), "r"(bar), "r"(c0), "r"(c1), "h"(mask) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d_mc(u32 dst, const TmaDesc* d, u32 bar, int c0, int c1,
+                                               int c2, u16 mask) {
+    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                 ".multicast::cluster [%0], [%1, {%3, %4, %5}], [%2], %6;"
+                 :: "r"(dst), "l"(d), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "h"(mask) : "memory");
+}
+
+__device__ __forceinline__ u32 cluster_rank() {
+    u32 r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+                 ::: "memory");
+}
+
+__device__ __forceinline__ void umma_bf16(u32 tmem_d, u64 adesc, u64 bdesc, u32 accumulate) {
+    asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0; "
+                 "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }"
+                 :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(u32 bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                 :: "r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void umma_commit_mc(u32 bar, u16 mask) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster"
+                 ".multicast::cluster.b64 [%0], %1;" :: "r"(bar), "h"(mask) : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void epi_bar() {   // the four epilogue warps only
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+}
+
+template <int N>
+__device__ __forceinline__ void tmem_load(u32 taddr, u32 (&v)[N]);
+
+template <>
+__device__ __forceinline__ void tmem_load<32>(u32 taddr, u32 (&v)[32]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+                 "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                 "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                   "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+                   "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]),
+                   "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+                   "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+                   "=r"(v[30]), "=r"(v[31])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <>
+__device__ __forceinline__ void tmem_load<16>(u32 taddr, u32 (&v)[16]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+                 "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                   "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+                   "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ u32 pack_bf16(float lo, float hi) {
+    u32 r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
+__device__ __forceinline__ void st_v4(void* p, u32 a, u32 b, u32 c, u32 d) {
+    asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" :: "l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
+}
+
+__device__ __forceinline__ float4 ld_cg_f4(const float* p) {
+    float4 r;
+    asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+    return r;
+}
+
+// Write EPI_COLS fp32 accumulator values (one row segment) as the output type.
+__device__ __forceinline__ void store_row(void* c_out, u64 off, const float* acc) {
+#if OPEVO_OUT_F32
+    float* dst = reinterpret_cast<float*>(c_out) + off;
+#pragma unroll
+    for (int j = 0; j < EPI_COLS; j += 4)
+        st_v4(dst + j, __float_as_uint(acc[j]), __float_as_uint(acc[j + 1]),
+              __float_as_uint(acc[j + 2]), __float_as_uint(acc[j + 3]));
+#else
+    u16* dst = reinterpret_cast<u16*>(c_out) + off;
+#pragma unroll
+    for (int j = 0; j < EPI_COLS; j += 8)
+        st_v4(dst + j, pack_bf16(acc[j], acc[j + 1]), pack_bf16(acc[j + 2], acc[j + 3]),
+              pack_bf16(acc[j + 4], acc[j + 5]), pack_bf16(acc[j + 6], acc[j + 7]));
+#endif
+}
+
+}  // namespace opevo
+
+using namespace opevo;
+
+extern "C" __global__ void __launch_bounds__(NUM_THREADS, 1)
+opevo_gemm(const __grid_constant__ TmaDesc tma_a,
+           const __grid_constant__ TmaDesc tma_b,
+           void* __restrict__ c_out,
+           float* __restrict__ ws,            // split-K partials [split][batch*rows][cols]
+           u32* __restrict__ counters,        // per-tile arrival counters (self-resetting)
+           int rows, int cols, int k_per_split, int split,
+           const ConvGeom geom)
+{
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<u64>(smem_raw) + SMEM_ALIGN - 1) & ~(u64)(SMEM_ALIGN - 1));
+    u64* full_bar = reinterpret_cast<u64*>(smem + STAGES * STAGE_BYTES);
+    u64* empty_bar = full_bar + STAGES;
+    u64* accum_bar = empty_bar + STAGES;
+    u32* tmem_slot = reinterpret_cast<u32*>(accum_bar + 1);
+    u32* last_flag = tmem_slot + 1;
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int col_tile = blockIdx.x;
+    const int row_tile = blockIdx.y;
+    const int batch = blockIdx.z / split;
+    const int kz = blockIdx.z - batch * split;
+    const int row0 = row_tile * BM;
+    const int col0 = col_tile * BN;
+    const int k0 = kz * k_per_split;
+    const int num_kb = k_per_split / BK;
+    const u32 crank = (CLUSTER > 1) ? cluster_rank() : 0u;
+    (void)crank;
+    (void)row0;
+    (void)geom;
+#if OPEVO_CONV
+    // row_tile enumerates (image tile, output-row tile, output-col tile)
+    const int w_tiles = geom.wo / TILE_W, h_tiles = geom.ho / TILE_H;
+    const int w0 = (row_tile % w_tiles) * TILE_W;
+    const int h0 = ((row_tile / w_tiles) % h_tiles) * TILE_H;
+    const int n0 = (row_tile / (w_tiles * h_tiles)) * TILE_N;
+#endif
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tma_a);
+        tma_prefetch(&tma_b);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(smem_u32(full_bar + s), 1);
+            // with multicast every CTA of the cluster must release a slot
+            // before any of them overwrites it
+            mbar_init(smem_u32(empty_bar + s), CLUSTER);
+        }
+        mbar_init(smem_u32(accum_bar), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     :: "r"(smem_u32(tmem_slot)), "r"(TMEM_COLS) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (CLUSTER > 1) cluster_sync();
+    tc_fence_after();
+    const u32 tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ------------------------------------------------ TMA producer
+            int s = 0;
+            u32 ph = 0;
+            for (int kb = 0; kb < num_kb; ++kb) {
+                mbar_wait(smem_u32(empty_bar + s), ph ^ 1);
+                const u32 fb = smem_u32(full_bar + s);
+                mbar_expect_tx(fb, STAGE_BYTES);
+                const u32 a_dst = smem_u32(smem + s * STAGE_BYTES);
+                const u32 b_dst = a_dst + A_TILE;
+                const int kk = k0 + kb * BK;
+#if OPEVO_CONV
+                const int kblk = kk / BK;                    // global K block
+                const int tap = kblk / geom.taps_cchunks;
+                const int cbase = (kblk - tap * geom.taps_cchunks) * BK;
+                const int di = tap / geom.kw - geom.pad, dj = tap % geom.kw - geom.pad;
+#pragma unroll
+                for (int ka = 0; ka < KATOMS; ++ka) {
+                    tma_load_4d(a_dst + ka * (BM * SWZ), &tma_a, fb, cbase + ka * ATOM_K,
+                                w0 + dj, h0 + di, n0);
+                    tma_load_2d(b_dst + ka * (BN * SWZ), &tma_b, fb, kk + ka * ATOM_K, col0);
+                }
+#else
+#pragma unroll
+                for (int ka = 0; ka < KATOMS; ++ka) {
+                    const int kc = kk + ka * ATOM_K;
+                    const u32 a_sub = a_dst + ka * (BM * SWZ);
+#if OPEVO_CLUSTER > 1
+                    // this CTA fetches one 1/CLUSTER slice of the shared A tile
+                    // and multicasts it into every CTA of the cluster
+                    const u32 a_part = a_sub + crank * (A_SLICE_ROWS * SWZ);
+                    const u16 mask = (u16)((1u << CLUSTER) - 1);
+#if OPEVO_BATCHED
+                    tma_load_3d_mc(a_part, &tma_a, fb, kc, row0 + crank * A_SLICE_ROWS, batch, mask);
+#else
+                    tma_load_2d_mc(a_part, &tma_a, fb, kc, row0 + crank * A_SLICE_ROWS, mask);
+#endif
+#else
+#if OPEVO_BATCHED
+                    tma_load_3d(a_sub, &tma_a, fb, kc, row0, batch);
+#else
+                    tma_load_2d(a_sub, &tma_a, fb, kc, row0);
+#endif
+#endif
+#if OPEVO_BATCHED
+                    tma_load_3d(b_dst + ka * (BN * SWZ), &tma_b, fb, kc, col0, batch);
+#else
+                    tma_load_2d(b_dst + ka * (BN * SWZ), &tma_b, fb, kc, col0);
+#endif
+                }
+#endif
+                if (++s == STAGES) { s = 0; ph ^= 1; }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ------------------------------------------------ MMA issuer
+            int s = 0;
+            u32 ph = 0;
+            for (int kb = 0; kb < num_kb; ++kb) {
+                mbar_wait(smem_u32(full_bar + s), ph);
+                tc_fence_after();
+                const u32 a_base = smem_u32(smem + s * STAGE_BYTES);
+                const u32 b_base = a_base + A_TILE;
+#pragma unroll
+                for (int ka = 0; ka < KATOMS; ++ka) {
+#pragma unroll
+                    for (int k16 = 0; k16 < ATOM_K / 16; ++k16) {
+                        const u32 koff = k16 * 32;
+                        const u64 bdesc = DESC_HI | (u64)(((b_base + ka * (BN * SWZ) + koff) >> 4) & 0x3FFF);
+#pragma unroll
+                        for (int ma = 0; ma < MATOMS; ++ma) {
+                            const u32 a_addr = a_base + ka * (BM * SWZ) + ma * (128 * SWZ) + koff;
+                            const u64 adesc = DESC_HI | (u64)((a_addr >> 4) & 0x3FFF);
+                            umma_bf16(tmem_base + ma * BN, adesc, bdesc,
+                                      (kb | ka | k16) != 0 ? 1u : 0u);
+                        }
+                    }
+                }
+#if OPEVO_CLUSTER > 1
+                // the slot is refilled by multicasts from every cluster CTA:
+                // release it in all of them once our MMAs have consumed it
+                umma_commit_mc(smem_u32(empty_bar + s), (u16)((1u << CLUSTER) - 1));
+#else
+                umma_commit(smem_u32(empty_bar + s));
+#endif
+                if (++s == STAGES) { s = 0; ph ^= 1; }
+            }
+            umma_commit(smem_u32(accum_bar));
+        }
+    } else {
+        // ---------------------------------------------------- epilogue
+        const int quarter = warp & 3;              // TMEM lane quarter of this warp
+        const int epi_tid = threadIdx.x - 64;
+        mbar_wait(smem_u32(accum_bar), 0);
+        tc_fence_after();
+        const u32 lane_addr = tmem_base + ((u32)(quarter * 32) << 16);
+        const u64 plane = (u64)rows * (u64)cols;   // one batch (or one split slice)
+#if OPEVO_CONV
+        // tile row -> NHWC output pixel row
+        auto out_row = [&](int lr) -> int {
+            const int n = n0 + lr / (TILE_H * TILE_W);
+            const int h = h0 + (lr / TILE_W) % TILE_H;
+            const int w = w0 + lr % TILE_W;
+            return (n * geom.ho + h) * geom.wo + w;
+        };
+#else
+        auto out_row = [&](int lr) -> int { return row0 + lr; };
+#endif
+        const u64 c_batch = (u64)batch * plane;
+
+        if (split == 1) {
+#pragma unroll 1
+            for (int ma = 0; ma < MATOMS; ++ma) {
+                const int r = out_row(ma * 128 + quarter * 32 + lane);
+#pragma unroll 1
+                for (int c = 0; c < BN; c += EPI_COLS) {
+                    u32 v[EPI_COLS];
+                    tmem_load<EPI_COLS>(lane_addr + ma * BN + c, v);
+                    if (BM == 64 && quarter >= 2) continue;
+                    store_row(c_out, c_batch + (u64)r * cols + col0 + c,
+                              reinterpret_cast<const float*>(v));
+                }
+            }
+        } else {
+            const u64 nbat = (u64)gridDim.z / (u64)split;
+            const u64 slice = nbat * plane;
+#pragma unroll 1
+            for (int ma = 0; ma < MATOMS; ++ma) {
+                const int r = out_row(ma * 128 + quarter * 32 + lane);
+#pragma unroll 1
+                for (int c = 0; c < BN; c += EPI_COLS) {
+                    u32 v[EPI_COLS];
+                    tmem_load<EPI_COLS>(lane_addr + ma * BN + c, v);
+                    if (BM == 64 && quarter >= 2) continue;
+                    float* dst = ws + (u64)kz * slice + c_batch + (u64)r * cols + col0 + c;
+#pragma unroll
+                    for (int j = 0; j < EPI_COLS; j += 4)
+                        st_v4(dst + j, v[j], v[j + 1], v[j + 2], v[j + 3]);
+                }
+            }
+            __threadfence();
+            epi_bar();
+            if (epi_tid == 0) {
+                const u32 tile = (u32)((batch * gridDim.y + row_tile) * gridDim.x + col_tile);
+                const u32 prev = atomicAdd(counters + tile, 1u);
+                const u32 last = (prev == (u32)(split - 1)) ? 1u : 0u;
+                if (last) counters[tile] = 0u;     // ready for the next launch
+                *last_flag = last;
+                __threadfence();
+            }
+            epi_bar();
+            if (*last_flag) {
+#pragma unroll 1
+                for (int ma = 0; ma < MATOMS; ++ma) {
+                    const int r = out_row(ma * 128 + quarter * 32 + lane);
+                    if (BM == 64 && quarter >= 2) continue;
+#pragma unroll 1
+                    for (int c = 0; c < BN; c += EPI_COLS) {
+                        float acc[EPI_COLS];
+#pragma unroll
+                        for (int j = 0; j < EPI_COLS; ++j) acc[j] = 0.0f;
+                        const u64 base = c_batch + (u64)r * cols + col0 + c;
+                        for (int z = 0; z < split; ++z) {
+                            const float* src = ws + (u64)z * slice + base;
+#pragma unroll
+                            for (int j = 0; j < EPI_COLS; j += 4) {
+                                const float4 p = ld_cg_f4(src + j);
+                                acc[j] += p.x; acc[j + 1] += p.y; acc[j + 2] += p.z; acc[j + 3] += p.w;
+                            }
+                        }
+                        store_row(c_out, base, acc);
+                    }
+                }
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (CLUSTER > 1) cluster_sync();
+    if (warp == 1) {
+        __syncwarp();
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;"
+                     :: "r"(tmem_base), "r"(TMEM_COLS) : "memory");
+    }
+}

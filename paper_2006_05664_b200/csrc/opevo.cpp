@@ -1,0 +1,1112 @@
+// libopevo: the C-ABI trial evaluator (see include/opevo.h).
+//
+// Replaces the reference's evaluation seam (pkg/src/topotune/engine.py:264-290,
+// benchmarks.py:278-302): one call per configuration compiles (NVRTC, cached),
+// verifies and CUDA-event-times a hand-written sm_100a kernel.
+//
+// libcuda and libnvrtc are dlopen'ed on first use, so the library loads (and
+// its compile-only entry point works) on a machine without a GPU.
+
+#include "opevo.h"
+
+#include <cuda.h>
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <sys/stat.h>
+#include <unistd.h>
+#include <unordered_map>
+#include <vector>
+
+extern "C" const unsigned char opevo_util_cubin[];
+extern "C" const size_t opevo_util_cubin_len;
+extern "C" const char opevo_gemm_source[];
+
+namespace {
+
+// ------------------------------------------------------------------ errors
+void put_err(char* err, size_t len, const char* fmt, ...) {
+    if (!err || len == 0) return;
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(err, len, fmt, ap);
+    va_end(ap);
+}
+
+double now_ms() {
+    using namespace std::chrono;
+    return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
+}
+
+// ------------------------------------------------------------- libcuda
+struct Driver {
+#define OPEVO_CU_FN(name, sym) decltype(&::sym) name = nullptr;
+#define OPEVO_CU_LIST(X)                                          \
+    X(Init, cuInit)                                               \
+    X(DeviceGet, cuDeviceGet)                                     \
+    X(DeviceGetAttribute, cuDeviceGetAttribute)                   \
+    X(PrimaryCtxRetain, cuDevicePrimaryCtxRetain)                 \
+    X(PrimaryCtxRelease, cuDevicePrimaryCtxRelease_v2)            \
+    X(CtxSetCurrent, cuCtxSetCurrent)                             \
+    X(CtxSynchronize, cuCtxSynchronize)                           \
+    X(ModuleLoadData, cuModuleLoadData)                           \
+    X(ModuleUnload, cuModuleUnload)                               \
+    X(ModuleGetFunction, cuModuleGetFunction)                     \
+    X(FuncSetAttribute, cuFuncSetAttribute)                       \
+    X(LaunchKernel, cuLaunchKernel)                               \
+    X(LaunchKernelEx, cuLaunchKernelEx)                           \
+    X(MemAlloc, cuMemAlloc_v2)                                    \
+    X(MemFree, cuMemFree_v2)                                      \
+    X(MemAllocHost, cuMemAllocHost_v2)                            \
+    X(MemFreeHost, cuMemFreeHost)                                 \
+    X(MemcpyHtoD, cuMemcpyHtoD_v2)                                \
+    X(MemcpyDtoH, cuMemcpyDtoH_v2)                                \
+    X(MemcpyHtoDAsync, cuMemcpyHtoDAsync_v2)                      \
+    X(MemcpyDtoHAsync, cuMemcpyDtoHAsync_v2)                      \
+    X(MemsetD8, cuMemsetD8_v2)                                    \
+    X(MemsetD8Async, cuMemsetD8Async)                             \
+    X(StreamCreate, cuStreamCreate)                               \
+    X(StreamDestroy, cuStreamDestroy_v2)                          \
+    X(StreamSynchronize, cuStreamSynchronize)                     \
+    X(StreamBeginCapture, cuStreamBeginCapture_v2)                \
+    X(StreamEndCapture, cuStreamEndCapture)                       \
+    X(GraphInstantiate, cuGraphInstantiateWithFlags)              \
+    X(GraphLaunch, cuGraphLaunch)                                 \
+    X(GraphExecDestroy, cuGraphExecDestroy)                       \
+    X(GraphDestroy, cuGraphDestroy)                               \
+    X(EventCreate, cuEventCreate)                                 \
+    X(EventDestroy, cuEventDestroy_v2)                            \
+    X(EventRecord, cuEventRecord)                                 \
+    X(EventSynchronize, cuEventSynchronize)                       \
+    X(EventElapsedTime, cuEventElapsedTime)                       \
+    X(TensorMapEncodeTiled, cuTensorMapEncodeTiled)               \
+    X(GetErrorString, cuGetErrorString)                           \
+    X(GetErrorName, cuGetErrorName)
+    OPEVO_CU_LIST(OPEVO_CU_FN)
+    void* handle = nullptr;
+    bool ok = false;
+    std::string why;
+};
+
+Driver g_cu;
+std::once_flag g_cu_once;
+
+void load_driver() {
+    std::call_once(g_cu_once, [] {
+        g_cu.handle = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
+        if (!g_cu.handle) g_cu.handle = dlopen("libcuda.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!g_cu.handle) {
+            g_cu.why = std::string("cannot dlopen libcuda.so.1: ") + dlerror();
+            return;
+        }
+#define OPEVO_CU_LOAD(name, sym)                                                     \
+    g_cu.name = reinterpret_cast<decltype(g_cu.name)>(dlsym(g_cu.handle, #sym));    \
+    if (!g_cu.name) { g_cu.why = "libcuda lacks " #sym; return; }
+        OPEVO_CU_LIST(OPEVO_CU_LOAD)
+        CUresult r = g_cu.Init(0);
+        if (r != CUDA_SUCCESS) {
+            g_cu.why = "cuInit failed (" + std::to_string((int)r) + ")";
+            return;
+        }
+        g_cu.ok = true;
+    });
+}
+
+const char* cu_str(CUresult r) {
+    const char* s = nullptr;
+    if (g_cu.GetErrorString) g_cu.GetErrorString(r, &s);
+    return s ? s : "unknown CUDA error";
+}
+
+// Errors after which the context is unusable (the worker must restart).
+bool is_sticky(CUresult r) {
+    return (r >= 700 && r <= 720) || r == CUDA_ERROR_UNKNOWN || r == CUDA_ERROR_CONTEXT_IS_DESTROYED;
+}
+
+// ------------------------------------------------------------- libnvrtc
+struct Nvrtc {
+#define OPEVO_RTC_LIST(X)                              \
+    X(Create, nvrtcCreateProgram)                      \
+    X(Compile, nvrtcCompileProgram)                    \
+    X(Destroy, nvrtcDestroyProgram)                    \
+    X(GetCUBINSize, nvrtcGetCUBINSize)                 \
+    X(GetCUBIN, nvrtcGetCUBIN)                         \
+    X(GetLogSize, nvrtcGetProgramLogSize)              \
+    X(GetLog, nvrtcGetProgramLog)                      \
+    X(ErrorString, nvrtcGetErrorString)                \
+    X(Version, nvrtcVersion)
+    OPEVO_RTC_LIST(OPEVO_CU_FN)
+    void* handle = nullptr;
+    bool ok = false;
+    std::string why;
+    int major = 0, minor = 0;
+};
+
+Nvrtc g_rtc;
+std::once_flag g_rtc_once;
+
+void load_nvrtc() {
+    std::call_once(g_rtc_once, [] {
+        const char* names[] = {"libnvrtc.so.12", "libnvrtc.so", "/usr/local/cuda/lib64/libnvrtc.so.12"};
+        for (const char* n : names) {
+            g_rtc.handle = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+            if (g_rtc.handle) break;
+        }
+        if (!g_rtc.handle) {
+            g_rtc.why = "cannot dlopen libnvrtc.so.12";
+            return;
+        }
+#define OPEVO_RTC_LOAD(name, sym)                                                     \
+    g_rtc.name = reinterpret_cast<decltype(g_rtc.name)>(dlsym(g_rtc.handle, #sym));  \
+    if (!g_rtc.name) { g_rtc.why = "libnvrtc lacks " #sym; return; }
+        OPEVO_RTC_LIST(OPEVO_RTC_LOAD)
+        g_rtc.Version(&g_rtc.major, &g_rtc.minor);
+        g_rtc.ok = true;
+    });
+}
+
+// ------------------------------------------------------------- knobs
+struct Knobs {
+    int bm, bn, bk, stages, split, cluster, tile_h, tile_w;
+};
+
+Knobs read_knobs(const int32_t* k, int n) {
+    int32_t v[OPEVO_NUM_KNOBS] = {128, 128, 64, 4, 1, 1, 1, 1};
+    for (int i = 0; i < n && i < OPEVO_NUM_KNOBS; ++i) v[i] = k[i];
+    return Knobs{v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7]};
+}
+
+int swizzle_bytes(int bk) { return bk * 2 >= 128 ? 128 : bk * 2; }
+
+size_t smem_bytes(const Knobs& k) {
+    return (size_t)k.stages * (size_t)(k.bm + k.bn) * (size_t)k.bk * 2 + 1024 + 256;
+}
+
+uint64_t fnv1a(const char* s, size_t n, uint64_t h = 1469598103934665603ull) {
+    for (size_t i = 0; i < n; ++i) { h ^= (unsigned char)s[i]; h *= 1099511628211ull; }
+    return h;
+}
+
+// Everything that changes the generated code is in the key; split-K is a
+// launch parameter and is not.
+// -lineinfo (for ncu source views) triples the cubin size; opt in with
+// OPEVO_LINEINFO=1.  It is part of the cache key.
+bool want_lineinfo() {
+    const char* v = getenv("OPEVO_LINEINFO");
+    return v && v[0] == '1';
+}
+
+std::string make_key(int family, const Knobs& k, int batched, int out_f32) {
+    static const uint64_t src_hash = fnv1a(opevo_gemm_source, strlen(opevo_gemm_source));
+    char buf[256];
+    snprintf(buf, sizeof buf, "f%d_m%d_n%d_k%d_s%d_b%d_o%d_c%d_h%d_w%d_%s%012llx", family, k.bm, k.bn,
+             k.bk, k.stages, batched, out_f32, k.cluster, family == 1 ? k.tile_h : 1,
+             family == 1 ? k.tile_w : 1, want_lineinfo() ? "L" : "",
+             (unsigned long long)(src_hash & 0xffffffffffffull));
+    return buf;
+}
+
+// Structural checks shared by compile and bind (operator-independent).
+bool knobs_compilable(int family, const Knobs& k, char* err, size_t len) {
+    if (!(k.bm == 128 || k.bm == 256)) {
+        put_err(err, len, "BM=%d unsupported (128 or 256)", k.bm);
+        return false;
+    }
+    if (k.bn < 16 || k.bn > 256 || k.bn % 16) {
+        put_err(err, len, "BN=%d must be a multiple of 16 in [16,256]", k.bn);
+        return false;
+    }
+    const bool bk_ok = k.bk == 16 || k.bk == 32 || (k.bk >= 64 && k.bk <= 256 && k.bk % 64 == 0);
+    if (!bk_ok) {
+        put_err(err, len, "BK=%d unsupported (16, 32 or a multiple of 64 up to 256)", k.bk);
+        return false;
+    }
+    if (k.stages < 1 || k.stages > 16) {
+        put_err(err, len, "stages=%d out of range", k.stages);
+        return false;
+    }
+    if ((k.bm == 256 ? 2 : 1) * k.bn > 512) {
+        put_err(err, len, "accumulator %dx%d exceeds 512 TMEM columns", k.bm, k.bn);
+        return false;
+    }
+    if (!(k.cluster == 1 || k.cluster == 2 || k.cluster == 4 || k.cluster == 8) ||
+        k.bm % (8 * k.cluster)) {
+        put_err(err, len, "cluster=%d unsupported for BM=%d", k.cluster, k.bm);
+        return false;
+    }
+    if (smem_bytes(k) > 232448) {
+        put_err(err, len, "shared memory %zu B exceeds 227 KB", smem_bytes(k));
+        return false;
+    }
+    if (family == 1) {
+        if (k.cluster != 1) {
+            put_err(err, len, "conv instances do not multicast");
+            return false;
+        }
+        if (k.tile_h < 1 || k.tile_w < 1 || k.bm % (k.tile_h * k.tile_w) || k.tile_w > 256 ||
+            k.tile_h > 256 || k.bm / (k.tile_h * k.tile_w) > 256) {
+            put_err(err, len, "conv tile %dx%d does not divide BM=%d", k.tile_h, k.tile_w, k.bm);
+            return false;
+        }
+    }
+    return true;
+}
+
+std::mutex g_fs_mu;
+
+bool read_file(const std::string& path, std::vector<char>& out) {
+    FILE* f = fopen(path.c_str(), "rb");
+    if (!f) return false;
+    fseek(f, 0, SEEK_END);
+    long n = ftell(f);
+    fseek(f, 0, SEEK_SET);
+    out.resize(n > 0 ? (size_t)n : 0);
+    size_t got = n > 0 ? fread(out.data(), 1, (size_t)n, f) : 0;
+    fclose(f);
+    return n > 0 && got == (size_t)n;
+}
+
+void write_file_atomic(const std::string& path, const std::vector<char>& data) {
+    char tmp[64];
+    static std::atomic<unsigned> seq{0};
+    snprintf(tmp, sizeof tmp, ".tmp.%d.%u", (int)getpid(), seq.fetch_add(1));
+    std::string t = path + tmp;
+    FILE* f = fopen(t.c_str(), "wb");
+    if (!f) return;
+    fwrite(data.data(), 1, data.size(), f);
+    fclose(f);
+    rename(t.c_str(), path.c_str());
+}
+
+void mkdirs(const std::string& dir) {
+    std::string cur;
+    for (size_t i = 0; i < dir.size(); ++i) {
+        cur.push_back(dir[i]);
+        if (dir[i] == '/' || i + 1 == dir.size()) mkdir(cur.c_str(), 0755);
+    }
+}
+
+// NVRTC compile of one instance.  Returns status; cubin in `out`.
+int nvrtc_build(int family, const Knobs& k, int batched, int out_f32, std::vector<char>& out,
+                char* err, size_t len) {
+    load_nvrtc();
+    if (!g_rtc.ok) {
+        put_err(err, len, "%s", g_rtc.why.c_str());
+        return OPEVO_ERR_NO_NVRTC;
+    }
+    nvrtcProgram prog;
+    if (g_rtc.Create(&prog, opevo_gemm_source, "gemm_sm100.cuh", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+        put_err(err, len, "nvrtcCreateProgram failed");
+        return OPEVO_COMPILE_ERROR;
+    }
+    std::vector<std::string> opts = {
+        "-arch=sm_100a", "-std=c++17", "-default-device",
+        "-DOPEVO_BM=" + std::to_string(k.bm), "-DOPEVO_BN=" + std::to_string(k.bn),
+        "-DOPEVO_BK=" + std::to_string(k.bk), "-DOPEVO_STAGES=" + std::to_string(k.stages),
+        "-DOPEVO_BATCHED=" + std::to_string(batched), "-DOPEVO_OUT_F32=" + std::to_string(out_f32),
+        "-DOPEVO_CLUSTER=" + std::to_string(k.cluster), "-DOPEVO_CONV=" + std::to_string(family == 1),
+        "-DOPEVO_TILE_H=" + std::to_string(family == 1 ? k.tile_h : 1),
+        "-DOPEVO_TILE_W=" + std::to_string(family == 1 ? k.tile_w : 1)};
+    if (want_lineinfo()) opts.push_back("-lineinfo");
+    std::vector<const char*> argv;
+    for (auto& o : opts) argv.push_back(o.c_str());
+    nvrtcResult r = g_rtc.Compile(prog, (int)argv.size(), argv.data());
+    if (r != NVRTC_SUCCESS) {
+        size_t n = 0;
+        g_rtc.GetLogSize(prog, &n);
+        std::string log(n, '\0');
+        if (n) g_rtc.GetLog(prog, &log[0]);
+        put_err(err, len, "NVRTC: %s: %s", g_rtc.ErrorString(r), log.c_str());
+        g_rtc.Destroy(&prog);
+        return OPEVO_COMPILE_ERROR;
+    }
+    size_t n = 0;
+    g_rtc.GetCUBINSize(prog, &n);
+    out.resize(n);
+    g_rtc.GetCUBIN(prog, out.data());
+    g_rtc.Destroy(&prog);
+    return OPEVO_OK;
+}
+
+// Disk-cached compile: cache hit -> 2, compiled -> 0, failure -> status.
+int get_cubin(int family, const Knobs& k, int batched, int out_f32, const std::string& cache_dir,
+              std::vector<char>& cubin, double* compile_ms, int* hit, char* err, size_t len) {
+    const std::string key = make_key(family, k, batched, out_f32);
+    const std::string path = cache_dir.empty() ? "" : cache_dir + "/" + key + ".cubin";
+    if (compile_ms) *compile_ms = 0.0;
+    if (!path.empty() && read_file(path, cubin)) {
+        if (hit) *hit = 2;
+        return OPEVO_OK;
+    }
+    const double t0 = now_ms();
+    int st = nvrtc_build(family, k, batched, out_f32, cubin, err, len);
+    if (compile_ms) *compile_ms = now_ms() - t0;
+    if (st != OPEVO_OK) return st;
+    if (hit) *hit = 0;
+    if (!path.empty()) {
+        std::lock_guard<std::mutex> g(g_fs_mu);
+        mkdirs(cache_dir);
+        write_file_atomic(path, cubin);
+    }
+    return OPEVO_OK;
+}
+
+struct LoadedModule {
+    CUmodule mod = nullptr;
+    CUfunction fn = nullptr;
+    int smem_set = 0;
+};
+
+}  // namespace
+
+// ===================================================================== ctx
+struct opevo_ctx {
+    int device = 0;
+    CUdevice dev = 0;
+    CUcontext cu = nullptr;
+    CUstream stream = nullptr;
+    CUmodule util = nullptr;
+    CUfunction k_fill_bf16 = nullptr, k_fill_f32 = nullptr, k_fill_u8 = nullptr, k_ref_gemm = nullptr,
+               k_ref_conv = nullptr, k_nchw2nhwc = nullptr, k_compare = nullptr, k_flush = nullptr;
+    CUdeviceptr flush_buf = 0;
+    size_t flush_bytes = 0;
+    CUdeviceptr cmp_buf = 0;
+    int sm_count = 0, smem_optin = 0, cc_major = 0, cc_minor = 0;
+    std::string cache_dir;
+    std::unordered_map<std::string, LoadedModule> modules;
+    bool poisoned = false;
+};
+
+struct opevo_op {
+    opevo_ctx* ctx = nullptr;
+    opevo_op_desc d{};
+    int64_t rows = 0, cols = 0, depth = 0, batch = 1;   // GEMM view
+    CUdeviceptr a = 0, b = 0, c = 0, ref = 0;
+    CUdeviceptr conv_x = 0, conv_w = 0;                 // paper layouts (NCHW / OIHW)
+    CUdeviceptr ws = 0, counters = 0;
+    size_t ws_bytes = 0, counter_bytes = 0;
+    size_t a_bytes = 0, b_bytes = 0, c_bytes = 0;
+    int in_f32 = 0, out_f32 = 0;
+};
+
+struct ConvGeomHost {
+    int cin, ho, wo, kw, pad, taps_cchunks;
+};
+
+struct opevo_kernel {
+    opevo_op* op = nullptr;
+    Knobs k{};
+    int family = 0;
+    CUfunction fn = nullptr;
+    alignas(64) CUtensorMap tma_a;
+    alignas(64) CUtensorMap tma_b;
+    unsigned grid[3] = {1, 1, 1};
+    size_t smem = 0;
+    int k_per_split = 0;
+    ConvGeomHost geom{};
+    double flops = 0.0;
+};
+
+namespace {
+
+int fail_cu(opevo_ctx* ctx, CUresult r, const char* what, char* err, size_t len) {
+    put_err(err, len, "%s: %s (%d)", what, cu_str(r), (int)r);
+    if (is_sticky(r)) {
+        if (ctx) ctx->poisoned = true;
+        return OPEVO_ERR_STICKY;
+    }
+    return OPEVO_ERR_CUDA;
+}
+
+#define CU_TRY(ctx, call, what)                                          \
+    do {                                                                 \
+        CUresult _r = (call);                                            \
+        if (_r != CUDA_SUCCESS) return fail_cu((ctx), _r, (what), err, errlen); \
+    } while (0)
+
+unsigned grid_for(uint64_t n) {
+    uint64_t g = (n + 255) / 256;
+    return (unsigned)std::min<uint64_t>(std::max<uint64_t>(g, 1), 148 * 32);
+}
+
+int launch_simple(opevo_ctx* ctx, CUfunction f, unsigned grid, unsigned block, void** args, char* err,
+                  size_t errlen) {
+    CU_TRY(ctx, g_cu.LaunchKernel(f, grid, 1, 1, block, 1, 1, 0, ctx->stream, args, nullptr), "launch");
+    return OPEVO_OK;
+}
+
+int fill(opevo_ctx* ctx, CUdeviceptr p, uint64_t n, uint64_t seed, int f32, char* err, size_t errlen) {
+    void* args[] = {&p, &n, &seed};
+    return launch_simple(ctx, f32 ? ctx->k_fill_f32 : ctx->k_fill_bf16, grid_for(n), 256, args, err,
+                         errlen);
+}
+
+int compute_reference(opevo_op* op, char* err, size_t errlen) {
+    opevo_ctx* ctx = op->ctx;
+    if (op->d.kind == OPEVO_CONV2D) {
+        const int32_t* c = op->d.conv;
+        int N = c[0], C = c[1], H = c[2], W = c[3], K = c[4], KH = c[5], KW = c[6], S = c[7], P = c[8];
+        int HO = (H + 2 * P - KH) / S + 1, WO = (W + 2 * P - KW) / S + 1;
+        void* args[] = {&op->conv_x, &op->conv_w, &op->ref, &N, &C, &H, &W, &K, &KH, &KW, &S, &P, &HO, &WO};
+        uint64_t total = (uint64_t)N * HO * WO * K;
+        int st = launch_simple(ctx, ctx->k_ref_conv, grid_for(total), 256, args, err, errlen);
+        if (st) return st;
+    } else {
+        int rows = (int)op->rows, cols = (int)op->cols, depth = (int)op->depth, in_f32 = op->in_f32;
+        void* args[] = {&op->a, &op->b, &op->ref, &rows, &cols, &depth, &in_f32};
+        CU_TRY(ctx, g_cu.LaunchKernel(ctx->k_ref_gemm, (unsigned)((cols + 63) / 64), (unsigned)((rows + 63) / 64),
+                                      (unsigned)op->batch, 256, 1, 1, 0, ctx->stream, args, nullptr),
+               "reference gemm");
+    }
+    CU_TRY(ctx, g_cu.StreamSynchronize(ctx->stream), "reference sync");
+    return OPEVO_OK;
+}
+
+int ensure_ws(opevo_op* op, size_t ws_need, size_t cnt_need, char* err, size_t errlen) {
+    opevo_ctx* ctx = op->ctx;
+    if (ws_need > op->ws_bytes) {
+        if (op->ws) g_cu.MemFree(op->ws);
+        op->ws = 0;
+        op->ws_bytes = 0;
+        CU_TRY(ctx, g_cu.MemAlloc(&op->ws, ws_need), "alloc split-K workspace");
+        op->ws_bytes = ws_need;
+    }
+    if (cnt_need > op->counter_bytes) {
+        if (op->counters) g_cu.MemFree(op->counters);
+        op->counters = 0;
+        op->counter_bytes = 0;
+        CU_TRY(ctx, g_cu.MemAlloc(&op->counters, cnt_need), "alloc tile counters");
+        CU_TRY(ctx, g_cu.MemsetD8(op->counters, 0, cnt_need), "zero tile counters");
+        op->counter_bytes = cnt_need;
+    }
+    return OPEVO_OK;
+}
+
+CUtensorMapSwizzle swz_enum(int bytes) {
+    return bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                        : bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+}
+
+int encode_map(CUtensorMap* map, CUdeviceptr base, int rank, const uint64_t* dims, const uint64_t* strides_b,
+               const uint32_t* box, int swz, char* err, size_t errlen) {
+    uint32_t es[5] = {1, 1, 1, 1, 1};
+    CUresult r = g_cu.TensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (cuuint32_t)rank,
+                                           (void*)base, (const cuuint64_t*)dims,
+                                           (const cuuint64_t*)strides_b, (const cuuint32_t*)box,
+                                           (const cuuint32_t*)es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                           swz_enum(swz), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        put_err(err, errlen, "cuTensorMapEncodeTiled: %s", cu_str(r));
+        return OPEVO_INVALID_CONFIG;
+    }
+    return OPEVO_OK;
+}
+
+int launch_kernel(opevo_kernel* kr, char* err, size_t errlen) {
+    opevo_op* op = kr->op;
+    opevo_ctx* ctx = op->ctx;
+    int rows = (int)op->rows;
+    int cols = (int)op->cols;
+    int kps = kr->k_per_split, split = kr->k.split;
+    void* cptr = (void*)op->c;
+    float* ws = (float*)op->ws;
+    unsigned* cnt = (unsigned*)op->counters;
+    void* args[] = {&kr->tma_a, &kr->tma_b, &cptr, &ws, &cnt, &rows, &cols, &kps, &split, &kr->geom};
+    CUlaunchConfig cfg{};
+    cfg.gridDimX = kr->grid[0];
+    cfg.gridDimY = kr->grid[1];
+    cfg.gridDimZ = kr->grid[2];
+    cfg.blockDimX = 192;
+    cfg.blockDimY = 1;
+    cfg.blockDimZ = 1;
+    cfg.sharedMemBytes = (unsigned)kr->smem;
+    cfg.hStream = ctx->stream;
+    CUlaunchAttribute attr[1];
+    if (kr->k.cluster > 1) {
+        attr[0].id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
+        attr[0].value.clusterDim.x = (unsigned)kr->k.cluster;
+        attr[0].value.clusterDim.y = 1;
+        attr[0].value.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    }
+    CUresult r = g_cu.LaunchKernelEx(&cfg, kr->fn, args, nullptr);
+    if (r != CUDA_SUCCESS) {
+        int st = fail_cu(ctx, r, "kernel launch", err, errlen);
+        return st == OPEVO_ERR_STICKY ? st : OPEVO_LAUNCH_ERROR;
+    }
+    return OPEVO_OK;
+}
+
+int sync_checked(opevo_ctx* ctx, const char* what, char* err, size_t errlen) {
+    CUresult r = g_cu.StreamSynchronize(ctx->stream);
+    if (r != CUDA_SUCCESS) {
+        int st = fail_cu(ctx, r, what, err, errlen);
+        return st == OPEVO_ERR_STICKY ? st : OPEVO_LAUNCH_ERROR;
+    }
+    return OPEVO_OK;
+}
+
+}  // namespace
+
+// ================================================================= exports
+extern "C" {
+
+int opevo_abi_version(void) { return OPEVO_ABI_VERSION; }
+
+int opevo_kernel_key(int family, const int32_t* knobs, int nknobs, int batched, int out_f32, char* key,
+                     size_t keylen) {
+    if (!knobs || !key) return OPEVO_ERR_ARG;
+    std::string s = make_key(family, read_knobs(knobs, nknobs), batched, out_f32);
+    snprintf(key, keylen, "%s", s.c_str());
+    return OPEVO_OK;
+}
+
+int opevo_compile(int family, const int32_t* knobs, int nknobs, int batched, int out_f32,
+                  const char* cache_dir, double* compile_ms, char* err, size_t errlen) {
+    if (!knobs) return OPEVO_ERR_ARG;
+    Knobs k = read_knobs(knobs, nknobs);
+    if (!knobs_compilable(family, k, err, errlen)) return OPEVO_INVALID_CONFIG;
+    std::vector<char> cubin;
+    int hit = 0;
+    return get_cubin(family, k, batched, out_f32, cache_dir ? cache_dir : "", cubin, compile_ms, &hit,
+                     err, errlen);
+}
+
+int opevo_ctx_create(int device, const char* cache_dir, opevo_ctx** out, char* err, size_t errlen) {
+    if (!out) return OPEVO_ERR_ARG;
+    *out = nullptr;
+    load_driver();
+    if (!g_cu.ok) {
+        put_err(err, errlen, "%s", g_cu.why.c_str());
+        return OPEVO_ERR_NO_DEVICE;
+    }
+    opevo_ctx* ctx = new opevo_ctx();
+    ctx->device = device;
+    ctx->cache_dir = cache_dir ? cache_dir : "";
+    CUresult r = g_cu.DeviceGet(&ctx->dev, device);
+    if (r != CUDA_SUCCESS) {
+        put_err(err, errlen, "cuDeviceGet(%d): %s", device, cu_str(r));
+        delete ctx;
+        return OPEVO_ERR_NO_DEVICE;
+    }
+    if ((r = g_cu.PrimaryCtxRetain(&ctx->cu, ctx->dev)) != CUDA_SUCCESS ||
+        (r = g_cu.CtxSetCurrent(ctx->cu)) != CUDA_SUCCESS) {
+        put_err(err, errlen, "primary context: %s", cu_str(r));
+        delete ctx;
+        return OPEVO_ERR_NO_DEVICE;
+    }
+    g_cu.DeviceGetAttribute(&ctx->sm_count, CU_DEVICE_ATTRIBUTE_MULTIPROCESSOR_COUNT, ctx->dev);
+    g_cu.DeviceGetAttribute(&ctx->smem_optin, CU_DEVICE_ATTRIBUTE_MAX_SHARED_MEMORY_PER_BLOCK_OPTIN, ctx->dev);
+    g_cu.DeviceGetAttribute(&ctx->cc_major, CU_DEVICE_ATTRIBUTE_COMPUTE_CAPABILITY_MAJOR, ctx->dev);
+    g_cu.DeviceGetAttribute(&ctx->cc_minor, CU_DEVICE_ATTRIBUTE_COMPUTE_CAPABILITY_MINOR, ctx->dev);
+    if (ctx->cc_major != 10) {
+        put_err(err, errlen, "device %d is sm_%d%d; this build targets sm_100a only", device,
+                ctx->cc_major, ctx->cc_minor);
+        g_cu.PrimaryCtxRelease(ctx->dev);
+        delete ctx;
+        return OPEVO_ERR_NO_DEVICE;
+    }
+    int st = OPEVO_OK;
+    auto bail = [&](CUresult rr, const char* what) {
+        st = fail_cu(ctx, rr, what, err, errlen);
+    };
+    if ((r = g_cu.StreamCreate(&ctx->stream, CU_STREAM_NON_BLOCKING)) != CUDA_SUCCESS) bail(r, "stream");
+    else if ((r = g_cu.ModuleLoadData(&ctx->util, opevo_util_cubin)) != CUDA_SUCCESS) bail(r, "load util cubin");
+    else if ((r = g_cu.MemAlloc(&ctx->cmp_buf, 16)) != CUDA_SUCCESS) bail(r, "alloc");
+    if (st == OPEVO_OK) {
+        struct { CUfunction* f; const char* n; } fns[] = {
+            {&ctx->k_fill_bf16, "opevo_fill_bf16"}, {&ctx->k_fill_f32, "opevo_fill_f32"},
+            {&ctx->k_fill_u8, "opevo_fill_u8"},     {&ctx->k_ref_gemm, "opevo_ref_gemm"},
+            {&ctx->k_ref_conv, "opevo_ref_conv"},   {&ctx->k_nchw2nhwc, "opevo_nchw_to_nhwc"},
+            {&ctx->k_compare, "opevo_compare"},     {&ctx->k_flush, "opevo_flush"}};
+        for (auto& f : fns) {
+            if ((r = g_cu.ModuleGetFunction(f.f, ctx->util, f.n)) != CUDA_SUCCESS) {
+                bail(r, f.n);
+                break;
+            }
+        }
+    }
+    if (st != OPEVO_OK) {
+        opevo_ctx_destroy(ctx);
+        return st;
+    }
+    *out = ctx;
+    return OPEVO_OK;
+}
+
+void opevo_ctx_destroy(opevo_ctx* ctx) {
+    if (!ctx) return;
+    if (g_cu.ok && !ctx->poisoned) {
+        g_cu.CtxSetCurrent(ctx->cu);
+        for (auto& kv : ctx->modules)
+            if (kv.second.mod) g_cu.ModuleUnload(kv.second.mod);
+        if (ctx->util) g_cu.ModuleUnload(ctx->util);
+        if (ctx->flush_buf) g_cu.MemFree(ctx->flush_buf);
+        if (ctx->cmp_buf) g_cu.MemFree(ctx->cmp_buf);
+        if (ctx->stream) g_cu.StreamDestroy(ctx->stream);
+        g_cu.PrimaryCtxRelease(ctx->dev);
+    }
+    delete ctx;
+}
+
+int opevo_ctx_info(opevo_ctx* ctx, int* sm_count, int* max_smem_optin, int* cc_major, int* cc_minor) {
+    if (!ctx) return OPEVO_ERR_ARG;
+    if (sm_count) *sm_count = ctx->sm_count;
+    if (max_smem_optin) *max_smem_optin = ctx->smem_optin;
+    if (cc_major) *cc_major = ctx->cc_major;
+    if (cc_minor) *cc_minor = ctx->cc_minor;
+    return OPEVO_OK;
+}
+
+void opevo_op_destroy(opevo_op* op) {
+    if (!op) return;
+    if (g_cu.ok && op->ctx && !op->ctx->poisoned) {
+        CUdeviceptr ps[] = {op->a, op->b, op->c, op->ref, op->conv_x, op->conv_w, op->ws, op->counters};
+        for (CUdeviceptr p : ps)
+            if (p) g_cu.MemFree(p);
+    }
+    delete op;
+}
+
+int opevo_op_prepare(opevo_ctx* ctx, const opevo_op_desc* desc, opevo_op** out, char* err, size_t errlen) {
+    if (!ctx || !desc || !out) return OPEVO_ERR_ARG;
+    if (ctx->poisoned) {
+        put_err(err, errlen, "context poisoned by an earlier fault");
+        return OPEVO_ERR_STICKY;
+    }
+    *out = nullptr;
+    g_cu.CtxSetCurrent(ctx->cu);
+    opevo_op* op = new opevo_op();
+    op->ctx = ctx;
+    op->d = *desc;
+    op->in_f32 = op->out_f32 = desc->dtype == OPEVO_F32 ? 1 : 0;
+    const size_t esz = op->in_f32 ? 4 : 2;
+    int st = OPEVO_OK;
+    auto alloc = [&](CUdeviceptr* p, size_t bytes, const char* what) -> bool {
+        CUresult r = g_cu.MemAlloc(p, std::max<size_t>(bytes, 16));
+        if (r != CUDA_SUCCESS) {
+            st = fail_cu(ctx, r, what, err, errlen);
+            return false;
+        }
+        return true;
+    };
+    if (desc->kind == OPEVO_MATMUL || desc->kind == OPEVO_BATCHMATMUL) {
+        op->batch = desc->kind == OPEVO_MATMUL ? 1 : desc->batch;
+        op->rows = desc->rows;
+        op->cols = desc->cols;
+        op->depth = desc->depth;
+        if (op->batch < 1 || op->rows < 1 || op->cols < 1 || op->depth < 1) {
+            put_err(err, errlen, "non-positive operator dimension");
+            delete op;
+            return OPEVO_ERR_ARG;
+        }
+        op->a_bytes = (size_t)op->batch * op->rows * op->depth * esz;
+        op->b_bytes = (size_t)op->batch * op->cols * op->depth * esz;
+        op->c_bytes = (size_t)op->batch * op->rows * op->cols * (op->out_f32 ? 4 : 2);
+        if (alloc(&op->a, op->a_bytes, "alloc A") && alloc(&op->b, op->b_bytes, "alloc B") &&
+            alloc(&op->c, op->c_bytes, "alloc C") &&
+            alloc(&op->ref, (size_t)op->batch * op->rows * op->cols * 4, "alloc reference")) {
+            st = fill(ctx, op->a, op->a_bytes / esz, desc->seed, op->in_f32, err, errlen);
+            if (!st) st = fill(ctx, op->b, op->b_bytes / esz, desc->seed + 1, op->in_f32, err, errlen);
+        }
+    } else if (desc->kind == OPEVO_CONV2D) {
+        const int32_t* c = desc->conv;
+        int N = c[0], C = c[1], H = c[2], W = c[3], K = c[4], KH = c[5], KW = c[6], S = c[7], P = c[8];
+        if (desc->dtype != OPEVO_BF16 || N < 1 || C < 1 || H < 1 || W < 1 || K < 1 || KH < 1 || KW < 1 ||
+            S < 1 || P < 0) {
+            put_err(err, errlen, "invalid conv2d descriptor");
+            delete op;
+            return OPEVO_ERR_ARG;
+        }
+        int HO = (H + 2 * P - KH) / S + 1, WO = (W + 2 * P - KW) / S + 1;
+        op->batch = 1;
+        op->rows = (int64_t)N * HO * WO;
+        op->cols = K;
+        op->depth = (int64_t)KH * KW * C;
+        op->a_bytes = (size_t)N * C * H * W * 2;
+        op->b_bytes = (size_t)K * C * KH * KW * 2;
+        op->c_bytes = (size_t)op->rows * op->cols * 2;
+        if (alloc(&op->conv_x, op->a_bytes, "alloc X") && alloc(&op->conv_w, op->b_bytes, "alloc W") &&
+            alloc(&op->a, op->a_bytes, "alloc X nhwc") && alloc(&op->b, op->b_bytes, "alloc W ohwi") &&
+            alloc(&op->c, op->c_bytes, "alloc C") && alloc(&op->ref, (size_t)op->rows * op->cols * 4, "alloc ref")) {
+            st = fill(ctx, op->conv_x, op->a_bytes / 2, desc->seed, 0, err, errlen);
+            if (!st) st = fill(ctx, op->conv_w, op->b_bytes / 2, desc->seed + 1, 0, err, errlen);
+            if (!st) {
+                uint64_t n1 = op->a_bytes / 2;
+                void* a1[] = {&op->conv_x, &op->a, &N, &C, &H, &W};
+                st = launch_simple(ctx, ctx->k_nchw2nhwc, grid_for(n1), 256, a1, err, errlen);
+            }
+            if (!st) {
+                // OIHW viewed as [O][I][KH][KW] -> [O][KH][KW][I]
+                uint64_t n2 = op->b_bytes / 2;
+                void* a2[] = {&op->conv_w, &op->b, &K, &C, &KH, &KW};
+                st = launch_simple(ctx, ctx->k_nchw2nhwc, grid_for(n2), 256, a2, err, errlen);
+            }
+        }
+    } else {
+        put_err(err, errlen, "unknown operator kind %d", desc->kind);
+        delete op;
+        return OPEVO_ERR_ARG;
+    }
+    if (!st) st = compute_reference(op, err, errlen);
+    if (st) {
+        opevo_op_destroy(op);
+        return st;
+    }
+    *out = op;
+    return OPEVO_OK;
+}
+
+int opevo_op_sizes(const opevo_op* op, size_t* a_bytes, size_t* b_bytes, size_t* c_bytes) {
+    if (!op) return OPEVO_ERR_ARG;
+    if (a_bytes) *a_bytes = op->a_bytes;
+    if (b_bytes) *b_bytes = op->b_bytes;
+    if (c_bytes) *c_bytes = op->c_bytes;
+    return OPEVO_OK;
+}
+
+int opevo_op_upload(opevo_op* op, const void* a_host, const void* b_host, char* err, size_t errlen) {
+    if (!op) return OPEVO_ERR_ARG;
+    opevo_ctx* ctx = op->ctx;
+    g_cu.CtxSetCurrent(ctx->cu);
+    if (a_host) CU_TRY(ctx, g_cu.MemcpyHtoDAsync(op->a, a_host, op->a_bytes, ctx->stream), "upload A");
+    if (b_host) CU_TRY(ctx, g_cu.MemcpyHtoDAsync(op->b, b_host, op->b_bytes, ctx->stream), "upload B");
+    return OPEVO_OK;
+}
+
+int opevo_op_download(opevo_op* op, void* c_host, size_t bytes, char* err, size_t errlen) {
+    if (!op || !c_host) return OPEVO_ERR_ARG;
+    opevo_ctx* ctx = op->ctx;
+    g_cu.CtxSetCurrent(ctx->cu);
+    CU_TRY(ctx, g_cu.MemcpyDtoHAsync(c_host, op->c, std::min(bytes, op->c_bytes), ctx->stream), "download C");
+    CU_TRY(ctx, g_cu.StreamSynchronize(ctx->stream), "download sync");
+    return OPEVO_OK;
+}
+
+int opevo_op_read_inputs(opevo_op* op, void* a_host, void* b_host, char* err, size_t errlen) {
+    if (!op) return OPEVO_ERR_ARG;
+    opevo_ctx* ctx = op->ctx;
+    g_cu.CtxSetCurrent(ctx->cu);
+    CU_TRY(ctx, g_cu.StreamSynchronize(ctx->stream), "sync");
+    if (a_host) CU_TRY(ctx, g_cu.MemcpyDtoH(a_host, op->a, op->a_bytes), "read A");
+    if (b_host) CU_TRY(ctx, g_cu.MemcpyDtoH(b_host, op->b, op->b_bytes), "read B");
+    return OPEVO_OK;
+}
+
+int opevo_op_reference(opevo_op* op, float* host, size_t count, char* err, size_t errlen) {
+    if (!op || !host) return OPEVO_ERR_ARG;
+    opevo_ctx* ctx = op->ctx;
+    g_cu.CtxSetCurrent(ctx->cu);
+    size_t n = std::min<size_t>(count, (size_t)op->batch * op->rows * op->cols);
+    CU_TRY(ctx, g_cu.StreamSynchronize(ctx->stream), "sync");
+    CU_TRY(ctx, g_cu.MemcpyDtoH(host, op->ref, n * 4), "download reference");
+    return OPEVO_OK;
+}
+
+int opevo_op_refresh_reference(opevo_op* op, char* err, size_t errlen) {
+    if (!op) return OPEVO_ERR_ARG;
+    g_cu.CtxSetCurrent(op->ctx->cu);
+    return compute_reference(op, err, errlen);
+}
+
+int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nknobs, opevo_kernel** out,
+                     opevo_trial_result* info, char* err, size_t errlen) {
+    if (!ctx || !op || !knobs || !out) return OPEVO_ERR_ARG;
+    *out = nullptr;
+    if (ctx->poisoned) {
+        put_err(err, errlen, "context poisoned by an earlier fault");
+        return OPEVO_ERR_STICKY;
+    }
+    g_cu.CtxSetCurrent(ctx->cu);
+    const double t0 = now_ms();
+    Knobs k = read_knobs(knobs, nknobs);
+    const int family = op->d.kind == OPEVO_CONV2D ? 1 : 0;
+    const int batched = op->d.kind == OPEVO_BATCHMATMUL ? 1 : 0;
+    if (op->in_f32) {
+        put_err(err, errlen, "fp32 operands are not served by the tcgen05 bf16 family");
+        return OPEVO_INVALID_CONFIG;
+    }
+    if (!knobs_compilable(family, k, err, errlen)) return OPEVO_INVALID_CONFIG;
+    if ((int)smem_bytes(k) > ctx->smem_optin) {
+        put_err(err, errlen, "shared memory %zu B exceeds the device limit %d", smem_bytes(k), ctx->smem_optin);
+        return OPEVO_INVALID_CONFIG;
+    }
+    // operator-dependent feasibility (divisibility: no tail handling by design)
+    if (op->rows % k.bm || op->cols % k.bn) {
+        put_err(err, errlen, "tile %dx%d does not divide %lldx%lld", k.bm, k.bn, (long long)op->rows,
+                (long long)op->cols);
+        return OPEVO_INVALID_CONFIG;
+    }
+    if (k.split < 1 || op->depth % ((int64_t)k.split * k.bk)) {
+        put_err(err, errlen, "split %d x BK %d does not divide K=%lld", k.split, k.bk, (long long)op->depth);
+        return OPEVO_INVALID_CONFIG;
+    }
+    const int64_t col_tiles = op->cols / k.bn, row_tiles = op->rows / k.bm;
+    if (col_tiles % k.cluster) {
+        put_err(err, errlen, "cluster %d does not divide %lld column tiles", k.cluster, (long long)col_tiles);
+        return OPEVO_INVALID_CONFIG;
+    }
+    opevo_kernel* kr = new opevo_kernel();
+    kr->op = op;
+    kr->k = k;
+    kr->family = family;
+    kr->k_per_split = (int)(op->depth / k.split);
+    kr->smem = smem_bytes(k);
+    kr->flops = 2.0 * (double)op->batch * (double)op->rows * (double)op->cols * (double)op->depth;
+    int st = OPEVO_OK;
+    const int swz = swizzle_bytes(k.bk);
+    const uint32_t atom_k = (uint32_t)(swz / 2);
+    if (family == 1) {
+        const int32_t* c = op->d.conv;
+        int N = c[0], C = c[1], H = c[2], W = c[3], KH = c[5], KW = c[6], S = c[7], P = c[8];
+        int HO = (H + 2 * P - KH) / S + 1, WO = (W + 2 * P - KW) / S + 1;
+        const int tile_n = k.bm / (k.tile_h * k.tile_w);
+        if (S != 1 || C % k.bk || HO % k.tile_h || WO % k.tile_w || N % tile_n) {
+            put_err(err, errlen, "conv tiling (n%d h%d w%d, BK %d, stride %d) does not divide the problem",
+                    tile_n, k.tile_h, k.tile_w, k.bk, S);
+            delete kr;
+            return OPEVO_INVALID_CONFIG;
+        }
+        kr->geom = ConvGeomHost{C, HO, WO, KW, P, C / k.bk};
+        uint64_t dims[4] = {(uint64_t)C, (uint64_t)W, (uint64_t)H, (uint64_t)N};
+        uint64_t strides[3] = {(uint64_t)C * 2, (uint64_t)C * W * 2, (uint64_t)C * W * H * 2};
+        uint32_t box[4] = {atom_k, (uint32_t)k.tile_w, (uint32_t)k.tile_h, (uint32_t)tile_n};
+        st = encode_map(&kr->tma_a, op->a, 4, dims, strides, box, swz, err, errlen);
+        uint64_t bd[2] = {(uint64_t)op->depth, (uint64_t)op->cols};
+        uint64_t bs[1] = {(uint64_t)op->depth * 2};
+        uint32_t bb[2] = {atom_k, (uint32_t)k.bn};
+        if (!st) st = encode_map(&kr->tma_b, op->b, 2, bd, bs, bb, swz, err, errlen);
+        kr->grid[0] = (unsigned)col_tiles;
+        kr->grid[1] = (unsigned)((N / tile_n) * (HO / k.tile_h) * (WO / k.tile_w));
+        kr->grid[2] = (unsigned)k.split;
+    } else {
+        const int rank = batched ? 3 : 2;
+        uint64_t ad[3] = {(uint64_t)op->depth, (uint64_t)op->rows, (uint64_t)op->batch};
+        uint64_t as[2] = {(uint64_t)op->depth * 2, (uint64_t)op->depth * op->rows * 2};
+        uint32_t ab[3] = {atom_k, (uint32_t)(k.bm / k.cluster), 1};
+        uint64_t bd[3] = {(uint64_t)op->depth, (uint64_t)op->cols, (uint64_t)op->batch};
+        uint64_t bs[2] = {(uint64_t)op->depth * 2, (uint64_t)op->depth * op->cols * 2};
+        uint32_t bb[3] = {atom_k, (uint32_t)k.bn, 1};
+        st = encode_map(&kr->tma_a, op->a, rank, ad, as, ab, swz, err, errlen);
+        if (!st) st = encode_map(&kr->tma_b, op->b, rank, bd, bs, bb, swz, err, errlen);
+        kr->grid[0] = (unsigned)col_tiles;
+        kr->grid[1] = (unsigned)row_tiles;
+        kr->grid[2] = (unsigned)(op->batch * k.split);
+    }
+    if (!st && k.split > 1) {
+        const size_t slice = (size_t)op->batch * op->rows * op->cols * 4;
+        const size_t tiles = (size_t)kr->grid[0] * kr->grid[1] * (size_t)op->batch;
+        st = ensure_ws(op, slice * k.split, tiles * 4, err, errlen);
+    }
+    if (st) {
+        delete kr;
+        return st;
+    }
+    // module: memory cache -> disk cache -> NVRTC
+    const std::string key = make_key(family, k, batched, op->out_f32);
+    auto it = ctx->modules.find(key);
+    double compile_ms = 0.0;
+    int hit = 1;
+    if (it == ctx->modules.end()) {
+        std::vector<char> cubin;
+        st = get_cubin(family, k, batched, op->out_f32, ctx->cache_dir, cubin, &compile_ms, &hit, err, errlen);
+        if (st) {
+            delete kr;
+            return st;
+        }
+        LoadedModule lm;
+        CUresult r = g_cu.ModuleLoadData(&lm.mod, cubin.data());
+        if (r == CUDA_SUCCESS) r = g_cu.ModuleGetFunction(&lm.fn, lm.mod, "opevo_gemm");
+        if (r != CUDA_SUCCESS) {
+            delete kr;
+            st = fail_cu(ctx, r, "load module", err, errlen);
+            return st == OPEVO_ERR_STICKY ? st : OPEVO_LAUNCH_ERROR;
+        }
+        it = ctx->modules.emplace(key, lm).first;
+    }
+    LoadedModule& lm = it->second;
+    if (lm.smem_set < (int)kr->smem) {
+        CUresult r = g_cu.FuncSetAttribute(lm.fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)kr->smem);
+        if (r != CUDA_SUCCESS) {
+            put_err(err, errlen, "set smem %zu: %s", kr->smem, cu_str(r));
+            delete kr;
+            return OPEVO_INVALID_CONFIG;
+        }
+        lm.smem_set = (int)kr->smem;
+    }
+    kr->fn = lm.fn;
+    if (info) {
+        info->compile_ms = compile_ms;
+        info->cache_hit = hit;
+        info->load_ms = now_ms() - t0 - compile_ms;
+        info->grid_ctas = (int32_t)(kr->grid[0] * kr->grid[1] * kr->grid[2]);
+        info->smem_bytes = (int32_t)kr->smem;
+    }
+    *out = kr;
+    return OPEVO_OK;
+}
+
+void opevo_kernel_release(opevo_kernel* k) { delete k; }
+
+int opevo_kernel_run(opevo_kernel* k, char* err, size_t errlen) {
+    if (!k) return OPEVO_ERR_ARG;
+    opevo_ctx* ctx = k->op->ctx;
+    g_cu.CtxSetCurrent(ctx->cu);
+    int st = launch_kernel(k, err, errlen);
+    if (st) return st;
+    return sync_checked(ctx, "kernel", err, errlen);
+}
+
+int opevo_kernel_check(opevo_kernel* k, double tol, double* rel_err, char* err, size_t errlen) {
+    if (!k) return OPEVO_ERR_ARG;
+    opevo_op* op = k->op;
+    opevo_ctx* ctx = op->ctx;
+    g_cu.CtxSetCurrent(ctx->cu);
+    // poison the output (0xFF.. = NaN) so a kernel that skips tiles fails
+    CU_TRY(ctx, g_cu.MemsetD8Async(op->c, 0xFF, op->c_bytes, ctx->stream), "poison C");
+    int st = launch_kernel(k, err, errlen);
+    if (st) return st;
+    st = sync_checked(ctx, "kernel", err, errlen);
+    if (st) return st;
+    CU_TRY(ctx, g_cu.MemsetD8Async(ctx->cmp_buf, 0, 16, ctx->stream), "zero compare");
+    uint64_t n = (uint64_t)op->batch * op->rows * op->cols;
+    int c_f32 = op->out_f32;
+    void* args[] = {&op->c, &op->ref, &n, &c_f32, &ctx->cmp_buf};
+    st = launch_simple(ctx, ctx->k_compare, grid_for(n), 256, args, err, errlen);
+    if (st) return st;
+    uint32_t res[4] = {0, 0, 0, 0};
+    CU_TRY(ctx, g_cu.StreamSynchronize(ctx->stream), "compare sync");
+    CU_TRY(ctx, g_cu.MemcpyDtoH(res, ctx->cmp_buf, 12), "compare readback");
+    float md, mr;
+    memcpy(&md, &res[0], 4);
+    memcpy(&mr, &res[1], 4);
+    double rel = res[2] ? INFINITY : (mr > 0 ? (double)md / (double)mr : (double)md);
+    if (rel_err) *rel_err = rel;
+    if (!(rel <= tol)) {
+        put_err(err, errlen, "output mismatch: rel err %.3g > tol %.3g (%u non-finite)", rel, tol, res[2]);
+        return OPEVO_VERIFY_FAILED;
+    }
+    return OPEVO_OK;
+}
+
+int opevo_kernel_time(opevo_kernel* k, int warmup, int reps, int flush_l2, double* ms_per_launch, char* err,
+                      size_t errlen) {
+    if (!k || reps < 1 || !ms_per_launch) return OPEVO_ERR_ARG;
+    opevo_ctx* ctx = k->op->ctx;
+    g_cu.CtxSetCurrent(ctx->cu);
+    for (int i = 0; i < warmup; ++i) {
+        int st = launch_kernel(k, err, errlen);
+        if (st) return st;
+    }
+    int st = sync_checked(ctx, "warmup", err, errlen);
+    if (st) return st;
+    CUevent e0, e1;
+    CU_TRY(ctx, g_cu.EventCreate(&e0, CU_EVENT_DEFAULT), "event");
+    CU_TRY(ctx, g_cu.EventCreate(&e1, CU_EVENT_DEFAULT), "event");
+    double total = 0.0;
+    if (!flush_l2) {
+        // back-to-back launches captured in one graph: no host launch gaps
+        CUgraph g = nullptr;
+        CUgraphExec ge = nullptr;
+        CU_TRY(ctx, g_cu.StreamBeginCapture(ctx->stream, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL), "capture");
+        for (int i = 0; i < reps && !st; ++i) st = launch_kernel(k, err, errlen);
+        CUresult r = g_cu.StreamEndCapture(ctx->stream, &g);
+        if (st || r != CUDA_SUCCESS) {
+            if (g) g_cu.GraphDestroy(g);
+            g_cu.EventDestroy(e0);
+            g_cu.EventDestroy(e1);
+            return st ? st : fail_cu(ctx, r, "end capture", err, errlen);
+        }
+        r = g_cu.GraphInstantiate(&ge, g, 0);
+        if (r == CUDA_SUCCESS) r = g_cu.GraphLaunch(ge, ctx->stream);   // graph warm-up
+        if (r == CUDA_SUCCESS) r = g_cu.EventRecord(e0, ctx->stream);
+        if (r == CUDA_SUCCESS) r = g_cu.GraphLaunch(ge, ctx->stream);
+        if (r == CUDA_SUCCESS) r = g_cu.EventRecord(e1, ctx->stream);
+        if (r == CUDA_SUCCESS) r = g_cu.EventSynchronize(e1);
+        float ms = 0.f;
+        if (r == CUDA_SUCCESS) r = g_cu.EventElapsedTime(&ms, e0, e1);
+        if (ge) g_cu.GraphExecDestroy(ge);
+        g_cu.GraphDestroy(g);
+        g_cu.EventDestroy(e0);
+        g_cu.EventDestroy(e1);
+        if (r != CUDA_SUCCESS) {
+            int s2 = fail_cu(ctx, r, "timed graph", err, errlen);
+            return s2 == OPEVO_ERR_STICKY ? s2 : OPEVO_LAUNCH_ERROR;
+        }
+        total = ms;
+    } else {
+        if (!ctx->flush_buf) {
+            ctx->flush_bytes = (size_t)256 << 20;   // 2x the 126 MB L2
+            CU_TRY(ctx, g_cu.MemAlloc(&ctx->flush_buf, ctx->flush_bytes), "alloc flush buffer");
+        }
+        uint64_t n16 = ctx->flush_bytes / 16;
+        for (int i = 0; i < reps; ++i) {
+            unsigned salt = (unsigned)i;
+            void* fa[] = {&ctx->flush_buf, &n16, &salt};
+            st = launch_simple(ctx, ctx->k_flush, (unsigned)ctx->sm_count * 4, 512, fa, err, errlen);
+            if (!st) st = g_cu.EventRecord(e0, ctx->stream) == CUDA_SUCCESS ? OPEVO_OK : OPEVO_ERR_CUDA;
+            if (!st) st = launch_kernel(k, err, errlen);
+            if (!st) st = g_cu.EventRecord(e1, ctx->stream) == CUDA_SUCCESS ? OPEVO_OK : OPEVO_ERR_CUDA;
+            if (!st) st = sync_checked(ctx, "timed launch", err, errlen);
+            float ms = 0.f;
+            if (!st) g_cu.EventElapsedTime(&ms, e0, e1);
+            if (st) break;
+            total += ms;
+        }
+        g_cu.EventDestroy(e0);
+        g_cu.EventDestroy(e1);
+        if (st) return st;
+    }
+    *ms_per_launch = total / reps;
+    return OPEVO_OK;
+}
+
+int opevo_trial(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nknobs, int warmup, int reps,
+                int flush_l2, double tol, opevo_trial_result* res, char* err, size_t errlen) {
+    if (!res) return OPEVO_ERR_ARG;
+    memset(res, 0, sizeof *res);
+    opevo_kernel* k = nullptr;
+    int st = opevo_kernel_get(ctx, op, knobs, nknobs, &k, res, err, errlen);
+    if (st) return st;
+    double rel = 0.0;
+    st = opevo_kernel_check(k, tol, &rel, err, errlen);
+    res->rel_err = rel;
+    if (!st) {
+        double ms = 0.0;
+        st = opevo_kernel_time(k, warmup, reps, flush_l2, &ms, err, errlen);
+        if (!st) {
+            res->ms = ms;
+            res->tflops = ms > 0 ? k->flops / (ms * 1e-3) / 1e12 : 0.0;
+        }
+    }
+    opevo_kernel_release(k);
+    return st;
+}
+
+void* opevo_host_alloc(size_t bytes) {
+    load_driver();
+    if (!g_cu.ok) return nullptr;
+    void* p = nullptr;
+    if (g_cu.MemAllocHost(&p, bytes) != CUDA_SUCCESS) return nullptr;
+    return p;
+}
+
+void opevo_host_free(void* p) {
+    if (p && g_cu.ok) g_cu.MemFreeHost(p);
+}
+
+}  // extern "C"

@@ -1,0 +1,179 @@
+"""The B200 trial evaluator behind the reference's objective contract.
+
+``make_gpu_objective(spec)`` returns ``(space, objective)`` exactly like the
+reference's ``make_objective`` (``pkg/src/topotune/benchmarks.py:294-302``),
+but the objective compiles, verifies and times a hand-written sm_100a kernel
+through ``libopevo.so`` and returns measured TFLOP/s.  ``GpuEvaluator`` also
+offers the batch interface the engine's ``run(..., evaluator=...)`` hook
+takes (the reference's ``evaluate_batch`` seam, ``engine.py:264-290``):
+kernels of a batch are NVRTC-compiled in parallel on host threads, then
+launched one after another on the device.
+
+Error semantics (reference ``engine.py:276-285``): an infeasible mapping, a
+compile or launch failure, or an output that differs from the reference
+scores 0; a missing device/driver/NVRTC raises ``FatalEvaluationError``; a
+sticky context fault raises :class:`WorkerFault` so a scheduler can replace
+the worker process.  There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass, field
+
+from . import capi
+from .engine import FatalEvaluationError
+from .mapping import FAMILY_CONV, config_to_knobs, gpu_operator_space
+from .operators import BatchMatMulSpec, Conv2dSpec, MatMulSpec, OperatorSpec
+from .spaces import SearchSpace
+
+BF16_TOL = 1e-2
+F32_TOL = 1e-4
+
+
+class WorkerFault(FatalEvaluationError):
+    """The CUDA context is poisoned; the worker process must be replaced."""
+
+
+@dataclass
+class EvalSettings:
+    warmup: int = 3
+    reps: int = 20
+    flush_l2: bool = False
+    seed: int = 1234
+    compile_threads: int = 0          # 0 -> min(8, cpu count)
+    cache_dir: str = capi.DEFAULT_CACHE
+    dtype: int = capi.BF16
+
+
+@dataclass
+class TrialInfo:
+    fitness: float
+    status: str
+    knobs: tuple | None = None
+    ms: float = 0.0
+    rel_err: float = 0.0
+    compile_ms: float = 0.0
+    cache_hit: int = 0
+    message: str = ""
+    extra: dict = field(default_factory=dict)
+
+    def as_extra(self, gpu: int) -> dict:
+        d = {"status": self.status, "device_ms": self.ms, "compile_ms": self.compile_ms,
+             "rel_err": self.rel_err, "gpu_id": gpu, "cache_hit": self.cache_hit}
+        if self.knobs is not None:
+            d["knobs"] = list(self.knobs)
+        if self.message:
+            d["message"] = self.message[:200]
+        return d
+
+
+def _op_args(spec: OperatorSpec) -> dict:
+    if isinstance(spec, MatMulSpec):
+        return {"kind": capi.MATMUL, "rows": spec.n, "cols": spec.m, "depth": spec.k}
+    if isinstance(spec, BatchMatMulSpec):
+        return {"kind": capi.BATCHMATMUL, "batch": spec.b, "rows": spec.n, "cols": spec.m,
+                "depth": spec.k}
+    if isinstance(spec, Conv2dSpec):
+        return {"kind": capi.CONV2D, "conv": [spec.batch, spec.in_channels, spec.in_height,
+                                              spec.in_width, spec.out_channels, spec.kernel_h,
+                                              spec.kernel_w, spec.stride, spec.padding]}
+    raise TypeError(f"unknown operator spec: {spec!r}")
+
+
+class GpuEvaluator:
+    """Objective + batch evaluator bound to one operator on one B200."""
+
+    def __init__(self, spec: OperatorSpec, space: SearchSpace | None = None, device: int = 0,
+                 settings: EvalSettings | None = None):
+        self.spec = spec
+        self.space = space if space is not None else gpu_operator_space(spec)
+        self.device_index = device
+        self.settings = settings or EvalSettings()
+        self.tol = F32_TOL if self.settings.dtype == capi.F32 else BF16_TOL
+        try:
+            self.dev = capi.Device(device, self.settings.cache_dir)
+            self.op = self.dev.prepare(dtype=self.settings.dtype, seed=self.settings.seed,
+                                       **_op_args(spec))
+        except (OSError, capi.OpevoError) as err:
+            raise FatalEvaluationError(f"B200 evaluator unavailable: {err}") from err
+        self.flops = float(spec.flops())
+        self.last_extras: list[dict] = []
+        self.history: list[TrialInfo] = []
+        nthreads = self.settings.compile_threads or min(8, os.cpu_count() or 1)
+        self._pool = ThreadPoolExecutor(max_workers=nthreads)
+
+    def close(self) -> None:
+        self._pool.shutdown(wait=False)
+        if getattr(self, "op", None) is not None:
+            self.op.close()
+            self.op = None
+        if getattr(self, "dev", None) is not None:
+            self.dev.close()
+            self.dev = None
+
+    # -- the reference objective contract -----------------------------------
+    def __call__(self, config: tuple) -> float:
+        return self.evaluate([config])[0]
+
+    # -- batch interface (engine.run evaluator hook) ----------------------------
+    def evaluate(self, configs: list[tuple]) -> list[float]:
+        infos = self.evaluate_infos(configs)
+        self.last_extras = [i.as_extra(self.device_index) for i in infos]
+        return [i.fitness for i in infos]
+
+    def precompile(self, mapped) -> None:
+        """NVRTC-compile the distinct kernels of a batch on the host pool."""
+        family_batched = {}
+        for m in mapped:
+            if m.valid:
+                family_batched[(m.family, m.batched, m.knobs.compile_key())] = m
+        out_f32 = self.settings.dtype == capi.F32
+
+        def build(m):
+            try:
+                capi.compile_kernel(m.family, m.knobs.as_tuple(), m.batched, out_f32,
+                                    self.settings.cache_dir)
+            except capi.OpevoError:
+                pass   # reported again (with status) by the trial itself
+
+        list(self._pool.map(build, family_batched.values()))
+
+    def evaluate_infos(self, configs: list[tuple]) -> list[TrialInfo]:
+        mapped = [config_to_knobs(self.spec, self.space, c) for c in configs]
+        self.precompile(mapped)
+        out = []
+        for m in mapped:
+            if not m.valid:
+                out.append(TrialInfo(0.0, "invalid_config", None, message=m.reason))
+                continue
+            out.append(self.run_knobs(m.knobs.as_tuple()))
+        self.history.extend(out)
+        return out
+
+    def run_knobs(self, knobs: tuple) -> TrialInfo:
+        s = self.settings
+        t = self.dev.trial(self.op, knobs, warmup=s.warmup, reps=s.reps, flush_l2=s.flush_l2,
+                           tol=self.tol)
+        if t.status == capi.ERR_STICKY:
+            raise WorkerFault(f"device {self.device_index}: {t.message}")
+        if t.status < 0:
+            raise FatalEvaluationError(f"device {self.device_index}: {t.message}")
+        if t.status != capi.OK:
+            return TrialInfo(0.0, capi.STATUS_NAMES.get(t.status, str(t.status)), knobs,
+                             rel_err=t.rel_err, compile_ms=t.compile_ms, cache_hit=t.cache_hit,
+                             message=t.message)
+        fit = self.flops / (t.ms * 1e-3) / 1e12 if t.ms > 0 else 0.0
+        if not math.isfinite(fit):
+            fit = 0.0
+        return TrialInfo(fit, "ok", knobs, ms=t.ms, rel_err=t.rel_err, compile_ms=t.compile_ms,
+                         cache_hit=t.cache_hit)
+
+
+def make_gpu_objective(spec: OperatorSpec, space: SearchSpace | None = None, device: int = 0,
+                       settings: EvalSettings | None = None):
+    """``(space, objective)`` with the objective measured on a B200 (TFLOP/s)."""
+    ev = GpuEvaluator(spec, space, device, settings)
+    return ev.space, ev

@@ -1,0 +1,204 @@
+"""OpEvo configuration -> sm_100a kernel knobs.
+
+The paper's MatMul space (reference ``benchmarks.py:113-146``)
+factors each output dimension into four levels -- blocks, virtual threads,
+threads per block, per-thread tile -- and K into (outer, shared, inner).  On
+Blackwell one thread issues each tensor-core MMA and the accumulator lives in
+TMEM, so the levels map as:
+
+=====================  ==============================================================
+configuration          B200 kernel knob
+=====================  ==============================================================
+``n[0]``, ``m[0]``     CTA grid; CTA tile ``BM = N / n[0]``, ``BN = M / m[0]``
+                       (UMMA shape: BM in {128, 256 = two M=128 atoms},
+                       BN multiple of 16 in [16, 256])
+``m[1]``               cluster level: CTAs of a cluster along the column-tile axis
+                       that share one TMA-multicast A tile,
+                       ``cluster = largest c in {4, 2, 1} dividing m[1] and m[0]``
+``n[1..3]``, ``m[2..3]`` the warp/thread split of the CTA tile: no tcgen05 counterpart
+                       (canonicalised away -- many configurations, one kernel)
+``k[0]``               split-K factor (CTAs along K, in-kernel deterministic reduce)
+``k[2]``               BK: K elements per TMA stage (16, 32 or a multiple of 64)
+``k[1]``               K blocks per CTA = K / (k[0] * k[2]) (derived)
+``stages`` (added)     TMA->MMA ring depth, clamped to what fits in 227 KB
+=====================  ==============================================================
+
+Conv2d (``conv2d_space``) is an implicit GEMM over NHWC:
+rows = output pixels, cols = Cout, K = (kh, kw, Cin).  ``co[0]`` -> BN =
+Cout / co[0]; ``ho[0]``, ``wo[0]`` -> the output tile TILE_H = Ho / ho[0],
+TILE_W = Wo / wo[0] (BM = 128 pixels = TILE_N x TILE_H x TILE_W); ``ci[0]`` ->
+BK = Cin / ci[0] channels per stage; ``kh[0] * kw[0]`` -> split-K over filter
+taps; ``unroll_step`` -> pipeline stages {0:2, 16:3, 64:4, 512:6, 1500:8};
+``unroll_explicit`` has no counterpart (the MMA issue loop is always
+unrolled).
+
+A configuration whose mapping is infeasible is *invalid* and scores 0, as an
+un-compilable TVM configuration does in the paper.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from .operators import (
+    BatchMatMulSpec,
+    Conv2dSpec,
+    MatMulSpec,
+    OperatorSpec,
+    batchmatmul_space,
+    conv2d_space,
+    matmul_space,
+)
+from .spaces import Discrete, SearchSpace
+
+SMEM_LIMIT = 232448          # 227 KB opt-in per CTA on B200
+SMEM_EXTRA = 1024 + 256      # alignment slack + barriers
+STAGE_VALUES = (2, 3, 4, 5, 6, 7, 8)
+UNROLL_TO_STAGES = {0: 2, 16: 3, 64: 4, 512: 6, 1500: 8}
+
+FAMILY_GEMM = 0
+FAMILY_CONV = 1
+
+
+@dataclass(frozen=True)
+class Knobs:
+    """Canonical kernel knobs (order = ``opevo_knob`` in include/opevo.h)."""
+
+    bm: int
+    bn: int
+    bk: int
+    stages: int
+    split: int = 1
+    cluster: int = 1
+    tile_h: int = 1
+    tile_w: int = 1
+
+    def as_tuple(self) -> tuple[int, ...]:
+        return (self.bm, self.bn, self.bk, self.stages, self.split, self.cluster,
+                self.tile_h, self.tile_w)
+
+    def compile_key(self) -> tuple[int, ...]:
+        """Fields that change the generated code (split-K is a launch arg)."""
+        return (self.bm, self.bn, self.bk, self.stages, self.cluster, self.tile_h, self.tile_w)
+
+    def smem_bytes(self) -> int:
+        return stage_bytes(self.bm, self.bn, self.bk) * self.stages + SMEM_EXTRA
+
+
+@dataclass(frozen=True)
+class Mapped:
+    """Result of mapping one configuration."""
+
+    knobs: Knobs | None
+    reason: str = ""
+    family: int = FAMILY_GEMM
+    batched: bool = False
+
+    @property
+    def valid(self) -> bool:
+        return self.knobs is not None
+
+
+def stage_bytes(bm: int, bn: int, bk: int) -> int:
+    return (bm + bn) * bk * 2
+
+
+def _bk_ok(bk: int) -> bool:
+    return bk in (16, 32) or (64 <= bk <= 256 and bk % 64 == 0)
+
+
+def _fit_stages(want: int, bm: int, bn: int, bk: int) -> int:
+    room = (SMEM_LIMIT - SMEM_EXTRA) // stage_bytes(bm, bn, bk)
+    return min(want, room)
+
+
+def _largest_pow2_divisor(*vals: int, cap: int = 4) -> int:
+    c = cap
+    while c > 1 and any(v % c for v in vals):
+        c //= 2
+    return c
+
+
+def gpu_operator_space(spec: OperatorSpec) -> SearchSpace:
+    """The reference space of ``spec`` plus the B200-only knob(s), declared in
+    the reference's JSON space format (so the reference engine can replay a
+    B200 trajectory)."""
+    if isinstance(spec, MatMulSpec):
+        base = matmul_space(spec)
+    elif isinstance(spec, BatchMatMulSpec):
+        base = batchmatmul_space(spec)
+    elif isinstance(spec, Conv2dSpec):
+        return conv2d_space(spec)
+    else:
+        raise TypeError(f"unknown operator spec: {spec!r}")
+    return SearchSpace(list(zip(base.names, base.spaces)) + [("stages", Discrete(STAGE_VALUES))])
+
+
+def _gemm_knobs(rows: int, cols: int, depth: int, vals: dict) -> tuple[Knobs | None, str]:
+    n, m, k = vals["n"], vals["m"], vals["k"]
+    bm, bn = rows // n[0], cols // m[0]
+    split, bk = k[0], k[2]
+    if bm not in (128, 256):
+        return None, f"BM={bm} is not a UMMA row tile (128 or 256)"
+    if bn % 16 or not 16 <= bn <= 256:
+        return None, f"BN={bn} is not a UMMA column tile (16..256, step 16)"
+    if (bm // 128 if bm == 256 else 1) * bn > 512:
+        return None, "accumulator exceeds TMEM"
+    if not _bk_ok(bk):
+        return None, f"BK={bk} is not a TMA/UMMA K stage (16, 32, 64k)"
+    stages = _fit_stages(int(vals.get("stages", 4)), bm, bn, bk)
+    if stages < 1:
+        return None, "one stage does not fit in shared memory"
+    cluster = _largest_pow2_divisor(m[1], m[0])
+    return Knobs(bm, bn, bk, stages, split, cluster), ""
+
+
+def _conv_knobs(spec: Conv2dSpec, vals: dict) -> tuple[Knobs | None, str]:
+    co, ho, wo, ci = vals["co"], vals["ho"], vals["wo"], vals["ci"]
+    kh, kw = vals["kh"], vals["kw"]
+    if spec.stride != 1:
+        return None, "strided convolution is not served by the TMA tiled implicit GEMM"
+    bn = spec.out_channels // co[0]
+    th, tw = spec.out_height // ho[0], spec.out_width // wo[0]
+    bk = spec.in_channels // ci[0]
+    bm = 128
+    if bn % 16 or not 16 <= bn <= 256:
+        return None, f"BN={bn} is not a UMMA column tile"
+    if th * tw > bm or bm % (th * tw):
+        return None, f"output tile {th}x{tw} does not divide 128 pixels"
+    tn = bm // (th * tw)
+    if spec.batch % tn or tn > 256 or th > 256 or tw > 256:
+        return None, f"image tile {tn} does not divide the batch {spec.batch}"
+    if not _bk_ok(bk):
+        return None, f"BK={bk} channels is not a TMA/UMMA K stage"
+    split = kh[0] * kw[0]
+    stages = _fit_stages(UNROLL_TO_STAGES[vals["unroll_step"]], bm, bn, bk)
+    if stages < 1:
+        return None, "one stage does not fit in shared memory"
+    return Knobs(bm, bn, bk, stages, split, 1, th, tw), ""
+
+
+def config_to_knobs(spec: OperatorSpec, space: SearchSpace, config: tuple) -> Mapped:
+    """Map one configuration of ``space`` to kernel knobs (or an invalid reason)."""
+    vals = dict(zip(space.names, config))
+    if isinstance(spec, MatMulSpec):
+        kn, why = _gemm_knobs(spec.n, spec.m, spec.k, vals)
+        return Mapped(kn, why, FAMILY_GEMM, False)
+    if isinstance(spec, BatchMatMulSpec):
+        kn, why = _gemm_knobs(spec.n, spec.m, spec.k, vals)
+        return Mapped(kn, why, FAMILY_GEMM, True)
+    if isinstance(spec, Conv2dSpec):
+        kn, why = _conv_knobs(spec, vals)
+        return Mapped(kn, why, FAMILY_CONV, False)
+    raise TypeError(f"unknown operator spec: {spec!r}")
+
+
+def valid_fraction(spec: OperatorSpec, space: SearchSpace, samples: int = 20000,
+                   seed: int = 0) -> float:
+    """Monte-Carlo fraction of uniformly drawn configurations that map."""
+    import numpy as np
+
+    rng = np.random.default_rng(seed)
+    ok = sum(config_to_knobs(spec, space, space.sample_uniform(rng)).valid
+             for _ in range(samples))
+    return ok / samples

@@ -1,0 +1,101 @@
+"""Ahead-of-time population of the cubin cache (host NVRTC pool, no GPU).
+
+Enumerates the distinct kernel instances that an operator's GPU search space
+can map to (``mapping.config_to_knobs``) and compiles each once into
+``kernel_cache/``.  A tuning run then pays only module loads; bench.py
+reports cache hits and the compile time a cold cache would have cost.
+"""
+
+from __future__ import annotations
+
+import itertools
+import os
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+from . import capi
+from .mapping import STAGE_VALUES, UNROLL_TO_STAGES, Knobs, _bk_ok, _fit_stages
+from .operators import BatchMatMulSpec, Conv2dSpec, MatMulSpec, parse_operator
+
+
+def _divisors(n: int) -> list[int]:
+    return [d for d in range(1, n + 1) if n % d == 0]
+
+
+def family_instances(spec) -> set[tuple[int, bool, tuple]]:
+    """All (family, batched, knobs) reachable from the operator's space."""
+    out = set()
+    if isinstance(spec, (MatMulSpec, BatchMatMulSpec)):
+        batched = isinstance(spec, BatchMatMulSpec)
+        for bm in (128, 256):
+            if spec.n % bm:
+                continue
+            for bn in range(16, 257, 16):
+                if spec.m % bn or (bm // 128 if bm == 256 else 1) * bn > 512:
+                    continue
+                grid_cols = spec.m // bn
+                clusters = {c for c in (1, 2, 4) if grid_cols % c == 0}
+                for bk in _divisors(spec.k):
+                    if not _bk_ok(bk):
+                        continue
+                    for st in STAGE_VALUES:
+                        s = _fit_stages(st, bm, bn, bk)
+                        if s < 1:
+                            continue
+                        for c in clusters:
+                            out.add((0, batched, Knobs(bm, bn, bk, s, 1, c).as_tuple()))
+    elif isinstance(spec, Conv2dSpec):
+        if spec.stride != 1:
+            return out
+        ths = [t for t in _divisors(spec.out_height) if 128 % t == 0]
+        tws = [t for t in _divisors(spec.out_width) if 128 % t == 0]
+        for th, tw in itertools.product(ths, tws):
+            if th * tw > 128 or spec.batch % (128 // (th * tw)):
+                continue
+            for bn in range(16, 257, 16):
+                if spec.out_channels % bn:
+                    continue
+                for bk in _divisors(spec.in_channels):
+                    if not _bk_ok(bk):
+                        continue
+                    for st in set(UNROLL_TO_STAGES.values()):
+                        s = _fit_stages(st, 128, bn, bk)
+                        if s >= 1:
+                            out.add((1, False, Knobs(128, bn, bk, s, 1, 1, th, tw).as_tuple()))
+    return out
+
+
+def prebuild_ops(ops, cache_dir: str = capi.DEFAULT_CACHE, threads: int | None = None,
+                 verbose: bool = True) -> dict:
+    todo = set()
+    for op in ops:
+        todo |= family_instances(parse_operator(op))
+    # dedupe by compile key (split is a launch argument)
+    keyed = {}
+    for fam, batched, kn in todo:
+        keyed[capi.kernel_key(fam, kn, batched, False)] = (fam, batched, kn)
+    os.makedirs(cache_dir, exist_ok=True)
+    have = set(os.listdir(cache_dir))
+    pending = [v for k, v in keyed.items() if k + ".cubin" not in have]
+    t0 = time.perf_counter()
+    failures = []
+
+    def one(item):
+        fam, batched, kn = item
+        try:
+            return capi.compile_kernel(fam, kn, batched, False, cache_dir)
+        except capi.OpevoError as err:
+            failures.append((item, str(err)[:200]))
+            return 0.0
+
+    nthreads = threads or min(16, os.cpu_count() or 1)
+    with ThreadPoolExecutor(nthreads) as pool:
+        ms = list(pool.map(one, pending))
+    stats = {"instances": len(keyed), "compiled": len(pending) - len(failures),
+             "failed": len(failures), "compile_s_total": sum(ms) / 1e3,
+             "wall_s": time.perf_counter() - t0}
+    if verbose:
+        print(f"[prebuild] {stats}")
+        for f in failures[:5]:
+            print("[prebuild] failure:", f)
+    return stats

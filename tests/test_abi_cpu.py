@@ -1,0 +1,81 @@
+"""CPU-side checks of the C-ABI library: it loads without a GPU, exports every
+symbol include/opevo.h declares, JIT-compiles kernel instances (NVRTC needs
+no device), rejects infeasible knobs, and fails loudly (no fallback) when
+asked for a device that is not there."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2006_05664_b200 import capi
+
+HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include",
+                      "opevo.h")
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(opevo_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(capi.library_path())
+    names = declared_functions()
+    assert len(names) >= 20
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(names) == set(capi.EXPORTS)
+
+
+def test_abi_version():
+    assert capi.load().opevo_abi_version() == capi.ABI_VERSION
+
+
+def test_nvrtc_compiles_instances_without_gpu(tmp_path):
+    cache = str(tmp_path)
+    ms = capi.compile_kernel(0, (128, 64, 64, 4, 1, 1), False, False, cache)
+    assert ms > 0
+    assert capi.compile_kernel(0, (128, 64, 64, 4, 1, 1), False, False, cache) == 0.0  # disk hit
+    capi.compile_kernel(0, (256, 128, 128, 2, 1, 2), False, False, cache)     # 2 atoms + multicast
+    capi.compile_kernel(0, (128, 48, 16, 8, 1, 1), True, False, cache)        # batched, SW32
+    capi.compile_kernel(1, (128, 64, 64, 4, 1, 1, 8, 8), False, False, cache)  # implicit-GEMM conv
+    files = os.listdir(cache)
+    assert len(files) == 4 and all(f.endswith(".cubin") for f in files)
+
+
+def test_split_is_not_part_of_the_compile_key():
+    k1 = capi.kernel_key(0, (128, 64, 64, 4, 1, 1), False, False)
+    k2 = capi.kernel_key(0, (128, 64, 64, 4, 8, 1), False, False)
+    k3 = capi.kernel_key(0, (128, 64, 64, 5, 1, 1), False, False)
+    assert k1 == k2 != k3
+
+
+@pytest.mark.parametrize("knobs", [(64, 64, 64, 4), (96, 64, 64, 4), (128, 8, 64, 4),
+                                   (128, 272, 64, 4), (128, 64, 48, 4), (128, 64, 64, 40),
+                                   (256, 256, 256, 2), (128, 64, 64, 4, 1, 3),
+                                   (256, 512, 64, 1)])
+def test_infeasible_knobs_rejected_before_compile(knobs, tmp_path):
+    with pytest.raises(capi.OpevoError) as err:
+        capi.compile_kernel(0, knobs, False, False, str(tmp_path))
+    assert err.value.status == capi.INVALID_CONFIG
+    assert os.listdir(tmp_path) == []
+
+
+def test_no_device_fails_loudly():
+    if os.path.exists("/dev/nvidia0"):
+        pytest.skip("a GPU is present")
+    with pytest.raises(capi.OpevoError) as err:
+        capi.Device(0)
+    assert err.value.status == capi.ERR_NO_DEVICE
+
+
+def test_gpu_evaluator_raises_fatal_without_device():
+    if os.path.exists("/dev/nvidia0"):
+        pytest.skip("a GPU is present")
+    from paper_2006_05664_b200 import FatalEvaluationError, MatMulSpec
+    from paper_2006_05664_b200.evaluator import GpuEvaluator
+
+    with pytest.raises(FatalEvaluationError):
+        GpuEvaluator(MatMulSpec(256, 256, 256))

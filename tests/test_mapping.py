@@ -1,0 +1,121 @@
+"""Configuration -> kernel-knob mapping (mapping.py) and the GPU spaces."""
+
+import numpy as np
+import pytest
+
+from paper_2006_05664_b200 import (
+    BatchMatMulSpec,
+    Conv2dSpec,
+    EngineConfig,
+    MatMulSpec,
+    SearchSpace,
+    matmul_space,
+    parse_operator,
+    run,
+)
+from paper_2006_05664_b200.mapping import (
+    SMEM_LIMIT,
+    Knobs,
+    config_to_knobs,
+    gpu_operator_space,
+    valid_fraction,
+)
+from paper_2006_05664_b200.prebuild import family_instances
+
+
+def test_gpu_space_extends_reference_space_in_json_format():
+    spec = MatMulSpec(1024, 1024, 1024)
+    sp = gpu_operator_space(spec)
+    assert sp.names == ("n", "m", "k", "stages")
+    assert sp.to_json()[:3] == matmul_space(spec).to_json()
+    assert SearchSpace.from_json(sp.to_json()).to_json() == sp.to_json()
+
+
+def test_matmul_mapping_levels():
+    spec = MatMulSpec(1024, 1024, 1024)
+    sp = gpu_operator_space(spec)
+    cfg = ((8, 2, 8, 8), (8, 4, 4, 8), (2, 8, 64), 4)
+    m = config_to_knobs(spec, sp, cfg)
+    assert m.valid
+    assert m.knobs == Knobs(bm=128, bn=128, bk=64, stages=4, split=2, cluster=4)
+    # sub-tile splits do not change the kernel
+    cfg2 = ((8, 128, 1, 1), (8, 1, 1, 128), (2, 8, 64), 4)
+    assert config_to_knobs(spec, sp, cfg2).knobs == Knobs(128, 128, 64, 4, 2, 1)
+
+
+@pytest.mark.parametrize("cfg,why", [
+    (((16, 4, 4, 4), (8, 2, 8, 8), (1, 16, 64), 4), "BM=64"),
+    (((8, 2, 8, 8), (2, 2, 16, 16), (1, 16, 64), 4), "BN=512"),
+    (((8, 2, 8, 8), (8, 2, 8, 8), (1, 128, 8), 4), "BK=8"),
+    (((8, 2, 8, 8), (8, 2, 8, 8), (2, 1, 512), 4), "BK=512"),
+])
+def test_infeasible_configs_are_invalid(cfg, why):
+    spec = MatMulSpec(1024, 1024, 1024)
+    m = config_to_knobs(spec, gpu_operator_space(spec), cfg)
+    assert not m.valid and why.split("=")[0] in m.reason
+
+
+def test_stages_clamped_to_shared_memory():
+    spec = MatMulSpec(1024, 1024, 1024)
+    sp = gpu_operator_space(spec)
+    m = config_to_knobs(spec, sp, ((4, 4, 8, 8), (4, 4, 8, 8), (1, 8, 128), 8))
+    assert m.valid and m.knobs.bm == 256 and m.knobs.bn == 256
+    assert m.knobs.smem_bytes() <= SMEM_LIMIT
+    assert m.knobs.stages < 8
+
+
+def test_conv_mapping():
+    spec = parse_operator("conv2d:32,64,56,56,64,3,3,1,1")
+    sp = gpu_operator_space(spec)
+    cfg = ((1, 2, 4, 8), (7, 1, 2, 4), (7, 2, 2, 2), (1, 64), (3, 1), (1, 3),
+           "explicit_unroll_on", 64)
+    m = config_to_knobs(spec, sp, cfg)
+    assert m.valid and m.family == 1
+    assert m.knobs == Knobs(128, 64, 64, 4, 3, 1, 8, 8)
+
+
+def test_bmm_mapping_is_batched():
+    spec = BatchMatMulSpec(960, 128, 64, 128)
+    sp = gpu_operator_space(spec)
+    m = config_to_knobs(spec, sp, ((960, 1), (1, 2, 8, 8), (1, 1, 8, 8), (1, 2, 64), 2))
+    assert m.valid and m.batched and m.knobs.bm == 128 and m.knobs.bn == 64
+
+
+def test_every_valid_mapping_is_prebuilt():
+    """Uniform samples that map must land in the enumerated (prebuilt) family."""
+    for op in ("matmul:1024,1024,1024", "batchmatmul:960,128,64,128",
+               "conv2d:32,64,56,56,64,3,3,1,1"):
+        spec = parse_operator(op)
+        sp = gpu_operator_space(spec)
+        fam = {(f, b, tuple(k[:4]) + tuple(k[5:])) for f, b, k in family_instances(spec)}
+        rng = np.random.default_rng(0)
+        hits = 0
+        for _ in range(4000):
+            m = config_to_knobs(spec, sp, sp.sample_uniform(rng))
+            if m.valid:
+                hits += 1
+                k = m.knobs.as_tuple()
+                assert (m.family, m.batched, tuple(k[:4]) + tuple(k[5:])) in fam, (op, k)
+        assert hits > 0
+
+
+def test_valid_fractions_recorded():
+    spec = MatMulSpec(1024, 1024, 1024)
+    f = valid_fraction(spec, gpu_operator_space(spec), samples=4000)
+    assert 0.02 < f < 0.2
+
+
+def test_opevo_runs_on_gpu_space_with_surrogate():
+    """The engine drives the extended space; a surrogate stands in for the GPU."""
+    spec = MatMulSpec(1024, 1024, 1024)
+    sp = gpu_operator_space(spec)
+
+    def surrogate(cfg):
+        m = config_to_knobs(spec, sp, cfg)
+        if not m.valid:
+            return 0.0
+        k = m.knobs
+        return 100.0 * k.bn * k.bm / (k.bn + k.bm) / (1 + abs(k.stages - 4)) / k.split ** 0.1
+
+    best, recs = run(sp, EngineConfig(seed=0, budget=200), surrogate)
+    assert best.fitness > 0 and len(recs) == 200
