@@ -63,7 +63,7 @@ GEMM_CASES = [
     (512, 1024, 1024, (128, 64, 16, 8, 1, 1)),
     (512, 1024, 1024, (128, 64, 32, 6, 1, 1)),
     (512, 1024, 1024, (128, 16, 64, 4, 1, 1)),
-    (512, 1024, 1024, (128, 128, 256, 2, 1, 1)),
+    (512, 1024, 1024, (128, 64, 256, 2, 1, 1)),
     (512, 1024, 1024, (128, 128, 64, 4, 2, 1)),
     (512, 1024, 1024, (128, 128, 64, 4, 4, 1)),
     (512, 1024, 1024, (128, 64, 64, 4, 1, 2)),
