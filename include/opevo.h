@@ -77,7 +77,8 @@ enum opevo_knob {
     OPEVO_KNOB_CLUSTER = 5,   /* CTAs per cluster sharing A (multicast)   */
     OPEVO_KNOB_TILE_H = 6,    /* conv: output rows per CTA tile           */
     OPEVO_KNOB_TILE_W = 7,    /* conv: output cols per CTA tile           */
-    OPEVO_NUM_KNOBS = 8
+    OPEVO_KNOB_ACC = 8,       /* K-interleaved TMEM accumulators (1,2,4)  */
+    OPEVO_NUM_KNOBS = 9
 };
 
 /* Result of one trial (opevo_trial). */
@@ -144,6 +145,10 @@ int opevo_kernel_time(opevo_kernel* k, int warmup, int reps, int flush_l2, doubl
 int opevo_trial(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nknobs, int warmup,
                 int reps, int flush_l2, double tol, opevo_trial_result* res, char* err,
                 size_t errlen);
+
+/* Debug: one launch of an instance compiled with OPEVO_EXTRA_FLAGS=-DOPEVO_TRACE=1;
+ * copies 16 uint64 per CTA (smid, %globaltimer phase stamps) to `host`. */
+int opevo_kernel_trace(opevo_kernel* k, uint64_t* host, size_t count, char* err, size_t errlen);
 
 /* Pinned host memory for honest end-to-end copies. */
 void* opevo_host_alloc(size_t bytes);

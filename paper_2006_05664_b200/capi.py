@@ -37,8 +37,8 @@ STATUS_NAMES = {OK: "ok", INVALID_CONFIG: "invalid_config", COMPILE_ERROR: "comp
 
 MATMUL, BATCHMATMUL, CONV2D = 0, 1, 2
 BF16, F32 = 0, 1
-NUM_KNOBS = 8
-KNOB_NAMES = ("bm", "bn", "bk", "stages", "split", "cluster", "tile_h", "tile_w")
+NUM_KNOBS = 9
+KNOB_NAMES = ("bm", "bn", "bk", "stages", "split", "cluster", "tile_h", "tile_w", "acc")
 
 EXPORTS = (
     "opevo_abi_version", "opevo_compile", "opevo_kernel_key", "opevo_ctx_create",
@@ -47,7 +47,7 @@ EXPORTS = (
     "opevo_op_reference",
     "opevo_op_refresh_reference", "opevo_kernel_get", "opevo_kernel_release",
     "opevo_kernel_run", "opevo_kernel_check", "opevo_kernel_time", "opevo_trial",
-    "opevo_host_alloc", "opevo_host_free",
+    "opevo_kernel_trace", "opevo_host_alloc", "opevo_host_free",
 )
 
 
@@ -113,6 +113,7 @@ def load() -> C.CDLL:
         "opevo_kernel_check": (I, [P, D, dp, cp, sz]),
         "opevo_kernel_time": (I, [P, I, I, I, dp, cp, sz]),
         "opevo_trial": (I, [P, P, i32p, I, I, I, I, D, C.POINTER(TrialResult), cp, sz]),
+        "opevo_kernel_trace": (I, [P, C.POINTER(C.c_uint64), sz, cp, sz]),
         "opevo_host_alloc": (P, [sz]),
         "opevo_host_free": (None, [P]),
     }
@@ -310,6 +311,16 @@ class Kernel:
         err = _errbuf()
         _check(self.dev.lib.opevo_kernel_check(self.handle, tol, C.byref(rel), err, len(err)), err)
         return rel.value
+
+    def trace(self, ctas: int):
+        """Phase stamps of one launch (instance built with -DOPEVO_TRACE=1)."""
+        import numpy as np
+
+        out = np.zeros(ctas * 16, dtype=np.uint64)
+        err = _errbuf()
+        _check(self.dev.lib.opevo_kernel_trace(
+            self.handle, out.ctypes.data_as(C.POINTER(C.c_uint64)), out.size, err, len(err)), err)
+        return out.reshape(ctas, 16)
 
     def time(self, warmup: int = 3, reps: int = 20, flush_l2: bool = False) -> float:
         ms = C.c_double()

@@ -15,6 +15,18 @@
 //                 tap; padding comes from TMA out-of-bounds zero fill.  B is
 //                 the O(HW)I weight matrix [Cout][Kh*Kw*Cin].
 //   OPEVO_TILE_H / OPEVO_TILE_W  conv output tile (BM = TILE_N*TILE_H*TILE_W)
+//   OPEVO_ACC     independent TMEM accumulators the K loop round-robins over
+//                 (summed in the epilogue).  Consecutive MMAs into one
+//                 accumulator form a dependent chain; for small N the chain
+//                 latency, not the tensor-pipe rate, bounds the mainloop, and
+//                 interleaving ACC chains hides it -- the tcgen05 analogue of
+//                 the paper's virtual threads.
+//
+// Programmatic dependent launch: every CTA signals launch_dependents on entry
+// and waits (griddepcontrol.wait) before its first global read/write, so a
+// following launch overlaps its prologue (barrier init, TMEM alloc,
+// descriptor prefetch) with this one's tail; the host sets the PDL launch
+// attribute.
 // Runtime: gridDim = (col tiles, row tiles, batch * split); split-K partials
 // are reduced in-kernel by the last-arriving CTA of each tile (deterministic
 // order z = 0..split-1).
@@ -61,6 +73,15 @@
 #ifndef OPEVO_TILE_W
 #define OPEVO_TILE_W 1
 #endif
+#ifndef OPEVO_ACC
+#define OPEVO_ACC 1        // K-interleaved TMEM accumulators (1, 2, 4)
+#endif
+#ifndef OPEVO_ABLATE
+#define OPEVO_ABLATE 0     // debug: 1 exit at entry, 2 no mainloop, 3 no TMA, 4 no MMA
+#endif
+#ifndef OPEVO_TRACE
+#define OPEVO_TRACE 0      // 1: per-CTA %globaltimer phase stamps into `ws` (debug)
+#endif
 
 #pragma nv_diag_suppress 177
 typedef unsigned int u32;
@@ -84,7 +105,8 @@ constexpr int A_TILE = BM * BK * 2;
 constexpr int B_TILE = BN * BK * 2;
 constexpr int STAGE_BYTES = A_TILE + B_TILE;
 constexpr int A_SLICE_ROWS = BM / CLUSTER;                // rows of A each cluster CTA fetches
-constexpr int TMEM_USED = MATOMS * BN;
+constexpr int ACC = OPEVO_ACC;
+constexpr int TMEM_USED = MATOMS * BN * ACC;
 constexpr int TMEM_COLS = TMEM_USED <= 32 ? 32 : TMEM_USED <= 64 ? 64 :
                           TMEM_USED <= 128 ? 128 : TMEM_USED <= 256 ? 256 : 512;
 constexpr u32 LAYOUT = SWZ == 128 ? 2u : SWZ == 64 ? 4u : 6u;
@@ -100,6 +122,8 @@ static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "BN must be a multiple of 1
 static_assert(BK % 16 == 0 && BK >= 16 && BK <= 256, "BK must be a multiple of 16 in [16, 256]");
 static_assert(BK % ATOM_K == 0, "BK must tile the swizzle atom");
 static_assert(TMEM_USED <= 512, "accumulator exceeds TMEM");
+static_assert(ACC == 1 || ACC == 2 || ACC == 4, "ACC must be 1, 2 or 4");
+static_assert((BK / 16) % ACC == 0, "each stage must feed every accumulator");
 static_assert(BM % (8 * CLUSTER) == 0, "multicast slice must be whole 8-row groups");
 static_assert(!OPEVO_CONV || (TILE_N * TILE_H * TILE_W == BM && CLUSTER == 1),
               "conv tile must cover BM pixels, no multicast");
@@ -132,7 +156,8 @@ __device__ __forceinline__ void mbar_init(u32 bar, u32 count) {
 }
 
 __device__ __forceinline__ void mbar_expect_tx(u32 bar, u32 bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+    asm volatile("{ .reg .pred e; elect.sync _|e, 0xffffffff; "
+                 "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1; }"
                  :: "r"(bar), "r"(bytes) : "memory");
 }
 
@@ -158,40 +183,60 @@ __device__ __forceinline__ void mbar_wait(u32 bar, u32 parity) {
     }
 }
 
+__device__ __forceinline__ void pdl_wait() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+__device__ __forceinline__ u32 sm_id() {
+    u32 r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
+
+#if OPEVO_TRACE
+#define TRACE(slot) do { trace[(slot)] = global_ns(); } while (0)
+#else
+#define TRACE(slot) do { } while (0)
+#endif
+
 __device__ __forceinline__ void tma_prefetch(const TmaDesc* d) {
     asm volatile("prefetch.tensormap [%0];" :: "l"(d) : "memory");
 }
 
 __device__ __forceinline__ void tma_load_2d(u32 dst, const TmaDesc* d, u32 bar, int c0, int c1) {
-    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
-                 "[%0], [%1, {%3, %4}], [%2];"
+    asm volatile("{ .reg .pred e; elect.sync _|e, 0xffffffff; @e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+                 "[%0], [%1, {%3, %4}], [%2]; }"
                  :: "r"(dst), "l"(d), "r"(bar), "r"(c0), "r"(c1) : "memory");
 }
 
 __device__ __forceinline__ void tma_load_3d(u32 dst, const TmaDesc* d, u32 bar, int c0, int c1, int c2) {
-    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
-                 "[%0], [%1, {%3, %4, %5}], [%2];"
+    asm volatile("{ .reg .pred e; elect.sync _|e, 0xffffffff; @e cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+                 "[%0], [%1, {%3, %4, %5}], [%2]; }"
                  :: "r"(dst), "l"(d), "r"(bar), "r"(c0), "r"(c1), "r"(c2) : "memory");
 }
 
 __device__ __forceinline__ void tma_load_4d(u32 dst, const TmaDesc* d, u32 bar, int c0, int c1, int c2,
                                             int c3) {
-    asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes "
-                 "[%0], [%1, {%3, %4, %5, %6}], [%2];"
+    asm volatile("{ .reg .pred e; elect.sync _|e, 0xffffffff; @e cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes "
+                 "[%0], [%1, {%3, %4, %5, %6}], [%2]; }"
                  :: "r"(dst), "l"(d), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3) : "memory");
 }
 
 __device__ __forceinline__ void tma_load_2d_mc(u32 dst, const TmaDesc* d, u32 bar, int c0, int c1,
                                                u16 mask) {
-    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-                 ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;"
+    asm volatile("{ .reg .pred e; elect.sync _|e, 0xffffffff; @e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                 ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5; }"
                  :: "r"(dst), "l"(d), "r"(bar), "r"(c0), "r"(c1), "h"(mask) : "memory");
 }
 
 __device__ __forceinline__ void tma_load_3d_mc(u32 dst, const TmaDesc* d, u32 bar, int c0, int c1,
                                                int c2, u16 mask) {
-    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-                 ".multicast::cluster [%0], [%1, {%3, %4, %5}], [%2], %6;"
+    asm volatile("{ .reg .pred e; elect.sync _|e, 0xffffffff; @e cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                 ".multicast::cluster [%0], [%1, {%3, %4, %5}], [%2], %6; }"
                  :: "r"(dst), "l"(d), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "h"(mask) : "memory");
 }
 
@@ -206,20 +251,24 @@ __device__ __forceinline__ void cluster_sync() {
                  ::: "memory");
 }
 
+// Issued by a converged warp: one elected lane executes the MMA, so every
+// operand stays in uniform registers (no per-MMA R2UR/ELECT loop).
 __device__ __forceinline__ void umma_bf16(u32 tmem_d, u64 adesc, u64 bdesc, u32 accumulate) {
-    asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0; "
-                 "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }"
+    asm volatile("{ .reg .pred e, p; elect.sync _|e, 0xffffffff; setp.ne.b32 p, %4, 0; "
+                 "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }"
                  :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
 }
 
 __device__ __forceinline__ void umma_commit(u32 bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+    asm volatile("{ .reg .pred e; elect.sync _|e, 0xffffffff; "
+                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0]; }"
                  :: "r"(bar) : "memory");
 }
 
 __device__ __forceinline__ void umma_commit_mc(u32 bar, u16 mask) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster"
-                 ".multicast::cluster.b64 [%0], %1;" :: "r"(bar), "h"(mask) : "memory");
+    asm volatile("{ .reg .pred e; elect.sync _|e, 0xffffffff; "
+                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster"
+                 ".multicast::cluster.b64 [%0], %1; }" :: "r"(bar), "h"(mask) : "memory");
 }
 
 __device__ __forceinline__ void tc_fence_after() {
@@ -281,6 +330,20 @@ __device__ __forceinline__ float4 ld_cg_f4(const float* p) {
     return r;
 }
 
+// Sum the ACC interleaved accumulators of one row segment (fixed order).
+__device__ __forceinline__ void gather_acc(u32 taddr, float (&out)[EPI_COLS]) {
+    u32 v[EPI_COLS];
+    tmem_load<EPI_COLS>(taddr, v);
+#pragma unroll
+    for (int j = 0; j < EPI_COLS; ++j) out[j] = __uint_as_float(v[j]);
+#pragma unroll
+    for (int a = 1; a < ACC; ++a) {
+        tmem_load<EPI_COLS>(taddr + a * MATOMS * BN, v);
+#pragma unroll
+        for (int j = 0; j < EPI_COLS; ++j) out[j] += __uint_as_float(v[j]);
+    }
+}
+
 // Write EPI_COLS fp32 accumulator values (one row segment) as the output type.
 __device__ __forceinline__ void store_row(void* c_out, u64 off, const float* acc) {
 #if OPEVO_OUT_F32
@@ -329,8 +392,15 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
     const int row0 = row_tile * BM;
     const int col0 = col_tile * BN;
     const int k0 = kz * k_per_split;
-    const int num_kb = k_per_split / BK;
+    const int num_kb = OPEVO_ABLATE == 2 ? 0 : k_per_split / BK;
     const u32 crank = (CLUSTER > 1) ? cluster_rank() : 0u;
+#if OPEVO_TRACE
+    u64* trace = reinterpret_cast<u64*>(ws) +
+                 16ull * ((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
+    if (threadIdx.x == 0) { trace[0] = sm_id(); TRACE(1); }
+#endif
+    if (threadIdx.x == 0) pdl_launch_dependents();
+    if (OPEVO_ABLATE == 1) return;
     (void)crank;
     (void)row0;
     (void)geom;
@@ -363,16 +433,26 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
     __syncthreads();
     if (CLUSTER > 1) cluster_sync();
     tc_fence_after();
-    const u32 tmem_base = *tmem_slot;
+    const u32 tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);   // warp-uniform
+    if (threadIdx.x == 0) TRACE(2);
 
     if (warp == 0) {
-        if (lane == 0) {
+        {
             // ------------------------------------------------ TMA producer
+            // (whole warp iterates; the tma_* / expect_tx helpers elect one lane)
             int s = 0;
             u32 ph = 0;
+            pdl_wait();                 // operands may be the previous launch's output
+            if (lane == 0) TRACE(9);
             for (int kb = 0; kb < num_kb; ++kb) {
                 mbar_wait(smem_u32(empty_bar + s), ph ^ 1);
                 const u32 fb = smem_u32(full_bar + s);
+                if (OPEVO_ABLATE == 3) {
+                    if (lane == 0)
+                        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(fb) : "memory");
+                    if (++s == STAGES) { s = 0; ph ^= 1; }
+                    continue;
+                }
                 mbar_expect_tx(fb, STAGE_BYTES);
                 const u32 a_dst = smem_u32(smem + s * STAGE_BYTES);
                 const u32 b_dst = a_dst + A_TILE;
@@ -417,17 +497,27 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
 #endif
                 }
 #endif
+                if (kb == 0 && lane == 0) TRACE(3);
                 if (++s == STAGES) { s = 0; ph ^= 1; }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        {
             // ------------------------------------------------ MMA issuer
+            // (whole warp iterates; umma_* elect one lane to issue)
             int s = 0;
             u32 ph = 0;
             for (int kb = 0; kb < num_kb; ++kb) {
                 mbar_wait(smem_u32(full_bar + s), ph);
                 tc_fence_after();
+                if (kb == 0 && lane == 0) TRACE(4);
+                if (OPEVO_ABLATE == 4) {
+                    if (lane == 0)
+                        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];"
+                                     :: "r"(smem_u32(empty_bar + s)) : "memory");
+                    if (++s == STAGES) { s = 0; ph ^= 1; }
+                    continue;
+                }
                 const u32 a_base = smem_u32(smem + s * STAGE_BYTES);
                 const u32 b_base = a_base + A_TILE;
 #pragma unroll
@@ -440,8 +530,10 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                         for (int ma = 0; ma < MATOMS; ++ma) {
                             const u32 a_addr = a_base + ka * (BM * SWZ) + ma * (128 * SWZ) + koff;
                             const u64 adesc = DESC_HI | (u64)((a_addr >> 4) & 0x3FFF);
-                            umma_bf16(tmem_base + ma * BN, adesc, bdesc,
-                                      (kb | ka | k16) != 0 ? 1u : 0u);
+                            const int step = ka * (ATOM_K / 16) + k16;     // k16 step in stage
+                            const int acc = step % ACC;                    // compile-time
+                            umma_bf16(tmem_base + (acc * MATOMS + ma) * BN, adesc, bdesc,
+                                      (kb != 0 || step >= ACC) ? 1u : 0u);
                         }
                     }
                 }
@@ -455,6 +547,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                 if (++s == STAGES) { s = 0; ph ^= 1; }
             }
             umma_commit(smem_u32(accum_bar));
+            if (lane == 0) TRACE(5);
         }
     } else {
         // ---------------------------------------------------- epilogue
@@ -462,6 +555,8 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
         const int epi_tid = threadIdx.x - 64;
         mbar_wait(smem_u32(accum_bar), 0);
         tc_fence_after();
+        pdl_wait();                     // C may still be written by the previous launch
+        if (epi_tid == 0) TRACE(6);
         const u32 lane_addr = tmem_base + ((u32)(quarter * 32) << 16);
         const u64 plane = (u64)rows * (u64)cols;   // one batch (or one split slice)
 #if OPEVO_CONV
@@ -483,13 +578,12 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                 const int r = out_row(ma * 128 + quarter * 32 + lane);
 #pragma unroll 1
                 for (int c = 0; c < BN; c += EPI_COLS) {
-                    u32 v[EPI_COLS];
-                    tmem_load<EPI_COLS>(lane_addr + ma * BN + c, v);
-                    if (BM == 64 && quarter >= 2) continue;
-                    store_row(c_out, c_batch + (u64)r * cols + col0 + c,
-                              reinterpret_cast<const float*>(v));
+                    float acc[EPI_COLS];
+                    gather_acc(lane_addr + ma * BN + c, acc);
+                    store_row(c_out, c_batch + (u64)r * cols + col0 + c, acc);
                 }
             }
+            if (epi_tid == 0) TRACE(7);
         } else {
             const u64 nbat = (u64)gridDim.z / (u64)split;
             const u64 slice = nbat * plane;
@@ -498,13 +592,13 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                 const int r = out_row(ma * 128 + quarter * 32 + lane);
 #pragma unroll 1
                 for (int c = 0; c < BN; c += EPI_COLS) {
-                    u32 v[EPI_COLS];
-                    tmem_load<EPI_COLS>(lane_addr + ma * BN + c, v);
-                    if (BM == 64 && quarter >= 2) continue;
+                    float acc[EPI_COLS];
+                    gather_acc(lane_addr + ma * BN + c, acc);
                     float* dst = ws + (u64)kz * slice + c_batch + (u64)r * cols + col0 + c;
 #pragma unroll
                     for (int j = 0; j < EPI_COLS; j += 4)
-                        st_v4(dst + j, v[j], v[j + 1], v[j + 2], v[j + 3]);
+                        st_v4(dst + j, __float_as_uint(acc[j]), __float_as_uint(acc[j + 1]),
+                              __float_as_uint(acc[j + 2]), __float_as_uint(acc[j + 3]));
                 }
             }
             __threadfence();
@@ -522,7 +616,6 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
 #pragma unroll 1
                 for (int ma = 0; ma < MATOMS; ++ma) {
                     const int r = out_row(ma * 128 + quarter * 32 + lane);
-                    if (BM == 64 && quarter >= 2) continue;
 #pragma unroll 1
                     for (int c = 0; c < BN; c += EPI_COLS) {
                         float acc[EPI_COLS];
@@ -546,6 +639,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
 
     tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) TRACE(8);
     if (CLUSTER > 1) cluster_sync();
     if (warp == 1) {
         __syncwarp();

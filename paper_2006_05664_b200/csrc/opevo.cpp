@@ -179,13 +179,13 @@ void load_nvrtc() {
 
 // ------------------------------------------------------------- knobs
 struct Knobs {
-    int bm, bn, bk, stages, split, cluster, tile_h, tile_w;
+    int bm, bn, bk, stages, split, cluster, tile_h, tile_w, acc;
 };
 
 Knobs read_knobs(const int32_t* k, int n) {
-    int32_t v[OPEVO_NUM_KNOBS] = {128, 128, 64, 4, 1, 1, 1, 1};
+    int32_t v[OPEVO_NUM_KNOBS] = {128, 128, 64, 4, 1, 1, 1, 1, 1};
     for (int i = 0; i < n && i < OPEVO_NUM_KNOBS; ++i) v[i] = k[i];
-    return Knobs{v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7]};
+    return Knobs{v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8]};
 }
 
 int swizzle_bytes(int bk) { return bk * 2 >= 128 ? 128 : bk * 2; }
@@ -208,13 +208,26 @@ bool want_lineinfo() {
     return v && v[0] == '1';
 }
 
+// Extra -D flags for debug instances (e.g. "-DOPEVO_TRACE=1"); part of the key.
+std::string extra_flags() {
+    const char* v = getenv("OPEVO_EXTRA_FLAGS");
+    return v ? v : "";
+}
+
+bool want_pdl() {
+    const char* v = getenv("OPEVO_NO_PDL");
+    return !(v && v[0] == '1');
+}
+
 std::string make_key(int family, const Knobs& k, int batched, int out_f32) {
     static const uint64_t src_hash = fnv1a(opevo_gemm_source, strlen(opevo_gemm_source));
+    const std::string extra = extra_flags();
+    const uint64_t h = fnv1a(extra.data(), extra.size(), src_hash);
     char buf[256];
-    snprintf(buf, sizeof buf, "f%d_m%d_n%d_k%d_s%d_b%d_o%d_c%d_h%d_w%d_%s%012llx", family, k.bm, k.bn,
-             k.bk, k.stages, batched, out_f32, k.cluster, family == 1 ? k.tile_h : 1,
-             family == 1 ? k.tile_w : 1, want_lineinfo() ? "L" : "",
-             (unsigned long long)(src_hash & 0xffffffffffffull));
+    snprintf(buf, sizeof buf, "f%d_m%d_n%d_k%d_s%d_b%d_o%d_c%d_h%d_w%d_a%d_%s%012llx", family, k.bm,
+             k.bn, k.bk, k.stages, batched, out_f32, k.cluster, family == 1 ? k.tile_h : 1,
+             family == 1 ? k.tile_w : 1, k.acc, want_lineinfo() ? "L" : "",
+             (unsigned long long)(h & 0xffffffffffffull));
     return buf;
 }
 
@@ -237,8 +250,12 @@ bool knobs_compilable(int family, const Knobs& k, char* err, size_t len) {
         put_err(err, len, "stages=%d out of range", k.stages);
         return false;
     }
-    if ((k.bm == 256 ? 2 : 1) * k.bn > 512) {
-        put_err(err, len, "accumulator %dx%d exceeds 512 TMEM columns", k.bm, k.bn);
+    if (!(k.acc == 1 || k.acc == 2 || k.acc == 4) || (k.bk / 16) % k.acc) {
+        put_err(err, len, "acc=%d unsupported for BK=%d (1, 2 or 4 dividing BK/16)", k.acc, k.bk);
+        return false;
+    }
+    if ((k.bm == 256 ? 2 : 1) * k.bn * k.acc > 512) {
+        put_err(err, len, "accumulators %dx%d x%d exceed 512 TMEM columns", k.bm, k.bn, k.acc);
         return false;
     }
     if (!(k.cluster == 1 || k.cluster == 2 || k.cluster == 4 || k.cluster == 8) ||
@@ -318,8 +335,14 @@ int nvrtc_build(int family, const Knobs& k, int batched, int out_f32, std::vecto
         "-DOPEVO_BATCHED=" + std::to_string(batched), "-DOPEVO_OUT_F32=" + std::to_string(out_f32),
         "-DOPEVO_CLUSTER=" + std::to_string(k.cluster), "-DOPEVO_CONV=" + std::to_string(family == 1),
         "-DOPEVO_TILE_H=" + std::to_string(family == 1 ? k.tile_h : 1),
-        "-DOPEVO_TILE_W=" + std::to_string(family == 1 ? k.tile_w : 1)};
+        "-DOPEVO_TILE_W=" + std::to_string(family == 1 ? k.tile_w : 1),
+        "-DOPEVO_ACC=" + std::to_string(k.acc)};
     if (want_lineinfo()) opts.push_back("-lineinfo");
+    {
+        std::istringstream extra(extra_flags());
+        std::string tok;
+        while (extra >> tok) opts.push_back(tok);
+    }
     std::vector<const char*> argv;
     for (auto& o : opts) argv.push_back(o.c_str());
     nvrtcResult r = g_rtc.Compile(prog, (int)argv.size(), argv.data());
@@ -534,15 +557,25 @@ int launch_kernel(opevo_kernel* kr, char* err, size_t errlen) {
     cfg.blockDimZ = 1;
     cfg.sharedMemBytes = (unsigned)kr->smem;
     cfg.hStream = ctx->stream;
-    CUlaunchAttribute attr[1];
+    CUlaunchAttribute attr[2];
+    unsigned na = 0;
     if (kr->k.cluster > 1) {
-        attr[0].id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
-        attr[0].value.clusterDim.x = (unsigned)kr->k.cluster;
-        attr[0].value.clusterDim.y = 1;
-        attr[0].value.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
+        attr[na].id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
+        attr[na].value.clusterDim.x = (unsigned)kr->k.cluster;
+        attr[na].value.clusterDim.y = 1;
+        attr[na].value.clusterDim.z = 1;
+        ++na;
     }
+    if (want_pdl()) {
+        // programmatic dependent launch: the kernel calls griddepcontrol.wait
+        // before touching global memory, so its prologue may overlap the
+        // previous kernel in the stream
+        attr[na].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+        attr[na].value.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = na ? attr : nullptr;
+    cfg.numAttrs = na;
     CUresult r = g_cu.LaunchKernelEx(&cfg, kr->fn, args, nullptr);
     if (r != CUDA_SUCCESS) {
         int st = fail_cu(ctx, r, "kernel launch", err, errlen);
@@ -1094,6 +1127,29 @@ int opevo_trial(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nknobs, 
         }
     }
     opevo_kernel_release(k);
+    return st;
+}
+
+int opevo_kernel_trace(opevo_kernel* k, uint64_t* host, size_t count, char* err, size_t errlen) {
+    if (!k || !host) return OPEVO_ERR_ARG;
+    opevo_op* op = k->op;
+    opevo_ctx* ctx = op->ctx;
+    g_cu.CtxSetCurrent(ctx->cu);
+    const size_t ctas = (size_t)k->grid[0] * k->grid[1] * k->grid[2];
+    const size_t bytes = ctas * 16 * sizeof(uint64_t);
+    CUdeviceptr buf = 0;
+    CU_TRY(ctx, g_cu.MemAlloc(&buf, bytes), "alloc trace");
+    CU_TRY(ctx, g_cu.MemsetD8(buf, 0, bytes), "zero trace");
+    CUdeviceptr saved = op->ws;
+    op->ws = buf;                       // trace instances write stamps through `ws`
+    int st = launch_kernel(k, err, errlen);
+    if (!st) st = sync_checked(ctx, "traced kernel", err, errlen);
+    op->ws = saved;
+    if (!st) {
+        CUresult r = g_cu.MemcpyDtoH(host, buf, std::min(bytes, count * sizeof(uint64_t)));
+        if (r != CUDA_SUCCESS) st = fail_cu(ctx, r, "read trace", err, errlen);
+    }
+    g_cu.MemFree(buf);
     return st;
 }
 
