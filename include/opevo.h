@@ -78,7 +78,12 @@ enum opevo_knob {
     OPEVO_KNOB_TILE_H = 6,    /* conv: output rows per CTA tile           */
     OPEVO_KNOB_TILE_W = 7,    /* conv: output cols per CTA tile           */
     OPEVO_KNOB_ACC = 8,       /* K-interleaved TMEM accumulators (1,2,4)  */
-    OPEVO_NUM_KNOBS = 9
+    OPEVO_KNOB_CTA_GROUP = 9, /* 2: CTA-pair MMA (cta_group::2), BM=256   */
+    OPEVO_KNOB_GRID = 10,     /* 0: persistent when work > residency
+                                 1: one CTA (cluster) per tile
+                                 2: persistent, partial last wave split
+                                    along K (stream-K style tail)         */
+    OPEVO_NUM_KNOBS = 11
 };
 
 /* Result of one trial (opevo_trial). */

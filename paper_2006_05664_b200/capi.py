@@ -37,8 +37,9 @@ STATUS_NAMES = {OK: "ok", INVALID_CONFIG: "invalid_config", COMPILE_ERROR: "comp
 
 MATMUL, BATCHMATMUL, CONV2D = 0, 1, 2
 BF16, F32 = 0, 1
-NUM_KNOBS = 9
-KNOB_NAMES = ("bm", "bn", "bk", "stages", "split", "cluster", "tile_h", "tile_w", "acc")
+NUM_KNOBS = 11
+KNOB_NAMES = ("bm", "bn", "bk", "stages", "split", "cluster", "tile_h", "tile_w", "acc",
+              "cta_group", "grid")
 
 EXPORTS = (
     "opevo_abi_version", "opevo_compile", "opevo_kernel_key", "opevo_ctx_create",
@@ -127,8 +128,11 @@ def load() -> C.CDLL:
     return lib
 
 
+_KNOB_DEFAULTS = (128, 128, 64, 4, 1, 1, 1, 1, 1, 1, 0)
+
+
 def _knob_array(knobs) -> "C.Array":
-    vals = list(knobs) + [1] * (NUM_KNOBS - len(knobs))
+    vals = list(knobs) + list(_KNOB_DEFAULTS[len(knobs):])
     return (C.c_int32 * NUM_KNOBS)(*vals[:NUM_KNOBS])
 
 

@@ -15,6 +15,11 @@
 //                 tap; padding comes from TMA out-of-bounds zero fill.  B is
 //                 the O(HW)I weight matrix [Cout][Kh*Kw*Cin].
 //   OPEVO_TILE_H / OPEVO_TILE_W  conv output tile (BM = TILE_N*TILE_H*TILE_W)
+//   OPEVO_CTA_GROUP 2: a cluster of two CTAs on neighbouring SMs computes a
+//                 256 x BN tile with tcgen05.mma.cta_group::2 (M=256); each
+//                 CTA stages 128 rows of A and BN/2 rows of B, so per-SM
+//                 operand traffic (TMA ingress and smem reads) drops versus a
+//                 single-CTA 256-row tile.  Only the leader CTA issues MMAs.
 //   OPEVO_ACC     independent TMEM accumulators the K loop round-robins over
 //                 (summed in the epilogue).  Consecutive MMAs into one
 //                 accumulator form a dependent chain; for small N the chain
@@ -73,6 +78,9 @@
 #ifndef OPEVO_TILE_W
 #define OPEVO_TILE_W 1
 #endif
+#ifndef OPEVO_CTA_GROUP
+#define OPEVO_CTA_GROUP 1  // 2: CTA-pair MMA (cta_group::2, M=256 across two SMs)
+#endif
 #ifndef OPEVO_ACC
 #define OPEVO_ACC 1        // K-interleaved TMEM accumulators (1, 2, 4)
 #endif
@@ -95,16 +103,20 @@ constexpr int BN = OPEVO_BN;
 constexpr int BK = OPEVO_BK;
 constexpr int STAGES = OPEVO_STAGES;
 constexpr int CLUSTER = OPEVO_CLUSTER;
+constexpr int CG = OPEVO_CTA_GROUP;
 
 constexpr int SWZ = (BK * 2 >= 128) ? 128 : BK * 2;     // swizzle span in bytes
 constexpr int ATOM_K = SWZ / 2;                          // K elements per swizzle row
 constexpr int KATOMS = BK / ATOM_K;                      // swizzle atoms along K
-constexpr int MATOMS = (BM == 256) ? 2 : 1;              // M=128 MMAs per k-step
-constexpr int UMMA_M = (BM == 256) ? 128 : BM;
-constexpr int A_TILE = BM * BK * 2;
-constexpr int B_TILE = BN * BK * 2;
+constexpr int BM_CTA = (CG == 2) ? 128 : BM;             // A rows resident in this CTA
+constexpr int BN_LOAD = BN / CG;                          // B rows this CTA stages
+constexpr int MATOMS = (CG == 1 && BM == 256) ? 2 : 1;    // M=128 MMAs per k-step
+constexpr int UMMA_M = (CG == 2) ? 256 : ((BM == 256) ? 128 : BM);
+constexpr int A_TILE = BM_CTA * BK * 2;
+constexpr int B_TILE = BN_LOAD * BK * 2;
 constexpr int STAGE_BYTES = A_TILE + B_TILE;
-constexpr int A_SLICE_ROWS = BM / CLUSTER;                // rows of A each cluster CTA fetches
+constexpr int TX_BYTES = STAGE_BYTES * CG;                // bytes landing per stage (pair)
+constexpr int A_SLICE_ROWS = BM_CTA / CLUSTER;            // rows of A each cluster CTA fetches
 constexpr int ACC = OPEVO_ACC;
 constexpr int TMEM_USED = MATOMS * BN * ACC;
 constexpr int TMEM_COLS = TMEM_USED <= 32 ? 32 : TMEM_USED <= 64 ? 64 :
@@ -125,6 +137,8 @@ static_assert(TMEM_USED <= 512, "accumulator exceeds TMEM");
 static_assert(ACC == 1 || ACC == 2 || ACC == 4, "ACC must be 1, 2 or 4");
 static_assert((BK / 16) % ACC == 0, "each stage must feed every accumulator");
 static_assert(BM % (8 * CLUSTER) == 0, "multicast slice must be whole 8-row groups");
+static_assert(CG == 1 || (CG == 2 && BM == 256 && CLUSTER == 1 && !OPEVO_CONV && BN % 16 == 0),
+              "CTA pairs: 256-row tiles, no extra multicast, GEMM only");
 static_assert(!OPEVO_CONV || (TILE_N * TILE_H * TILE_W == BM && CLUSTER == 1),
               "conv tile must cover BM pixels, no multicast");
 
@@ -138,7 +152,28 @@ constexpr u64 DESC_HI = ((u64)1 << 16)                          // LBO (unused f
                       | ((u64)1 << 46)                           // descriptor version (sm_100)
                       | ((u64)LAYOUT << 61);
 
+// TMEM accumulator buffers: two when they fit, so the epilogue of one tile
+// overlaps the mainloop of the next (persistent schedule).
+constexpr int NBUF = (2 * TMEM_USED <= 512) ? 2 : 1;
+constexpr int TMEM_ALLOC = (NBUF * TMEM_USED <= 32) ? 32 : (NBUF * TMEM_USED <= 64) ? 64 :
+                           (NBUF * TMEM_USED <= 128) ? 128 : (NBUF * TMEM_USED <= 256) ? 256 : 512;
+constexpr int CLSZ = CLUSTER * CG;     // CTAs per cluster (launch cluster dim x)
+
 struct __align__(64) TmaDesc { u64 raw[16]; };
+
+// Work decomposition.  A *unit* is what one cluster computes at a time: one
+// output tile (CLSZ == 1), CLUSTER column tiles sharing the multicast A tile,
+// or one 256-row pair tile (CG == 2); for split-K, one K slice of it.  CTAs
+// loop over units (persistent when gridDim < units).
+struct Sched {
+    int row_tiles;     // tiles along rows (pair tiles for CG == 2)
+    int col_groups;    // column tiles / CLUSTER
+    int batches;
+    int split;         // K slices of every tile (split-K knob)
+    int head_tiles;    // tiles computed with `split` slices ...
+    int tail_split;    // ... the rest (the last partial wave) with split*tail_split
+    int units;         // head_tiles*split + (tiles-head_tiles)*split*tail_split
+};
 
 // Conv geometry (unused by the GEMM instances).
 struct ConvGeom {
@@ -165,6 +200,15 @@ __device__ __forceinline__ u64 global_ns() {
     u64 t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
+}
+
+__device__ __forceinline__ void mbar_arrive(u32 bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(u32 cluster_bar) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];"
+                 :: "r"(cluster_bar) : "memory");
 }
 
 // Parity wait with a watchdog: a configuration that deadlocks traps after
@@ -263,6 +307,39 @@ __device__ __forceinline__ void umma_commit(u32 bar) {
     asm volatile("{ .reg .pred e; elect.sync _|e, 0xffffffff; "
                  "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0]; }"
                  :: "r"(bar) : "memory");
+}
+
+// CTA-pair variants (cta_group::2)
+__device__ __forceinline__ void umma2_bf16(u32 tmem_d, u64 adesc, u64 bdesc, u32 accumulate) {
+    asm volatile("{ .reg .pred e, p; elect.sync _|e, 0xffffffff; setp.ne.b32 p, %4, 0; "
+                 "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p; }"
+                 :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma2_commit_mc(u32 bar, u16 mask) {
+    asm volatile("{ .reg .pred e; elect.sync _|e, 0xffffffff; "
+                 "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster"
+                 ".multicast::cluster.b64 [%0], %1; }" :: "r"(bar), "h"(mask) : "memory");
+}
+
+// TMA load whose completion is credited to the pair leader's mbarrier
+// (`bar` is a shared::cluster address from mapa).
+__device__ __forceinline__ void tma2_load_2d(u32 dst, const TmaDesc* d, u32 bar, int c0, int c1) {
+    asm volatile("{ .reg .pred e; elect.sync _|e, 0xffffffff; @e cp.async.bulk.tensor.2d.cta_group::2"
+                 ".shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2]; }"
+                 :: "r"(dst), "l"(d), "r"(bar), "r"(c0), "r"(c1) : "memory");
+}
+
+__device__ __forceinline__ void tma2_load_3d(u32 dst, const TmaDesc* d, u32 bar, int c0, int c1, int c2) {
+    asm volatile("{ .reg .pred e; elect.sync _|e, 0xffffffff; @e cp.async.bulk.tensor.3d.cta_group::2"
+                 ".shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2]; }"
+                 :: "r"(dst), "l"(d), "r"(bar), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
+
+__device__ __forceinline__ u32 mapa_cta(u32 addr, u32 rank) {
+    u32 r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
 }
 
 __device__ __forceinline__ void umma_commit_mc(u32 bar, u16 mask) {
@@ -371,7 +448,8 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
            void* __restrict__ c_out,
            float* __restrict__ ws,            // split-K partials [split][batch*rows][cols]
            u32* __restrict__ counters,        // per-tile arrival counters (self-resetting)
-           int rows, int cols, int k_per_split, int split,
+           int rows, int cols, int depth,      // depth = K (per batch)
+           const Sched sched,
            const ConvGeom geom)
 {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -379,38 +457,55 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
         (reinterpret_cast<u64>(smem_raw) + SMEM_ALIGN - 1) & ~(u64)(SMEM_ALIGN - 1));
     u64* full_bar = reinterpret_cast<u64*>(smem + STAGES * STAGE_BYTES);
     u64* empty_bar = full_bar + STAGES;
-    u64* accum_bar = empty_bar + STAGES;
-    u32* tmem_slot = reinterpret_cast<u32*>(accum_bar + 1);
+    u64* tfull_bar = empty_bar + STAGES;      // MMA -> epilogue, per TMEM buffer
+    u64* tempty_bar = tfull_bar + NBUF;       // epilogue -> MMA, per TMEM buffer
+    u32* tmem_slot = reinterpret_cast<u32*>(tempty_bar + NBUF);
     u32* last_flag = tmem_slot + 1;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int col_tile = blockIdx.x;
-    const int row_tile = blockIdx.y;
-    const int batch = blockIdx.z / split;
-    const int kz = blockIdx.z - batch * split;
-    const int row0 = row_tile * BM;
-    const int col0 = col_tile * BN;
-    const int k0 = kz * k_per_split;
-    const int num_kb = OPEVO_ABLATE == 2 ? 0 : k_per_split / BK;
-    const u32 crank = (CLUSTER > 1) ? cluster_rank() : 0u;
+    const u32 crank = (CLSZ > 1) ? cluster_rank() : 0u;
+    const u32 prank = (CG == 2) ? crank : 0u;                 // rank in the CTA pair
+    const u32 mrank = (CG == 2) ? 0u : crank;                 // rank in a multicast cluster
+    const int cl_id = (int)(blockIdx.x / CLSZ);
+    const int cl_count = (int)(gridDim.x / CLSZ);
+    const int head_items = sched.head_tiles * sched.split;
 #if OPEVO_TRACE
-    u64* trace = reinterpret_cast<u64*>(ws) +
-                 16ull * ((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
+    u64* trace = reinterpret_cast<u64*>(ws) + 16ull * blockIdx.x;
     if (threadIdx.x == 0) { trace[0] = sm_id(); TRACE(1); }
 #endif
     if (threadIdx.x == 0) pdl_launch_dependents();
     if (OPEVO_ABLATE == 1) return;
-    (void)crank;
-    (void)row0;
+    (void)mrank;
     (void)geom;
-#if OPEVO_CONV
-    // row_tile enumerates (image tile, output-row tile, output-col tile)
-    const int w_tiles = geom.wo / TILE_W, h_tiles = geom.ho / TILE_H;
-    const int w0 = (row_tile % w_tiles) * TILE_W;
-    const int h0 = ((row_tile / w_tiles) % h_tiles) * TILE_H;
-    const int n0 = (row_tile / (w_tiles * h_tiles)) * TILE_N;
-#endif
+
+    // unit -> (batch, row tile, column group, K slice); column groups vary
+    // fastest so concurrently running clusters share A row panels in L2.
+    // Tiles past head_tiles (the last, partial wave of a persistent grid)
+    // are cut into tail_split times more K slices so the wave fills up.
+    struct Unit { int batch, row_tile, col_tile, kz, split, k0, num_kb; };
+    auto decode = [&](int u) -> Unit {
+        Unit t;
+        if (u < head_items) {
+            t.split = sched.split;
+            t.kz = u % t.split;
+            u /= t.split;
+        } else {
+            const int v = u - head_items;
+            t.split = sched.split * sched.tail_split;
+            t.kz = v % t.split;
+            u = sched.head_tiles + v / t.split;
+        }
+        const int klen = depth / t.split;
+        t.k0 = t.kz * klen;
+        t.num_kb = OPEVO_ABLATE == 2 ? 0 : klen / BK;
+        const int colg = u % sched.col_groups;
+        u /= sched.col_groups;
+        t.row_tile = u % sched.row_tiles;
+        t.batch = u / sched.row_tiles;
+        t.col_tile = colg * CLUSTER + (int)mrank;
+        return t;
+    };
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tma_a);
@@ -419,41 +514,65 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
             mbar_init(smem_u32(full_bar + s), 1);
             // with multicast every CTA of the cluster must release a slot
             // before any of them overwrites it
-            mbar_init(smem_u32(empty_bar + s), CLUSTER);
+            mbar_init(smem_u32(empty_bar + s), CG == 2 ? 1 : CLUSTER);
         }
-        mbar_init(smem_u32(accum_bar), 1);
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(smem_u32(tfull_bar + b), 1);
+            // one arrival per epilogue warp; a pair leader's MMAs also write
+            // the peer's TMEM, so it waits for both CTAs' epilogues
+            mbar_init(smem_u32(tempty_bar + b), 4 * CG);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                     :: "r"(smem_u32(tmem_slot)), "r"(TMEM_COLS) : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        if (CG == 2) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                         :: "r"(smem_u32(tmem_slot)), "r"(TMEM_ALLOC) : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                         :: "r"(smem_u32(tmem_slot)), "r"(TMEM_ALLOC) : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
     }
     tc_fence_before();
     __syncthreads();
-    if (CLUSTER > 1) cluster_sync();
+    if (CLSZ > 1) cluster_sync();
     tc_fence_after();
     const u32 tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);   // warp-uniform
     if (threadIdx.x == 0) TRACE(2);
 
     if (warp == 0) {
-        {
-            // ------------------------------------------------ TMA producer
-            // (whole warp iterates; the tma_* / expect_tx helpers elect one lane)
-            int s = 0;
-            u32 ph = 0;
-            pdl_wait();                 // operands may be the previous launch's output
-            if (lane == 0) TRACE(9);
+        // ---------------------------------------------------- TMA producer
+        // (whole warp iterates; the tma_* / expect_tx helpers elect one lane)
+        int s = 0;
+        u32 ph = 0;
+        bool first = true;
+        pdl_wait();                     // operands may be the previous launch's output
+        if (lane == 0) TRACE(9);
+        for (int u = cl_id; u < sched.units; u += cl_count) {
+            const Unit t = decode(u);
+            const int k0 = t.k0;
+            const int num_kb = t.num_kb;
+            const int col0 = t.col_tile * BN;
+#if OPEVO_CONV
+            const int w_tiles = geom.wo / TILE_W, h_tiles = geom.ho / TILE_H;
+            const int w0 = (t.row_tile % w_tiles) * TILE_W;
+            const int h0 = ((t.row_tile / w_tiles) % h_tiles) * TILE_H;
+            const int n0 = (t.row_tile / (w_tiles * h_tiles)) * TILE_N;
+#else
+            const int row0 = t.row_tile * BM + (int)prank * BM_CTA;   // first A row here
+            const int b_row0 = col0 + (int)prank * BN_LOAD;         // first B row here
+#endif
             for (int kb = 0; kb < num_kb; ++kb) {
                 mbar_wait(smem_u32(empty_bar + s), ph ^ 1);
-                const u32 fb = smem_u32(full_bar + s);
+                const u32 fb = (CG == 2) ? mapa_cta(smem_u32(full_bar + s), 0) : smem_u32(full_bar + s);
                 if (OPEVO_ABLATE == 3) {
-                    if (lane == 0)
-                        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(fb) : "memory");
+                    if (lane == 0) mbar_arrive(fb);
                     if (++s == STAGES) { s = 0; ph ^= 1; }
                     continue;
                 }
-                mbar_expect_tx(fb, STAGE_BYTES);
+                if (prank == 0) mbar_expect_tx(smem_u32(full_bar + s), TX_BYTES);
                 const u32 a_dst = smem_u32(smem + s * STAGE_BYTES);
                 const u32 b_dst = a_dst + A_TILE;
                 const int kk = k0 + kb * BK;
@@ -464,187 +583,247 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                 const int di = tap / geom.kw - geom.pad, dj = tap % geom.kw - geom.pad;
 #pragma unroll
                 for (int ka = 0; ka < KATOMS; ++ka) {
-                    tma_load_4d(a_dst + ka * (BM * SWZ), &tma_a, fb, cbase + ka * ATOM_K,
+                    tma_load_4d(a_dst + ka * (BM_CTA * SWZ), &tma_a, fb, cbase + ka * ATOM_K,
                                 w0 + dj, h0 + di, n0);
-                    tma_load_2d(b_dst + ka * (BN * SWZ), &tma_b, fb, kk + ka * ATOM_K, col0);
+                    tma_load_2d(b_dst + ka * (BN_LOAD * SWZ), &tma_b, fb, kk + ka * ATOM_K, col0);
                 }
 #else
 #pragma unroll
                 for (int ka = 0; ka < KATOMS; ++ka) {
                     const int kc = kk + ka * ATOM_K;
-                    const u32 a_sub = a_dst + ka * (BM * SWZ);
+                    const u32 a_sub = a_dst + ka * (BM_CTA * SWZ);
+                    const u32 b_sub = b_dst + ka * (BN_LOAD * SWZ);
+#if OPEVO_CTA_GROUP == 2
+#if OPEVO_BATCHED
+                    tma2_load_3d(a_sub, &tma_a, fb, kc, row0, t.batch);
+                    tma2_load_3d(b_sub, &tma_b, fb, kc, b_row0, t.batch);
+#else
+                    tma2_load_2d(a_sub, &tma_a, fb, kc, row0);
+                    tma2_load_2d(b_sub, &tma_b, fb, kc, b_row0);
+#endif
+#else
 #if OPEVO_CLUSTER > 1
                     // this CTA fetches one 1/CLUSTER slice of the shared A tile
                     // and multicasts it into every CTA of the cluster
-                    const u32 a_part = a_sub + crank * (A_SLICE_ROWS * SWZ);
+                    const u32 a_part = a_sub + mrank * (A_SLICE_ROWS * SWZ);
                     const u16 mask = (u16)((1u << CLUSTER) - 1);
 #if OPEVO_BATCHED
-                    tma_load_3d_mc(a_part, &tma_a, fb, kc, row0 + crank * A_SLICE_ROWS, batch, mask);
+                    tma_load_3d_mc(a_part, &tma_a, fb, kc, row0 + mrank * A_SLICE_ROWS, t.batch, mask);
 #else
-                    tma_load_2d_mc(a_part, &tma_a, fb, kc, row0 + crank * A_SLICE_ROWS, mask);
+                    tma_load_2d_mc(a_part, &tma_a, fb, kc, row0 + mrank * A_SLICE_ROWS, mask);
 #endif
 #else
 #if OPEVO_BATCHED
-                    tma_load_3d(a_sub, &tma_a, fb, kc, row0, batch);
+                    tma_load_3d(a_sub, &tma_a, fb, kc, row0, t.batch);
 #else
                     tma_load_2d(a_sub, &tma_a, fb, kc, row0);
 #endif
 #endif
 #if OPEVO_BATCHED
-                    tma_load_3d(b_dst + ka * (BN * SWZ), &tma_b, fb, kc, col0, batch);
+                    tma_load_3d(b_sub, &tma_b, fb, kc, b_row0, t.batch);
 #else
-                    tma_load_2d(b_dst + ka * (BN * SWZ), &tma_b, fb, kc, col0);
+                    tma_load_2d(b_sub, &tma_b, fb, kc, b_row0);
+#endif
 #endif
                 }
 #endif
-                if (kb == 0 && lane == 0) TRACE(3);
+                if (first && lane == 0) { TRACE(3); first = false; }
                 if (++s == STAGES) { s = 0; ph ^= 1; }
             }
         }
     } else if (warp == 1) {
-        {
+        if (CG == 1 || prank == 0) {
             // ------------------------------------------------ MMA issuer
             // (whole warp iterates; umma_* elect one lane to issue)
-            int s = 0;
-            u32 ph = 0;
-            for (int kb = 0; kb < num_kb; ++kb) {
-                mbar_wait(smem_u32(full_bar + s), ph);
+            int s = 0, buf = 0;
+            u32 ph = 0, bph = 0;
+            bool first = true;
+            for (int u = cl_id; u < sched.units; u += cl_count) {
+                const int num_kb = decode(u).num_kb;
+                // the epilogue must have drained this accumulator buffer
+                mbar_wait(smem_u32(tempty_bar + buf), bph ^ 1);
                 tc_fence_after();
-                if (kb == 0 && lane == 0) TRACE(4);
-                if (OPEVO_ABLATE == 4) {
-                    if (lane == 0)
-                        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];"
-                                     :: "r"(smem_u32(empty_bar + s)) : "memory");
-                    if (++s == STAGES) { s = 0; ph ^= 1; }
-                    continue;
-                }
-                const u32 a_base = smem_u32(smem + s * STAGE_BYTES);
-                const u32 b_base = a_base + A_TILE;
+                const u32 acc_base = tmem_base + (u32)(buf * TMEM_USED);
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    mbar_wait(smem_u32(full_bar + s), ph);
+                    tc_fence_after();
+                    if (first && lane == 0) { TRACE(4); first = false; }
+                    if (OPEVO_ABLATE == 4) {
+                        if (lane == 0) mbar_arrive(smem_u32(empty_bar + s));
+                        if (++s == STAGES) { s = 0; ph ^= 1; }
+                        continue;
+                    }
+                    const u32 a_base = smem_u32(smem + s * STAGE_BYTES);
+                    const u32 b_base = a_base + A_TILE;
 #pragma unroll
-                for (int ka = 0; ka < KATOMS; ++ka) {
+                    for (int ka = 0; ka < KATOMS; ++ka) {
 #pragma unroll
-                    for (int k16 = 0; k16 < ATOM_K / 16; ++k16) {
-                        const u32 koff = k16 * 32;
-                        const u64 bdesc = DESC_HI | (u64)(((b_base + ka * (BN * SWZ) + koff) >> 4) & 0x3FFF);
+                        for (int k16 = 0; k16 < ATOM_K / 16; ++k16) {
+                            const u32 koff = k16 * 32;
+                            const u64 bdesc = DESC_HI |
+                                (u64)(((b_base + ka * (BN_LOAD * SWZ) + koff) >> 4) & 0x3FFF);
 #pragma unroll
-                        for (int ma = 0; ma < MATOMS; ++ma) {
-                            const u32 a_addr = a_base + ka * (BM * SWZ) + ma * (128 * SWZ) + koff;
-                            const u64 adesc = DESC_HI | (u64)((a_addr >> 4) & 0x3FFF);
-                            const int step = ka * (ATOM_K / 16) + k16;     // k16 step in stage
-                            const int acc = step % ACC;                    // compile-time
-                            umma_bf16(tmem_base + (acc * MATOMS + ma) * BN, adesc, bdesc,
-                                      (kb != 0 || step >= ACC) ? 1u : 0u);
+                            for (int ma = 0; ma < MATOMS; ++ma) {
+                                const u32 a_addr = a_base + ka * (BM_CTA * SWZ) + ma * (128 * SWZ) + koff;
+                                const u64 adesc = DESC_HI | (u64)((a_addr >> 4) & 0x3FFF);
+                                const int step = ka * (ATOM_K / 16) + k16;   // k16 step in stage
+                                const int acc = step % ACC;                  // compile-time
+                                const u32 d = acc_base + (u32)((acc * MATOMS + ma) * BN);
+                                const u32 accumulate = (kb != 0 || step >= ACC) ? 1u : 0u;
+                                if (CG == 2) umma2_bf16(d, adesc, bdesc, accumulate);
+                                else         umma_bf16(d, adesc, bdesc, accumulate);
+                            }
                         }
                     }
-                }
-#if OPEVO_CLUSTER > 1
-                // the slot is refilled by multicasts from every cluster CTA:
-                // release it in all of them once our MMAs have consumed it
-                umma_commit_mc(smem_u32(empty_bar + s), (u16)((1u << CLUSTER) - 1));
+#if OPEVO_CTA_GROUP == 2
+                    // both CTAs staged this slot: release it in both
+                    umma2_commit_mc(smem_u32(empty_bar + s), (u16)3);
+#elif OPEVO_CLUSTER > 1
+                    // the slot is refilled by multicasts from every cluster CTA:
+                    // release it in all of them once our MMAs have consumed it
+                    umma_commit_mc(smem_u32(empty_bar + s), (u16)((1u << CLUSTER) - 1));
 #else
-                umma_commit(smem_u32(empty_bar + s));
+                    umma_commit(smem_u32(empty_bar + s));
 #endif
-                if (++s == STAGES) { s = 0; ph ^= 1; }
+                    if (++s == STAGES) { s = 0; ph ^= 1; }
+                }
+                if (CG == 2) umma2_commit_mc(smem_u32(tfull_bar + buf), (u16)3);   // both halves
+                else         umma_commit(smem_u32(tfull_bar + buf));
+                if (++buf == NBUF) { buf = 0; bph ^= 1; }
             }
-            umma_commit(smem_u32(accum_bar));
             if (lane == 0) TRACE(5);
         }
     } else {
         // ---------------------------------------------------- epilogue
         const int quarter = warp & 3;              // TMEM lane quarter of this warp
         const int epi_tid = threadIdx.x - 64;
-        mbar_wait(smem_u32(accum_bar), 0);
-        tc_fence_after();
-        pdl_wait();                     // C may still be written by the previous launch
-        if (epi_tid == 0) TRACE(6);
-        const u32 lane_addr = tmem_base + ((u32)(quarter * 32) << 16);
         const u64 plane = (u64)rows * (u64)cols;   // one batch (or one split slice)
+        const u64 slice = (u64)sched.batches * plane;
+        // TMEM release target: the pair leader's barrier for CG == 2
+        const u32 tempty_leader0 = (CG == 2) ? mapa_cta(smem_u32(tempty_bar), 0) : 0u;
+        int buf = 0;
+        u32 bph = 0;
+        bool first = true;
+        for (int u = cl_id; u < sched.units; u += cl_count) {
+            const Unit t = decode(u);
+            const int col0 = t.col_tile * BN;
 #if OPEVO_CONV
-        // tile row -> NHWC output pixel row
-        auto out_row = [&](int lr) -> int {
-            const int n = n0 + lr / (TILE_H * TILE_W);
-            const int h = h0 + (lr / TILE_W) % TILE_H;
-            const int w = w0 + lr % TILE_W;
-            return (n * geom.ho + h) * geom.wo + w;
-        };
+            const int w_tiles = geom.wo / TILE_W, h_tiles = geom.ho / TILE_H;
+            const int w0 = (t.row_tile % w_tiles) * TILE_W;
+            const int h0 = ((t.row_tile / w_tiles) % h_tiles) * TILE_H;
+            const int n0 = (t.row_tile / (w_tiles * h_tiles)) * TILE_N;
+            // tile row -> NHWC output pixel row
+            auto out_row = [&](int lr) -> int {
+                const int n = n0 + lr / (TILE_H * TILE_W);
+                const int h = h0 + (lr / TILE_W) % TILE_H;
+                const int w = w0 + lr % TILE_W;
+                return (n * geom.ho + h) * geom.wo + w;
+            };
 #else
-        auto out_row = [&](int lr) -> int { return row0 + lr; };
+            const int row0 = t.row_tile * BM + (int)prank * BM_CTA;
+            auto out_row = [&](int lr) -> int { return row0 + lr; };
 #endif
-        const u64 c_batch = (u64)batch * plane;
-
-        if (split == 1) {
-#pragma unroll 1
-            for (int ma = 0; ma < MATOMS; ++ma) {
-                const int r = out_row(ma * 128 + quarter * 32 + lane);
-#pragma unroll 1
-                for (int c = 0; c < BN; c += EPI_COLS) {
-                    float acc[EPI_COLS];
-                    gather_acc(lane_addr + ma * BN + c, acc);
-                    store_row(c_out, c_batch + (u64)r * cols + col0 + c, acc);
+            const u64 c_batch = (u64)t.batch * plane;
+            mbar_wait(smem_u32(tfull_bar + buf), bph);
+            tc_fence_after();
+            if (first) {
+                pdl_wait();                 // C may still be written by the previous launch
+                if (epi_tid == 0) TRACE(6);
+            }
+            const u32 lane_addr = tmem_base + (u32)(buf * TMEM_USED) + ((u32)(quarter * 32) << 16);
+            // drain the accumulator into registers, chunk by chunk; the last
+            // chunk's TMEM load releases the buffer before its global stores
+            auto release = [&]() {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (CG == 2) mbar_arrive_cluster(tempty_leader0 + 8u * (u32)buf);
+                    else         mbar_arrive(smem_u32(tempty_bar + buf));
                 }
-            }
-            if (epi_tid == 0) TRACE(7);
-        } else {
-            const u64 nbat = (u64)gridDim.z / (u64)split;
-            const u64 slice = nbat * plane;
-#pragma unroll 1
-            for (int ma = 0; ma < MATOMS; ++ma) {
-                const int r = out_row(ma * 128 + quarter * 32 + lane);
-#pragma unroll 1
-                for (int c = 0; c < BN; c += EPI_COLS) {
-                    float acc[EPI_COLS];
-                    gather_acc(lane_addr + ma * BN + c, acc);
-                    float* dst = ws + (u64)kz * slice + c_batch + (u64)r * cols + col0 + c;
-#pragma unroll
-                    for (int j = 0; j < EPI_COLS; j += 4)
-                        st_v4(dst + j, __float_as_uint(acc[j]), __float_as_uint(acc[j + 1]),
-                              __float_as_uint(acc[j + 2]), __float_as_uint(acc[j + 3]));
-                }
-            }
-            __threadfence();
-            epi_bar();
-            if (epi_tid == 0) {
-                const u32 tile = (u32)((batch * gridDim.y + row_tile) * gridDim.x + col_tile);
-                const u32 prev = atomicAdd(counters + tile, 1u);
-                const u32 last = (prev == (u32)(split - 1)) ? 1u : 0u;
-                if (last) counters[tile] = 0u;     // ready for the next launch
-                *last_flag = last;
-                __threadfence();
-            }
-            epi_bar();
-            if (*last_flag) {
+            };
+            const int split = t.split;
+            if (split == 1) {
 #pragma unroll 1
                 for (int ma = 0; ma < MATOMS; ++ma) {
                     const int r = out_row(ma * 128 + quarter * 32 + lane);
 #pragma unroll 1
                     for (int c = 0; c < BN; c += EPI_COLS) {
                         float acc[EPI_COLS];
-#pragma unroll
-                        for (int j = 0; j < EPI_COLS; ++j) acc[j] = 0.0f;
-                        const u64 base = c_batch + (u64)r * cols + col0 + c;
-                        for (int z = 0; z < split; ++z) {
-                            const float* src = ws + (u64)z * slice + base;
-#pragma unroll
-                            for (int j = 0; j < EPI_COLS; j += 4) {
-                                const float4 p = ld_cg_f4(src + j);
-                                acc[j] += p.x; acc[j + 1] += p.y; acc[j + 2] += p.z; acc[j + 3] += p.w;
-                            }
-                        }
-                        store_row(c_out, base, acc);
+                        gather_acc(lane_addr + ma * BN + c, acc);
+                        if (ma == MATOMS - 1 && c + EPI_COLS >= BN) release();
+                        store_row(c_out, c_batch + (u64)r * cols + col0 + c, acc);
                     }
                 }
+                if (first && epi_tid == 0) TRACE(7);
+            } else {
+#pragma unroll 1
+                for (int ma = 0; ma < MATOMS; ++ma) {
+                    const int r = out_row(ma * 128 + quarter * 32 + lane);
+#pragma unroll 1
+                    for (int c = 0; c < BN; c += EPI_COLS) {
+                        float acc[EPI_COLS];
+                        gather_acc(lane_addr + ma * BN + c, acc);
+                        if (ma == MATOMS - 1 && c + EPI_COLS >= BN) release();
+                        float* dst = ws + (u64)t.kz * slice + c_batch + (u64)r * cols + col0 + c;
+#pragma unroll
+                        for (int j = 0; j < EPI_COLS; j += 4)
+                            st_v4(dst + j, __float_as_uint(acc[j]), __float_as_uint(acc[j + 1]),
+                                  __float_as_uint(acc[j + 2]), __float_as_uint(acc[j + 3]));
+                    }
+                }
+                __threadfence();
+                epi_bar();
+                if (epi_tid == 0) {
+                    const u32 tile = (u32)((((t.batch * sched.row_tiles + t.row_tile) * sched.col_groups
+                                            + t.col_tile / CLUSTER) * CLSZ) + crank);
+                    const u32 prev = atomicAdd(counters + tile, 1u);
+                    const u32 last = (prev == (u32)(split - 1)) ? 1u : 0u;
+                    if (last) counters[tile] = 0u;     // ready for the next launch
+                    *last_flag = last;
+                    __threadfence();
+                }
+                epi_bar();
+                if (*last_flag) {
+#pragma unroll 1
+                    for (int ma = 0; ma < MATOMS; ++ma) {
+                        const int r = out_row(ma * 128 + quarter * 32 + lane);
+#pragma unroll 1
+                        for (int c = 0; c < BN; c += EPI_COLS) {
+                            float acc[EPI_COLS];
+#pragma unroll
+                            for (int j = 0; j < EPI_COLS; ++j) acc[j] = 0.0f;
+                            const u64 base = c_batch + (u64)r * cols + col0 + c;
+                            for (int z = 0; z < split; ++z) {
+                                const float* src = ws + (u64)z * slice + base;
+#pragma unroll
+                                for (int j = 0; j < EPI_COLS; j += 4) {
+                                    const float4 p = ld_cg_f4(src + j);
+                                    acc[j] += p.x; acc[j + 1] += p.y; acc[j + 2] += p.z; acc[j + 3] += p.w;
+                                }
+                            }
+                            store_row(c_out, base, acc);
+                        }
+                    }
+                }
+                epi_bar();                  // last_flag is reused by the next unit
             }
+            first = false;
+            if (++buf == NBUF) { buf = 0; bph ^= 1; }
         }
     }
 
     tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0) TRACE(8);
-    if (CLUSTER > 1) cluster_sync();
+    if (CLSZ > 1) cluster_sync();
     if (warp == 1) {
         __syncwarp();
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;"
-                     :: "r"(tmem_base), "r"(TMEM_COLS) : "memory");
+        if (CG == 2)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;"
+                         :: "r"(tmem_base), "r"(TMEM_ALLOC) : "memory");
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;"
+                         :: "r"(tmem_base), "r"(TMEM_ALLOC) : "memory");
     }
 }

@@ -92,6 +92,7 @@ struct Driver {
     X(EventSynchronize, cuEventSynchronize)                       \
     X(EventElapsedTime, cuEventElapsedTime)                       \
     X(TensorMapEncodeTiled, cuTensorMapEncodeTiled)               \
+    X(OccupancyMaxBlocks, cuOccupancyMaxActiveBlocksPerMultiprocessor) \
     X(GetErrorString, cuGetErrorString)                           \
     X(GetErrorName, cuGetErrorName)
     OPEVO_CU_LIST(OPEVO_CU_FN)
@@ -179,19 +180,31 @@ void load_nvrtc() {
 
 // ------------------------------------------------------------- knobs
 struct Knobs {
-    int bm, bn, bk, stages, split, cluster, tile_h, tile_w, acc;
+    int bm, bn, bk, stages, split, cluster, tile_h, tile_w, acc, cg, grid_mode;
 };
 
 Knobs read_knobs(const int32_t* k, int n) {
-    int32_t v[OPEVO_NUM_KNOBS] = {128, 128, 64, 4, 1, 1, 1, 1, 1};
+    int32_t v[OPEVO_NUM_KNOBS] = {128, 128, 64, 4, 1, 1, 1, 1, 1, 1, 0};
     for (int i = 0; i < n && i < OPEVO_NUM_KNOBS; ++i) v[i] = k[i];
-    return Knobs{v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8]};
+    return Knobs{v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8], v[9], v[10]};
+}
+
+// TMEM columns the kernel allocates (two accumulator buffers when they fit).
+int tmem_alloc_cols(const Knobs& k) {
+    const int used = (k.cg == 1 && k.bm == 256 ? 2 : 1) * k.bn * k.acc;
+    const int want = (2 * used <= 512 ? 2 : 1) * used;
+    int cols = 32;
+    while (cols < want) cols *= 2;
+    return cols;
 }
 
 int swizzle_bytes(int bk) { return bk * 2 >= 128 ? 128 : bk * 2; }
 
+// per-CTA: a CTA pair stages 128 rows of A and BN/2 rows of B each
 size_t smem_bytes(const Knobs& k) {
-    return (size_t)k.stages * (size_t)(k.bm + k.bn) * (size_t)k.bk * 2 + 1024 + 256;
+    const int a_rows = k.cg == 2 ? 128 : k.bm;
+    const int b_rows = k.bn / (k.cg == 2 ? 2 : 1);
+    return (size_t)k.stages * (size_t)(a_rows + b_rows) * (size_t)k.bk * 2 + 1024 + 256;
 }
 
 uint64_t fnv1a(const char* s, size_t n, uint64_t h = 1469598103934665603ull) {
@@ -224,9 +237,9 @@ std::string make_key(int family, const Knobs& k, int batched, int out_f32) {
     const std::string extra = extra_flags();
     const uint64_t h = fnv1a(extra.data(), extra.size(), src_hash);
     char buf[256];
-    snprintf(buf, sizeof buf, "f%d_m%d_n%d_k%d_s%d_b%d_o%d_c%d_h%d_w%d_a%d_%s%012llx", family, k.bm,
-             k.bn, k.bk, k.stages, batched, out_f32, k.cluster, family == 1 ? k.tile_h : 1,
-             family == 1 ? k.tile_w : 1, k.acc, want_lineinfo() ? "L" : "",
+    snprintf(buf, sizeof buf, "f%d_m%d_n%d_k%d_s%d_b%d_o%d_c%d_h%d_w%d_a%d_g%d_%s%012llx", family,
+             k.bm, k.bn, k.bk, k.stages, batched, out_f32, k.cluster, family == 1 ? k.tile_h : 1,
+             family == 1 ? k.tile_w : 1, k.acc, k.cg, want_lineinfo() ? "L" : "",
              (unsigned long long)(h & 0xffffffffffffull));
     return buf;
 }
@@ -254,7 +267,12 @@ bool knobs_compilable(int family, const Knobs& k, char* err, size_t len) {
         put_err(err, len, "acc=%d unsupported for BK=%d (1, 2 or 4 dividing BK/16)", k.acc, k.bk);
         return false;
     }
-    if ((k.bm == 256 ? 2 : 1) * k.bn * k.acc > 512) {
+    if (!(k.cg == 1 || k.cg == 2) ||
+        (k.cg == 2 && (k.bm != 256 || k.cluster != 1 || family != 0))) {
+        put_err(err, len, "cta_group=%d needs BM=256, no multicast cluster, GEMM family", k.cg);
+        return false;
+    }
+    if ((k.cg == 1 && k.bm == 256 ? 2 : 1) * k.bn * k.acc > 512) {
         put_err(err, len, "accumulators %dx%d x%d exceed 512 TMEM columns", k.bm, k.bn, k.acc);
         return false;
     }
@@ -336,7 +354,8 @@ int nvrtc_build(int family, const Knobs& k, int batched, int out_f32, std::vecto
         "-DOPEVO_CLUSTER=" + std::to_string(k.cluster), "-DOPEVO_CONV=" + std::to_string(family == 1),
         "-DOPEVO_TILE_H=" + std::to_string(family == 1 ? k.tile_h : 1),
         "-DOPEVO_TILE_W=" + std::to_string(family == 1 ? k.tile_w : 1),
-        "-DOPEVO_ACC=" + std::to_string(k.acc)};
+        "-DOPEVO_ACC=" + std::to_string(k.acc),
+        "-DOPEVO_CTA_GROUP=" + std::to_string(k.cg)};
     if (want_lineinfo()) opts.push_back("-lineinfo");
     {
         std::istringstream extra(extra_flags());
@@ -428,6 +447,11 @@ struct ConvGeomHost {
     int cin, ho, wo, kw, pad, taps_cchunks;
 };
 
+// mirrors `Sched` in gemm_sm100.cuh
+struct SchedHost {
+    int row_tiles, col_groups, batches, split, head_tiles, tail_split, units;
+};
+
 struct opevo_kernel {
     opevo_op* op = nullptr;
     Knobs k{};
@@ -439,6 +463,7 @@ struct opevo_kernel {
     size_t smem = 0;
     int k_per_split = 0;
     ConvGeomHost geom{};
+    SchedHost sched{};
     double flops = 0.0;
 };
 
@@ -543,11 +568,11 @@ int launch_kernel(opevo_kernel* kr, char* err, size_t errlen) {
     opevo_ctx* ctx = op->ctx;
     int rows = (int)op->rows;
     int cols = (int)op->cols;
-    int kps = kr->k_per_split, split = kr->k.split;
+    int depth = (int)op->depth;
     void* cptr = (void*)op->c;
     float* ws = (float*)op->ws;
     unsigned* cnt = (unsigned*)op->counters;
-    void* args[] = {&kr->tma_a, &kr->tma_b, &cptr, &ws, &cnt, &rows, &cols, &kps, &split, &kr->geom};
+    void* args[] = {&kr->tma_a, &kr->tma_b, &cptr, &ws, &cnt, &rows, &cols, &depth, &kr->sched, &kr->geom};
     CUlaunchConfig cfg{};
     cfg.gridDimX = kr->grid[0];
     cfg.gridDimY = kr->grid[1];
@@ -559,9 +584,9 @@ int launch_kernel(opevo_kernel* kr, char* err, size_t errlen) {
     cfg.hStream = ctx->stream;
     CUlaunchAttribute attr[2];
     unsigned na = 0;
-    if (kr->k.cluster > 1) {
+    if (kr->k.cluster > 1 || kr->k.cg == 2) {
         attr[na].id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
-        attr[na].value.clusterDim.x = (unsigned)kr->k.cluster;
+        attr[na].value.clusterDim.x = (unsigned)(kr->k.cluster * kr->k.cg);
         attr[na].value.clusterDim.y = 1;
         attr[na].value.clusterDim.z = 1;
         ++na;
@@ -923,28 +948,23 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
         uint64_t bs[1] = {(uint64_t)op->depth * 2};
         uint32_t bb[2] = {atom_k, (uint32_t)k.bn};
         if (!st) st = encode_map(&kr->tma_b, op->b, 2, bd, bs, bb, swz, err, errlen);
-        kr->grid[0] = (unsigned)col_tiles;
-        kr->grid[1] = (unsigned)((N / tile_n) * (HO / k.tile_h) * (WO / k.tile_w));
-        kr->grid[2] = (unsigned)k.split;
+        kr->sched = SchedHost{(N / tile_n) * (HO / k.tile_h) * (WO / k.tile_w), (int)col_tiles, 1,
+                              k.split, 0, 1, 0};
     } else {
         const int rank = batched ? 3 : 2;
         uint64_t ad[3] = {(uint64_t)op->depth, (uint64_t)op->rows, (uint64_t)op->batch};
         uint64_t as[2] = {(uint64_t)op->depth * 2, (uint64_t)op->depth * op->rows * 2};
-        uint32_t ab[3] = {atom_k, (uint32_t)(k.bm / k.cluster), 1};
+        const uint32_t a_rows = (uint32_t)((k.cg == 2 ? 128 : k.bm) / k.cluster);
+        uint32_t ab[3] = {atom_k, a_rows, 1};
         uint64_t bd[3] = {(uint64_t)op->depth, (uint64_t)op->cols, (uint64_t)op->batch};
         uint64_t bs[2] = {(uint64_t)op->depth * 2, (uint64_t)op->depth * op->cols * 2};
-        uint32_t bb[3] = {atom_k, (uint32_t)k.bn, 1};
+        uint32_t bb[3] = {atom_k, (uint32_t)(k.bn / k.cg), 1};
         st = encode_map(&kr->tma_a, op->a, rank, ad, as, ab, swz, err, errlen);
         if (!st) st = encode_map(&kr->tma_b, op->b, rank, bd, bs, bb, swz, err, errlen);
-        kr->grid[0] = (unsigned)col_tiles;
-        kr->grid[1] = (unsigned)row_tiles;
-        kr->grid[2] = (unsigned)(op->batch * k.split);
+        kr->sched = SchedHost{(int)row_tiles, (int)(col_tiles / k.cluster), (int)op->batch, k.split,
+                              0, 1, 0};
     }
-    if (!st && k.split > 1) {
-        const size_t slice = (size_t)op->batch * op->rows * op->cols * 4;
-        const size_t tiles = (size_t)kr->grid[0] * kr->grid[1] * (size_t)op->batch;
-        st = ensure_ws(op, slice * k.split, tiles * 4, err, errlen);
-    }
+    const int clsz = k.cluster * k.cg;
     if (st) {
         delete kr;
         return st;
@@ -982,6 +1002,44 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
         lm.smem_set = (int)kr->smem;
     }
     kr->fn = lm.fn;
+    // grid: one cluster per unit, or (grid_mode 0) at most what is resident at
+    // once, in which case CTAs loop over units (persistent schedule)
+    {
+        int per_sm = 1;
+        if (g_cu.OccupancyMaxBlocks(&per_sm, kr->fn, 192, kr->smem) != CUDA_SUCCESS || per_sm < 1) per_sm = 1;
+        per_sm = std::min(per_sm, 512 / tmem_alloc_cols(k));
+        const int capacity = std::max(1, (ctx->sm_count / clsz) * per_sm);
+        SchedHost& sc = kr->sched;
+        const int tiles = sc.row_tiles * sc.col_groups * sc.batches;
+        sc.head_tiles = tiles;
+        sc.tail_split = 1;
+        // grid_mode 2: a persistent grid whose last wave would be partial cuts
+        // the tiles of that wave into more K slices (stream-K style tail).
+        // Measured slower than plain persistence on 4096^3 (the fp32 partials
+        // cost more than the filled wave saves), so it is opt-in.
+        if (k.grid_mode == 2 && k.split == 1 && tiles > capacity && tiles % capacity) {
+            const int rem = tiles % capacity;
+            int ts = 1;
+            while (ts < 8 && 2 * ts * rem <= capacity && op->depth % ((int64_t)2 * ts * k.bk) == 0) ts *= 2;
+            if (ts > 1) {
+                sc.head_tiles = tiles - rem;
+                sc.tail_split = ts;
+            }
+        }
+        sc.units = sc.head_tiles * sc.split + (tiles - sc.head_tiles) * sc.split * sc.tail_split;
+        const int clusters = k.grid_mode == 1 ? sc.units : std::min(sc.units, capacity);
+        kr->grid[0] = (unsigned)(clusters * clsz);
+        kr->grid[1] = kr->grid[2] = 1;
+        const int max_split = sc.split * sc.tail_split;
+        if (max_split > 1) {
+            const size_t slice = (size_t)op->batch * op->rows * op->cols * 4;
+            st = ensure_ws(op, slice * max_split, (size_t)tiles * clsz * 4, err, errlen);
+            if (st) {
+                delete kr;
+                return st;
+            }
+        }
+    }
     if (info) {
         info->compile_ms = compile_ms;
         info->cache_hit = hit;

@@ -72,17 +72,20 @@ class Knobs:
     cluster: int = 1
     tile_h: int = 1
     tile_w: int = 1
+    acc: int = 1
+    cta_group: int = 1
 
     def as_tuple(self) -> tuple[int, ...]:
         return (self.bm, self.bn, self.bk, self.stages, self.split, self.cluster,
-                self.tile_h, self.tile_w)
+                self.tile_h, self.tile_w, self.acc, self.cta_group)
 
     def compile_key(self) -> tuple[int, ...]:
         """Fields that change the generated code (split-K is a launch arg)."""
-        return (self.bm, self.bn, self.bk, self.stages, self.cluster, self.tile_h, self.tile_w)
+        return (self.bm, self.bn, self.bk, self.stages, self.cluster, self.tile_h, self.tile_w,
+                self.acc, self.cta_group)
 
     def smem_bytes(self) -> int:
-        return stage_bytes(self.bm, self.bn, self.bk) * self.stages + SMEM_EXTRA
+        return stage_bytes(self.bm, self.bn, self.bk, self.cta_group) * self.stages + SMEM_EXTRA
 
 
 @dataclass(frozen=True)
@@ -99,7 +102,11 @@ class Mapped:
         return self.knobs is not None
 
 
-def stage_bytes(bm: int, bn: int, bk: int) -> int:
+def stage_bytes(bm: int, bn: int, bk: int, cta_group: int = 1) -> int:
+    """Shared memory per pipeline stage of one CTA (a CTA pair stages 128 rows
+    of A and BN/2 rows of B in each CTA)."""
+    if cta_group == 2:
+        return (128 + bn // 2) * bk * 2
     return (bm + bn) * bk * 2
 
 
@@ -107,8 +114,8 @@ def _bk_ok(bk: int) -> bool:
     return bk in (16, 32) or (64 <= bk <= 256 and bk % 64 == 0)
 
 
-def _fit_stages(want: int, bm: int, bn: int, bk: int) -> int:
-    room = (SMEM_LIMIT - SMEM_EXTRA) // stage_bytes(bm, bn, bk)
+def _fit_stages(want: int, bm: int, bn: int, bk: int, cta_group: int = 1) -> int:
+    room = (SMEM_LIMIT - SMEM_EXTRA) // stage_bytes(bm, bn, bk, cta_group)
     return min(want, room)
 
 
@@ -142,15 +149,18 @@ def _gemm_knobs(rows: int, cols: int, depth: int, vals: dict) -> tuple[Knobs | N
         return None, f"BM={bm} is not a UMMA row tile (128 or 256)"
     if bn % 16 or not 16 <= bn <= 256:
         return None, f"BN={bn} is not a UMMA column tile (16..256, step 16)"
-    if (bm // 128 if bm == 256 else 1) * bn > 512:
-        return None, "accumulator exceeds TMEM"
     if not _bk_ok(bk):
         return None, f"BK={bk} is not a TMA/UMMA K stage (16, 32, 64k)"
-    stages = _fit_stages(int(vals.get("stages", 4)), bm, bn, bk)
+    # a 256-row tile with an even row vthread split runs on a CTA pair
+    # (cta_group::2): the pair's two SMs each hold 128 rows
+    cta_group = 2 if (bm == 256 and n[1] % 2 == 0) else 1
+    if (2 if (bm == 256 and cta_group == 1) else 1) * bn > 512:
+        return None, "accumulator exceeds TMEM"
+    stages = _fit_stages(int(vals.get("stages", 4)), bm, bn, bk, cta_group)
     if stages < 1:
         return None, "one stage does not fit in shared memory"
-    cluster = _largest_pow2_divisor(m[1], m[0])
-    return Knobs(bm, bn, bk, stages, split, cluster), ""
+    cluster = 1 if cta_group == 2 else _largest_pow2_divisor(m[1], m[0])
+    return Knobs(bm, bn, bk, stages, split, cluster, cta_group=cta_group), ""
 
 
 def _conv_knobs(spec: Conv2dSpec, vals: dict) -> tuple[Knobs | None, str]:

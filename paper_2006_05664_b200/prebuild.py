@@ -31,19 +31,23 @@ def family_instances(spec) -> set[tuple[int, bool, tuple]]:
             if spec.n % bm:
                 continue
             for bn in range(16, 257, 16):
-                if spec.m % bn or (bm // 128 if bm == 256 else 1) * bn > 512:
+                if spec.m % bn:
                     continue
                 grid_cols = spec.m // bn
                 clusters = {c for c in (1, 2, 4) if grid_cols % c == 0}
                 for bk in _divisors(spec.k):
                     if not _bk_ok(bk):
                         continue
-                    for st in STAGE_VALUES:
-                        s = _fit_stages(st, bm, bn, bk)
-                        if s < 1:
+                    for cg in ((1, 2) if bm == 256 else (1,)):
+                        if cg == 1 and bm == 256 and bn > 256:
                             continue
-                        for c in clusters:
-                            out.add((0, batched, Knobs(bm, bn, bk, s, 1, c).as_tuple()))
+                        for st in STAGE_VALUES:
+                            s = _fit_stages(st, bm, bn, bk, cg)
+                            if s < 1:
+                                continue
+                            for c in (clusters if cg == 1 else {1}):
+                                out.add((0, batched, Knobs(bm, bn, bk, s, 1, c,
+                                                           cta_group=cg).as_tuple()))
     elif isinstance(spec, Conv2dSpec):
         if spec.stride != 1:
             return out

@@ -70,6 +70,22 @@ GEMM_CASES = [
     (512, 1024, 1024, (128, 64, 64, 4, 1, 4)),
     (512, 1024, 1024, (256, 64, 64, 4, 2, 2)),
     (1024, 1024, 1024, (128, 128, 64, 4, 1, 1)),
+    # CTA pairs (cta_group::2): knobs ..., tile_h, tile_w, acc, cta_group
+    (512, 1024, 1024, (256, 128, 64, 4, 1, 1, 1, 1, 1, 2)),
+    (512, 1024, 1024, (256, 64, 128, 4, 1, 1, 1, 1, 1, 2)),
+    (512, 1024, 1024, (256, 256, 64, 4, 1, 1, 1, 1, 1, 2)),
+    (512, 1024, 1024, (256, 32, 64, 6, 2, 1, 1, 1, 1, 2)),
+    (1024, 1024, 1024, (256, 128, 128, 3, 2, 1, 1, 1, 2, 2)),
+    # persistent grid with a K-split last wave (stream-K style tail), and the
+    # one-CTA-per-tile grid (knob 10 = 1)
+    (2048, 2048, 512, (128, 64, 64, 4, 1, 1, 1, 1, 1, 1, 2)),
+    (2048, 4096, 256, (256, 128, 64, 4, 1, 1, 1, 1, 1, 2, 2)),
+    (2048, 4096, 256, (256, 128, 64, 4, 1, 1, 1, 1, 1, 2)),
+    (2048, 2048, 512, (128, 64, 64, 4, 1, 1, 1, 1, 1, 1, 1)),
+    (2048, 2048, 512, (256, 256, 64, 3, 1, 1, 1, 1, 1, 1, 0)),
+    # K-interleaved accumulators
+    (512, 1024, 1024, (128, 64, 128, 3, 1, 1, 1, 1, 4, 1)),
+    (512, 1024, 1024, (256, 64, 64, 3, 1, 1, 1, 1, 2, 1)),
 ]
 
 
@@ -91,11 +107,11 @@ def test_matmul_parity(dev, rows, cols, depth, knobs):
 
 
 @pytest.mark.parametrize("knobs", [(128, 64, 64, 2, 1, 1), (128, 64, 64, 2, 2, 1),
-                                   (128, 32, 64, 4, 1, 2)])
+                                   (128, 32, 64, 4, 1, 2), (256, 64, 64, 3, 1, 1, 1, 1, 1, 2)])
 def test_batchmatmul_parity(dev, knobs):
     from paper_2006_05664_b200 import capi
 
-    b, n, m, k = 12, 128, 64, 128     # BMM1 per-batch shape
+    b, n, m, k = 12, 256, 64, 128     # BMM1-like per-batch shape
     op = dev.prepare(capi.BATCHMATMUL, batch=b, rows=n, cols=m, depth=k, seed=77)
     try:
         t = dev.trial(op, knobs, warmup=1, reps=3)

@@ -38,6 +38,11 @@ def test_matmul_mapping_levels():
     m = config_to_knobs(spec, sp, cfg)
     assert m.valid
     assert m.knobs == Knobs(bm=128, bn=128, bk=64, stages=4, split=2, cluster=4)
+    # 256-row tile with an even row vthread split -> CTA pair
+    pair = config_to_knobs(spec, sp, ((4, 2, 16, 8), (8, 4, 4, 8), (1, 16, 64), 4)).knobs
+    assert pair.bm == 256 and pair.cta_group == 2 and pair.cluster == 1
+    single = config_to_knobs(spec, sp, ((4, 1, 32, 8), (8, 4, 4, 8), (1, 16, 64), 4)).knobs
+    assert single.bm == 256 and single.cta_group == 1
     # sub-tile splits do not change the kernel
     cfg2 = ((8, 128, 1, 1), (8, 1, 1, 128), (2, 8, 64), 4)
     assert config_to_knobs(spec, sp, cfg2).knobs == Knobs(128, 128, 64, 4, 2, 1)
@@ -88,6 +93,7 @@ def test_every_valid_mapping_is_prebuilt():
         spec = parse_operator(op)
         sp = gpu_operator_space(spec)
         fam = {(f, b, tuple(k[:4]) + tuple(k[5:])) for f, b, k in family_instances(spec)}
+        assert any(k[9] == 2 for _, _, k in family_instances(spec)) == op.startswith("matmul")
         rng = np.random.default_rng(0)
         hits = 0
         for _ in range(4000):
