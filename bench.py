@@ -353,15 +353,16 @@ def main() -> None:
 
 
 def _ncu_traffic(knobs) -> float | None:
-    """dram read+write bytes per launch from the committed ncu summary, if any."""
+    """DRAM read+write bytes per launch of this exact instance from the
+    committed ncu capture (profiles/ncu_summary.json), else None."""
     path = os.path.join(REPO, "profiles", "ncu_summary.json")
     try:
         with open(path) as fh:
             d = json.load(fh)
-        entry = d.get("kernels", {}).get(",".join(map(str, knobs)))
-        return entry.get("dram_bytes") if entry else d.get("best_dram_bytes")
     except (OSError, ValueError):
         return None
+    entry = d.get("kernels", {}).get(",".join(map(str, knobs)))
+    return entry.get("dram_bytes") if entry else None
 
 
 if __name__ == "__main__":
