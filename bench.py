@@ -216,9 +216,10 @@ def main() -> None:
         return float(t.item())
 
     def launches_of(extras) -> int:
-        # per verified trial: check launch + compare + warm-up + graph warm-up + timed graph
-        per = 1 + 1 + settings.warmup + 2 * settings.reps
-        return sum(per for e in extras if e.get("status") == "ok")
+        # tuned-kernel launches reported by the C ABI, plus one compare
+        # kernel per verified trial
+        return sum(int(e.get("launches", 0)) + (1 if e.get("status") in ("ok", "verify_failed")
+                                                else 0) for e in extras)
 
     budget = RHO * (args.steps + args.warmup)
     engine = OpEvo(space, EngineConfig(seed=args.seed, budget=budget, parents=RHO, offspring=RHO))
@@ -236,7 +237,7 @@ def main() -> None:
         extras = owner.last_extras
         for c, f, e in zip(asked.configs, fits, extras):
             recorder.record(c, f, e)
-        return len(asked.configs), launches_of(extras[rank::world] if world > 1 else extras)
+        return len(asked.configs), launches_of(extras)
 
     for _ in range(args.warmup):
         generation()
@@ -343,7 +344,7 @@ def main() -> None:
             "wallclock_to_95pct_s": wallclock_to_fraction(records) / 1e3,
             "valid_fraction": sum(r.fitness > 0 for r in records) / len(records),
             "trials_total": len(records), "wall_s_timed": wall,
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches * world,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)

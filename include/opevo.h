@@ -96,6 +96,7 @@ typedef struct opevo_trial_result {
     int32_t cache_hit;        /* 1: memory, 2: disk, 0: compiled          */
     int32_t grid_ctas;
     int32_t smem_bytes;
+    int32_t launches;         /* tuned-kernel launches this trial made    */
 } opevo_trial_result;
 
 typedef struct opevo_ctx opevo_ctx;

@@ -61,7 +61,7 @@ class OpDesc(C.Structure):
 class TrialResult(C.Structure):
     _fields_ = [("tflops", C.c_double), ("ms", C.c_double), ("rel_err", C.c_double),
                 ("compile_ms", C.c_double), ("load_ms", C.c_double), ("cache_hit", C.c_int32),
-                ("grid_ctas", C.c_int32), ("smem_bytes", C.c_int32)]
+                ("grid_ctas", C.c_int32), ("smem_bytes", C.c_int32), ("launches", C.c_int32)]
 
 
 class OpevoError(RuntimeError):
@@ -178,6 +178,7 @@ class Trial:
     grid_ctas: int
     smem_bytes: int
     message: str
+    launches: int = 0
 
     @property
     def ok(self) -> bool:
@@ -231,7 +232,7 @@ class Device:
                                   reps, int(flush_l2), tol, C.byref(res), err, len(err))
         return Trial(st, res.tflops, res.ms, res.rel_err, res.compile_ms, res.load_ms,
                      res.cache_hit, res.grid_ctas, res.smem_bytes,
-                     err.value.decode(errors="replace") if st != OK else "")
+                     err.value.decode(errors="replace") if st != OK else "", res.launches)
 
     def kernel(self, op: "Operand", knobs) -> "Kernel":
         h = C.c_void_p()

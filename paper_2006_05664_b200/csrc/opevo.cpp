@@ -464,6 +464,7 @@ struct opevo_kernel {
     int k_per_split = 0;
     ConvGeomHost geom{};
     SchedHost sched{};
+    int launches = 0;                   // launches of this instance (all paths)
     double flops = 0.0;
 };
 
@@ -602,6 +603,7 @@ int launch_kernel(opevo_kernel* kr, char* err, size_t errlen) {
     cfg.attrs = na ? attr : nullptr;
     cfg.numAttrs = na;
     CUresult r = g_cu.LaunchKernelEx(&cfg, kr->fn, args, nullptr);
+    ++kr->launches;
     if (r != CUDA_SUCCESS) {
         int st = fail_cu(ctx, r, "kernel launch", err, errlen);
         return st == OPEVO_ERR_STICKY ? st : OPEVO_LAUNCH_ERROR;
@@ -1108,6 +1110,28 @@ int opevo_kernel_time(opevo_kernel* k, int warmup, int reps, int flush_l2, doubl
     CUevent e0, e1;
     CU_TRY(ctx, g_cu.EventCreate(&e0, CU_EVENT_DEFAULT), "event");
     CU_TRY(ctx, g_cu.EventCreate(&e1, CU_EVENT_DEFAULT), "event");
+    // Device-time budget per measurement (OPEVO_TIME_BUDGET_MS, default 4):
+    // a one-launch estimate caps the repetitions of slow candidates at
+    // budget/estimate (min 3), so a 10 ms instance does not cost 40 launches;
+    // fast instances keep all `reps`.
+    {
+        double budget = 4.0;
+        if (const char* b = getenv("OPEVO_TIME_BUDGET_MS")) budget = atof(b);
+        float est = 0.f;
+        CUresult r = g_cu.EventRecord(e0, ctx->stream);
+        if (r == CUDA_SUCCESS && !(st = launch_kernel(k, err, errlen))) {
+            r = g_cu.EventRecord(e1, ctx->stream);
+            if (r == CUDA_SUCCESS) r = g_cu.EventSynchronize(e1);
+            if (r == CUDA_SUCCESS) r = g_cu.EventElapsedTime(&est, e0, e1);
+        }
+        if (st || r != CUDA_SUCCESS) {
+            g_cu.EventDestroy(e0);
+            g_cu.EventDestroy(e1);
+            return st ? st : fail_cu(ctx, r, "estimate launch", err, errlen);
+        }
+        if (budget > 0 && est > 0 && est * reps > budget)
+            reps = std::max(3, (int)(budget / est));
+    }
     double total = 0.0;
     if (!flush_l2) {
         // back-to-back launches captured in one graph: no host launch gaps
@@ -1184,6 +1208,7 @@ int opevo_trial(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nknobs, 
             res->tflops = ms > 0 ? k->flops / (ms * 1e-3) / 1e12 : 0.0;
         }
     }
+    res->launches = k->launches;
     opevo_kernel_release(k);
     return st;
 }

@@ -58,11 +58,13 @@ class TrialInfo:
     compile_ms: float = 0.0
     cache_hit: int = 0
     message: str = ""
+    launches: int = 0
     extra: dict = field(default_factory=dict)
 
     def as_extra(self, gpu: int) -> dict:
         d = {"status": self.status, "device_ms": self.ms, "compile_ms": self.compile_ms,
-             "rel_err": self.rel_err, "gpu_id": gpu, "cache_hit": self.cache_hit}
+             "rel_err": self.rel_err, "gpu_id": gpu, "cache_hit": self.cache_hit,
+             "launches": self.launches}
         if self.knobs is not None:
             d["knobs"] = list(self.knobs)
         if self.message:
@@ -164,12 +166,12 @@ class GpuEvaluator:
         if t.status != capi.OK:
             return TrialInfo(0.0, capi.STATUS_NAMES.get(t.status, str(t.status)), knobs,
                              rel_err=t.rel_err, compile_ms=t.compile_ms, cache_hit=t.cache_hit,
-                             message=t.message)
+                             message=t.message, launches=t.launches)
         fit = self.flops / (t.ms * 1e-3) / 1e12 if t.ms > 0 else 0.0
         if not math.isfinite(fit):
             fit = 0.0
         return TrialInfo(fit, "ok", knobs, ms=t.ms, rel_err=t.rel_err, compile_ms=t.compile_ms,
-                         cache_hit=t.cache_hit)
+                         cache_hit=t.cache_hit, launches=t.launches)
 
 
 def make_gpu_objective(spec: OperatorSpec, space: SearchSpace | None = None, device: int = 0,

@@ -31,7 +31,8 @@ from .evaluator import EvalSettings, GpuEvaluator, TrialInfo, WorkerFault
 from .spaces import SearchSpace
 
 # result row layout for the all-reduce
-_COLS = ("fitness", "device_ms", "compile_ms", "rel_err", "status", "cache_hit", "gpu_id", "present")
+_COLS = ("fitness", "device_ms", "compile_ms", "rel_err", "status", "cache_hit", "gpu_id", "present",
+         "launches")
 _STATUS = ("ok", "invalid_config", "compile_error", "launch_error", "verify_failed", "fault")
 
 
@@ -70,8 +71,8 @@ class ShardedEvaluator:
         rows = torch.zeros((len(configs), len(_COLS)), dtype=torch.float64)
         for i, info in zip(mine, infos):
             rows[i] = torch.tensor([info.fitness, info.ms, info.compile_ms, info.rel_err,
-                                    _status_code(info.status), info.cache_hit, self.rank, 1.0],
-                                   dtype=torch.float64)
+                                    _status_code(info.status), info.cache_hit, self.rank, 1.0,
+                                    info.launches], dtype=torch.float64)
         if self.device is not None:
             rows = rows.to(self.device)
         dist.all_reduce(rows, group=self.group)
@@ -84,7 +85,8 @@ class ShardedEvaluator:
             code = int(r[4])
             self.last_extras.append({"status": _STATUS[code] if code < len(_STATUS) else "error",
                                      "device_ms": r[1], "compile_ms": r[2], "rel_err": r[3],
-                                     "cache_hit": int(r[5]), "gpu_id": int(r[6])})
+                                     "cache_hit": int(r[5]), "gpu_id": int(r[6]),
+                                     "launches": int(r[8])})
             fits.append(r[0])
         return fits
 
