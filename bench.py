@@ -37,6 +37,9 @@ sys.path.insert(0, REPO)
 RHO = 8
 DEFAULT_OP = "matmul:1024,1024,1024"
 METRIC = "best-found TFLOP/s (% of tensor peak) vs trials; trials/sec at 1/2/4/8 B200"
+# CUDA-core fp32 FMA peak: 148 SMs x 128 lanes x 2 flop x 1.965 GHz (nominal
+# clock; no measured figure exists for this pipe)
+FP32_PEAK = 148 * 128 * 2 * 1.965e9 / 1e12
 
 
 def peaks() -> dict:
@@ -171,6 +174,8 @@ def main() -> None:
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--reps", type=int, default=20, help="timed launches per trial")
     ap.add_argument("--l2", default="warm", choices=("warm", "cold"))
+    ap.add_argument("--dtype", default="bf16", choices=("bf16", "f32"),
+                    help="f32: the SIMT family on the reference space (cfg1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--log", default="")
@@ -194,9 +199,12 @@ def main() -> None:
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2006_05664_b200 import capi
+
     spec = parse_operator(args.op)
-    space = gpu_operator_space(spec)
-    settings = EvalSettings(reps=args.reps, flush_l2=(args.l2 == "cold"))
+    space = gpu_operator_space(spec, args.dtype)
+    settings = EvalSettings(reps=args.reps, flush_l2=(args.l2 == "cold"),
+                            dtype=capi.F32 if args.dtype == "f32" else capi.BF16)
     local_ev = GpuEvaluator(spec, space, local, settings)
     if world > 1:
         evaluator = ShardedEvaluator(local_ev, rank, world, device=torch.device("cuda", local))
@@ -302,16 +310,19 @@ def main() -> None:
     best_knobs = None
     best_cold = None
     if best.fitness > 0:
-        mapped = config_to_knobs(spec, space, best.config)
+        mapped = config_to_knobs(spec, space, best.config, args.dtype)
         best_knobs = mapped.knobs.as_tuple()
         k = local_ev.dev.kernel(local_ev.op, best_knobs)
         ms = k.time(warmup=5, reps=100, flush_l2=False)
         best_cold = spec.flops() / (k.time(warmup=2, reps=20, flush_l2=True) * 1e-3) / 1e12
         k.close()
         ach = spec.flops() / (ms * 1e-3) / 1e12
-        roof = {"bound": "tensor", "achieved": ach, "peak": pk["tflops"], "unit": "TFLOP/s",
-                "frac": ach / pk["tflops"], "traffic": _ncu_traffic(best_knobs),
-                "peak_source": f"{pk['source']} burst bf16 (MEASURED_PEAKS.json)",
+        peak = pk["tflops"] if args.dtype == "bf16" else FP32_PEAK
+        roof = {"bound": "tensor" if args.dtype == "bf16" else "fp32-fma", "achieved": ach,
+                "peak": peak, "unit": "TFLOP/s",
+                "frac": ach / peak, "traffic": _ncu_traffic(best_knobs),
+                "peak_source": (f"{pk['source']} burst bf16 (MEASURED_PEAKS.json)" if args.dtype == "bf16"
+                                else "nominal fp32 FMA peak at 1965 MHz (no measured figure)"),
                 "kernel_ms": ms, "per_launch_flops": spec.flops()}
 
     if rank == 0:
@@ -325,19 +336,25 @@ def main() -> None:
             "metric": METRIC, "value": trials_per_s, "unit": "trials/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"OpEvo tuning of the sm_100a tcgen05 kernel family on "
-                                   f"{args.op} bf16 (BASELINE configs[1])",
+            "dtype": args.dtype, "data": "synthetic",
+            "config": {"workload": (f"OpEvo tuning of the sm_100a tcgen05 kernel family on {args.op} "
+                                    f"bf16" if args.dtype == "bf16" else
+                                    f"OpEvo tuning of the sm_100a fp32 SIMT family (paper TVM dense "
+                                    f"schedule) on {args.op} fp32")
+                                   + (" (BASELINE configs[1])" if args.op == DEFAULT_OP
+                                      and args.dtype == "bf16" else ""),
                        "operator": args.op, "rho": RHO, "lambda": RHO, "q": 0.5,
                        "seed": args.seed, "trials_timed": trials,
-                       "space": "reference matmul_space + stages (mapping.py)",
+                       "space": ("reference operator space (fp32 SIMT family)" if args.dtype == "f32"
+                                 else "reference operator space + stages (mapping.py)"),
                        "fitness_timing": f"{settings.reps} back-to-back launches in one CUDA "
                                          f"graph after {settings.warmup} warm-up, L2 "
                                          f"{args.l2} (operands fit in L2)",
                        "l2_between_steps": "inputs < L2; each step re-verifies every kernel "
                                            "(output poisoned, recomputed, compared)",
                        "parallelism": f"trial sharding x{world}"},
-            "best_tflops": best.fitness, "best_frac_of_peak": best.fitness / pk["tflops"],
+            "best_tflops": best.fitness,
+            "best_frac_of_peak": best.fitness / (pk["tflops"] if args.dtype == "bf16" else FP32_PEAK),
             "best_knobs": best_knobs, "best_config": space.config_to_json(best.config),
             "best_tflops_cold_l2": best_cold,
             "trials_to_95pct": trials_to_fraction(records),

@@ -2,9 +2,10 @@
 import sys
 
 
-def main(out, cubin_path, source_path):
+def main(out, cubin_path, source_path, simt_path):
     blob = open(cubin_path, "rb").read()
     src = open(source_path, "rb").read()
+    simt = open(simt_path, "rb").read()
     with open(out, "w") as fh:
         fh.write("#include <stddef.h>\n")
         fh.write('extern "C" {\n')
@@ -16,8 +17,12 @@ def main(out, cubin_path, source_path):
         fh.write("extern const char opevo_gemm_source[] = {\n")
         for i in range(0, len(src), 24):
             fh.write(",".join(str(b) for b in src[i:i + 24]) + ",\n")
+        fh.write("0};\n")
+        fh.write("extern const char opevo_sgemm_source[] = {\n")
+        for i in range(0, len(simt), 24):
+            fh.write(",".join(str(b) for b in simt[i:i + 24]) + ",\n")
         fh.write("0};\n}\n")
 
 
 if __name__ == "__main__":
-    main(*sys.argv[1:4])
+    main(*sys.argv[1:5])

@@ -33,6 +33,7 @@
 extern "C" const unsigned char opevo_util_cubin[];
 extern "C" const size_t opevo_util_cubin_len;
 extern "C" const char opevo_gemm_source[];
+extern "C" const char opevo_sgemm_source[];
 
 namespace {
 
@@ -234,9 +235,17 @@ bool want_pdl() {
 
 std::string make_key(int family, const Knobs& k, int batched, int out_f32) {
     static const uint64_t src_hash = fnv1a(opevo_gemm_source, strlen(opevo_gemm_source));
+    static const uint64_t simt_hash = fnv1a(opevo_sgemm_source, strlen(opevo_sgemm_source));
     const std::string extra = extra_flags();
-    const uint64_t h = fnv1a(extra.data(), extra.size(), src_hash);
+    const uint64_t h = fnv1a(extra.data(), extra.size(), family == 2 ? simt_hash : src_hash);
     char buf[256];
+    if (family == 2) {
+        // fp32 SIMT family: slots 0..7 hold (n2, n3, n4, m2, m3, m4, k2, k3)
+        snprintf(buf, sizeof buf, "f2_n%d.%d.%d_m%d.%d.%d_k%d.%d_b%d_%s%012llx", k.bm, k.bn, k.bk,
+                 k.stages, k.split, k.cluster, k.tile_h, k.tile_w, batched,
+                 want_lineinfo() ? "L" : "", (unsigned long long)(h & 0xffffffffffffull));
+        return buf;
+    }
     snprintf(buf, sizeof buf, "f%d_m%d_n%d_k%d_s%d_b%d_o%d_c%d_h%d_w%d_a%d_g%d_%s%012llx", family,
              k.bm, k.bn, k.bk, k.stages, batched, out_f32, k.cluster, family == 1 ? k.tile_h : 1,
              family == 1 ? k.tile_w : 1, k.acc, k.cg, want_lineinfo() ? "L" : "",
@@ -244,8 +253,45 @@ std::string make_key(int family, const Knobs& k, int batched, int out_f32) {
     return buf;
 }
 
+// fp32 SIMT family geometry from the knob slots (n2,n3,n4,m2,m3,m4,k2,k3).
+struct Simt {
+    int n2, n3, n4, m2, m3, m4, k2, k3;
+    int threads() const { return n3 * m3; }
+    int bm() const { return n2 * n3 * n4; }
+    int bn() const { return m2 * m3 * m4; }
+    int ks() const { return k2 * k3; }
+    size_t smem() const { return (size_t)ks() * (size_t)(bm() + bn() + 2) * 4; }
+};
+
+Simt simt_of(const Knobs& k) {
+    return Simt{k.bm, k.bn, k.bk, k.stages, k.split, k.cluster, k.tile_h, k.tile_w};
+}
+
 // Structural checks shared by compile and bind (operator-independent).
 bool knobs_compilable(int family, const Knobs& k, char* err, size_t len) {
+    if (family == 2) {
+        const Simt g = simt_of(k);
+        const int f[8] = {g.n2, g.n3, g.n4, g.m2, g.m3, g.m4, g.k2, g.k3};
+        for (int v : f)
+            if (v < 1) {
+                put_err(err, len, "SIMT factors must be >= 1");
+                return false;
+            }
+        if (g.threads() > 1024) {
+            put_err(err, len, "n3*m3 = %d threads per block exceeds 1024", g.threads());
+            return false;
+        }
+        if (g.n2 * g.n4 * g.m2 * g.m4 > 256) {
+            put_err(err, len, "per-thread tile %dx%d exceeds the register file",
+                    g.n2 * g.n4, g.m2 * g.m4);
+            return false;
+        }
+        if (g.k3 > 64 || g.smem() > 232448) {
+            put_err(err, len, "shared tile %zu B (k3=%d) too large", g.smem(), g.k3);
+            return false;
+        }
+        return true;
+    }
     if (!(k.bm == 128 || k.bm == 256)) {
         put_err(err, len, "BM=%d unsupported (128 or 256)", k.bm);
         return false;
@@ -342,11 +388,21 @@ int nvrtc_build(int family, const Knobs& k, int batched, int out_f32, std::vecto
         return OPEVO_ERR_NO_NVRTC;
     }
     nvrtcProgram prog;
-    if (g_rtc.Create(&prog, opevo_gemm_source, "gemm_sm100.cuh", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+    const bool simt = family == 2;
+    if (g_rtc.Create(&prog, simt ? opevo_sgemm_source : opevo_gemm_source,
+                     simt ? "sgemm_simt.cuh" : "gemm_sm100.cuh", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
         put_err(err, len, "nvrtcCreateProgram failed");
         return OPEVO_COMPILE_ERROR;
     }
-    std::vector<std::string> opts = {
+    std::vector<std::string> opts;
+    if (simt) {
+        const Simt g = simt_of(k);
+        opts = {"-arch=sm_100a", "-std=c++17", "-default-device",
+                "-DOPEVO_N2=" + std::to_string(g.n2), "-DOPEVO_N3=" + std::to_string(g.n3),
+                "-DOPEVO_N4=" + std::to_string(g.n4), "-DOPEVO_M2=" + std::to_string(g.m2),
+                "-DOPEVO_M3=" + std::to_string(g.m3), "-DOPEVO_M4=" + std::to_string(g.m4),
+                "-DOPEVO_K2=" + std::to_string(g.k2), "-DOPEVO_K3=" + std::to_string(g.k3)};
+    } else opts = {
         "-arch=sm_100a", "-std=c++17", "-default-device",
         "-DOPEVO_BM=" + std::to_string(k.bm), "-DOPEVO_BN=" + std::to_string(k.bn),
         "-DOPEVO_BK=" + std::to_string(k.bk), "-DOPEVO_STAGES=" + std::to_string(k.stages),
@@ -465,6 +521,7 @@ struct opevo_kernel {
     ConvGeomHost geom{};
     SchedHost sched{};
     int launches = 0;                   // launches of this instance (all paths)
+    unsigned block = 192;
     double flops = 0.0;
 };
 
@@ -567,6 +624,32 @@ int encode_map(CUtensorMap* map, CUdeviceptr base, int rank, const uint64_t* dim
 int launch_kernel(opevo_kernel* kr, char* err, size_t errlen) {
     opevo_op* op = kr->op;
     opevo_ctx* ctx = op->ctx;
+    if (kr->family == 2) {
+        int rows = (int)op->rows, cols = (int)op->cols, depth = (int)op->depth;
+        void* args[] = {&op->a, &op->b, &op->c, &rows, &cols, &depth};
+        CUlaunchConfig cfg{};
+        cfg.gridDimX = kr->grid[0];
+        cfg.gridDimY = kr->grid[1];
+        cfg.gridDimZ = kr->grid[2];
+        cfg.blockDimX = kr->block;
+        cfg.blockDimY = cfg.blockDimZ = 1;
+        cfg.sharedMemBytes = (unsigned)kr->smem;
+        cfg.hStream = ctx->stream;
+        CUlaunchAttribute attr[1];
+        if (want_pdl()) {
+            attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+            attr[0].value.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+        }
+        CUresult r = g_cu.LaunchKernelEx(&cfg, kr->fn, args, nullptr);
+        ++kr->launches;
+        if (r != CUDA_SUCCESS) {
+            int st = fail_cu(ctx, r, "kernel launch", err, errlen);
+            return st == OPEVO_ERR_STICKY ? st : OPEVO_LAUNCH_ERROR;
+        }
+        return OPEVO_OK;
+    }
     int rows = (int)op->rows;
     int cols = (int)op->cols;
     int depth = (int)op->depth;
@@ -617,6 +700,81 @@ int sync_checked(opevo_ctx* ctx, const char* what, char* err, size_t errlen) {
         int st = fail_cu(ctx, r, what, err, errlen);
         return st == OPEVO_ERR_STICKY ? st : OPEVO_LAUNCH_ERROR;
     }
+    return OPEVO_OK;
+}
+
+// Module for an instance: per-context memory cache -> disk cache -> NVRTC.
+int get_function(opevo_ctx* ctx, int family, const Knobs& k, int batched, int out_f32, const char* name,
+                 size_t smem, CUfunction* fn, double* compile_ms, int* hit, char* err, size_t errlen) {
+    const std::string key = make_key(family, k, batched, out_f32);
+    auto it = ctx->modules.find(key);
+    *compile_ms = 0.0;
+    *hit = 1;
+    if (it == ctx->modules.end()) {
+        std::vector<char> cubin;
+        int st = get_cubin(family, k, batched, out_f32, ctx->cache_dir, cubin, compile_ms, hit, err, errlen);
+        if (st) return st;
+        LoadedModule lm;
+        CUresult r = g_cu.ModuleLoadData(&lm.mod, cubin.data());
+        if (r == CUDA_SUCCESS) r = g_cu.ModuleGetFunction(&lm.fn, lm.mod, name);
+        if (r != CUDA_SUCCESS) {
+            st = fail_cu(ctx, r, "load module", err, errlen);
+            return st == OPEVO_ERR_STICKY ? st : OPEVO_LAUNCH_ERROR;
+        }
+        it = ctx->modules.emplace(key, lm).first;
+    }
+    LoadedModule& lm = it->second;
+    if (lm.smem_set < (int)smem) {
+        CUresult r = g_cu.FuncSetAttribute(lm.fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
+        if (r != CUDA_SUCCESS) {
+            put_err(err, errlen, "set smem %zu: %s", smem, cu_str(r));
+            return OPEVO_INVALID_CONFIG;
+        }
+        lm.smem_set = (int)smem;
+    }
+    *fn = lm.fn;
+    return OPEVO_OK;
+}
+
+// fp32 SIMT family (paper TVM dense schedule): plain pointers, 3-D grid.
+int simt_kernel_get(opevo_ctx* ctx, opevo_op* op, const Knobs& k, opevo_kernel** out,
+                    opevo_trial_result* info, double t0, char* err, size_t errlen) {
+    const Simt g = simt_of(k);
+    if (op->rows % g.bm() || op->cols % g.bn() || op->depth % g.ks()) {
+        put_err(err, errlen, "SIMT tile %dx%d (k chunk %d) does not divide %lldx%lldx%lld", g.bm(), g.bn(),
+                g.ks(), (long long)op->rows, (long long)op->cols, (long long)op->depth);
+        return OPEVO_INVALID_CONFIG;
+    }
+    if ((int)g.smem() > ctx->smem_optin) {
+        put_err(err, errlen, "shared memory %zu B exceeds the device limit", g.smem());
+        return OPEVO_INVALID_CONFIG;
+    }
+    opevo_kernel* kr = new opevo_kernel();
+    kr->op = op;
+    kr->k = k;
+    kr->family = 2;
+    kr->smem = g.smem();
+    kr->block = (unsigned)g.threads();
+    kr->grid[0] = (unsigned)(op->cols / g.bn());
+    kr->grid[1] = (unsigned)(op->rows / g.bm());
+    kr->grid[2] = (unsigned)op->batch;
+    kr->flops = 2.0 * (double)op->batch * (double)op->rows * (double)op->cols * (double)op->depth;
+    double compile_ms = 0.0;
+    int hit = 1;
+    int st = get_function(ctx, 2, k, op->d.kind == OPEVO_BATCHMATMUL, 1, "opevo_sgemm", kr->smem, &kr->fn,
+                          &compile_ms, &hit, err, errlen);
+    if (st) {
+        delete kr;
+        return st;
+    }
+    if (info) {
+        info->compile_ms = compile_ms;
+        info->cache_hit = hit;
+        info->load_ms = now_ms() - t0 - compile_ms;
+        info->grid_ctas = (int32_t)(kr->grid[0] * kr->grid[1] * kr->grid[2]);
+        info->smem_bytes = (int32_t)kr->smem;
+    }
+    *out = kr;
     return OPEVO_OK;
 }
 
@@ -894,13 +1052,11 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
     g_cu.CtxSetCurrent(ctx->cu);
     const double t0 = now_ms();
     Knobs k = read_knobs(knobs, nknobs);
-    const int family = op->d.kind == OPEVO_CONV2D ? 1 : 0;
+    // fp32 operands are served by the SIMT family (the tcgen05 family is bf16)
+    const int family = op->d.kind == OPEVO_CONV2D ? 1 : (op->in_f32 ? 2 : 0);
     const int batched = op->d.kind == OPEVO_BATCHMATMUL ? 1 : 0;
-    if (op->in_f32) {
-        put_err(err, errlen, "fp32 operands are not served by the tcgen05 bf16 family");
-        return OPEVO_INVALID_CONFIG;
-    }
     if (!knobs_compilable(family, k, err, errlen)) return OPEVO_INVALID_CONFIG;
+    if (family == 2) return simt_kernel_get(ctx, op, k, out, info, t0, err, errlen);
     if ((int)smem_bytes(k) > ctx->smem_optin) {
         put_err(err, errlen, "shared memory %zu B exceeds the device limit %d", smem_bytes(k), ctx->smem_optin);
         return OPEVO_INVALID_CONFIG;
@@ -971,39 +1127,20 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
         delete kr;
         return st;
     }
-    // module: memory cache -> disk cache -> NVRTC
-    const std::string key = make_key(family, k, batched, op->out_f32);
-    auto it = ctx->modules.find(key);
-    double compile_ms = 0.0;
-    int hit = 1;
-    if (it == ctx->modules.end()) {
-        std::vector<char> cubin;
-        st = get_cubin(family, k, batched, op->out_f32, ctx->cache_dir, cubin, &compile_ms, &hit, err, errlen);
+    {
+        double compile_ms_ = 0.0;
+        int hit_ = 1;
+        st = get_function(ctx, family, k, batched, op->out_f32, "opevo_gemm", kr->smem, &kr->fn, &compile_ms_,
+                          &hit_, err, errlen);
         if (st) {
             delete kr;
             return st;
         }
-        LoadedModule lm;
-        CUresult r = g_cu.ModuleLoadData(&lm.mod, cubin.data());
-        if (r == CUDA_SUCCESS) r = g_cu.ModuleGetFunction(&lm.fn, lm.mod, "opevo_gemm");
-        if (r != CUDA_SUCCESS) {
-            delete kr;
-            st = fail_cu(ctx, r, "load module", err, errlen);
-            return st == OPEVO_ERR_STICKY ? st : OPEVO_LAUNCH_ERROR;
+        if (info) {
+            info->compile_ms = compile_ms_;
+            info->cache_hit = hit_;
         }
-        it = ctx->modules.emplace(key, lm).first;
     }
-    LoadedModule& lm = it->second;
-    if (lm.smem_set < (int)kr->smem) {
-        CUresult r = g_cu.FuncSetAttribute(lm.fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)kr->smem);
-        if (r != CUDA_SUCCESS) {
-            put_err(err, errlen, "set smem %zu: %s", kr->smem, cu_str(r));
-            delete kr;
-            return OPEVO_INVALID_CONFIG;
-        }
-        lm.smem_set = (int)kr->smem;
-    }
-    kr->fn = lm.fn;
     // grid: one cluster per unit, or (grid_mode 0) at most what is resident at
     // once, in which case CTAs loop over units (persistent schedule)
     {
@@ -1043,9 +1180,7 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
         }
     }
     if (info) {
-        info->compile_ms = compile_ms;
-        info->cache_hit = hit;
-        info->load_ms = now_ms() - t0 - compile_ms;
+        info->load_ms = now_ms() - t0 - info->compile_ms;
         info->grid_ctas = (int32_t)(kr->grid[0] * kr->grid[1] * kr->grid[2]);
         info->smem_bytes = (int32_t)kr->smem;
     }

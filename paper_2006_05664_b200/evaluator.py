@@ -91,9 +91,10 @@ class GpuEvaluator:
     def __init__(self, spec: OperatorSpec, space: SearchSpace | None = None, device: int = 0,
                  settings: EvalSettings | None = None):
         self.spec = spec
-        self.space = space if space is not None else gpu_operator_space(spec)
-        self.device_index = device
         self.settings = settings or EvalSettings()
+        self.dtype = "f32" if self.settings.dtype == capi.F32 else "bf16"
+        self.space = space if space is not None else gpu_operator_space(spec, self.dtype)
+        self.device_index = device
         self.tol = F32_TOL if self.settings.dtype == capi.F32 else BF16_TOL
         try:
             self.dev = capi.Device(device, self.settings.cache_dir)
@@ -144,7 +145,7 @@ class GpuEvaluator:
         list(self._pool.map(build, family_batched.values()))
 
     def evaluate_infos(self, configs: list[tuple]) -> list[TrialInfo]:
-        mapped = [config_to_knobs(self.spec, self.space, c) for c in configs]
+        mapped = [config_to_knobs(self.spec, self.space, c, self.dtype) for c in configs]
         self.precompile(mapped)
         out = []
         for m in mapped:

@@ -58,6 +58,7 @@ UNROLL_TO_STAGES = {0: 2, 16: 3, 64: 4, 512: 6, 1500: 8}
 
 FAMILY_GEMM = 0
 FAMILY_CONV = 1
+FAMILY_SIMT = 2            # fp32 MatMul: the paper's TVM dense schedule on CUDA cores
 
 
 @dataclass(frozen=True)
@@ -126,10 +127,15 @@ def _largest_pow2_divisor(*vals: int, cap: int = 4) -> int:
     return c
 
 
-def gpu_operator_space(spec: OperatorSpec) -> SearchSpace:
+def gpu_operator_space(spec: OperatorSpec, dtype: str = "bf16") -> SearchSpace:
     """The reference space of ``spec`` plus the B200-only knob(s), declared in
     the reference's JSON space format (so the reference engine can replay a
-    B200 trajectory)."""
+    B200 trajectory).  fp32 MatMul uses the reference space unchanged: every
+    factor is a knob of the SIMT family."""
+    if dtype == "f32":
+        if not isinstance(spec, (MatMulSpec, BatchMatMulSpec)):
+            raise TypeError("fp32 is served for MatMul / BatchMatMul only")
+        return matmul_space(spec) if isinstance(spec, MatMulSpec) else batchmatmul_space(spec)
     if isinstance(spec, MatMulSpec):
         base = matmul_space(spec)
     elif isinstance(spec, BatchMatMulSpec):
@@ -188,9 +194,29 @@ def _conv_knobs(spec: Conv2dSpec, vals: dict) -> tuple[Knobs | None, str]:
     return Knobs(bm, bn, bk, stages, split, 1, th, tw), ""
 
 
-def config_to_knobs(spec: OperatorSpec, space: SearchSpace, config: tuple) -> Mapped:
+def _simt_knobs(vals: dict) -> tuple[Knobs | None, str]:
+    """fp32 SIMT family: the paper's levels map one to one (knob slots 0..7 =
+    n2, n3, n4, m2, m3, m4, k2, k3; n1, m1 follow from the shape, k1 = K/(k2 k3))."""
+    n, m, k = vals["n"], vals["m"], vals["k"]
+    threads = n[2] * m[2]
+    if threads > 1024:
+        return None, f"n3*m3 = {threads} threads per block exceeds 1024"
+    if n[1] * n[3] * m[1] * m[3] > 256:
+        return None, "per-thread tile exceeds the register file"
+    ks = k[1] * k[2]
+    smem = ks * (n[1] * n[2] * n[3] + m[1] * m[2] * m[3] + 2) * 4
+    if k[2] > 64 or smem > SMEM_LIMIT:
+        return None, f"shared tile {smem} B (k3={k[2]}) too large"
+    return Knobs(n[1], n[2], n[3], m[1], m[2], m[3], k[1], k[2]), ""
+
+
+def config_to_knobs(spec: OperatorSpec, space: SearchSpace, config: tuple,
+                    dtype: str = "bf16") -> Mapped:
     """Map one configuration of ``space`` to kernel knobs (or an invalid reason)."""
     vals = dict(zip(space.names, config))
+    if dtype == "f32":
+        kn, why = _simt_knobs(vals)
+        return Mapped(kn, why, FAMILY_SIMT, isinstance(spec, BatchMatMulSpec))
     if isinstance(spec, MatMulSpec):
         kn, why = _gemm_knobs(spec.n, spec.m, spec.k, vals)
         return Mapped(kn, why, FAMILY_GEMM, False)
@@ -204,11 +230,11 @@ def config_to_knobs(spec: OperatorSpec, space: SearchSpace, config: tuple) -> Ma
 
 
 def valid_fraction(spec: OperatorSpec, space: SearchSpace, samples: int = 20000,
-                   seed: int = 0) -> float:
+                   seed: int = 0, dtype: str = "bf16") -> float:
     """Monte-Carlo fraction of uniformly drawn configurations that map."""
     import numpy as np
 
     rng = np.random.default_rng(seed)
-    ok = sum(config_to_knobs(spec, space, space.sample_uniform(rng)).valid
+    ok = sum(config_to_knobs(spec, space, space.sample_uniform(rng), dtype).valid
              for _ in range(samples))
     return ok / samples

@@ -146,6 +146,51 @@ def test_conv2d_parity(dev, knobs):
         op.close()
 
 
+F32_TOL = 1e-4   # north star: fp32 within 1e-4 relative
+
+
+@pytest.mark.parametrize("knobs", [
+    # SIMT family: (n2, n3, n4, m2, m3, m4, k2, k3) -- the paper's dense schedule
+    (1, 16, 4, 1, 16, 4, 4, 4),
+    (2, 8, 4, 2, 16, 2, 8, 2),
+    (1, 32, 1, 1, 32, 1, 16, 1),
+    (4, 8, 2, 1, 8, 8, 2, 8),
+    (1, 4, 8, 2, 32, 4, 1, 16),
+])
+def test_fp32_simt_matmul_parity(dev, knobs):
+    """cfg1 shape MM1 (512 x 1024 x 1024, fp32)."""
+    import oracle
+    from paper_2006_05664_b200 import capi
+
+    rows, cols, depth = 512, 1024, 1024
+    op = dev.prepare(capi.MATMUL, dtype=capi.F32, rows=rows, cols=cols, depth=depth, seed=31)
+    try:
+        t = dev.trial(op, knobs, warmup=1, reps=3, tol=F32_TOL)
+        assert t.ok, t.message
+        a = oracle.operand(rows * depth, 31, bf16=False)
+        b = oracle.operand(cols * depth, 32, bf16=False)
+        ref = oracle.gemm(a, b, 1, rows, cols, depth)
+        assert _rel(op.output(), ref) < F32_TOL
+    finally:
+        op.close()
+
+
+def test_fp32_simt_batched(dev):
+    import oracle
+    from paper_2006_05664_b200 import capi
+
+    b_, n, m, k = 6, 128, 64, 128
+    op = dev.prepare(capi.BATCHMATMUL, dtype=capi.F32, batch=b_, rows=n, cols=m, depth=k, seed=41)
+    try:
+        t = dev.trial(op, (1, 16, 4, 1, 16, 4, 4, 4), warmup=1, reps=3, tol=F32_TOL)
+        assert t.ok, t.message
+        ref = oracle.gemm(oracle.operand(b_ * n * k, 41, bf16=False),
+                          oracle.operand(b_ * m * k, 42, bf16=False), b_, n, m, k)
+        assert _rel(op.output(), ref) < F32_TOL
+    finally:
+        op.close()
+
+
 def test_invalid_knobs_score_invalid(dev):
     from paper_2006_05664_b200 import capi
 
