@@ -1,0 +1,129 @@
+"""Command line: tune one operator on a B200, or compare optimisers.
+
+    python -m paper_2006_05664_b200 tune --operator matmul:1024,1024,1024 --algo opevo \\
+        --budget 500 --seed 0 --out out/
+    python -m paper_2006_05664_b200 compare --operator matmul:1024,1024,1024 \\
+        --algo opevo,random,sa,gbfs --seeds 0,1,2 --budget 300 --out out/
+
+Mirrors the reference CLI's ``tune`` / ``bench`` subcommands
+(``pkg/src/topotune/cli.py:164-233``): same trial-log schema and
+summary/curve CSVs, with ``--evaluator gpu`` (default) measuring TFLOP/s on
+the device and ``--evaluator synthetic`` using the reference's CPU model.
+Exit codes: 0 ok, 2 usage error, 3 evaluator unavailable.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+from . import (
+    EngineConfig,
+    FatalEvaluationError,
+    make_objective,
+    parse_operator,
+    run,
+)
+from .baselines import GbfsConfig, SaConfig, greedy_bfs, random_search, simulated_annealing
+from .logs import write_trial_log
+from .reporting import curve_rows, summarize, summary_row_dict, tuning_report, write_curves_csv, \
+    write_summary_csv
+
+ALGORITHMS = ("opevo", "random", "sa", "gbfs")
+
+
+def _objective(args):
+    spec = parse_operator(args.operator)
+    if args.evaluator == "synthetic":
+        return make_objective(spec)
+    from . import capi
+    from .evaluator import EvalSettings, GpuEvaluator
+
+    ev = GpuEvaluator(spec, None, args.device,
+                      EvalSettings(reps=args.reps, dtype=capi.F32 if args.dtype == "f32" else capi.BF16))
+    return ev.space, ev
+
+
+def _run(algo, space, objective, seed, budget):
+    if algo == "opevo":
+        evaluator = getattr(objective, "evaluate", None)
+        return run(space, EngineConfig(seed=seed, budget=budget), objective, evaluator=evaluator)
+    if algo == "random":
+        return random_search(space, budget, seed, objective)
+    if algo == "sa":
+        return simulated_annealing(space, SaConfig(), budget, seed, objective)
+    if algo == "gbfs":
+        return greedy_bfs(space, GbfsConfig(), budget, seed, objective)
+    raise ValueError(f"unknown algorithm {algo!r}")
+
+
+def cmd_tune(args) -> int:
+    space, objective = _objective(args)
+    t0 = time.perf_counter()
+    best, recs = _run(args.algo, space, objective, args.seed, args.budget)
+    wall = time.perf_counter() - t0
+    os.makedirs(args.out, exist_ok=True)
+    path = os.path.join(args.out, f"trials_{args.algo}_seed{args.seed}.jsonl")
+    write_trial_log(path, recs)
+    rep = tuning_report(recs, wall, 1639.1)
+    print(json.dumps({"operator": args.operator, "algorithm": args.algo, "seed": args.seed,
+                      "best_fitness": best.fitness, "best_config": space.config_to_json(best.config),
+                      "log": path, **rep}))
+    return 0
+
+
+def cmd_compare(args) -> int:
+    space, objective = _objective(args)
+    algos = [a for a in args.algo.split(",") if a]
+    seeds = [int(s) for s in args.seeds.split(",") if s]
+    rows, curves = [], []
+    os.makedirs(args.out, exist_ok=True)
+    for algo in algos:
+        logs = []
+        for seed in seeds:
+            _, recs = _run(algo, space, objective, seed, args.budget)
+            write_trial_log(os.path.join(args.out, f"trials_{algo}_seed{seed}.jsonl"), recs)
+            logs.append(recs)
+        row = summarize(algo, args.operator, logs)
+        rows.append(summary_row_dict(row))
+        curves += curve_rows(algo, logs, args.budget)
+        print(json.dumps(summary_row_dict(row)), flush=True)
+    write_summary_csv(os.path.join(args.out, "summary.csv"), rows)
+    write_curves_csv(os.path.join(args.out, "curves.csv"), curves)
+    return 0
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(prog="paper_2006_05664_b200")
+    sub = ap.add_subparsers(dest="cmd", required=True)
+    for name in ("tune", "compare"):
+        p = sub.add_parser(name)
+        p.add_argument("--operator", required=True)
+        p.add_argument("--evaluator", default="gpu", choices=("gpu", "synthetic"))
+        p.add_argument("--dtype", default="bf16", choices=("bf16", "f32"))
+        p.add_argument("--device", type=int, default=0)
+        p.add_argument("--reps", type=int, default=20)
+        p.add_argument("--budget", type=int, default=500)
+        p.add_argument("--out", default="out")
+        if name == "tune":
+            p.add_argument("--algo", default="opevo", choices=ALGORITHMS)
+            p.add_argument("--seed", type=int, default=int(os.environ.get("TOPO_TUNE_SEED", 0)))
+        else:
+            p.add_argument("--algo", default=",".join(ALGORITHMS))
+            p.add_argument("--seeds", default="0,1,2")
+    args = ap.parse_args(argv)
+    try:
+        return cmd_tune(args) if args.cmd == "tune" else cmd_compare(args)
+    except FatalEvaluationError as err:
+        print(f"evaluator unavailable: {err}", file=sys.stderr)
+        return 3
+    except ValueError as err:
+        print(f"usage error: {err}", file=sys.stderr)
+        return 2
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -105,6 +105,21 @@ def main() -> None:
     with open(os.path.join(HERE, "replay_hash_objective.json"), "w") as fh:
         json.dump(replay, fh, separators=(",", ":"))
 
+    # baselines (ref baselines.py) on MM1 and the desk conv, synthetic objective
+    base = {"numpy": np.__version__, "runs": {}}
+    for op in ("matmul:512,1024,1024", "conv2d:1,4,8,8,8,3,3,1,1"):
+        spec = tt.parse_operator(op)
+        space, obj = tt.make_objective(spec)
+        for seed in SEEDS:
+            for name, fn in (("random", lambda: tt.random_search(space, 300, seed, obj)),
+                             ("sa", lambda: tt.simulated_annealing(space, tt.SaConfig(), 300, seed, obj)),
+                             ("gbfs", lambda: tt.greedy_bfs(space, tt.GbfsConfig(), 300, seed, obj))):
+                best, recs = fn()
+                base["runs"][f"{op}|{name}|{seed}"] = {"hash": traj_hash(recs), "trials": len(recs),
+                                                        "best": best.fitness}
+    with open(os.path.join(HERE, "baselines.json"), "w") as fh:
+        json.dump(base, fh, indent=1)
+
     # known answers: unrank, neighbours, sizes, walk laws
     ka: dict = {"factorization": [], "permutation": [], "walk": []}
     for prod, arity in [(8, 3), (1024, 4), (1024, 3), (960, 2), (56, 4), (720, 3), (64, 4)]:
