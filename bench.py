@@ -258,6 +258,7 @@ def main() -> None:
         e0.record()
         t_wall0 = time.perf_counter()
         for _ in range(args.steps):
+            local_ev.dev.flush_l2()     # every step starts with a cold L2
             n, nl = generation()
             trials += n
             launches += nl
@@ -290,6 +291,7 @@ def main() -> None:
         f0.record()
         e2e_trials = 0
         for _ in range(e2e_steps):
+            local_ev.dev.flush_l2()
             n, _ = generation(upload)
             e2e_trials += n
         barrier()
@@ -350,8 +352,10 @@ def main() -> None:
                        "fitness_timing": f"{settings.reps} back-to-back launches in one CUDA "
                                          f"graph after {settings.warmup} warm-up, L2 "
                                          f"{args.l2} (operands fit in L2)",
-                       "l2_between_steps": "inputs < L2; each step re-verifies every kernel "
-                                           "(output poisoned, recomputed, compared)",
+                       "l2_between_steps": "flushed: a 256 MB write (2x L2) before every timed "
+                                           "step; within a trial the fitness is L2-warm "
+                                           "back-to-back launches (use --l2 cold to flush "
+                                           "before every timed launch)",
                        "parallelism": f"trial sharding x{world}"},
             "best_tflops": best.fitness,
             "best_frac_of_peak": best.fitness / (pk["tflops"] if args.dtype == "bf16" else FP32_PEAK),

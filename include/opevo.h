@@ -156,6 +156,10 @@ int opevo_trial(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nknobs, 
  * copies 16 uint64 per CTA (smid, %globaltimer phase stamps) to `host`. */
 int opevo_kernel_trace(opevo_kernel* k, uint64_t* host, size_t count, char* err, size_t errlen);
 
+/* Write a 256 MB buffer (2x L2) on the context's stream so the next work
+ * starts with a cold L2; returns after the flush completes. */
+int opevo_ctx_flush_l2(opevo_ctx* ctx, char* err, size_t errlen);
+
 /* Pinned host memory for honest end-to-end copies. */
 void* opevo_host_alloc(size_t bytes);
 void opevo_host_free(void* p);

@@ -48,7 +48,7 @@ EXPORTS = (
     "opevo_op_reference",
     "opevo_op_refresh_reference", "opevo_kernel_get", "opevo_kernel_release",
     "opevo_kernel_run", "opevo_kernel_check", "opevo_kernel_time", "opevo_trial",
-    "opevo_kernel_trace", "opevo_host_alloc", "opevo_host_free",
+    "opevo_kernel_trace", "opevo_ctx_flush_l2", "opevo_host_alloc", "opevo_host_free",
 )
 
 
@@ -115,6 +115,7 @@ def load() -> C.CDLL:
         "opevo_kernel_time": (I, [P, I, I, I, dp, cp, sz]),
         "opevo_trial": (I, [P, P, i32p, I, I, I, I, D, C.POINTER(TrialResult), cp, sz]),
         "opevo_kernel_trace": (I, [P, C.POINTER(C.c_uint64), sz, cp, sz]),
+        "opevo_ctx_flush_l2": (I, [P, cp, sz]),
         "opevo_host_alloc": (P, [sz]),
         "opevo_host_free": (None, [P]),
     }
@@ -211,6 +212,11 @@ class Device:
 
     def __exit__(self, *exc):
         self.close()
+
+    def flush_l2(self) -> None:
+        """Evict L2 (write 2x its size) and wait."""
+        err = _errbuf()
+        _check(self.lib.opevo_ctx_flush_l2(self.handle, err, len(err)), err)
 
     def prepare(self, kind: int, dtype: int = BF16, batch: int = 1, rows: int = 0, cols: int = 0,
                 depth: int = 0, conv=None, seed: int = 1234) -> "Operand":

@@ -20,6 +20,13 @@
 //                 CTA stages 128 rows of A and BN/2 rows of B, so per-SM
 //                 operand traffic (TMA ingress and smem reads) drops versus a
 //                 single-CTA 256-row tile.  Only the leader CTA issues MMAs.
+//   OPEVO_SPLIT_CLUSTER S: split-K whose S slices of one tile run as one
+//                 thread-block cluster.  After the mainloop each CTA stages
+//                 its fp32 partial in shared memory and bulk-copies the row
+//                 block owned by each peer into that peer's shared memory
+//                 (cp.async.bulk shared::cluster, DSMEM); every CTA then sums
+//                 its own row block in z order and writes it.  No partials
+//                 touch global memory.
 //   OPEVO_ACC     independent TMEM accumulators the K loop round-robins over
 //                 (summed in the epilogue).  Consecutive MMAs into one
 //                 accumulator form a dependent chain; for small N the chain
@@ -80,6 +87,9 @@
 #endif
 #ifndef OPEVO_CTA_GROUP
 #define OPEVO_CTA_GROUP 1  // 2: CTA-pair MMA (cta_group::2, M=256 across two SMs)
+#endif
+#ifndef OPEVO_SPLIT_CLUSTER
+#define OPEVO_SPLIT_CLUSTER 0  // S > 1: the S K-slices of a tile form a cluster and reduce via DSMEM
 #endif
 #ifndef OPEVO_ACC
 #define OPEVO_ACC 1        // K-interleaved TMEM accumulators (1, 2, 4)
@@ -157,7 +167,21 @@ constexpr u64 DESC_HI = ((u64)1 << 16)                          // LBO (unused f
 constexpr int NBUF = (2 * TMEM_USED <= 512) ? 2 : 1;
 constexpr int TMEM_ALLOC = (NBUF * TMEM_USED <= 32) ? 32 : (NBUF * TMEM_USED <= 64) ? 64 :
                            (NBUF * TMEM_USED <= 128) ? 128 : (NBUF * TMEM_USED <= 256) ? 256 : 512;
-constexpr int CLSZ = CLUSTER * CG;     // CTAs per cluster (launch cluster dim x)
+constexpr int SPLITCL = OPEVO_SPLIT_CLUSTER;   // DSMEM split-K cluster size (0: off)
+constexpr int CLSZ = CLUSTER * CG * (SPLITCL > 1 ? SPLITCL : 1);   // CTAs per cluster (launch dim x)
+// DSMEM reduction buffers (reusing the pipeline smem after the mainloop):
+// OWN [BM][RED_LD] fp32, then RECV [SPLITCL-1][BM/SPLITCL][RED_LD] fp32.  Rows
+// are padded by 16 B: each epilogue thread stages its own row, and an
+// unpadded 512 B row stride would put all 32 lanes on the same banks.
+constexpr int RED_LD = BN + 4;
+constexpr int RED_ROWS = (SPLITCL > 1) ? BM / SPLITCL : BM;
+constexpr int RED_OWN_BYTES = BM * RED_LD * 4;
+constexpr int RED_BLOCK_BYTES = RED_ROWS * RED_LD * 4;
+constexpr int RED_BYTES = (SPLITCL > 1) ? RED_OWN_BYTES + (SPLITCL - 1) * RED_BLOCK_BYTES : 0;
+constexpr int PIPE_BYTES = (STAGES * STAGE_BYTES > RED_BYTES) ? STAGES * STAGE_BYTES : RED_BYTES;
+static_assert(SPLITCL == 0 || ((SPLITCL == 2 || SPLITCL == 4 || SPLITCL == 8) && CG == 1 && CLUSTER == 1 &&
+                           MATOMS == 1 && BM % (SPLITCL * 8) == 0),
+              "DSMEM split-K: S in {2,4,8}, single-CTA 128-row tiles");
 
 struct __align__(64) TmaDesc { u64 raw[16]; };
 
@@ -400,6 +424,16 @@ __device__ __forceinline__ void st_v4(void* p, u32 a, u32 b, u32 c, u32 d) {
                  : "memory");
 }
 
+__device__ __forceinline__ u32 atom_add_release_gpu(u32* p, u32 v) {
+    u32 old;
+    asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
+__device__ __forceinline__ void fence_acq_rel_gpu() {
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+
 __device__ __forceinline__ float4 ld_cg_f4(const float* p) {
     float4 r;
     asm volatile("ld.global.cg.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -442,7 +476,7 @@ __device__ __forceinline__ void store_row(void* c_out, u64 off, const float* acc
 
 using namespace opevo;
 
-extern "C" __global__ void __launch_bounds__(NUM_THREADS, 1)
+extern "C" __global__ void __launch_bounds__(NUM_THREADS, 2)   // 2: keep <= 168 regs so two CTAs can co-reside
 opevo_gemm(const __grid_constant__ TmaDesc tma_a,
            const __grid_constant__ TmaDesc tma_b,
            void* __restrict__ c_out,
@@ -455,20 +489,25 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<u64>(smem_raw) + SMEM_ALIGN - 1) & ~(u64)(SMEM_ALIGN - 1));
-    u64* full_bar = reinterpret_cast<u64*>(smem + STAGES * STAGE_BYTES);
+    u64* full_bar = reinterpret_cast<u64*>(smem + PIPE_BYTES);
     u64* empty_bar = full_bar + STAGES;
     u64* tfull_bar = empty_bar + STAGES;      // MMA -> epilogue, per TMEM buffer
     u64* tempty_bar = tfull_bar + NBUF;       // epilogue -> MMA, per TMEM buffer
-    u32* tmem_slot = reinterpret_cast<u32*>(tempty_bar + NBUF);
+    u64* red_bar = tempty_bar + NBUF;         // DSMEM split-K: peers' partial rows landed
+    u32* tmem_slot = reinterpret_cast<u32*>(red_bar + 1);
     u32* last_flag = tmem_slot + 1;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const u32 crank = (CLSZ > 1) ? cluster_rank() : 0u;
     const u32 prank = (CG == 2) ? crank : 0u;                 // rank in the CTA pair
-    const u32 mrank = (CG == 2) ? 0u : crank;                 // rank in a multicast cluster
+    const u32 mrank = (CLUSTER > 1) ? crank : 0u;            // rank in a multicast cluster
     const int cl_id = (int)(blockIdx.x / CLSZ);
     const int cl_count = (int)(gridDim.x / CLSZ);
+    // work items: one per cluster at a time; a DSMEM split-K cluster's CTAs
+    // each own one K slice (unit) of the same tile
+    const int u_first = (SPLITCL > 1) ? (int)blockIdx.x : cl_id;
+    const int u_step = (SPLITCL > 1) ? (int)gridDim.x : cl_count;
     const int head_items = sched.head_tiles * sched.split;
 #if OPEVO_TRACE
     u64* trace = reinterpret_cast<u64*>(ws) + 16ull * blockIdx.x;
@@ -522,7 +561,14 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
             // the peer's TMEM, so it waits for both CTAs' epilogues
             mbar_init(smem_u32(tempty_bar + b), 4 * CG);
         }
+        if (SPLITCL > 1) {
+            // one phase per launch: expect the (SPLITCL-1) row blocks the peers push
+            mbar_init(smem_u32(red_bar), 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (SPLITCL > 1)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                         :: "r"(smem_u32(red_bar)), "r"((u32)((SPLITCL - 1) * RED_BLOCK_BYTES)) : "memory");
     }
     if (warp == 1) {
         if (CG == 2) {
@@ -550,7 +596,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
         bool first = true;
         pdl_wait();                     // operands may be the previous launch's output
         if (lane == 0) TRACE(9);
-        for (int u = cl_id; u < sched.units; u += cl_count) {
+        for (int u = u_first; u < sched.units; u += u_step) {
             const Unit t = decode(u);
             const int k0 = t.k0;
             const int num_kb = t.num_kb;
@@ -638,7 +684,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
             int s = 0, buf = 0;
             u32 ph = 0, bph = 0;
             bool first = true;
-            for (int u = cl_id; u < sched.units; u += cl_count) {
+            for (int u = u_first; u < sched.units; u += u_step) {
                 const int num_kb = decode(u).num_kb;
                 // the epilogue must have drained this accumulator buffer
                 mbar_wait(smem_u32(tempty_bar + buf), bph ^ 1);
@@ -704,7 +750,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
         int buf = 0;
         u32 bph = 0;
         bool first = true;
-        for (int u = cl_id; u < sched.units; u += cl_count) {
+        for (int u = u_first; u < sched.units; u += u_step) {
             const Unit t = decode(u);
             const int col0 = t.col_tile * BN;
 #if OPEVO_CONV
@@ -755,7 +801,32 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                     }
                 }
                 if (first && epi_tid == 0) TRACE(7);
-            } else {
+            } else if (SPLITCL > 1) {
+                // ---- DSMEM split-K: this CTA is slice kz == cluster rank
+                float* own = reinterpret_cast<float*>(smem);
+                // 1. TMEM -> own partial in shared memory (row-major [BM][BN])
+#pragma unroll 1
+                for (int c = 0; c < BN; c += EPI_COLS) {
+                    float acc[EPI_COLS];
+                    const int lr = quarter * 32 + lane;
+                    gather_acc(lane_addr + c, acc);
+                    float* dst = own + lr * RED_LD + c;
+#pragma unroll
+                    for (int j = 0; j < EPI_COLS; j += 4)
+                        *reinterpret_cast<float4*>(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+                }
+                release();
+                // generic-proxy smem writes -> visible to the bulk-copy (async) proxy
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                epi_bar();
+            }
+            if (SPLITCL > 1) {
+                // steps 2-4 (DSMEM exchange + reduction) run after the role
+                // loops with every thread of the CTA, see below
+            } else if (split > 1) {
+                // split-K: publish this slice's fp32 partial, count arrivals; the
+                // last CTA of the tile sums all slices in z order (its own from
+                // TMEM, the rest from L2) and writes the output
 #pragma unroll 1
                 for (int ma = 0; ma < MATOMS; ++ma) {
                     const int r = out_row(ma * 128 + quarter * 32 + lane);
@@ -763,7 +834,6 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                     for (int c = 0; c < BN; c += EPI_COLS) {
                         float acc[EPI_COLS];
                         gather_acc(lane_addr + ma * BN + c, acc);
-                        if (ma == MATOMS - 1 && c + EPI_COLS >= BN) release();
                         float* dst = ws + (u64)t.kz * slice + c_batch + (u64)r * cols + col0 + c;
 #pragma unroll
                         for (int j = 0; j < EPI_COLS; j += 4)
@@ -771,16 +841,18 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                                   __float_as_uint(acc[j + 2]), __float_as_uint(acc[j + 3]));
                     }
                 }
-                __threadfence();
-                epi_bar();
+                epi_bar();                  // all partial stores issued (CTA scope)
                 if (epi_tid == 0) {
                     const u32 tile = (u32)((((t.batch * sched.row_tiles + t.row_tile) * sched.col_groups
                                             + t.col_tile / CLUSTER) * CLSZ) + crank);
-                    const u32 prev = atomicAdd(counters + tile, 1u);
+                    // release: cumulative over the CTA's partial stores ordered by the barrier
+                    const u32 prev = atom_add_release_gpu(counters + tile, 1u);
                     const u32 last = (prev == (u32)(split - 1)) ? 1u : 0u;
-                    if (last) counters[tile] = 0u;     // ready for the next launch
+                    if (last) {
+                        fence_acq_rel_gpu();            // acquire the other slices' partials
+                        counters[tile] = 0u;            // ready for the next launch
+                    }
                     *last_flag = last;
-                    __threadfence();
                 }
                 epi_bar();
                 if (*last_flag) {
@@ -789,22 +861,53 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                         const int r = out_row(ma * 128 + quarter * 32 + lane);
 #pragma unroll 1
                         for (int c = 0; c < BN; c += EPI_COLS) {
-                            float acc[EPI_COLS];
+                            float own[EPI_COLS], acc[EPI_COLS];
+                            gather_acc(lane_addr + ma * BN + c, own);
 #pragma unroll
                             for (int j = 0; j < EPI_COLS; ++j) acc[j] = 0.0f;
                             const u64 base = c_batch + (u64)r * cols + col0 + c;
-                            for (int z = 0; z < split; ++z) {
-                                const float* src = ws + (u64)z * slice + base;
+                            // two slices in flight per step; summation order is z = 0..split-1
+                            for (int z = 0; z < split; z += 2) {
+                                float4 p0[EPI_COLS / 4], p1[EPI_COLS / 4];
+                                const bool use1 = z + 1 < split;
+                                if (z != t.kz) {
+                                    const float* src = ws + (u64)z * slice + base;
 #pragma unroll
-                                for (int j = 0; j < EPI_COLS; j += 4) {
-                                    const float4 p = ld_cg_f4(src + j);
-                                    acc[j] += p.x; acc[j + 1] += p.y; acc[j + 2] += p.z; acc[j + 3] += p.w;
+                                    for (int j = 0; j < EPI_COLS / 4; ++j) p0[j] = ld_cg_f4(src + 4 * j);
+                                }
+                                if (use1 && z + 1 != t.kz) {
+                                    const float* src = ws + (u64)(z + 1) * slice + base;
+#pragma unroll
+                                    for (int j = 0; j < EPI_COLS / 4; ++j) p1[j] = ld_cg_f4(src + 4 * j);
+                                }
+#pragma unroll
+                                for (int j = 0; j < EPI_COLS / 4; ++j) {
+                                    if (z == t.kz) {
+                                        acc[4 * j] += own[4 * j]; acc[4 * j + 1] += own[4 * j + 1];
+                                        acc[4 * j + 2] += own[4 * j + 2]; acc[4 * j + 3] += own[4 * j + 3];
+                                    } else {
+                                        acc[4 * j] += p0[j].x; acc[4 * j + 1] += p0[j].y;
+                                        acc[4 * j + 2] += p0[j].z; acc[4 * j + 3] += p0[j].w;
+                                    }
+                                }
+                                if (use1) {
+#pragma unroll
+                                    for (int j = 0; j < EPI_COLS / 4; ++j) {
+                                        if (z + 1 == t.kz) {
+                                            acc[4 * j] += own[4 * j]; acc[4 * j + 1] += own[4 * j + 1];
+                                            acc[4 * j + 2] += own[4 * j + 2]; acc[4 * j + 3] += own[4 * j + 3];
+                                        } else {
+                                            acc[4 * j] += p1[j].x; acc[4 * j + 1] += p1[j].y;
+                                            acc[4 * j + 2] += p1[j].z; acc[4 * j + 3] += p1[j].w;
+                                        }
+                                    }
                                 }
                             }
                             store_row(c_out, base, acc);
                         }
                     }
                 }
+                release();                  // TMEM buffer (kept for the own-slice read)
                 epi_bar();                  // last_flag is reused by the next unit
             }
             first = false;
@@ -814,6 +917,79 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
 
     tc_fence_before();
     __syncthreads();
+#if OPEVO_SPLIT_CLUSTER > 1
+    {
+        // ---- DSMEM split-K reduction (one unit per cluster; slice kz == rank)
+        // 2. every slice has staged its partial and finished its mainloop
+        cluster_sync();
+        const float* own = reinterpret_cast<const float*>(smem);
+        if (threadIdx.x == 0) {
+            // push the row block each peer owns into that peer's RECV slot
+            for (int z = 0; z < SPLITCL; ++z) {
+                if (z == (int)crank) continue;
+                const int slot = (int)crank < z ? (int)crank : (int)crank - 1;
+                const u32 dst = mapa_cta(smem_u32(smem + RED_OWN_BYTES + slot * RED_BLOCK_BYTES), (u32)z);
+                const u32 bar = mapa_cta(smem_u32(red_bar), (u32)z);
+                asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes "
+                             "[%0], [%1], %2, [%3];"
+                             :: "r"(dst), "r"(smem_u32(own + z * RED_ROWS * RED_LD)),
+                                "r"((u32)RED_BLOCK_BYTES), "r"(bar) : "memory");
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        // 3. the peers' blocks of my rows have landed: sum in z order, write
+        mbar_wait(smem_u32(red_bar), 0);
+        const Unit t = decode(u_first);
+        const int col0 = t.col_tile * BN;
+        const u64 c_batch = (u64)t.batch * (u64)rows * (u64)cols;
+#if OPEVO_CONV
+        const int w_tiles = geom.wo / TILE_W, h_tiles = geom.ho / TILE_H;
+        const int w0 = (t.row_tile % w_tiles) * TILE_W;
+        const int h0 = ((t.row_tile / w_tiles) % h_tiles) * TILE_H;
+        const int n0 = (t.row_tile / (w_tiles * h_tiles)) * TILE_N;
+#endif
+        const float* recv = reinterpret_cast<const float*>(smem + RED_OWN_BYTES);
+        const int my_row0 = (int)crank * RED_ROWS;
+        constexpr int SEGS = BN / 8;                     // 8 outputs per thread-step
+#pragma unroll 1
+        for (int e = threadIdx.x; e < RED_ROWS * SEGS; e += NUM_THREADS) {
+            const int rr = e / SEGS, c8 = (e - rr * SEGS) * 8;
+            float acc[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
+            for (int z = 0; z < SPLITCL; ++z) {
+                const float* src = (z == (int)crank)
+                    ? own + (my_row0 + rr) * RED_LD + c8
+                    : recv + ((z < (int)crank ? z : z - 1) * RED_ROWS + rr) * RED_LD + c8;
+                const float4 x = *reinterpret_cast<const float4*>(src);
+                const float4 y = *reinterpret_cast<const float4*>(src + 4);
+                acc[0] += x.x; acc[1] += x.y; acc[2] += x.z; acc[3] += x.w;
+                acc[4] += y.x; acc[5] += y.y; acc[6] += y.z; acc[7] += y.w;
+            }
+            const int lr = my_row0 + rr;
+#if OPEVO_CONV
+            const int r = (n0 + lr / (TILE_H * TILE_W)) * geom.ho * geom.wo +
+                          (h0 + (lr / TILE_W) % TILE_H) * geom.wo + (w0 + lr % TILE_W);
+#else
+            const int r = t.row_tile * BM + lr;
+#endif
+#if OPEVO_OUT_F32
+            float* dst = reinterpret_cast<float*>(c_out) + c_batch + (u64)r * cols + col0 + c8;
+            st_v4(dst, __float_as_uint(acc[0]), __float_as_uint(acc[1]),
+                  __float_as_uint(acc[2]), __float_as_uint(acc[3]));
+            st_v4(dst + 4, __float_as_uint(acc[4]), __float_as_uint(acc[5]),
+                  __float_as_uint(acc[6]), __float_as_uint(acc[7]));
+#else
+            u16* dst = reinterpret_cast<u16*>(c_out) + c_batch + (u64)r * cols + col0 + c8;
+            st_v4(dst, pack_bf16(acc[0], acc[1]), pack_bf16(acc[2], acc[3]),
+                  pack_bf16(acc[4], acc[5]), pack_bf16(acc[6], acc[7]));
+#endif
+        }
+        // 4. my outgoing copies have finished reading `own`
+        if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncthreads();
+    }
+#endif
     if (threadIdx.x == 0) TRACE(8);
     if (CLSZ > 1) cluster_sync();
     if (warp == 1) {

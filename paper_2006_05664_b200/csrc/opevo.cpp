@@ -201,11 +201,25 @@ int tmem_alloc_cols(const Knobs& k) {
 
 int swizzle_bytes(int bk) { return bk * 2 >= 128 ? 128 : bk * 2; }
 
+// DSMEM split-K (the split slices of a tile form a cluster and reduce in
+// shared memory) when the shape allows it; split is then compiled in.
+size_t dsmem_red_bytes(const Knobs& k) {
+    const int s = k.split, ld = k.bn + 4;   // rows padded by 16 B (bank conflicts)
+    return (size_t)k.bm * ld * 4 + (size_t)(s - 1) * (k.bm / s) * ld * 4;
+}
+
+bool dsmem_split(const Knobs& k, int family) {
+    return family != 2 && (k.split == 2 || k.split == 4 || k.split == 8) && k.cg == 1 &&
+           k.cluster == 1 && k.bm == 128 && dsmem_red_bytes(k) + 1024 + 256 <= 232448;
+}
+
 // per-CTA: a CTA pair stages 128 rows of A and BN/2 rows of B each
-size_t smem_bytes(const Knobs& k) {
+size_t smem_bytes(const Knobs& k, int family = 0) {
     const int a_rows = k.cg == 2 ? 128 : k.bm;
     const int b_rows = k.bn / (k.cg == 2 ? 2 : 1);
-    return (size_t)k.stages * (size_t)(a_rows + b_rows) * (size_t)k.bk * 2 + 1024 + 256;
+    size_t pipe = (size_t)k.stages * (size_t)(a_rows + b_rows) * (size_t)k.bk * 2;
+    if (dsmem_split(k, family)) pipe = std::max(pipe, dsmem_red_bytes(k));
+    return pipe + 1024 + 256;
 }
 
 uint64_t fnv1a(const char* s, size_t n, uint64_t h = 1469598103934665603ull) {
@@ -248,7 +262,8 @@ std::string make_key(int family, const Knobs& k, int batched, int out_f32) {
     }
     snprintf(buf, sizeof buf, "f%d_m%d_n%d_k%d_s%d_b%d_o%d_c%d_h%d_w%d_a%d_g%d_%s%012llx", family,
              k.bm, k.bn, k.bk, k.stages, batched, out_f32, k.cluster, family == 1 ? k.tile_h : 1,
-             family == 1 ? k.tile_w : 1, k.acc, k.cg, want_lineinfo() ? "L" : "",
+             family == 1 ? k.tile_w : 1, k.acc, k.cg * 100 + (dsmem_split(k, family) ? k.split : 0),
+             want_lineinfo() ? "L" : "",
              (unsigned long long)(h & 0xffffffffffffull));
     return buf;
 }
@@ -327,8 +342,8 @@ bool knobs_compilable(int family, const Knobs& k, char* err, size_t len) {
         put_err(err, len, "cluster=%d unsupported for BM=%d", k.cluster, k.bm);
         return false;
     }
-    if (smem_bytes(k) > 232448) {
-        put_err(err, len, "shared memory %zu B exceeds 227 KB", smem_bytes(k));
+    if (smem_bytes(k, family) > 232448) {
+        put_err(err, len, "shared memory %zu B exceeds 227 KB", smem_bytes(k, family));
         return false;
     }
     if (family == 1) {
@@ -411,7 +426,8 @@ int nvrtc_build(int family, const Knobs& k, int batched, int out_f32, std::vecto
         "-DOPEVO_TILE_H=" + std::to_string(family == 1 ? k.tile_h : 1),
         "-DOPEVO_TILE_W=" + std::to_string(family == 1 ? k.tile_w : 1),
         "-DOPEVO_ACC=" + std::to_string(k.acc),
-        "-DOPEVO_CTA_GROUP=" + std::to_string(k.cg)};
+        "-DOPEVO_CTA_GROUP=" + std::to_string(k.cg),
+        "-DOPEVO_SPLIT_CLUSTER=" + std::to_string(dsmem_split(k, family) ? k.split : 0)};
     if (want_lineinfo()) opts.push_back("-lineinfo");
     {
         std::istringstream extra(extra_flags());
@@ -668,9 +684,10 @@ int launch_kernel(opevo_kernel* kr, char* err, size_t errlen) {
     cfg.hStream = ctx->stream;
     CUlaunchAttribute attr[2];
     unsigned na = 0;
-    if (kr->k.cluster > 1 || kr->k.cg == 2) {
+    const unsigned clx = (unsigned)(kr->k.cluster * kr->k.cg * (dsmem_split(kr->k, kr->family) ? kr->k.split : 1));
+    if (clx > 1) {
         attr[na].id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
-        attr[na].value.clusterDim.x = (unsigned)(kr->k.cluster * kr->k.cg);
+        attr[na].value.clusterDim.x = clx;
         attr[na].value.clusterDim.y = 1;
         attr[na].value.clusterDim.z = 1;
         ++na;
@@ -1057,8 +1074,9 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
     const int batched = op->d.kind == OPEVO_BATCHMATMUL ? 1 : 0;
     if (!knobs_compilable(family, k, err, errlen)) return OPEVO_INVALID_CONFIG;
     if (family == 2) return simt_kernel_get(ctx, op, k, out, info, t0, err, errlen);
-    if ((int)smem_bytes(k) > ctx->smem_optin) {
-        put_err(err, errlen, "shared memory %zu B exceeds the device limit %d", smem_bytes(k), ctx->smem_optin);
+    if ((int)smem_bytes(k, family) > ctx->smem_optin) {
+        put_err(err, errlen, "shared memory %zu B exceeds the device limit %d", smem_bytes(k, family),
+                ctx->smem_optin);
         return OPEVO_INVALID_CONFIG;
     }
     // operator-dependent feasibility (divisibility: no tail handling by design)
@@ -1081,7 +1099,7 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
     kr->k = k;
     kr->family = family;
     kr->k_per_split = (int)(op->depth / k.split);
-    kr->smem = smem_bytes(k);
+    kr->smem = smem_bytes(k, family);
     kr->flops = 2.0 * (double)op->batch * (double)op->rows * (double)op->cols * (double)op->depth;
     int st = OPEVO_OK;
     const int swz = swizzle_bytes(k.bk);
@@ -1122,7 +1140,8 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
         kr->sched = SchedHost{(int)row_tiles, (int)(col_tiles / k.cluster), (int)op->batch, k.split,
                               0, 1, 0};
     }
-    const int clsz = k.cluster * k.cg;
+    const bool dsm = dsmem_split(k, family);
+    const int clsz = k.cluster * k.cg * (dsm ? k.split : 1);
     if (st) {
         delete kr;
         return st;
@@ -1166,11 +1185,13 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
             }
         }
         sc.units = sc.head_tiles * sc.split + (tiles - sc.head_tiles) * sc.split * sc.tail_split;
-        const int clusters = k.grid_mode == 1 ? sc.units : std::min(sc.units, capacity);
+        // DSMEM split-K clusters each own exactly one unit (no persistence)
+        const int clusters = (k.grid_mode == 1 || dsm) ? sc.units / (dsm ? k.split : 1)
+                                                      : std::min(sc.units, capacity);
         kr->grid[0] = (unsigned)(clusters * clsz);
         kr->grid[1] = kr->grid[2] = 1;
         const int max_split = sc.split * sc.tail_split;
-        if (max_split > 1) {
+        if (max_split > 1 && !dsm) {
             const size_t slice = (size_t)op->batch * op->rows * op->cols * 4;
             st = ensure_ws(op, slice * max_split, (size_t)tiles * clsz * 4, err, errlen);
             if (st) {
@@ -1346,6 +1367,21 @@ int opevo_trial(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nknobs, 
     res->launches = k->launches;
     opevo_kernel_release(k);
     return st;
+}
+
+int opevo_ctx_flush_l2(opevo_ctx* ctx, char* err, size_t errlen) {
+    if (!ctx) return OPEVO_ERR_ARG;
+    g_cu.CtxSetCurrent(ctx->cu);
+    if (!ctx->flush_buf) {
+        ctx->flush_bytes = (size_t)256 << 20;
+        CU_TRY(ctx, g_cu.MemAlloc(&ctx->flush_buf, ctx->flush_bytes), "alloc flush buffer");
+    }
+    uint64_t n16 = ctx->flush_bytes / 16;
+    unsigned salt = 0x5eed;
+    void* fa[] = {&ctx->flush_buf, &n16, &salt};
+    int st = launch_simple(ctx, ctx->k_flush, (unsigned)ctx->sm_count * 4, 512, fa, err, errlen);
+    if (st) return st;
+    return sync_checked(ctx, "flush", err, errlen);
 }
 
 int opevo_kernel_trace(opevo_kernel* k, uint64_t* host, size_t count, char* err, size_t errlen) {

@@ -80,10 +80,21 @@ class Knobs:
         return (self.bm, self.bn, self.bk, self.stages, self.split, self.cluster,
                 self.tile_h, self.tile_w, self.acc, self.cta_group)
 
+    def dsmem_split(self) -> int:
+        """Split factor compiled in when the K slices reduce through DSMEM
+        (mirrors ``dsmem_split`` in csrc/opevo.cpp), else 0."""
+        s = self.split
+        ld = self.bn + 4
+        red = self.bm * ld * 4 + (s - 1) * (self.bm // max(s, 1)) * ld * 4
+        ok = (s in (2, 4, 8) and self.cta_group == 1 and self.cluster == 1 and self.bm == 128
+              and red + SMEM_EXTRA <= SMEM_LIMIT)
+        return s if ok else 0
+
     def compile_key(self) -> tuple[int, ...]:
-        """Fields that change the generated code (split-K is a launch arg)."""
+        """Fields that change the generated code (split-K is a launch arg
+        except for DSMEM-reduced splits)."""
         return (self.bm, self.bn, self.bk, self.stages, self.cluster, self.tile_h, self.tile_w,
-                self.acc, self.cta_group)
+                self.acc, self.cta_group, self.dsmem_split())
 
     def smem_bytes(self) -> int:
         return stage_bytes(self.bm, self.bn, self.bk, self.cta_group) * self.stages + SMEM_EXTRA

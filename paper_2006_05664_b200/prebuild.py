@@ -48,6 +48,12 @@ def family_instances(spec) -> set[tuple[int, bool, tuple]]:
                             for c in (clusters if cg == 1 else {1}):
                                 out.add((0, batched, Knobs(bm, bn, bk, s, 1, c,
                                                            cta_group=cg).as_tuple()))
+                            # DSMEM split-K instances compile the split in
+                            if cg == 1 and bm == 128:
+                                for sp in (2, 4, 8):
+                                    kn = Knobs(bm, bn, bk, s, sp, 1)
+                                    if kn.dsmem_split() and spec.k % (sp * bk) == 0:
+                                        out.add((0, batched, kn.as_tuple()))
     elif isinstance(spec, Conv2dSpec):
         if spec.stride != 1:
             return out

@@ -45,11 +45,14 @@ def test_nvrtc_compiles_instances_without_gpu(tmp_path):
     assert len(files) == 4 and all(f.endswith(".cubin") for f in files)
 
 
-def test_split_is_not_part_of_the_compile_key():
+def test_split_is_a_launch_argument_unless_reduced_in_dsmem():
     k1 = capi.kernel_key(0, (128, 64, 64, 4, 1, 1), False, False)
-    k2 = capi.kernel_key(0, (128, 64, 64, 4, 8, 1), False, False)
+    k16 = capi.kernel_key(0, (128, 64, 64, 4, 16, 1), False, False)   # global reduction
     k3 = capi.kernel_key(0, (128, 64, 64, 5, 1, 1), False, False)
-    assert k1 == k2 != k3
+    assert k1 == k16 != k3
+    k2 = capi.kernel_key(0, (128, 64, 64, 4, 2, 1), False, False)     # DSMEM cluster of 2
+    k8 = capi.kernel_key(0, (128, 64, 64, 4, 8, 1), False, False)
+    assert len({k1, k2, k8}) == 3
 
 
 @pytest.mark.parametrize("knobs", [(64, 64, 64, 4), (96, 64, 64, 4), (128, 8, 64, 4),

@@ -83,6 +83,13 @@ GEMM_CASES = [
     (2048, 4096, 256, (256, 128, 64, 4, 1, 1, 1, 1, 1, 2)),
     (2048, 2048, 512, (128, 64, 64, 4, 1, 1, 1, 1, 1, 1, 1)),
     (2048, 2048, 512, (256, 256, 64, 3, 1, 1, 1, 1, 1, 1, 0)),
+    # DSMEM split-K (the K slices of a tile form a cluster, reduce in smem)
+    (512, 1024, 1024, (128, 128, 64, 4, 2)),
+    (512, 1024, 1024, (128, 64, 128, 3, 4)),
+    (512, 1024, 1024, (128, 32, 64, 4, 8)),
+    (512, 960, 1024, (128, 48, 64, 4, 2)),
+    # split 16 falls back to the global-memory reduction
+    (512, 1024, 1024, (128, 64, 64, 2, 16)),
     # K-interleaved accumulators
     (512, 1024, 1024, (128, 64, 128, 3, 1, 1, 1, 1, 4, 1)),
     (512, 1024, 1024, (256, 64, 64, 3, 1, 1, 1, 1, 2, 1)),
@@ -106,7 +113,7 @@ def test_matmul_parity(dev, rows, cols, depth, knobs):
         op.close()
 
 
-@pytest.mark.parametrize("knobs", [(128, 64, 64, 2, 1, 1), (128, 64, 64, 2, 2, 1),
+@pytest.mark.parametrize("knobs", [(128, 64, 64, 2, 1, 1), (128, 64, 64, 2, 2, 1), (128, 64, 32, 4, 4, 1),
                                    (128, 32, 64, 4, 1, 2), (256, 64, 64, 3, 1, 1, 1, 1, 1, 2)])
 def test_batchmatmul_parity(dev, knobs):
     from paper_2006_05664_b200 import capi
