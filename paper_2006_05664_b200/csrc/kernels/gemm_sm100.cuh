@@ -95,7 +95,8 @@
 #define OPEVO_ACC 1        // K-interleaved TMEM accumulators (1, 2, 4)
 #endif
 #ifndef OPEVO_ABLATE
-#define OPEVO_ABLATE 0     // debug: 1 exit at entry, 2 no mainloop, 3 no TMA, 4 no MMA
+#define OPEVO_ABLATE 0     // debug: 1 exit at entry, 2 no mainloop, 3 no TMA, 4 no MMA,
+                           // 5 trap (fault injection: poisons the context)
 #endif
 #ifndef OPEVO_TRACE
 #define OPEVO_TRACE 0      // 1: per-CTA %globaltimer phase stamps into `ws` (debug)
@@ -515,6 +516,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
 #endif
     if (threadIdx.x == 0) pdl_launch_dependents();
     if (OPEVO_ABLATE == 1) return;
+    if (OPEVO_ABLATE == 5) asm volatile("trap;");
     (void)mrank;
     (void)geom;
 
