@@ -142,18 +142,31 @@ void opevo_kernel_release(opevo_kernel* k);
 int opevo_kernel_run(opevo_kernel* k, char* err, size_t errlen);
 /* Output vs reference; *rel_err = max|C-R|/max|R| (inf if non-finite). */
 int opevo_kernel_check(opevo_kernel* k, double tol, double* rel_err, char* err, size_t errlen);
-/* flush_l2 = 0: `reps` back-to-back launches in one CUDA graph (L2 warm);
- * flush_l2 = 1: an L2-sized write before every launch, each launch timed. */
+/* flush_l2 = 0: `reps` back-to-back launches in one CUDA graph (PDL edges,
+ *               L2 warm; captured while the warm-up runs) -- the fitness;
+ * flush_l2 = 1: an L2-sized write before every launch, each launch timed;
+ * flush_l2 = 2: `reps` back-to-back stream launches released together from a
+ *               device-side gate (no graph, no host gaps). */
 int opevo_kernel_time(opevo_kernel* k, int warmup, int reps, int flush_l2, double* ms_per_launch,
                       char* err, size_t errlen);
 
-/* One complete trial: get + check (tol) + time.  Fitness in res->tflops. */
+/* One complete trial: get + check (tol) + time, with one host synchronisation
+ * before the timed launches.  Fitness in res->tflops. */
 int opevo_trial(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nknobs, int warmup,
                 int reps, int flush_l2, double tol, opevo_trial_result* res, char* err,
                 size_t errlen);
 
-/* Debug: one launch of an instance compiled with OPEVO_EXTRA_FLAGS=-DOPEVO_TRACE=1;
- * copies 16 uint64 per CTA (smid, %globaltimer phase stamps) to `host`. */
+/* Compile-or-read and load the module of one instance into the context's
+ * module cache (no launch).  Thread-safe with respect to other preloads and
+ * to the trial thread, so a host pool can stage the next batch's modules.
+ * Status as for opevo_kernel_get's structural checks. */
+int opevo_op_preload(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nknobs,
+                     double* compile_ms, int* cache_hit, char* err, size_t errlen);
+
+/* Debug: launches of an instance compiled with OPEVO_EXTRA_FLAGS=-DOPEVO_TRACE=1;
+ * copies 16 uint64 per CTA (smid, %globaltimer phase stamps) to `host`.  When
+ * `count` holds L > 1 launches' worth (L <= 8), L launches run back to back
+ * (as in timing) and launch i's stamps follow launch i-1's. */
 int opevo_kernel_trace(opevo_kernel* k, uint64_t* host, size_t count, char* err, size_t errlen);
 
 /* Write a 256 MB buffer (2x L2) on the context's stream so the next work

@@ -49,6 +49,7 @@ EXPORTS = (
     "opevo_op_refresh_reference", "opevo_kernel_get", "opevo_kernel_release",
     "opevo_kernel_run", "opevo_kernel_check", "opevo_kernel_time", "opevo_trial",
     "opevo_kernel_trace", "opevo_ctx_flush_l2", "opevo_host_alloc", "opevo_host_free",
+    "opevo_op_preload",
 )
 
 
@@ -118,6 +119,7 @@ def load() -> C.CDLL:
         "opevo_ctx_flush_l2": (I, [P, cp, sz]),
         "opevo_host_alloc": (P, [sz]),
         "opevo_host_free": (None, [P]),
+        "opevo_op_preload": (I, [P, P, i32p, I, dp, C.POINTER(I), cp, sz]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -240,6 +242,15 @@ class Device:
                      res.cache_hit, res.grid_ctas, res.smem_bytes,
                      err.value.decode(errors="replace") if st != OK else "", res.launches)
 
+    def preload(self, op: "Operand", knobs) -> tuple[int, float, int, str]:
+        """Compile-or-read and load one instance's module (thread-safe; no
+        launch).  Returns (status, compile_ms, cache_hit, message)."""
+        cms, hit = C.c_double(), C.c_int()
+        err = _errbuf()
+        st = self.lib.opevo_op_preload(self.handle, op.handle, _knob_array(knobs), NUM_KNOBS,
+                                       C.byref(cms), C.byref(hit), err, len(err))
+        return st, cms.value, hit.value, err.value.decode(errors="replace") if st != OK else ""
+
     def kernel(self, op: "Operand", knobs) -> "Kernel":
         h = C.c_void_p()
         info = TrialResult()
@@ -323,15 +334,17 @@ class Kernel:
         _check(self.dev.lib.opevo_kernel_check(self.handle, tol, C.byref(rel), err, len(err)), err)
         return rel.value
 
-    def trace(self, ctas: int):
-        """Phase stamps of one launch (instance built with -DOPEVO_TRACE=1)."""
+    def trace(self, ctas: int, launches: int = 1):
+        """Phase stamps of `launches` back-to-back launches (instance built with
+        -DOPEVO_TRACE=1): array [launches][ctas][16] (squeezed for one launch)."""
         import numpy as np
 
-        out = np.zeros(ctas * 16, dtype=np.uint64)
+        out = np.zeros(launches * ctas * 16, dtype=np.uint64)
         err = _errbuf()
         _check(self.dev.lib.opevo_kernel_trace(
             self.handle, out.ctypes.data_as(C.POINTER(C.c_uint64)), out.size, err, len(err)), err)
-        return out.reshape(ctas, 16)
+        out = out.reshape(launches, ctas, 16)
+        return out[0] if launches == 1 else out
 
     def time(self, warmup: int = 3, reps: int = 20, flush_l2: bool = False) -> float:
         ms = C.c_double()

@@ -180,6 +180,16 @@ constexpr int RED_OWN_BYTES = BM * RED_LD * 4;
 constexpr int RED_BLOCK_BYTES = RED_ROWS * RED_LD * 4;
 constexpr int RED_BYTES = (SPLITCL > 1) ? RED_OWN_BYTES + (SPLITCL - 1) * RED_BLOCK_BYTES : 0;
 constexpr int PIPE_BYTES = (STAGES * STAGE_BYTES > RED_BYTES) ? STAGES * STAGE_BYTES : RED_BYTES;
+// Epilogue staging for TMA stores: per epilogue warp two buffers of
+// 32 rows x EPI_COLS outputs, laid out in the swizzle the C tensor map uses
+// (row bytes 32/64/128 -> SW32/64/128), so the warp's smem writes are
+// conflict-free and each chunk leaves as one cp.async.bulk.tensor store.
+constexpr int OUT_BYTES = OPEVO_OUT_F32 ? 4 : 2;
+constexpr int EPI_ROW_BYTES = EPI_COLS * OUT_BYTES;       // 32, 64 or 128
+constexpr int EPI_BUF = 32 * EPI_ROW_BYTES;               // one chunk of one warp
+constexpr int EPI_OFF = (PIPE_BYTES + 1023) / 1024 * 1024;
+constexpr int EPI_BYTES = 4 * 2 * EPI_BUF;
+constexpr int BAR_OFF = EPI_OFF + EPI_BYTES;
 static_assert(SPLITCL == 0 || ((SPLITCL == 2 || SPLITCL == 4 || SPLITCL == 8) && CG == 1 && CLUSTER == 1 &&
                            MATOMS == 1 && BM % (SPLITCL * 8) == 0),
               "DSMEM split-K: S in {2,4,8}, single-CTA 128-row tiles");
@@ -307,6 +317,40 @@ __device__ __forceinline__ void tma_load_3d_mc(u32 dst, const TmaDesc* d, u32 ba
     asm volatile("{ .reg .pred e; elect.sync _|e, 0xffffffff; @e cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
                  ".multicast::cluster [%0], [%1, {%3, %4, %5}], [%2], %6; }"
                  :: "r"(dst), "l"(d), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "h"(mask) : "memory");
+}
+
+// TMA stores (smem -> global) of one epilogue chunk, bulk-group completion
+__device__ __forceinline__ void tma_store_2d(const TmaDesc* d, u32 src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
+                 :: "l"(d), "r"(src), "r"(c0), "r"(c1) : "memory");
+}
+
+__device__ __forceinline__ void tma_store_3d(const TmaDesc* d, u32 src, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];"
+                 :: "l"(d), "r"(src), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
+
+__device__ __forceinline__ void tma_store_4d(const TmaDesc* d, u32 src, int c0, int c1, int c2, int c3) {
+    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];"
+                 :: "l"(d), "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3) : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" :: "n"(N) : "memory");
+}
+
+__device__ __forceinline__ void fence_async_smem() {   // generic-proxy smem writes -> async proxy
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void st_shared_v4(u32 addr, u32 a, u32 b, u32 c, u32 d) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" :: "r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
 }
 
 __device__ __forceinline__ u32 cluster_rank() {
@@ -456,6 +500,26 @@ __device__ __forceinline__ void gather_acc(u32 taddr, float (&out)[EPI_COLS]) {
     }
 }
 
+// Stage one thread's row (EPI_COLS outputs) of a 32-row epilogue chunk in the
+// TMA swizzle of the C map: 16-byte unit j of row r lands at unit
+// j ^ ((r * EPI_ROW_BYTES / 128) mod units), i.e. SW128/SW64/SW32 for 128/64/32-byte rows.
+__device__ __forceinline__ void stage_row(u32 buf, int r, const float* acc) {
+    constexpr int UNITS = EPI_ROW_BYTES / 16;
+    const u32 row = buf + (u32)(r * EPI_ROW_BYTES);
+    const int x = ((r * EPI_ROW_BYTES) >> 7) & (UNITS - 1);
+#pragma unroll
+    for (int j = 0; j < UNITS; ++j) {
+        const u32 dst = row + (u32)((j ^ x) << 4);
+#if OPEVO_OUT_F32
+        st_shared_v4(dst, __float_as_uint(acc[4 * j]), __float_as_uint(acc[4 * j + 1]),
+                     __float_as_uint(acc[4 * j + 2]), __float_as_uint(acc[4 * j + 3]));
+#else
+        st_shared_v4(dst, pack_bf16(acc[8 * j], acc[8 * j + 1]), pack_bf16(acc[8 * j + 2], acc[8 * j + 3]),
+                     pack_bf16(acc[8 * j + 4], acc[8 * j + 5]), pack_bf16(acc[8 * j + 6], acc[8 * j + 7]));
+#endif
+    }
+}
+
 // Write EPI_COLS fp32 accumulator values (one row segment) as the output type.
 __device__ __forceinline__ void store_row(void* c_out, u64 off, const float* acc) {
 #if OPEVO_OUT_F32
@@ -480,6 +544,7 @@ using namespace opevo;
 extern "C" __global__ void __launch_bounds__(NUM_THREADS, 2)   // 2: keep <= 168 regs so two CTAs can co-reside
 opevo_gemm(const __grid_constant__ TmaDesc tma_a,
            const __grid_constant__ TmaDesc tma_b,
+           const __grid_constant__ TmaDesc tma_c,   // C, box = 32 rows x EPI_COLS (TMA-store epilogue)
            void* __restrict__ c_out,
            float* __restrict__ ws,            // split-K partials [split][batch*rows][cols]
            u32* __restrict__ counters,        // per-tile arrival counters (self-resetting)
@@ -490,7 +555,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<u64>(smem_raw) + SMEM_ALIGN - 1) & ~(u64)(SMEM_ALIGN - 1));
-    u64* full_bar = reinterpret_cast<u64*>(smem + PIPE_BYTES);
+    u64* full_bar = reinterpret_cast<u64*>(smem + BAR_OFF);
     u64* empty_bar = full_bar + STAGES;
     u64* tfull_bar = empty_bar + STAGES;      // MMA -> epilogue, per TMEM buffer
     u64* tempty_bar = tfull_bar + NBUF;       // epilogue -> MMA, per TMEM buffer
@@ -551,6 +616,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tma_a);
         tma_prefetch(&tma_b);
+        tma_prefetch(&tma_c);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(smem_u32(full_bar + s), 1);
             // with multicast every CTA of the cluster must release a slot
@@ -596,10 +662,12 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
         int s = 0;
         u32 ph = 0;
         bool first = true;
+        // everything up to the first global read happens before the PDL wait
+        const Unit t_first = decode(u_first < sched.units ? u_first : 0);
         pdl_wait();                     // operands may be the previous launch's output
         if (lane == 0) TRACE(9);
         for (int u = u_first; u < sched.units; u += u_step) {
-            const Unit t = decode(u);
+            const Unit t = (u == u_first) ? t_first : decode(u);
             const int k0 = t.k0;
             const int num_kb = t.num_kb;
             const int col0 = t.col_tile * BN;
@@ -614,6 +682,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
 #endif
             for (int kb = 0; kb < num_kb; ++kb) {
                 mbar_wait(smem_u32(empty_bar + s), ph ^ 1);
+                if (first && lane == 0) TRACE(10);
                 const u32 fb = (CG == 2) ? mapa_cta(smem_u32(full_bar + s), 0) : smem_u32(full_bar + s);
                 if (OPEVO_ABLATE == 3) {
                     if (lane == 0) mbar_arrive(fb);
@@ -621,6 +690,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                     continue;
                 }
                 if (prank == 0) mbar_expect_tx(smem_u32(full_bar + s), TX_BYTES);
+                if (first && lane == 0) TRACE(11);
                 const u32 a_dst = smem_u32(smem + s * STAGE_BYTES);
                 const u32 b_dst = a_dst + A_TILE;
                 const int kk = k0 + kb * BK;
@@ -752,6 +822,8 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
         int buf = 0;
         u32 bph = 0;
         bool first = true;
+        const u32 epi_stage = smem_u32(smem + EPI_OFF) + (u32)(quarter * 2 * EPI_BUF);
+        int nchunk = 0;                            // TMA-store chunks issued by this warp
         for (int u = u_first; u < sched.units; u += u_step) {
             const Unit t = decode(u);
             const int col0 = t.col_tile * BN;
@@ -791,15 +863,40 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
             };
             const int split = t.split;
             if (split == 1) {
+                // TMEM -> registers -> swizzled smem chunk -> TMA store (one
+                // bulk store per 32 x EPI_COLS chunk; two buffers per warp)
 #pragma unroll 1
                 for (int ma = 0; ma < MATOMS; ++ma) {
-                    const int r = out_row(ma * 128 + quarter * 32 + lane);
+                    const int lr0 = ma * 128 + quarter * 32;           // first tile row of the chunk
 #pragma unroll 1
                     for (int c = 0; c < BN; c += EPI_COLS) {
                         float acc[EPI_COLS];
                         gather_acc(lane_addr + ma * BN + c, acc);
+                        if (first && c == 0 && epi_tid == 0) TRACE(12);
                         if (ma == MATOMS - 1 && c + EPI_COLS >= BN) release();
-                        store_row(c_out, c_batch + (u64)r * cols + col0 + c, acc);
+                        const u32 buf = epi_stage + (u32)((nchunk & 1) * EPI_BUF);
+                        if (nchunk >= 2) {             // this buffer's previous store has read it
+                            if (lane == 0) bulk_wait_read<1>();
+                            __syncwarp();
+                        }
+                        stage_row(buf, lane, acc);
+                        fence_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+#if OPEVO_CONV
+                            const int n_l = lr0 / (TILE_H * TILE_W);
+                            const int h_l = (lr0 / TILE_W) % TILE_H;
+                            const int w_l = lr0 % TILE_W;
+                            tma_store_4d(&tma_c, buf, col0 + c, w0 + w_l, h0 + h_l, n0 + n_l);
+#elif OPEVO_BATCHED
+                            tma_store_3d(&tma_c, buf, col0 + c, out_row(lr0), t.batch);
+#else
+                            tma_store_2d(&tma_c, buf, col0 + c, out_row(lr0));
+#endif
+                            bulk_commit();
+                        }
+                        ++nchunk;
+                        if (first && c == 0 && epi_tid == 0) TRACE(13);
                     }
                 }
                 if (first && epi_tid == 0) TRACE(7);
@@ -915,6 +1012,9 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
             first = false;
             if (++buf == NBUF) { buf = 0; bph ^= 1; }
         }
+        // staged chunks must be read out before the CTA's smem goes away
+        if (lane == 0) bulk_wait_read<0>();
+        __syncwarp();
     }
 
     tc_fence_before();

@@ -186,3 +186,22 @@ extern "C" __global__ void opevo_flush(uint4* buf, u64 n16, u32 salt) {
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n16; i += (u64)gridDim.x * blockDim.x)
         buf[i] = make_uint4(salt, (u32)i, salt, (u32)(i >> 32));
 }
+
+// Launch gate for timing: the stream stalls here while the host enqueues the
+// timed launches, then the host writes `seq` into the mapped flag and the
+// launches run back to back with no host gaps.  A %globaltimer timeout (the
+// host never fails to open the gate, but a hung device would be a strike)
+// releases the stream regardless.
+extern "C" __global__ void opevo_gate(const u32* flag, u32 seq, u64 timeout_ns) {
+    u64 t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (true) {
+        u32 v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+        if ((int)(v - seq) >= 0) return;
+        u64 t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > timeout_ns) return;
+        __nanosleep(200);
+    }
+}

@@ -72,6 +72,8 @@ struct Driver {
     X(MemFree, cuMemFree_v2)                                      \
     X(MemAllocHost, cuMemAllocHost_v2)                            \
     X(MemFreeHost, cuMemFreeHost)                                 \
+    X(MemHostAlloc, cuMemHostAlloc)                               \
+    X(MemHostGetDevicePointer, cuMemHostGetDevicePointer_v2)      \
     X(MemcpyHtoD, cuMemcpyHtoD_v2)                                \
     X(MemcpyDtoH, cuMemcpyDtoH_v2)                                \
     X(MemcpyHtoDAsync, cuMemcpyHtoDAsync_v2)                      \
@@ -85,6 +87,7 @@ struct Driver {
     X(StreamEndCapture, cuStreamEndCapture)                       \
     X(GraphInstantiate, cuGraphInstantiateWithFlags)              \
     X(GraphLaunch, cuGraphLaunch)                                 \
+    X(GraphUpload, cuGraphUpload)                                 \
     X(GraphExecDestroy, cuGraphExecDestroy)                       \
     X(GraphDestroy, cuGraphDestroy)                               \
     X(EventCreate, cuEventCreate)                                 \
@@ -208,18 +211,32 @@ size_t dsmem_red_bytes(const Knobs& k) {
     return (size_t)k.bm * ld * 4 + (size_t)(s - 1) * (k.bm / s) * ld * 4;
 }
 
+size_t epi_stage_bytes(const Knobs& k, int out_f32);
+
 bool dsmem_split(const Knobs& k, int family) {
     return family != 2 && (k.split == 2 || k.split == 4 || k.split == 8) && k.cg == 1 &&
-           k.cluster == 1 && k.bm == 128 && dsmem_red_bytes(k) + 1024 + 256 <= 232448;
+           k.cluster == 1 && k.bm == 128 &&
+           (dsmem_red_bytes(k) + 1023) / 1024 * 1024 + epi_stage_bytes(k, 0) + 1024 + 256 <= 232448;
 }
 
-// per-CTA: a CTA pair stages 128 rows of A and BN/2 rows of B each
-size_t smem_bytes(const Knobs& k, int family = 0) {
+// Epilogue chunk width (mirrors EPI_COLS in gemm_sm100.cuh).
+int epi_cols(const Knobs& k) { return k.bn % 32 == 0 ? 32 : 16; }
+
+// TMA-store staging: 4 epilogue warps x 2 buffers x 32 rows x EPI_COLS outputs.
+size_t epi_stage_bytes(const Knobs& k, int out_f32) {
+    return (size_t)4 * 2 * 32 * epi_cols(k) * (out_f32 ? 4 : 2);
+}
+
+// per-CTA: a CTA pair stages 128 rows of A and BN/2 rows of B each; then the
+// epilogue staging (1024-aligned) and the barriers (mirrors EPI_OFF/BAR_OFF)
+size_t smem_bytes(const Knobs& k, int family = 0, int out_f32 = 0) {
+    if (family == 2) return 0;
     const int a_rows = k.cg == 2 ? 128 : k.bm;
     const int b_rows = k.bn / (k.cg == 2 ? 2 : 1);
     size_t pipe = (size_t)k.stages * (size_t)(a_rows + b_rows) * (size_t)k.bk * 2;
     if (dsmem_split(k, family)) pipe = std::max(pipe, dsmem_red_bytes(k));
-    return pipe + 1024 + 256;
+    pipe = (pipe + 1023) / 1024 * 1024;
+    return pipe + epi_stage_bytes(k, out_f32) + 1024 + 256;
 }
 
 uint64_t fnv1a(const char* s, size_t n, uint64_t h = 1469598103934665603ull) {
@@ -491,15 +508,21 @@ struct opevo_ctx {
     CUdevice dev = 0;
     CUcontext cu = nullptr;
     CUstream stream = nullptr;
+    CUstream cap_stream = nullptr;      // graph capture of timed launches (overlaps the check)
     CUmodule util = nullptr;
     CUfunction k_fill_bf16 = nullptr, k_fill_f32 = nullptr, k_fill_u8 = nullptr, k_ref_gemm = nullptr,
-               k_ref_conv = nullptr, k_nchw2nhwc = nullptr, k_compare = nullptr, k_flush = nullptr;
+               k_ref_conv = nullptr, k_nchw2nhwc = nullptr, k_compare = nullptr, k_flush = nullptr,
+               k_gate = nullptr;
+    volatile uint32_t* gate_host = nullptr;   // mapped pinned flag opening the timing gate
+    CUdeviceptr gate_dev = 0;
+    uint32_t gate_seq = 0;
     CUdeviceptr flush_buf = 0;
     size_t flush_bytes = 0;
     CUdeviceptr cmp_buf = 0;
     int sm_count = 0, smem_optin = 0, cc_major = 0, cc_minor = 0;
     std::string cache_dir;
     std::unordered_map<std::string, LoadedModule> modules;
+    std::mutex modules_mu;              // modules may be preloaded from host pool threads
     bool poisoned = false;
 };
 
@@ -531,6 +554,7 @@ struct opevo_kernel {
     CUfunction fn = nullptr;
     alignas(64) CUtensorMap tma_a;
     alignas(64) CUtensorMap tma_b;
+    alignas(64) CUtensorMap tma_c;      // output, box = one 32-row epilogue chunk
     unsigned grid[3] = {1, 1, 1};
     size_t smem = 0;
     int k_per_split = 0;
@@ -622,9 +646,10 @@ CUtensorMapSwizzle swz_enum(int bytes) {
 }
 
 int encode_map(CUtensorMap* map, CUdeviceptr base, int rank, const uint64_t* dims, const uint64_t* strides_b,
-               const uint32_t* box, int swz, char* err, size_t errlen) {
+               const uint32_t* box, int swz, char* err, size_t errlen, int f32 = 0) {
     uint32_t es[5] = {1, 1, 1, 1, 1};
-    CUresult r = g_cu.TensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (cuuint32_t)rank,
+    CUresult r = g_cu.TensorMapEncodeTiled(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                                           (cuuint32_t)rank,
                                            (void*)base, (const cuuint64_t*)dims,
                                            (const cuuint64_t*)strides_b, (const cuuint32_t*)box,
                                            (const cuuint32_t*)es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -637,9 +662,10 @@ int encode_map(CUtensorMap* map, CUdeviceptr base, int rank, const uint64_t* dim
     return OPEVO_OK;
 }
 
-int launch_kernel(opevo_kernel* kr, char* err, size_t errlen) {
+int launch_kernel(opevo_kernel* kr, char* err, size_t errlen, CUstream on = nullptr) {
     opevo_op* op = kr->op;
     opevo_ctx* ctx = op->ctx;
+    CUstream strm = on ? on : ctx->stream;
     if (kr->family == 2) {
         int rows = (int)op->rows, cols = (int)op->cols, depth = (int)op->depth;
         void* args[] = {&op->a, &op->b, &op->c, &rows, &cols, &depth};
@@ -650,7 +676,7 @@ int launch_kernel(opevo_kernel* kr, char* err, size_t errlen) {
         cfg.blockDimX = kr->block;
         cfg.blockDimY = cfg.blockDimZ = 1;
         cfg.sharedMemBytes = (unsigned)kr->smem;
-        cfg.hStream = ctx->stream;
+        cfg.hStream = strm;
         CUlaunchAttribute attr[1];
         if (want_pdl()) {
             attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
@@ -672,7 +698,8 @@ int launch_kernel(opevo_kernel* kr, char* err, size_t errlen) {
     void* cptr = (void*)op->c;
     float* ws = (float*)op->ws;
     unsigned* cnt = (unsigned*)op->counters;
-    void* args[] = {&kr->tma_a, &kr->tma_b, &cptr, &ws, &cnt, &rows, &cols, &depth, &kr->sched, &kr->geom};
+    void* args[] = {&kr->tma_a, &kr->tma_b, &kr->tma_c, &cptr, &ws, &cnt, &rows, &cols, &depth, &kr->sched,
+                    &kr->geom};
     CUlaunchConfig cfg{};
     cfg.gridDimX = kr->grid[0];
     cfg.gridDimY = kr->grid[1];
@@ -681,7 +708,7 @@ int launch_kernel(opevo_kernel* kr, char* err, size_t errlen) {
     cfg.blockDimY = 1;
     cfg.blockDimZ = 1;
     cfg.sharedMemBytes = (unsigned)kr->smem;
-    cfg.hStream = ctx->stream;
+    cfg.hStream = strm;
     CUlaunchAttribute attr[2];
     unsigned na = 0;
     const unsigned clx = (unsigned)(kr->k.cluster * kr->k.cg * (dsmem_split(kr->k, kr->family) ? kr->k.split : 1));
@@ -724,10 +751,13 @@ int sync_checked(opevo_ctx* ctx, const char* what, char* err, size_t errlen) {
 int get_function(opevo_ctx* ctx, int family, const Knobs& k, int batched, int out_f32, const char* name,
                  size_t smem, CUfunction* fn, double* compile_ms, int* hit, char* err, size_t errlen) {
     const std::string key = make_key(family, k, batched, out_f32);
-    auto it = ctx->modules.find(key);
     *compile_ms = 0.0;
     *hit = 1;
+    std::unique_lock<std::mutex> lock(ctx->modules_mu);
+    auto it = ctx->modules.find(key);
     if (it == ctx->modules.end()) {
+        // compile / read and load outside the lock (preload threads run this too)
+        lock.unlock();
         std::vector<char> cubin;
         int st = get_cubin(family, k, batched, out_f32, ctx->cache_dir, cubin, compile_ms, hit, err, errlen);
         if (st) return st;
@@ -738,10 +768,13 @@ int get_function(opevo_ctx* ctx, int family, const Knobs& k, int batched, int ou
             st = fail_cu(ctx, r, "load module", err, errlen);
             return st == OPEVO_ERR_STICKY ? st : OPEVO_LAUNCH_ERROR;
         }
-        it = ctx->modules.emplace(key, lm).first;
+        lock.lock();
+        auto ins = ctx->modules.emplace(key, lm);
+        if (!ins.second) g_cu.ModuleUnload(lm.mod);      // another thread won the race
+        it = ins.first;
     }
     LoadedModule& lm = it->second;
-    if (lm.smem_set < (int)smem) {
+    if (smem > 0 && lm.smem_set < (int)smem) {
         CUresult r = g_cu.FuncSetAttribute(lm.fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
         if (r != CUDA_SUCCESS) {
             put_err(err, errlen, "set smem %zu: %s", smem, cu_str(r));
@@ -860,6 +893,8 @@ int opevo_ctx_create(int device, const char* cache_dir, opevo_ctx** out, char* e
         st = fail_cu(ctx, rr, what, err, errlen);
     };
     if ((r = g_cu.StreamCreate(&ctx->stream, CU_STREAM_NON_BLOCKING)) != CUDA_SUCCESS) bail(r, "stream");
+    else if ((r = g_cu.StreamCreate(&ctx->cap_stream, CU_STREAM_NON_BLOCKING)) != CUDA_SUCCESS)
+        bail(r, "capture stream");
     else if ((r = g_cu.ModuleLoadData(&ctx->util, opevo_util_cubin)) != CUDA_SUCCESS) bail(r, "load util cubin");
     else if ((r = g_cu.MemAlloc(&ctx->cmp_buf, 16)) != CUDA_SUCCESS) bail(r, "alloc");
     if (st == OPEVO_OK) {
@@ -867,12 +902,24 @@ int opevo_ctx_create(int device, const char* cache_dir, opevo_ctx** out, char* e
             {&ctx->k_fill_bf16, "opevo_fill_bf16"}, {&ctx->k_fill_f32, "opevo_fill_f32"},
             {&ctx->k_fill_u8, "opevo_fill_u8"},     {&ctx->k_ref_gemm, "opevo_ref_gemm"},
             {&ctx->k_ref_conv, "opevo_ref_conv"},   {&ctx->k_nchw2nhwc, "opevo_nchw_to_nhwc"},
-            {&ctx->k_compare, "opevo_compare"},     {&ctx->k_flush, "opevo_flush"}};
+            {&ctx->k_compare, "opevo_compare"},     {&ctx->k_flush, "opevo_flush"},
+            {&ctx->k_gate, "opevo_gate"}};
         for (auto& f : fns) {
             if ((r = g_cu.ModuleGetFunction(f.f, ctx->util, f.n)) != CUDA_SUCCESS) {
                 bail(r, f.n);
                 break;
             }
+        }
+    }
+    if (st == OPEVO_OK) {
+        void* hp = nullptr;
+        if ((r = g_cu.MemHostAlloc(&hp, 64, CU_MEMHOSTALLOC_DEVICEMAP | CU_MEMHOSTALLOC_PORTABLE)) != CUDA_SUCCESS)
+            bail(r, "alloc gate flag");
+        else if ((r = g_cu.MemHostGetDevicePointer(&ctx->gate_dev, hp, 0)) != CUDA_SUCCESS)
+            bail(r, "map gate flag");
+        if (hp) {
+            ctx->gate_host = static_cast<volatile uint32_t*>(hp);
+            *ctx->gate_host = 0;
         }
     }
     if (st != OPEVO_OK) {
@@ -892,7 +939,9 @@ void opevo_ctx_destroy(opevo_ctx* ctx) {
         if (ctx->util) g_cu.ModuleUnload(ctx->util);
         if (ctx->flush_buf) g_cu.MemFree(ctx->flush_buf);
         if (ctx->cmp_buf) g_cu.MemFree(ctx->cmp_buf);
+        if (ctx->gate_host) g_cu.MemFreeHost((void*)ctx->gate_host);
         if (ctx->stream) g_cu.StreamDestroy(ctx->stream);
+        if (ctx->cap_stream) g_cu.StreamDestroy(ctx->cap_stream);
         g_cu.PrimaryCtxRelease(ctx->dev);
     }
     delete ctx;
@@ -1074,8 +1123,8 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
     const int batched = op->d.kind == OPEVO_BATCHMATMUL ? 1 : 0;
     if (!knobs_compilable(family, k, err, errlen)) return OPEVO_INVALID_CONFIG;
     if (family == 2) return simt_kernel_get(ctx, op, k, out, info, t0, err, errlen);
-    if ((int)smem_bytes(k, family) > ctx->smem_optin) {
-        put_err(err, errlen, "shared memory %zu B exceeds the device limit %d", smem_bytes(k, family),
+    if ((int)smem_bytes(k, family, op->out_f32) > ctx->smem_optin) {
+        put_err(err, errlen, "shared memory %zu B exceeds the device limit %d", smem_bytes(k, family, op->out_f32),
                 ctx->smem_optin);
         return OPEVO_INVALID_CONFIG;
     }
@@ -1099,7 +1148,7 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
     kr->k = k;
     kr->family = family;
     kr->k_per_split = (int)(op->depth / k.split);
-    kr->smem = smem_bytes(k, family);
+    kr->smem = smem_bytes(k, family, op->out_f32);
     kr->flops = 2.0 * (double)op->batch * (double)op->rows * (double)op->cols * (double)op->depth;
     int st = OPEVO_OK;
     const int swz = swizzle_bytes(k.bk);
@@ -1124,6 +1173,24 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
         uint64_t bs[1] = {(uint64_t)op->depth * 2};
         uint32_t bb[2] = {atom_k, (uint32_t)k.bn};
         if (!st) st = encode_map(&kr->tma_b, op->b, 2, bd, bs, bb, swz, err, errlen);
+        if (!st) {
+            // output NHWC {Cout, Wo, Ho, N}; a 32-pixel epilogue chunk of the
+            // TILE_N x TILE_H x TILE_W tile is the box {EPI_COLS, bw, bh, bn}
+            const int ob = op->out_f32 ? 4 : 2, ec = epi_cols(k);
+            const int bw = std::min(k.tile_w, 32);
+            const int bh = k.tile_w >= 32 ? 1 : std::min(k.tile_h, 32 / k.tile_w);
+            const int bn = k.tile_w * k.tile_h >= 32 ? 1 : 32 / (k.tile_w * k.tile_h);
+            if (bw * bh * bn != 32 || k.tile_w % bw || k.tile_h % bh || tile_n % bn) {
+                put_err(err, errlen, "conv tile %dx%d cannot be stored in 32-pixel boxes", k.tile_h, k.tile_w);
+                st = OPEVO_INVALID_CONFIG;
+            } else {
+                const int co = c[4];
+                uint64_t cd[4] = {(uint64_t)co, (uint64_t)WO, (uint64_t)HO, (uint64_t)N};
+                uint64_t cs[3] = {(uint64_t)co * ob, (uint64_t)co * WO * ob, (uint64_t)co * WO * HO * ob};
+                uint32_t cb[4] = {(uint32_t)ec, (uint32_t)bw, (uint32_t)bh, (uint32_t)bn};
+                st = encode_map(&kr->tma_c, op->c, 4, cd, cs, cb, ec * ob, err, errlen, op->out_f32);
+            }
+        }
         kr->sched = SchedHost{(N / tile_n) * (HO / k.tile_h) * (WO / k.tile_w), (int)col_tiles, 1,
                               k.split, 0, 1, 0};
     } else {
@@ -1137,6 +1204,13 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
         uint32_t bb[3] = {atom_k, (uint32_t)(k.bn / k.cg), 1};
         st = encode_map(&kr->tma_a, op->a, rank, ad, as, ab, swz, err, errlen);
         if (!st) st = encode_map(&kr->tma_b, op->b, rank, bd, bs, bb, swz, err, errlen);
+        if (!st) {
+            const int ob = op->out_f32 ? 4 : 2, ec = epi_cols(k);
+            uint64_t cd[3] = {(uint64_t)op->cols, (uint64_t)op->rows, (uint64_t)op->batch};
+            uint64_t cs[2] = {(uint64_t)op->cols * ob, (uint64_t)op->cols * op->rows * ob};
+            uint32_t cb[3] = {(uint32_t)ec, 32, 1};
+            st = encode_map(&kr->tma_c, op->c, rank, cd, cs, cb, ec * ob, err, errlen, op->out_f32);
+        }
         kr->sched = SchedHost{(int)row_tiles, (int)(col_tiles / k.cluster), (int)op->batch, k.split,
                               0, 1, 0};
     }
@@ -1220,25 +1294,30 @@ int opevo_kernel_run(opevo_kernel* k, char* err, size_t errlen) {
     return sync_checked(ctx, "kernel", err, errlen);
 }
 
-int opevo_kernel_check(opevo_kernel* k, double tol, double* rel_err, char* err, size_t errlen) {
-    if (!k) return OPEVO_ERR_ARG;
+}  // extern "C"
+
+namespace {
+
+// Enqueue the verification of one launch: poison C (NaN bytes, so a kernel
+// that skips tiles fails), launch, compare against the reference into
+// ctx->cmp_buf.  No synchronisation; see finish_check.
+int enqueue_check(opevo_kernel* k, char* err, size_t errlen) {
     opevo_op* op = k->op;
     opevo_ctx* ctx = op->ctx;
-    g_cu.CtxSetCurrent(ctx->cu);
-    // poison the output (0xFF.. = NaN) so a kernel that skips tiles fails
     CU_TRY(ctx, g_cu.MemsetD8Async(op->c, 0xFF, op->c_bytes, ctx->stream), "poison C");
     int st = launch_kernel(k, err, errlen);
-    if (st) return st;
-    st = sync_checked(ctx, "kernel", err, errlen);
     if (st) return st;
     CU_TRY(ctx, g_cu.MemsetD8Async(ctx->cmp_buf, 0, 16, ctx->stream), "zero compare");
     uint64_t n = (uint64_t)op->batch * op->rows * op->cols;
     int c_f32 = op->out_f32;
     void* args[] = {&op->c, &op->ref, &n, &c_f32, &ctx->cmp_buf};
-    st = launch_simple(ctx, ctx->k_compare, grid_for(n), 256, args, err, errlen);
-    if (st) return st;
+    return launch_simple(ctx, ctx->k_compare, grid_for(n), 256, args, err, errlen);
+}
+
+// After the stream has drained: read the comparison and judge it.
+int finish_check(opevo_kernel* k, double tol, double* rel_err, char* err, size_t errlen) {
+    opevo_ctx* ctx = k->op->ctx;
     uint32_t res[4] = {0, 0, 0, 0};
-    CU_TRY(ctx, g_cu.StreamSynchronize(ctx->stream), "compare sync");
     CU_TRY(ctx, g_cu.MemcpyDtoH(res, ctx->cmp_buf, 12), "compare readback");
     float md, mr;
     memcpy(&md, &res[0], 4);
@@ -1252,120 +1331,275 @@ int opevo_kernel_check(opevo_kernel* k, double tol, double* rel_err, char* err, 
     return OPEVO_OK;
 }
 
-int opevo_kernel_time(opevo_kernel* k, int warmup, int reps, int flush_l2, double* ms_per_launch, char* err,
-                      size_t errlen) {
-    if (!k || reps < 1 || !ms_per_launch) return OPEVO_ERR_ARG;
+// Device-time budget per measurement (OPEVO_TIME_BUDGET_MS, default 4): a
+// one-launch estimate caps the repetitions of slow candidates at
+// budget/estimate (min 3), so a 10 ms instance does not cost 40 launches;
+// fast instances keep all `reps`.
+int capped_reps(int reps, float est_ms) {
+    double budget = 4.0;
+    if (const char* b = getenv("OPEVO_TIME_BUDGET_MS")) budget = atof(b);
+    if (budget > 0 && est_ms > 0 && est_ms * reps > budget) reps = std::max(3, (int)(budget / est_ms));
+    return reps;
+}
+
+// `reps` back-to-back launches timed with CUDA events on the library stream.
+// The stream first parks on a device-side gate (opevo_gate polling a mapped
+// host flag); the host enqueues e0, the launches and e1, then opens the
+// gate, so the launches run with no host gaps (PDL between them, as in a
+// CUDA graph) without paying for graph instantiation on every trial.
+// Segments of at most 64 launches keep the launch queue from filling while
+// the gate is closed.
+int time_gated(opevo_kernel* k, int reps, double* total_ms, char* err, size_t errlen) {
     opevo_ctx* ctx = k->op->ctx;
-    g_cu.CtxSetCurrent(ctx->cu);
+    CUevent e0, e1;
+    CU_TRY(ctx, g_cu.EventCreate(&e0, CU_EVENT_DEFAULT), "event");
+    CUresult r = g_cu.EventCreate(&e1, CU_EVENT_DEFAULT);
+    if (r != CUDA_SUCCESS) {
+        g_cu.EventDestroy(e0);
+        return fail_cu(ctx, r, "event", err, errlen);
+    }
+    int st = OPEVO_OK;
+    double total = 0.0;
+    for (int done = 0; done < reps && !st;) {
+        const int n = std::min(64, reps - done);
+        uint32_t seq = ++ctx->gate_seq;
+        uint64_t timeout_ns = 2000000000ull;
+        void* ga[] = {&ctx->gate_dev, &seq, &timeout_ns};
+        st = launch_simple(ctx, ctx->k_gate, 1, 32, ga, err, errlen);
+        r = CUDA_SUCCESS;
+        if (!st) r = g_cu.EventRecord(e0, ctx->stream);
+        for (int i = 0; i < n && !st && r == CUDA_SUCCESS; ++i) st = launch_kernel(k, err, errlen);
+        if (!st && r == CUDA_SUCCESS) r = g_cu.EventRecord(e1, ctx->stream);
+        __atomic_store_n(const_cast<uint32_t*>(ctx->gate_host), seq, __ATOMIC_SEQ_CST);   // open
+        if (!st && r == CUDA_SUCCESS) r = g_cu.EventSynchronize(e1);
+        float ms = 0.f;
+        if (!st && r == CUDA_SUCCESS) r = g_cu.EventElapsedTime(&ms, e0, e1);
+        if (!st && r != CUDA_SUCCESS) {
+            st = fail_cu(ctx, r, "timed launches", err, errlen);
+            if (st != OPEVO_ERR_STICKY) st = OPEVO_LAUNCH_ERROR;
+        }
+        total += ms;
+        done += n;
+    }
+    g_cu.EventDestroy(e0);
+    g_cu.EventDestroy(e1);
+    if (st) {
+        // a failed launch leaves the stream parked: drain it
+        g_cu.StreamSynchronize(ctx->stream);
+        return st;
+    }
+    *total_ms = total;
+    return OPEVO_OK;
+}
+
+// `reps` launches captured (on the side stream, so this host work overlaps
+// device work already queued on ctx->stream) into one executable graph.
+int build_graph(opevo_kernel* k, int reps, CUgraphExec* out, char* err, size_t errlen) {
+    opevo_ctx* ctx = k->op->ctx;
+    CUgraph g = nullptr;
+    CU_TRY(ctx, g_cu.StreamBeginCapture(ctx->cap_stream, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL), "capture");
+    int st = OPEVO_OK;
+    for (int i = 0; i < reps && !st; ++i) st = launch_kernel(k, err, errlen, ctx->cap_stream);
+    CUresult r = g_cu.StreamEndCapture(ctx->cap_stream, &g);
+    if (!st && r == CUDA_SUCCESS) r = g_cu.GraphInstantiate(out, g, 0);
+    if (g) g_cu.GraphDestroy(g);
+    if (st) return st;
+    if (r != CUDA_SUCCESS) return fail_cu(ctx, r, "graph", err, errlen);
+    return OPEVO_OK;
+}
+
+// The graph's launches back to back (PDL edges between them, as captured),
+// timed with CUDA events on the library stream; the graph is uploaded first
+// so the timed launch carries no first-launch setup.
+int time_graph(opevo_kernel* k, CUgraphExec ge, double* total_ms, char* err, size_t errlen) {
+    opevo_ctx* ctx = k->op->ctx;
+    CUevent e0, e1;
+    CU_TRY(ctx, g_cu.EventCreate(&e0, CU_EVENT_DEFAULT), "event");
+    CUresult r = g_cu.EventCreate(&e1, CU_EVENT_DEFAULT);
+    if (r == CUDA_SUCCESS) r = g_cu.GraphUpload(ge, ctx->stream);
+    if (r == CUDA_SUCCESS) r = g_cu.EventRecord(e0, ctx->stream);
+    if (r == CUDA_SUCCESS) r = g_cu.GraphLaunch(ge, ctx->stream);
+    if (r == CUDA_SUCCESS) r = g_cu.EventRecord(e1, ctx->stream);
+    if (r == CUDA_SUCCESS) r = g_cu.EventSynchronize(e1);
+    float ms = 0.f;
+    if (r == CUDA_SUCCESS) r = g_cu.EventElapsedTime(&ms, e0, e1);
+    g_cu.EventDestroy(e0);
+    g_cu.EventDestroy(e1);
+    if (r != CUDA_SUCCESS) {
+        int st = fail_cu(ctx, r, "timed graph", err, errlen);
+        return st == OPEVO_ERR_STICKY ? st : OPEVO_LAUNCH_ERROR;
+    }
+    *total_ms = ms;
+    return OPEVO_OK;
+}
+
+// Cold-L2 timing: a 2x-L2 write before every launch, each launch timed alone.
+int time_flushed(opevo_kernel* k, int reps, double* total_ms, char* err, size_t errlen) {
+    opevo_ctx* ctx = k->op->ctx;
+    if (!ctx->flush_buf) {
+        ctx->flush_bytes = (size_t)256 << 20;   // 2x the 126 MB L2
+        CU_TRY(ctx, g_cu.MemAlloc(&ctx->flush_buf, ctx->flush_bytes), "alloc flush buffer");
+    }
+    CUevent e0, e1;
+    CU_TRY(ctx, g_cu.EventCreate(&e0, CU_EVENT_DEFAULT), "event");
+    CU_TRY(ctx, g_cu.EventCreate(&e1, CU_EVENT_DEFAULT), "event");
+    uint64_t n16 = ctx->flush_bytes / 16;
+    double total = 0.0;
+    int st = OPEVO_OK;
+    for (int i = 0; i < reps; ++i) {
+        unsigned salt = (unsigned)i;
+        void* fa[] = {&ctx->flush_buf, &n16, &salt};
+        st = launch_simple(ctx, ctx->k_flush, (unsigned)ctx->sm_count * 4, 512, fa, err, errlen);
+        if (!st) st = g_cu.EventRecord(e0, ctx->stream) == CUDA_SUCCESS ? OPEVO_OK : OPEVO_ERR_CUDA;
+        if (!st) st = launch_kernel(k, err, errlen);
+        if (!st) st = g_cu.EventRecord(e1, ctx->stream) == CUDA_SUCCESS ? OPEVO_OK : OPEVO_ERR_CUDA;
+        if (!st) st = sync_checked(ctx, "timed launch", err, errlen);
+        float ms = 0.f;
+        if (!st) g_cu.EventElapsedTime(&ms, e0, e1);
+        if (st) break;
+        total += ms;
+    }
+    g_cu.EventDestroy(e0);
+    g_cu.EventDestroy(e1);
+    if (st) return st;
+    *total_ms = total;
+    return OPEVO_OK;
+}
+
+// Warm-up launches plus a one-launch estimate between events; the caller
+// synchronises (alone or together with an enqueued check).
+int enqueue_warmup_estimate(opevo_kernel* k, int warmup, CUevent e0, CUevent e1, char* err,
+                            size_t errlen) {
+    opevo_ctx* ctx = k->op->ctx;
     for (int i = 0; i < warmup; ++i) {
         int st = launch_kernel(k, err, errlen);
         if (st) return st;
     }
-    int st = sync_checked(ctx, "warmup", err, errlen);
+    CU_TRY(ctx, g_cu.EventRecord(e0, ctx->stream), "event");
+    int st = launch_kernel(k, err, errlen);
     if (st) return st;
+    CU_TRY(ctx, g_cu.EventRecord(e1, ctx->stream), "event");
+    return OPEVO_OK;
+}
+
+// Timing modes (the `flush_l2` argument of the ABI):
+//   0  R back-to-back launches in one CUDA graph (L2 warm) -- the fitness
+//   1  a 2x-L2 write before every launch, each launch timed (cold L2)
+//   2  R back-to-back stream launches behind a device gate (no graph)
+// check (optional, tol >= 0) + warm-up + estimate with ONE synchronisation,
+// then the timed launches.  In mode 0 the graph is captured and
+// instantiated while the check runs on the device.
+int check_and_time(opevo_kernel* k, double tol, double* rel_err, int warmup, int reps, int mode,
+                   double* ms_per_launch, char* err, size_t errlen) {
+    opevo_ctx* ctx = k->op->ctx;
+    int st = OPEVO_OK;
+    CUgraphExec ge = nullptr;
+    int graph_reps = 0;
+    if (tol >= 0) {
+        st = enqueue_check(k, err, errlen);
+        if (st) return st;
+        warmup = std::max(0, warmup - 1);        // the checked launch warms up too
+    }
     CUevent e0, e1;
     CU_TRY(ctx, g_cu.EventCreate(&e0, CU_EVENT_DEFAULT), "event");
     CU_TRY(ctx, g_cu.EventCreate(&e1, CU_EVENT_DEFAULT), "event");
-    // Device-time budget per measurement (OPEVO_TIME_BUDGET_MS, default 4):
-    // a one-launch estimate caps the repetitions of slow candidates at
-    // budget/estimate (min 3), so a 10 ms instance does not cost 40 launches;
-    // fast instances keep all `reps`.
-    {
-        double budget = 4.0;
-        if (const char* b = getenv("OPEVO_TIME_BUDGET_MS")) budget = atof(b);
-        float est = 0.f;
-        CUresult r = g_cu.EventRecord(e0, ctx->stream);
-        if (r == CUDA_SUCCESS && !(st = launch_kernel(k, err, errlen))) {
-            r = g_cu.EventRecord(e1, ctx->stream);
-            if (r == CUDA_SUCCESS) r = g_cu.EventSynchronize(e1);
-            if (r == CUDA_SUCCESS) r = g_cu.EventElapsedTime(&est, e0, e1);
-        }
-        if (st || r != CUDA_SUCCESS) {
-            g_cu.EventDestroy(e0);
-            g_cu.EventDestroy(e1);
-            return st ? st : fail_cu(ctx, r, "estimate launch", err, errlen);
-        }
-        if (budget > 0 && est > 0 && est * reps > budget)
-            reps = std::max(3, (int)(budget / est));
+    float est = 0.f;
+    st = enqueue_warmup_estimate(k, warmup, e0, e1, err, errlen);
+    if (!st && mode == 0 && ms_per_launch) {
+        st = build_graph(k, reps, &ge, err, errlen);
+        graph_reps = reps;
     }
-    double total = 0.0;
-    if (!flush_l2) {
-        // back-to-back launches captured in one graph: no host launch gaps
-        CUgraph g = nullptr;
-        CUgraphExec ge = nullptr;
-        CU_TRY(ctx, g_cu.StreamBeginCapture(ctx->stream, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL), "capture");
-        for (int i = 0; i < reps && !st; ++i) st = launch_kernel(k, err, errlen);
-        CUresult r = g_cu.StreamEndCapture(ctx->stream, &g);
-        if (st || r != CUDA_SUCCESS) {
-            if (g) g_cu.GraphDestroy(g);
-            g_cu.EventDestroy(e0);
-            g_cu.EventDestroy(e1);
-            return st ? st : fail_cu(ctx, r, "end capture", err, errlen);
-        }
-        r = g_cu.GraphInstantiate(&ge, g, 0);
-        if (r == CUDA_SUCCESS) r = g_cu.GraphLaunch(ge, ctx->stream);   // graph warm-up
-        if (r == CUDA_SUCCESS) r = g_cu.EventRecord(e0, ctx->stream);
-        if (r == CUDA_SUCCESS) r = g_cu.GraphLaunch(ge, ctx->stream);
-        if (r == CUDA_SUCCESS) r = g_cu.EventRecord(e1, ctx->stream);
-        if (r == CUDA_SUCCESS) r = g_cu.EventSynchronize(e1);
-        float ms = 0.f;
-        if (r == CUDA_SUCCESS) r = g_cu.EventElapsedTime(&ms, e0, e1);
+    if (!st) st = sync_checked(ctx, "check/warm-up", err, errlen);
+    if (!st) {
+        CUresult r = g_cu.EventElapsedTime(&est, e0, e1);
+        if (r != CUDA_SUCCESS) st = fail_cu(ctx, r, "estimate", err, errlen);
+    }
+    g_cu.EventDestroy(e0);
+    g_cu.EventDestroy(e1);
+    if (!st && tol >= 0) st = finish_check(k, tol, rel_err, err, errlen);
+    if (st || !ms_per_launch) {
         if (ge) g_cu.GraphExecDestroy(ge);
-        g_cu.GraphDestroy(g);
-        g_cu.EventDestroy(e0);
-        g_cu.EventDestroy(e1);
-        if (r != CUDA_SUCCESS) {
-            int s2 = fail_cu(ctx, r, "timed graph", err, errlen);
-            return s2 == OPEVO_ERR_STICKY ? s2 : OPEVO_LAUNCH_ERROR;
-        }
-        total = ms;
-    } else {
-        if (!ctx->flush_buf) {
-            ctx->flush_bytes = (size_t)256 << 20;   // 2x the 126 MB L2
-            CU_TRY(ctx, g_cu.MemAlloc(&ctx->flush_buf, ctx->flush_bytes), "alloc flush buffer");
-        }
-        uint64_t n16 = ctx->flush_bytes / 16;
-        for (int i = 0; i < reps; ++i) {
-            unsigned salt = (unsigned)i;
-            void* fa[] = {&ctx->flush_buf, &n16, &salt};
-            st = launch_simple(ctx, ctx->k_flush, (unsigned)ctx->sm_count * 4, 512, fa, err, errlen);
-            if (!st) st = g_cu.EventRecord(e0, ctx->stream) == CUDA_SUCCESS ? OPEVO_OK : OPEVO_ERR_CUDA;
-            if (!st) st = launch_kernel(k, err, errlen);
-            if (!st) st = g_cu.EventRecord(e1, ctx->stream) == CUDA_SUCCESS ? OPEVO_OK : OPEVO_ERR_CUDA;
-            if (!st) st = sync_checked(ctx, "timed launch", err, errlen);
-            float ms = 0.f;
-            if (!st) g_cu.EventElapsedTime(&ms, e0, e1);
-            if (st) break;
-            total += ms;
-        }
-        g_cu.EventDestroy(e0);
-        g_cu.EventDestroy(e1);
-        if (st) return st;
+        return st;
     }
+    reps = capped_reps(reps, est);
+    double total = 0.0;
+    if (mode == 0) {
+        if (reps != graph_reps) {            // a slow candidate: fewer launches
+            g_cu.GraphExecDestroy(ge);
+            ge = nullptr;
+            st = build_graph(k, reps, &ge, err, errlen);
+        }
+        if (!st) st = time_graph(k, ge, &total, err, errlen);
+        if (ge) g_cu.GraphExecDestroy(ge);
+    } else if (mode == 1) {
+        st = time_flushed(k, reps, &total, err, errlen);
+    } else {
+        st = time_gated(k, reps, &total, err, errlen);
+    }
+    if (st) return st;
     *ms_per_launch = total / reps;
     return OPEVO_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
+int opevo_kernel_check(opevo_kernel* k, double tol, double* rel_err, char* err, size_t errlen) {
+    if (!k) return OPEVO_ERR_ARG;
+    opevo_ctx* ctx = k->op->ctx;
+    g_cu.CtxSetCurrent(ctx->cu);
+    int st = enqueue_check(k, err, errlen);
+    if (!st) st = sync_checked(ctx, "check", err, errlen);
+    if (!st) st = finish_check(k, tol < 0 ? 0.0 : tol, rel_err, err, errlen);
+    return st;
+}
+
+int opevo_kernel_time(opevo_kernel* k, int warmup, int reps, int flush_l2, double* ms_per_launch, char* err,
+                      size_t errlen) {
+    if (!k || reps < 1 || !ms_per_launch) return OPEVO_ERR_ARG;
+    g_cu.CtxSetCurrent(k->op->ctx->cu);
+    return check_and_time(k, -1.0, nullptr, warmup, reps, flush_l2, ms_per_launch, err, errlen);
+}
+
 int opevo_trial(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nknobs, int warmup, int reps,
                 int flush_l2, double tol, opevo_trial_result* res, char* err, size_t errlen) {
-    if (!res) return OPEVO_ERR_ARG;
+    if (!res || reps < 1) return OPEVO_ERR_ARG;
     memset(res, 0, sizeof *res);
     opevo_kernel* k = nullptr;
     int st = opevo_kernel_get(ctx, op, knobs, nknobs, &k, res, err, errlen);
     if (st) return st;
-    double rel = 0.0;
-    st = opevo_kernel_check(k, tol, &rel, err, errlen);
+    double rel = 0.0, ms = 0.0;
+    st = check_and_time(k, tol < 0 ? 0.0 : tol, &rel, warmup, reps, flush_l2, &ms, err, errlen);
     res->rel_err = rel;
     if (!st) {
-        double ms = 0.0;
-        st = opevo_kernel_time(k, warmup, reps, flush_l2, &ms, err, errlen);
-        if (!st) {
-            res->ms = ms;
-            res->tflops = ms > 0 ? k->flops / (ms * 1e-3) / 1e12 : 0.0;
-        }
+        res->ms = ms;
+        res->tflops = ms > 0 ? k->flops / (ms * 1e-3) / 1e12 : 0.0;
     }
     res->launches = k->launches;
     opevo_kernel_release(k);
+    return st;
+}
+
+int opevo_op_preload(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nknobs, double* compile_ms,
+                     int* cache_hit, char* err, size_t errlen) {
+    if (!ctx || !op || !knobs) return OPEVO_ERR_ARG;
+    if (ctx->poisoned) {
+        put_err(err, errlen, "context poisoned by an earlier fault");
+        return OPEVO_ERR_STICKY;
+    }
+    g_cu.CtxSetCurrent(ctx->cu);
+    Knobs k = read_knobs(knobs, nknobs);
+    const int family = op->d.kind == OPEVO_CONV2D ? 1 : (op->in_f32 ? 2 : 0);
+    const int batched = op->d.kind == OPEVO_BATCHMATMUL ? 1 : 0;
+    if (!knobs_compilable(family, k, err, errlen)) return OPEVO_INVALID_CONFIG;
+    CUfunction fn = nullptr;
+    double cms = 0.0;
+    int hit = 1;
+    int st = get_function(ctx, family, k, batched, family == 2 ? 1 : op->out_f32,
+                          family == 2 ? "opevo_sgemm" : "opevo_gemm", 0, &fn, &cms, &hit, err, errlen);
+    if (compile_ms) *compile_ms = cms;
+    if (cache_hit) *cache_hit = hit;
     return st;
 }
 
@@ -1390,13 +1624,20 @@ int opevo_kernel_trace(opevo_kernel* k, uint64_t* host, size_t count, char* err,
     opevo_ctx* ctx = op->ctx;
     g_cu.CtxSetCurrent(ctx->cu);
     const size_t ctas = (size_t)k->grid[0] * k->grid[1] * k->grid[2];
-    const size_t bytes = ctas * 16 * sizeof(uint64_t);
+    const size_t per = ctas * 16;       // 16 stamps per CTA per launch
+    // room for several launches in `host`: that many back-to-back launches
+    // (PDL as in timing), each stamping its own block -> steady-state timeline
+    const int nl = (int)std::max<size_t>(1, std::min<size_t>(8, count / per));
+    const size_t bytes = per * nl * sizeof(uint64_t);
     CUdeviceptr buf = 0;
     CU_TRY(ctx, g_cu.MemAlloc(&buf, bytes), "alloc trace");
     CU_TRY(ctx, g_cu.MemsetD8(buf, 0, bytes), "zero trace");
     CUdeviceptr saved = op->ws;
-    op->ws = buf;                       // trace instances write stamps through `ws`
-    int st = launch_kernel(k, err, errlen);
+    int st = OPEVO_OK;
+    for (int i = 0; i < nl && !st; ++i) {
+        op->ws = buf + (CUdeviceptr)(i * per * sizeof(uint64_t));   // stamps go through `ws`
+        st = launch_kernel(k, err, errlen);
+    }
     if (!st) st = sync_checked(ctx, "traced kernel", err, errlen);
     op->ws = saved;
     if (!st) {

@@ -128,21 +128,19 @@ class GpuEvaluator:
         return [i.fitness for i in infos]
 
     def precompile(self, mapped) -> None:
-        """NVRTC-compile the distinct kernels of a batch on the host pool."""
-        family_batched = {}
+        """Stage the distinct kernels of a batch on the host pool: NVRTC
+        compile (or cubin-cache read) and module load into this device's
+        context, in parallel, so the trials themselves only bind and launch."""
+        distinct = {}
         for m in mapped:
             if m.valid:
-                family_batched[(m.family, m.batched, m.knobs.compile_key())] = m
-        out_f32 = self.settings.dtype == capi.F32
+                distinct[(m.family, m.batched, m.knobs.compile_key())] = m
 
         def build(m):
-            try:
-                capi.compile_kernel(m.family, m.knobs.as_tuple(), m.batched, out_f32,
-                                    self.settings.cache_dir)
-            except capi.OpevoError:
-                pass   # reported again (with status) by the trial itself
+            # failures are reported again (with status) by the trial itself
+            self.dev.preload(self.op, m.knobs.as_tuple())
 
-        list(self._pool.map(build, family_batched.values()))
+        list(self._pool.map(build, distinct.values()))
 
     def evaluate_infos(self, configs: list[tuple]) -> list[TrialInfo]:
         mapped = [config_to_knobs(self.spec, self.space, c, self.dtype) for c in configs]

@@ -87,7 +87,7 @@ class Knobs:
         ld = self.bn + 4
         red = self.bm * ld * 4 + (s - 1) * (self.bm // max(s, 1)) * ld * 4
         ok = (s in (2, 4, 8) and self.cta_group == 1 and self.cluster == 1 and self.bm == 128
-              and red + SMEM_EXTRA <= SMEM_LIMIT)
+              and _align1k(red) + epi_bytes(self.bn) + SMEM_EXTRA <= SMEM_LIMIT)
         return s if ok else 0
 
     def compile_key(self) -> tuple[int, ...]:
@@ -97,7 +97,12 @@ class Knobs:
                 self.acc, self.cta_group, self.dsmem_split())
 
     def smem_bytes(self) -> int:
-        return stage_bytes(self.bm, self.bn, self.bk, self.cta_group) * self.stages + SMEM_EXTRA
+        """Mirrors ``smem_bytes`` in csrc/opevo.cpp (bf16 output)."""
+        pipe = stage_bytes(self.bm, self.bn, self.bk, self.cta_group) * self.stages
+        if self.dsmem_split():
+            ld = self.bn + 4
+            pipe = max(pipe, self.bm * ld * 4 + (self.split - 1) * (self.bm // self.split) * ld * 4)
+        return _align1k(pipe) + epi_bytes(self.bn) + SMEM_EXTRA
 
 
 @dataclass(frozen=True)
@@ -114,6 +119,16 @@ class Mapped:
         return self.knobs is not None
 
 
+def _align1k(n: int) -> int:
+    return (n + 1023) // 1024 * 1024
+
+
+def epi_bytes(bn: int) -> int:
+    """TMA-store staging of the epilogue (bf16 output): 4 warps x 2 buffers
+    x 32 rows x EPI_COLS (32, or 16 when BN is not a multiple of 32)."""
+    return 4 * 2 * 32 * (32 if bn % 32 == 0 else 16) * 2
+
+
 def stage_bytes(bm: int, bn: int, bk: int, cta_group: int = 1) -> int:
     """Shared memory per pipeline stage of one CTA (a CTA pair stages 128 rows
     of A and BN/2 rows of B in each CTA)."""
@@ -127,8 +142,13 @@ def _bk_ok(bk: int) -> bool:
 
 
 def _fit_stages(want: int, bm: int, bn: int, bk: int, cta_group: int = 1) -> int:
-    room = (SMEM_LIMIT - SMEM_EXTRA) // stage_bytes(bm, bn, bk, cta_group)
-    return min(want, room)
+    """Largest ring depth <= want whose shared memory (pipeline, epilogue
+    staging, barriers) fits in 227 KB; 0 when not even one stage fits."""
+    sb = stage_bytes(bm, bn, bk, cta_group)
+    s = want
+    while s > 0 and _align1k(s * sb) + epi_bytes(bn) + SMEM_EXTRA > SMEM_LIMIT:
+        s -= 1
+    return s
 
 
 def _largest_pow2_divisor(*vals: int, cap: int = 4) -> int:
