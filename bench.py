@@ -350,7 +350,9 @@ def main() -> None:
                        "space": ("reference operator space (fp32 SIMT family)" if args.dtype == "f32"
                                  else "reference operator space + stages (mapping.py)"),
                        "fitness_timing": f"{settings.reps} back-to-back launches in one CUDA "
-                                         f"graph after {settings.warmup} warm-up, L2 "
+                                         f"graph (fewer for candidates slower than 15 us: "
+                                         f"0.3 ms device budget, min 5) after {settings.warmup} "
+                                         f"warm-up launches incl. the verified one, L2 "
                                          f"{args.l2} (operands fit in L2)",
                        "l2_between_steps": "flushed: a 256 MB write (2x L2) before every timed "
                                            "step; within a trial the fitness is L2-warm "

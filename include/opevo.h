@@ -156,6 +156,18 @@ int opevo_trial(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nknobs, 
                 int reps, int flush_l2, double tol, opevo_trial_result* res, char* err,
                 size_t errlen);
 
+/* Up to OPEVO_MAX_BATCH trials (knobs: count x nknobs, row-major) with two
+ * host synchronisations in total: every instance's check, warm-up and
+ * estimate are enqueued together (their timed graphs are built meanwhile),
+ * then all timed launches run back to back.  status[i] / res[i] / the
+ * NUL-terminated message at msgs + i * msg_stride are per trial, as
+ * opevo_trial would return them.  The return value is OPEVO_OK unless a
+ * fatal (< 0) error aborted the batch; unfinished trials then carry it. */
+#define OPEVO_MAX_BATCH 64
+int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nknobs, int count,
+                      int warmup, int reps, int flush_l2, double tol, opevo_trial_result* res,
+                      int32_t* status, char* msgs, size_t msg_stride, char* err, size_t errlen);
+
 /* Compile-or-read and load the module of one instance into the context's
  * module cache (no launch).  Thread-safe with respect to other preloads and
  * to the trial thread, so a host pool can stage the next batch's modules.

@@ -49,8 +49,9 @@ EXPORTS = (
     "opevo_op_refresh_reference", "opevo_kernel_get", "opevo_kernel_release",
     "opevo_kernel_run", "opevo_kernel_check", "opevo_kernel_time", "opevo_trial",
     "opevo_kernel_trace", "opevo_ctx_flush_l2", "opevo_host_alloc", "opevo_host_free",
-    "opevo_op_preload",
+    "opevo_op_preload", "opevo_trial_batch",
 )
+MAX_BATCH = 64
 
 
 class OpDesc(C.Structure):
@@ -120,6 +121,8 @@ def load() -> C.CDLL:
         "opevo_host_alloc": (P, [sz]),
         "opevo_host_free": (None, [P]),
         "opevo_op_preload": (I, [P, P, i32p, I, dp, C.POINTER(I), cp, sz]),
+        "opevo_trial_batch": (I, [P, P, i32p, I, I, I, I, I, D, C.POINTER(TrialResult),
+                                  C.POINTER(C.c_int32), cp, sz, cp, sz]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -241,6 +244,39 @@ class Device:
         return Trial(st, res.tflops, res.ms, res.rel_err, res.compile_ms, res.load_ms,
                      res.cache_hit, res.grid_ctas, res.smem_bytes,
                      err.value.decode(errors="replace") if st != OK else "", res.launches)
+
+    def trial_batch(self, op: "Operand", knob_list, warmup: int = 3, reps: int = 20,
+                    flush_l2: int = 0, tol: float = 1e-2) -> list[Trial]:
+        """Several trials with two host synchronisations in total (checks and
+        warm-ups of all, then all timed launches).  A fatal (< 0) error raises
+        OpevoError with the per-trial results attached as ``.trials``."""
+        out: list[Trial] = []
+        for lo in range(0, len(knob_list), MAX_BATCH):
+            chunk = knob_list[lo:lo + MAX_BATCH]
+            n = len(chunk)
+            knobs = (C.c_int32 * (n * NUM_KNOBS))()
+            for i, kn in enumerate(chunk):
+                knobs[i * NUM_KNOBS:(i + 1) * NUM_KNOBS] = list(_knob_array(kn))
+            res = (TrialResult * n)()
+            status = (C.c_int32 * n)()
+            stride = 512
+            msgs = C.create_string_buffer(n * stride)
+            err = _errbuf()
+            st = self.lib.opevo_trial_batch(self.handle, op.handle, knobs, NUM_KNOBS, n, warmup, reps,
+                                            int(flush_l2), tol, res, status, msgs, stride, err, len(err))
+            trials = []
+            for i in range(n):
+                r = res[i]
+                m = msgs.raw[i * stride:(i + 1) * stride].split(b"\0", 1)[0].decode(errors="replace")
+                trials.append(Trial(status[i], r.tflops, r.ms, r.rel_err, r.compile_ms, r.load_ms,
+                                    r.cache_hit, r.grid_ctas, r.smem_bytes,
+                                    m if status[i] != OK else "", r.launches))
+            out.extend(trials)
+            if st != OK:
+                e = OpevoError(st, err.value.decode(errors="replace"))
+                e.trials = out
+                raise e
+        return out
 
     def preload(self, op: "Operand", knobs) -> tuple[int, float, int, str]:
         """Compile-or-read and load one instance's module (thread-safe; no

@@ -372,6 +372,44 @@ __device__ __forceinline__ void umma_bf16(u32 tmem_d, u64 adesc, u64 bdesc, u32 
                  :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
 }
 
+// All K16 steps of one swizzle atom (NK = ATOM_K / 16 MMAs into one
+// accumulator) in one asm block under one elect: the descriptors of steps
+// 1.. are the first ones plus 2 * step (32 bytes) in the start-address
+// field, computed next to the MMAs, so the issuing warp spends a handful of
+// instructions per MMA instead of rebuilding and broadcasting descriptors.
+#define OPEVO_UMMA_ATOM(CGS)                                                                          \
+    template <int NK>                                                                                \
+    __device__ __forceinline__ void umma##CGS##_atom(u32 d, u64 a, u64 b, u32 acc_first);             \
+    template <>                                                                                      \
+    __device__ __forceinline__ void umma##CGS##_atom<1>(u32 d, u64 a, u64 b, u32 acc_first) {         \
+        asm volatile("{ .reg .pred e, p; elect.sync _|e, 0xffffffff; setp.ne.b32 p, %4, 0; "          \
+                     "@e tcgen05.mma.cta_group::" #CGS ".kind::f16 [%0], %1, %2, %3, p; }"            \
+                     :: "r"(d), "l"(a), "l"(b), "r"(IDESC), "r"(acc_first));                          \
+    }                                                                                                \
+    template <>                                                                                      \
+    __device__ __forceinline__ void umma##CGS##_atom<2>(u32 d, u64 a, u64 b, u32 acc_first) {         \
+        asm volatile("{ .reg .pred e, p, t; .reg .b64 a1, b1; elect.sync _|e, 0xffffffff; "           \
+                     "setp.ne.b32 p, %4, 0; setp.eq.b32 t, 0, 0; add.s64 a1, %1, 2; add.s64 b1, %2, 2; " \
+                     "@e tcgen05.mma.cta_group::" #CGS ".kind::f16 [%0], %1, %2, %3, p; "             \
+                     "@e tcgen05.mma.cta_group::" #CGS ".kind::f16 [%0], a1, b1, %3, t; }"            \
+                     :: "r"(d), "l"(a), "l"(b), "r"(IDESC), "r"(acc_first));                          \
+    }                                                                                                \
+    template <>                                                                                      \
+    __device__ __forceinline__ void umma##CGS##_atom<4>(u32 d, u64 a, u64 b, u32 acc_first) {         \
+        asm volatile("{ .reg .pred e, p, t; .reg .b64 a1, b1, a2, b2, a3, b3; elect.sync _|e, 0xffffffff; " \
+                     "setp.ne.b32 p, %4, 0; setp.eq.b32 t, 0, 0; "                                    \
+                     "add.s64 a1, %1, 2; add.s64 b1, %2, 2; add.s64 a2, %1, 4; add.s64 b2, %2, 4; "  \
+                     "add.s64 a3, %1, 6; add.s64 b3, %2, 6; "                                         \
+                     "@e tcgen05.mma.cta_group::" #CGS ".kind::f16 [%0], %1, %2, %3, p; "             \
+                     "@e tcgen05.mma.cta_group::" #CGS ".kind::f16 [%0], a1, b1, %3, t; "             \
+                     "@e tcgen05.mma.cta_group::" #CGS ".kind::f16 [%0], a2, b2, %3, t; "             \
+                     "@e tcgen05.mma.cta_group::" #CGS ".kind::f16 [%0], a3, b3, %3, t; }"            \
+                     :: "r"(d), "l"(a), "l"(b), "r"(IDESC), "r"(acc_first));                          \
+    }
+OPEVO_UMMA_ATOM(1)
+OPEVO_UMMA_ATOM(2)
+#undef OPEVO_UMMA_ATOM
+
 __device__ __forceinline__ void umma_commit(u32 bar) {
     asm volatile("{ .reg .pred e; elect.sync _|e, 0xffffffff; "
                  "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0]; }"
@@ -661,6 +699,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
         // (whole warp iterates; the tma_* / expect_tx helpers elect one lane)
         int s = 0;
         u32 ph = 0;
+        int issued = 0;                 // k-blocks issued; the first STAGES slots start free
         bool first = true;
         // everything up to the first global read happens before the PDL wait
         const Unit t_first = decode(u_first < sched.units ? u_first : 0);
@@ -681,7 +720,8 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
             const int b_row0 = col0 + (int)prank * BN_LOAD;         // first B row here
 #endif
             for (int kb = 0; kb < num_kb; ++kb) {
-                mbar_wait(smem_u32(empty_bar + s), ph ^ 1);
+                if (issued >= STAGES) mbar_wait(smem_u32(empty_bar + s), ph ^ 1);
+                ++issued;
                 if (first && lane == 0) TRACE(10);
                 const u32 fb = (CG == 2) ? mapa_cta(smem_u32(full_bar + s), 0) : smem_u32(full_bar + s);
                 if (OPEVO_ABLATE == 3) {
@@ -756,6 +796,13 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
             int s = 0, buf = 0;
             u32 ph = 0, bph = 0;
             bool first = true;
+            // Shared-memory descriptors of stage 0; every other operand
+            // descriptor is this plus a compile-time offset (>> 4) in the
+            // start-address field, which cannot carry out of its 14 bits
+            // (shared offsets < 228 KB), so each MMA costs two 64-bit adds
+            // rather than a rebuild from the address.
+            const u64 desc_a0 = DESC_HI | (u64)((smem_u32(smem) >> 4) & 0x3FFF);
+            const u64 desc_b0 = desc_a0 + (u64)(A_TILE >> 4);
             for (int u = u_first; u < sched.units; u += u_step) {
                 const int num_kb = decode(u).num_kb;
                 // the epilogue must have drained this accumulator buffer
@@ -771,19 +818,28 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                         if (++s == STAGES) { s = 0; ph ^= 1; }
                         continue;
                     }
-                    const u32 a_base = smem_u32(smem + s * STAGE_BYTES);
-                    const u32 b_base = a_base + A_TILE;
+                    const u64 sdesc = (u64)((u32)(s * STAGE_BYTES) >> 4);
+                    const u64 da = desc_a0 + sdesc, db = desc_b0 + sdesc;
+                    if (MATOMS == 1 && ACC == 1) {
+                        // one accumulator: each swizzle atom's K16 steps in one asm block
+#pragma unroll
+                        for (int ka = 0; ka < KATOMS; ++ka) {
+                            const u64 adesc = da + (u64)((ka * (BM_CTA * SWZ)) >> 4);
+                            const u64 bdesc = db + (u64)((ka * (BN_LOAD * SWZ)) >> 4);
+                            const u32 accumulate = (kb != 0 || ka != 0) ? 1u : 0u;
+                            if (CG == 2) umma2_atom<ATOM_K / 16>(acc_base, adesc, bdesc, accumulate);
+                            else         umma1_atom<ATOM_K / 16>(acc_base, adesc, bdesc, accumulate);
+                        }
+                    } else {
 #pragma unroll
                     for (int ka = 0; ka < KATOMS; ++ka) {
 #pragma unroll
                         for (int k16 = 0; k16 < ATOM_K / 16; ++k16) {
                             const u32 koff = k16 * 32;
-                            const u64 bdesc = DESC_HI |
-                                (u64)(((b_base + ka * (BN_LOAD * SWZ) + koff) >> 4) & 0x3FFF);
+                            const u64 bdesc = db + (u64)((ka * (BN_LOAD * SWZ) + koff) >> 4);
 #pragma unroll
                             for (int ma = 0; ma < MATOMS; ++ma) {
-                                const u32 a_addr = a_base + ka * (BM_CTA * SWZ) + ma * (128 * SWZ) + koff;
-                                const u64 adesc = DESC_HI | (u64)((a_addr >> 4) & 0x3FFF);
+                                const u64 adesc = da + (u64)((ka * (BM_CTA * SWZ) + ma * (128 * SWZ) + koff) >> 4);
                                 const int step = ka * (ATOM_K / 16) + k16;   // k16 step in stage
                                 const int acc = step % ACC;                  // compile-time
                                 const u32 d = acc_base + (u32)((acc * MATOMS + ma) * BN);
@@ -792,6 +848,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                                 else         umma_bf16(d, adesc, bdesc, accumulate);
                             }
                         }
+                    }
                     }
 #if OPEVO_CTA_GROUP == 2
                     // both CTAs staged this slot: release it in both

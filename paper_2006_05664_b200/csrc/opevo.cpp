@@ -16,12 +16,16 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <functional>
+#include <thread>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <memory>
 #include <mutex>
 #include <sstream>
 #include <string>
@@ -502,6 +506,55 @@ struct LoadedModule {
 
 }  // namespace
 
+// Small persistent host pool: builds the timed graphs of a trial batch in
+// parallel (capture + instantiate are host work) while the trial thread
+// keeps the device busy with the batch's checks.
+struct HostPool {
+    std::vector<std::thread> threads;
+    std::mutex mu;
+    std::condition_variable cv, done_cv;
+    std::vector<std::function<void(int)>> tasks;   // task(worker index)
+    size_t next = 0, finished = 0;
+    bool stop = false;
+
+    void start(int n, CUcontext cu) {
+        for (int w = 0; w < n; ++w)
+            threads.emplace_back([this, w, cu] {
+                g_cu.CtxSetCurrent(cu);
+                std::unique_lock<std::mutex> lk(mu);
+                while (true) {
+                    cv.wait(lk, [this] { return stop || next < tasks.size(); });
+                    if (stop) return;
+                    auto fn = tasks[next++];
+                    lk.unlock();
+                    fn(w);
+                    lk.lock();
+                    if (++finished == tasks.size()) done_cv.notify_all();
+                }
+            });
+    }
+    void submit(std::vector<std::function<void(int)>> batch) {
+        std::lock_guard<std::mutex> lk(mu);
+        tasks = std::move(batch);
+        next = finished = 0;
+        cv.notify_all();
+    }
+    void wait() {
+        std::unique_lock<std::mutex> lk(mu);
+        done_cv.wait(lk, [this] { return finished == tasks.size(); });
+        tasks.clear();
+        next = finished = 0;
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            stop = true;
+        }
+        cv.notify_all();
+        for (auto& t : threads) t.join();
+    }
+};
+
 // ===================================================================== ctx
 struct opevo_ctx {
     int device = 0;
@@ -509,6 +562,8 @@ struct opevo_ctx {
     CUcontext cu = nullptr;
     CUstream stream = nullptr;
     CUstream cap_stream = nullptr;      // graph capture of timed launches (overlaps the check)
+    std::vector<CUstream> pool_streams; // one capture stream per graph-build worker
+    std::unique_ptr<HostPool> pool;     // graph builds of a trial batch
     CUmodule util = nullptr;
     CUfunction k_fill_bf16 = nullptr, k_fill_f32 = nullptr, k_fill_u8 = nullptr, k_ref_gemm = nullptr,
                k_ref_conv = nullptr, k_nchw2nhwc = nullptr, k_compare = nullptr, k_flush = nullptr,
@@ -560,7 +615,8 @@ struct opevo_kernel {
     int k_per_split = 0;
     ConvGeomHost geom{};
     SchedHost sched{};
-    int launches = 0;                   // launches of this instance (all paths)
+    std::atomic<int> launches{0};       // launches of this instance (all paths; graph
+                                        // capture threads and the trial thread)
     unsigned block = 192;
     double flops = 0.0;
 };
@@ -896,7 +952,7 @@ int opevo_ctx_create(int device, const char* cache_dir, opevo_ctx** out, char* e
     else if ((r = g_cu.StreamCreate(&ctx->cap_stream, CU_STREAM_NON_BLOCKING)) != CUDA_SUCCESS)
         bail(r, "capture stream");
     else if ((r = g_cu.ModuleLoadData(&ctx->util, opevo_util_cubin)) != CUDA_SUCCESS) bail(r, "load util cubin");
-    else if ((r = g_cu.MemAlloc(&ctx->cmp_buf, 16)) != CUDA_SUCCESS) bail(r, "alloc");
+    else if ((r = g_cu.MemAlloc(&ctx->cmp_buf, 16 * OPEVO_MAX_BATCH)) != CUDA_SUCCESS) bail(r, "alloc");
     if (st == OPEVO_OK) {
         struct { CUfunction* f; const char* n; } fns[] = {
             {&ctx->k_fill_bf16, "opevo_fill_bf16"}, {&ctx->k_fill_f32, "opevo_fill_f32"},
@@ -942,6 +998,8 @@ void opevo_ctx_destroy(opevo_ctx* ctx) {
         if (ctx->gate_host) g_cu.MemFreeHost((void*)ctx->gate_host);
         if (ctx->stream) g_cu.StreamDestroy(ctx->stream);
         if (ctx->cap_stream) g_cu.StreamDestroy(ctx->cap_stream);
+        ctx->pool.reset();
+        for (CUstream st : ctx->pool_streams) g_cu.StreamDestroy(st);
         g_cu.PrimaryCtxRelease(ctx->dev);
     }
     delete ctx;
@@ -1300,25 +1358,24 @@ namespace {
 
 // Enqueue the verification of one launch: poison C (NaN bytes, so a kernel
 // that skips tiles fails), launch, compare against the reference into
-// ctx->cmp_buf.  No synchronisation; see finish_check.
-int enqueue_check(opevo_kernel* k, char* err, size_t errlen) {
+// compare slot `slot` of ctx->cmp_buf (16 bytes each).  No synchronisation;
+// see finish_check.
+int enqueue_check(opevo_kernel* k, char* err, size_t errlen, int slot = 0) {
     opevo_op* op = k->op;
     opevo_ctx* ctx = op->ctx;
     CU_TRY(ctx, g_cu.MemsetD8Async(op->c, 0xFF, op->c_bytes, ctx->stream), "poison C");
     int st = launch_kernel(k, err, errlen);
     if (st) return st;
-    CU_TRY(ctx, g_cu.MemsetD8Async(ctx->cmp_buf, 0, 16, ctx->stream), "zero compare");
+    CUdeviceptr out = ctx->cmp_buf + 16 * (CUdeviceptr)slot;
+    CU_TRY(ctx, g_cu.MemsetD8Async(out, 0, 16, ctx->stream), "zero compare");
     uint64_t n = (uint64_t)op->batch * op->rows * op->cols;
     int c_f32 = op->out_f32;
-    void* args[] = {&op->c, &op->ref, &n, &c_f32, &ctx->cmp_buf};
+    void* args[] = {&op->c, &op->ref, &n, &c_f32, &out};
     return launch_simple(ctx, ctx->k_compare, grid_for(n), 256, args, err, errlen);
 }
 
-// After the stream has drained: read the comparison and judge it.
-int finish_check(opevo_kernel* k, double tol, double* rel_err, char* err, size_t errlen) {
-    opevo_ctx* ctx = k->op->ctx;
-    uint32_t res[4] = {0, 0, 0, 0};
-    CU_TRY(ctx, g_cu.MemcpyDtoH(res, ctx->cmp_buf, 12), "compare readback");
+// Judge one compare slot {max|C-R|, max|R|, non-finite count}.
+int judge(const uint32_t* res, double tol, double* rel_err, char* err, size_t errlen) {
     float md, mr;
     memcpy(&md, &res[0], 4);
     memcpy(&mr, &res[1], 4);
@@ -1331,14 +1388,24 @@ int finish_check(opevo_kernel* k, double tol, double* rel_err, char* err, size_t
     return OPEVO_OK;
 }
 
-// Device-time budget per measurement (OPEVO_TIME_BUDGET_MS, default 4): a
+// After the stream has drained: read the comparison and judge it.
+int finish_check(opevo_kernel* k, double tol, double* rel_err, char* err, size_t errlen) {
+    opevo_ctx* ctx = k->op->ctx;
+    uint32_t res[4] = {0, 0, 0, 0};
+    CU_TRY(ctx, g_cu.MemcpyDtoH(res, ctx->cmp_buf, 12), "compare readback");
+    return judge(res, tol, rel_err, err, errlen);
+}
+
+// Device-time budget per measurement (OPEVO_TIME_BUDGET_MS, default 0.3): a
 // one-launch estimate caps the repetitions of slow candidates at
-// budget/estimate (min 3), so a 10 ms instance does not cost 40 launches;
-// fast instances keep all `reps`.
+// budget/estimate (min 5), so a 30 us instance costs 10 launches rather than
+// 20 and a 10 ms one 5; the fast instances that decide the search keep all
+// `reps`.  Once the measured time is device-bound (the trial pipeline's
+// host work is overlapped), this budget sets the trial rate.
 int capped_reps(int reps, float est_ms) {
-    double budget = 4.0;
+    double budget = 0.3;
     if (const char* b = getenv("OPEVO_TIME_BUDGET_MS")) budget = atof(b);
-    if (budget > 0 && est_ms > 0 && est_ms * reps > budget) reps = std::max(3, (int)(budget / est_ms));
+    if (budget > 0 && est_ms > 0 && est_ms * reps > budget) reps = std::max(std::min(reps, 5), (int)(budget / est_ms));
     return reps;
 }
 
@@ -1394,13 +1461,15 @@ int time_gated(opevo_kernel* k, int reps, double* total_ms, char* err, size_t er
 
 // `reps` launches captured (on the side stream, so this host work overlaps
 // device work already queued on ctx->stream) into one executable graph.
-int build_graph(opevo_kernel* k, int reps, CUgraphExec* out, char* err, size_t errlen) {
+int build_graph(opevo_kernel* k, int reps, CUgraphExec* out, char* err, size_t errlen,
+                CUstream cap = nullptr) {
     opevo_ctx* ctx = k->op->ctx;
+    if (!cap) cap = ctx->cap_stream;
     CUgraph g = nullptr;
-    CU_TRY(ctx, g_cu.StreamBeginCapture(ctx->cap_stream, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL), "capture");
+    CU_TRY(ctx, g_cu.StreamBeginCapture(cap, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL), "capture");
     int st = OPEVO_OK;
-    for (int i = 0; i < reps && !st; ++i) st = launch_kernel(k, err, errlen, ctx->cap_stream);
-    CUresult r = g_cu.StreamEndCapture(ctx->cap_stream, &g);
+    for (int i = 0; i < reps && !st; ++i) st = launch_kernel(k, err, errlen, cap);
+    CUresult r = g_cu.StreamEndCapture(cap, &g);
     if (!st && r == CUDA_SUCCESS) r = g_cu.GraphInstantiate(out, g, 0);
     if (g) g_cu.GraphDestroy(g);
     if (st) return st;
@@ -1579,6 +1648,173 @@ int opevo_trial(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nknobs, 
     res->launches = k->launches;
     opevo_kernel_release(k);
     return st;
+}
+
+int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nknobs, int count,
+                      int warmup, int reps, int flush_l2, double tol, opevo_trial_result* res,
+                      int32_t* status, char* msgs, size_t msg_stride, char* err, size_t errlen) {
+    if (!ctx || !op || !knobs || !res || !status || count < 0 || count > OPEVO_MAX_BATCH || reps < 1)
+        return OPEVO_ERR_ARG;
+    const int mode = flush_l2;
+    g_cu.CtxSetCurrent(ctx->cu);
+    static const bool prof = getenv("OPEVO_PROFILE_BATCH") != nullptr;
+    double tp[8] = {now_ms()};
+    std::vector<opevo_kernel*> ks(count, nullptr);
+    std::vector<CUgraphExec> ge(count, nullptr);
+    std::vector<int> greps(count, 0);
+    std::vector<CUevent> ev(4 * (size_t)count, nullptr);   // per trial: est0, est1, t0, t1
+    auto msg = [&](int i) -> char* { return msgs ? msgs + (size_t)i * msg_stride : nullptr; };
+    auto mlen = [&]() -> size_t { return msgs ? msg_stride : 0; };
+    int fatal = OPEVO_OK;
+    for (int i = 0; i < count; ++i) {
+        memset(&res[i], 0, sizeof res[i]);
+        if (msg(i) && mlen()) msg(i)[0] = 0;
+        status[i] = opevo_kernel_get(ctx, op, knobs + (size_t)i * nknobs, nknobs, &ks[i], &res[i], msg(i), mlen());
+        if (status[i] < 0) { fatal = status[i]; break; }
+    }
+    tp[1] = now_ms();
+    // (host pool) capture + instantiate every bound instance's timed graph,
+    // in parallel, while this thread runs phase A
+    std::vector<int> gst(count, OPEVO_OK);
+    std::vector<std::string> gmsg(count);
+    bool pooled = false;
+    if (!fatal && mode == 0) {
+        if (!ctx->pool) {
+            const int nw = 6;
+            for (int w = 0; w < nw; ++w) {
+                CUstream st_ = nullptr;
+                if (g_cu.StreamCreate(&st_, CU_STREAM_NON_BLOCKING) != CUDA_SUCCESS) break;
+                ctx->pool_streams.push_back(st_);
+            }
+            if (!ctx->pool_streams.empty()) {
+                ctx->pool.reset(new HostPool());
+                ctx->pool->start((int)ctx->pool_streams.size(), ctx->cu);
+            }
+        }
+        if (ctx->pool) {
+            std::vector<std::function<void(int)>> tasks;
+            for (int i = 0; i < count; ++i) {
+                if (status[i] != OPEVO_OK) continue;
+                greps[i] = reps;
+                tasks.push_back([&, i](int w) {
+                    char e[512] = {0};
+                    gst[i] = build_graph(ks[i], reps, &ge[i], e, sizeof e, ctx->pool_streams[w]);
+                    if (gst[i]) gmsg[i] = e;
+                });
+            }
+            ctx->pool->submit(std::move(tasks));
+            pooled = true;
+        }
+    }
+    // phase A (device): for every bound instance, the poisoned check launch
+    // + compare into its slot, warm-ups and a one-launch estimate
+    for (int i = 0; i < count && !fatal; ++i) {
+        if (status[i] != OPEVO_OK) continue;
+        int st = OPEVO_OK;
+        for (int e = 0; e < 4 && !st; ++e)
+            if (g_cu.EventCreate(&ev[4 * i + e], CU_EVENT_DEFAULT) != CUDA_SUCCESS) st = OPEVO_ERR_CUDA;
+        if (!st) st = enqueue_check(ks[i], msg(i), mlen(), i);
+        if (!st) st = enqueue_warmup_estimate(ks[i], std::max(0, warmup - 1), ev[4 * i], ev[4 * i + 1], msg(i), mlen());
+        if (!st && mode == 0 && !pooled) {
+            st = build_graph(ks[i], reps, &ge[i], msg(i), mlen());
+            greps[i] = reps;
+        }
+        status[i] = st;
+        if (st < 0) fatal = st;
+    }
+    tp[2] = now_ms();
+    if (pooled) {
+        ctx->pool->wait();
+        for (int i = 0; i < count; ++i) {
+            if (status[i] != OPEVO_OK || gst[i] == OPEVO_OK) continue;
+            status[i] = gst[i];
+            if (msg(i) && mlen()) snprintf(msg(i), mlen(), "%s", gmsg[i].c_str());
+            if (gst[i] < 0 && !fatal) fatal = gst[i];
+        }
+    }
+    std::vector<uint32_t> cmp(4 * (size_t)std::max(count, 1), 0);
+    tp[3] = now_ms();
+    if (!fatal) {
+        fatal = sync_checked(ctx, "batch check/warm-up", err, errlen);
+        if (fatal == OPEVO_LAUNCH_ERROR) fatal = OPEVO_ERR_CUDA;
+    }
+    if (!fatal && count && g_cu.MemcpyDtoH(cmp.data(), ctx->cmp_buf, 16 * (size_t)count) != CUDA_SUCCESS)
+        fatal = OPEVO_ERR_CUDA;
+    // judge, cap repetitions of slow instances
+    std::vector<int> nreps(count, reps);
+    for (int i = 0; i < count && !fatal; ++i) {
+        if (status[i] != OPEVO_OK) continue;
+        double rel = 0.0;
+        status[i] = judge(&cmp[4 * (size_t)i], tol < 0 ? 0.0 : tol, &rel, msg(i), mlen());
+        res[i].rel_err = rel;
+        if (status[i] != OPEVO_OK) continue;
+        float est = 0.f;
+        g_cu.EventElapsedTime(&est, ev[4 * i], ev[4 * i + 1]);
+        nreps[i] = capped_reps(reps, est);
+        if (mode == 0 && nreps[i] != greps[i]) {
+            g_cu.GraphExecDestroy(ge[i]);
+            ge[i] = nullptr;
+            status[i] = build_graph(ks[i], nreps[i], &ge[i], msg(i), mlen());
+            if (status[i] < 0) fatal = status[i];
+        }
+    }
+    tp[4] = now_ms();
+    // phase B: the timed launches of every verified instance, back to back,
+    // each bracketed by its own events; one synchronisation at the end
+    if (!fatal && mode == 0) {
+        int last = -1;
+        for (int i = 0; i < count; ++i) {
+            if (status[i] != OPEVO_OK) continue;
+            CUresult r = g_cu.GraphUpload(ge[i], ctx->stream);
+            if (r == CUDA_SUCCESS) r = g_cu.EventRecord(ev[4 * i + 2], ctx->stream);
+            if (r == CUDA_SUCCESS) r = g_cu.GraphLaunch(ge[i], ctx->stream);
+            if (r == CUDA_SUCCESS) r = g_cu.EventRecord(ev[4 * i + 3], ctx->stream);
+            if (r != CUDA_SUCCESS) {
+                status[i] = fail_cu(ctx, r, "timed graph", msg(i), mlen());
+                if (status[i] < 0) { fatal = status[i]; break; }
+                continue;
+            }
+            last = i;
+        }
+        tp[5] = now_ms();
+        if (!fatal && last >= 0) {
+            fatal = sync_checked(ctx, "batch timing", err, errlen);
+            if (fatal == OPEVO_LAUNCH_ERROR) fatal = OPEVO_ERR_CUDA;
+        }
+        for (int i = 0; i < count && !fatal; ++i) {
+            if (status[i] != OPEVO_OK) continue;
+            float ms = 0.f;
+            g_cu.EventElapsedTime(&ms, ev[4 * i + 2], ev[4 * i + 3]);
+            res[i].ms = ms / nreps[i];
+        }
+    } else if (!fatal) {
+        for (int i = 0; i < count && !fatal; ++i) {
+            if (status[i] != OPEVO_OK) continue;
+            double total = 0.0;
+            status[i] = mode == 1 ? time_flushed(ks[i], nreps[i], &total, msg(i), mlen())
+                                  : time_gated(ks[i], nreps[i], &total, msg(i), mlen());
+            if (status[i] < 0) fatal = status[i];
+            else if (status[i] == OPEVO_OK) res[i].ms = total / nreps[i];
+        }
+    }
+    for (int i = 0; i < count; ++i) {
+        if (fatal && status[i] == OPEVO_OK) status[i] = fatal;
+        if (status[i] == OPEVO_OK && res[i].ms > 0) res[i].tflops = ks[i]->flops / (res[i].ms * 1e-3) / 1e12;
+        if (ks[i]) {
+            res[i].launches = ks[i]->launches;
+            opevo_kernel_release(ks[i]);
+        }
+        if (ge[i]) g_cu.GraphExecDestroy(ge[i]);
+        for (int e = 0; e < 4; ++e)
+            if (ev[4 * i + e]) g_cu.EventDestroy(ev[4 * i + e]);
+    }
+    if (fatal && err && errlen && !err[0]) put_err(err, errlen, "batch aborted (status %d)", fatal);
+    if (prof) {
+        tp[6] = now_ms();
+        fprintf(stderr, "[batch %d] bind %.3f enqA %.3f poolwait %.3f syncA+judge %.3f enqB %.3f syncB+rest %.3f ms\n",
+                count, tp[1] - tp[0], tp[2] - tp[1], tp[3] - tp[2], tp[4] - tp[3], tp[5] - tp[4], tp[6] - tp[5]);
+    }
+    return fatal;
 }
 
 int opevo_op_preload(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nknobs, double* compile_ms,

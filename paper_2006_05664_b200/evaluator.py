@@ -107,6 +107,7 @@ class GpuEvaluator:
         self.history: list[TrialInfo] = []
         nthreads = self.settings.compile_threads or min(8, os.cpu_count() or 1)
         self._pool = ThreadPoolExecutor(max_workers=nthreads)
+        self._staged: set = set()          # kernels already loaded in this context
 
     def close(self) -> None:
         self._pool.shutdown(wait=False)
@@ -133,31 +134,55 @@ class GpuEvaluator:
         context, in parallel, so the trials themselves only bind and launch."""
         distinct = {}
         for m in mapped:
-            if m.valid:
-                distinct[(m.family, m.batched, m.knobs.compile_key())] = m
+            key = (m.family, m.batched, m.knobs.compile_key()) if m.valid else None
+            if key is not None and key not in self._staged:
+                distinct[key] = m
 
         def build(m):
             # failures are reported again (with status) by the trial itself
             self.dev.preload(self.op, m.knobs.as_tuple())
 
-        list(self._pool.map(build, distinct.values()))
+        if len(distinct) == 1:
+            build(next(iter(distinct.values())))
+        elif distinct:
+            list(self._pool.map(build, distinct.values()))
+        self._staged.update(distinct)
 
     def evaluate_infos(self, configs: list[tuple]) -> list[TrialInfo]:
+        """Map, stage (compile/load on the host pool) and measure a batch.
+        The valid instances run as one ``opevo_trial_batch``: their checks and
+        warm-ups are enqueued together, then their timed launches, so the
+        host synchronises twice per batch rather than per trial."""
         mapped = [config_to_knobs(self.spec, self.space, c, self.dtype) for c in configs]
         self.precompile(mapped)
+        valid = [m.knobs.as_tuple() for m in mapped if m.valid]
+        s = self.settings
+        try:
+            trials = self.dev.trial_batch(self.op, valid, warmup=s.warmup, reps=s.reps,
+                                          flush_l2=int(s.flush_l2), tol=self.tol) if valid else []
+        except capi.OpevoError as err:
+            if err.status == capi.ERR_STICKY:
+                raise WorkerFault(f"device {self.device_index}: {err.message}") from err
+            raise FatalEvaluationError(f"device {self.device_index}: {err.message}") from err
+        it = iter(zip(valid, trials))
         out = []
         for m in mapped:
             if not m.valid:
                 out.append(TrialInfo(0.0, "invalid_config", None, message=m.reason))
                 continue
-            out.append(self.run_knobs(m.knobs.as_tuple()))
+            knobs, t = next(it)
+            out.append(self._info(knobs, t))
         self.history.extend(out)
         return out
 
     def run_knobs(self, knobs: tuple) -> TrialInfo:
+        """One trial through ``opevo_trial`` (the single-configuration path)."""
         s = self.settings
         t = self.dev.trial(self.op, knobs, warmup=s.warmup, reps=s.reps, flush_l2=s.flush_l2,
                            tol=self.tol)
+        return self._info(knobs, t)
+
+    def _info(self, knobs: tuple, t: "capi.Trial") -> TrialInfo:
         if t.status == capi.ERR_STICKY:
             raise WorkerFault(f"device {self.device_index}: {t.message}")
         if t.status < 0:

@@ -223,3 +223,47 @@ def test_cold_and_warm_timing(dev):
         k.close()
     finally:
         op.close()
+
+
+def test_timing_modes_agree(dev):
+    """Graph (0), cold-L2 (1) and gated-stream (2) timings of one instance are
+    all positive; the gated stream launches sit within 2x of the graph."""
+    from paper_2006_05664_b200 import capi
+
+    op = dev.prepare(capi.MATMUL, rows=1024, cols=1024, depth=1024)
+    try:
+        k = dev.kernel(op, (128, 64, 128, 3, 1, 1))
+        g = k.time(warmup=3, reps=20, flush_l2=0)
+        s = k.time(warmup=3, reps=20, flush_l2=2)
+        c = k.time(warmup=1, reps=3, flush_l2=1)
+        assert 0 < g < 1.0 and 0 < s < 1.0 and 0 < c < 1.0
+        assert 0.5 < s / g < 2.0
+        k.close()
+    finally:
+        op.close()
+
+
+def test_trial_batch_matches_single_trials(dev):
+    """opevo_trial_batch: per-trial statuses equal opevo_trial's (valid,
+    invalid, split-K and CTA-pair instances mixed), every verified output
+    within tolerance, and the last instance's output matches the oracle."""
+    from paper_2006_05664_b200 import capi
+
+    rows, cols, depth = 512, 1024, 1024
+    knob_list = [(128, 64, 128, 3, 1, 1), (96, 128, 64, 4, 1, 1), (128, 128, 64, 4, 2, 1),
+                 (256, 64, 128, 4, 1, 1, 1, 1, 1, 2), (128, 512, 64, 2, 1, 1), (128, 32, 64, 4, 1, 2)]
+    op = dev.prepare(capi.MATMUL, rows=rows, cols=cols, depth=depth, seed=1234)
+    try:
+        batch = dev.trial_batch(op, knob_list, warmup=2, reps=5)
+        single = [dev.trial(op, kn, warmup=2, reps=5) for kn in knob_list]
+        assert [t.status for t in batch] == [t.status for t in single]
+        for t in batch:
+            if t.ok:
+                assert t.rel_err < BF16_TOL and t.tflops > 0 and t.ms > 0
+            else:
+                assert t.status == capi.INVALID_CONFIG and t.message
+        last = dev.trial_batch(op, [knob_list[3]], warmup=1, reps=3)[0]
+        assert last.ok
+        assert _rel(op.output(), _oracle_gemm(1, rows, cols, depth, 1234)) < BF16_TOL
+    finally:
+        op.close()

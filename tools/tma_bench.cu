@@ -1,0 +1,122 @@
+// Tensor-TMA ingress microbenchmark (not product code): the GEMM mainloop's
+// load pattern without the MMA.  Each CTA streams an A tile (a_rows x K) and
+// a B tile (b_rows x K) of L2-resident bf16 matrices through a ring of
+// `stages` stages of BK columns (128-byte swizzled boxes of 64 x rows), the
+// way opevo_gemm's producer does, and the consumer only waits for arrival.
+// Reports per-SM bytes/clk and the loop time versus grid size, to tell a
+// per-SM ingress limit from a chip-wide (L2) one.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/bin/tma_bench tools/tma_bench.cu -lcuda
+#include <cstdio>
+#include <cstdlib>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+typedef unsigned int u32;
+typedef unsigned long long u64;
+
+__device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ u64 gtimer() { u64 t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t)); return t; }
+
+__global__ void __launch_bounds__(64, 1) tma_ingress(const __grid_constant__ CUtensorMap ma,
+                                                     const __grid_constant__ CUtensorMap mb, int a_rows,
+                                                     int b_rows, int K, int bk, int stages, int row_tiles,
+                                                     u64* out) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    __shared__ __align__(8) u64 full[16];
+    unsigned char* smem = (unsigned char*)(((u64)smem_raw + 1023) & ~1023ull);
+    const int stage_bytes = (a_rows + b_rows) * bk * 2;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&full[s])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" :: "l"(&ma) : "memory");
+        asm volatile("prefetch.tensormap [%0];" :: "l"(&mb) : "memory");
+    }
+    __syncthreads();
+    const int arow0 = (blockIdx.x % row_tiles) * a_rows;
+    const int brow0 = (blockIdx.x / row_tiles) * b_rows;
+    const int nkb = K / bk;
+    u64 c0 = clock64(), t0 = gtimer();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < nkb + stages; ++i) {
+            if (i >= stages) {      // consume stage (i - stages): wait for its bytes
+                const int s = (i - stages) % stages;
+                const u32 par = ((i - stages) / stages) & 1;
+                asm volatile("{ .reg .pred p; W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra W; }"
+                             :: "r"(smem_u32(&full[s])), "r"(par) : "memory");
+            }
+            if (i < nkb) {
+                const int s = i % stages;
+                const u32 bar = smem_u32(&full[s]);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(stage_bytes) : "memory");
+                const u32 a_dst = smem_u32(smem + s * stage_bytes);
+                const u32 b_dst = a_dst + a_rows * bk * 2;
+                for (int ka = 0; ka < bk / 64; ++ka) {
+                    const int kc = i * bk + ka * 64;
+                    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+                                 :: "r"(a_dst + ka * a_rows * 128), "l"(&ma), "r"(bar), "r"(kc), "r"(arow0) : "memory");
+                    if (b_rows > 0)
+                        asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+                                     :: "r"(b_dst + ka * b_rows * 128), "l"(&mb), "r"(bar), "r"(kc), "r"(brow0) : "memory");
+                }
+            }
+        }
+    }
+    __syncthreads();
+    u64 c1 = clock64(), t1 = gtimer();
+    if (threadIdx.x == 0) {
+        out[blockIdx.x * 2] = c1 - c0;
+        out[blockIdx.x * 2 + 1] = t1 - t0;
+    }
+}
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); exit(1); } } while (0)
+
+static CUtensorMap make_map(void* base, int rows, int K, int box_rows) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+    cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = cuTensorMapEncodeTiled(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, es,
+                                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) { printf("encode failed %d\n", (int)r); exit(1); }
+    return m;
+}
+
+int main() {
+    const int N = 1024, K = 1024;
+    void *a, *b;
+    CK(cudaMalloc(&a, (size_t)N * K * 2));
+    CK(cudaMalloc(&b, (size_t)N * K * 2));
+    CK(cudaMemset(a, 0, (size_t)N * K * 2));
+    CK(cudaMemset(b, 0, (size_t)N * K * 2));
+    u64* d_out;
+    CK(cudaMalloc(&d_out, sizeof(u64) * 2 * 1024));
+    CK(cudaFuncSetAttribute(tma_ingress, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    struct Cfg { int a_rows, b_rows, bk, stages; } cfgs[] = {
+        {128, 64, 128, 3}, {128, 64, 128, 4}, {128, 64, 64, 6}, {128, 128, 128, 3}, {128, 32, 128, 4},
+        {128, 32, 256, 2}, {256, 0, 128, 3}, {128, 0, 128, 4}, {128, 0, 256, 3}};
+    for (auto c : cfgs) {
+        CUtensorMap ma = make_map(a, N, K, c.a_rows);
+        CUtensorMap mb = make_map(b, N, K, c.b_rows > 0 ? c.b_rows : 8);
+        const int row_tiles = N / c.a_rows;
+        const int smem = (c.a_rows + c.b_rows) * c.bk * 2 * c.stages + 1024;
+        for (int grid : {1, 16, 64, 128, 148}) {
+            for (int rep = 0; rep < 3; ++rep)
+                tma_ingress<<<grid, 64, smem>>>(ma, mb, c.a_rows, c.b_rows, K, c.bk, c.stages, row_tiles, d_out);
+            CK(cudaDeviceSynchronize());
+            u64 h[2 * 148];
+            CK(cudaMemcpy(h, d_out, sizeof(u64) * 2 * grid, cudaMemcpyDeviceToHost));
+            double cyc = 0, ns = 0, mx = 0;
+            for (int i = 0; i < grid; ++i) { cyc += h[2 * i]; ns += h[2 * i + 1]; if (h[2 * i + 1] > mx) mx = h[2 * i + 1]; }
+            cyc /= grid; ns /= grid;
+            const double bytes = (double)(c.a_rows + c.b_rows) * K * 2;
+            printf("tile A%3d+B%3d BK%3d st%d grid=%3d: %6.1f B/clk/SM  %6.1f GB/s/SM  loop %.2f us (slowest %.2f)  chip %.1f TB/s\n",
+                   c.a_rows, c.b_rows, c.bk, c.stages, grid, bytes / cyc, bytes / ns, ns / 1e3, mx / 1e3,
+                   grid * bytes / mx / 1e3);
+        }
+    }
+    return 0;
+}

@@ -48,6 +48,13 @@ def main():
         rows["time"].append(t3 - t2)
         rows["get_warm"].append(t5 - t4)
         rows["trial"].append(tr1 - tr0)
+    valid = [kn for kn in cands]
+    bt = []
+    for lo in range(0, len(valid), 8):
+        t0 = time.perf_counter()
+        res = dev.trial_batch(op, valid[lo:lo + 8])
+        bt.append((time.perf_counter() - t0) / max(1, sum(r.ok for r in res)))
+    rows["batch_per_ok_trial"] = bt
     for name, v in rows.items():
         print(f"{name:9s} n={len(v)} median {1e3 * statistics.median(v):.3f} ms  "
               f"mean {1e3 * statistics.mean(v):.3f} ms  max {1e3 * max(v):.3f} ms")
