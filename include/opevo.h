@@ -83,7 +83,10 @@ enum opevo_knob {
                                  1: one CTA (cluster) per tile
                                  2: persistent, partial last wave split
                                     along K (stream-K style tail)         */
-    OPEVO_NUM_KNOBS = 11
+    OPEVO_KNOB_B_RES = 11,    /* conv: 1 = the whole weight panel (BN = Cout
+                                 x K) is loaded once into shared memory and
+                                 stays resident across the CTA's tiles     */
+    OPEVO_NUM_KNOBS = 12
 };
 
 /* Result of one trial (opevo_trial). */

@@ -37,7 +37,7 @@ STATUS_NAMES = {OK: "ok", INVALID_CONFIG: "invalid_config", COMPILE_ERROR: "comp
 
 MATMUL, BATCHMATMUL, CONV2D = 0, 1, 2
 BF16, F32 = 0, 1
-NUM_KNOBS = 11
+NUM_KNOBS = 12
 KNOB_NAMES = ("bm", "bn", "bk", "stages", "split", "cluster", "tile_h", "tile_w", "acc",
               "cta_group", "grid")
 
@@ -134,7 +134,7 @@ def load() -> C.CDLL:
     return lib
 
 
-_KNOB_DEFAULTS = (128, 128, 64, 4, 1, 1, 1, 1, 1, 1, 0)
+_KNOB_DEFAULTS = (128, 128, 64, 4, 1, 1, 1, 1, 1, 1, 0, 0)
 
 
 def _knob_array(knobs) -> "C.Array":

@@ -91,6 +91,9 @@
 #ifndef OPEVO_SPLIT_CLUSTER
 #define OPEVO_SPLIT_CLUSTER 0  // S > 1: the S K-slices of a tile form a cluster and reduce via DSMEM
 #endif
+#ifndef OPEVO_B_RES
+#define OPEVO_B_RES 0      // conv: the BN x K weight panel stays resident in shared memory
+#endif
 #ifndef OPEVO_ACC
 #define OPEVO_ACC 1        // K-interleaved TMEM accumulators (1, 2, 4)
 #endif
@@ -124,16 +127,27 @@ constexpr int BN_LOAD = BN / CG;                          // B rows this CTA sta
 constexpr int MATOMS = (CG == 1 && BM == 256) ? 2 : 1;    // M=128 MMAs per k-step
 constexpr int UMMA_M = (CG == 2) ? 256 : ((BM == 256) ? 128 : BM);
 constexpr int A_TILE = BM_CTA * BK * 2;
-constexpr int B_TILE = BN_LOAD * BK * 2;
+constexpr bool B_RES = OPEVO_B_RES != 0;
+constexpr int B_TILE = B_RES ? 0 : BN_LOAD * BK * 2;          // per stage (0: panel resident)
 constexpr int STAGE_BYTES = A_TILE + B_TILE;
 constexpr int TX_BYTES = STAGE_BYTES * CG;                // bytes landing per stage (pair)
 constexpr int A_SLICE_ROWS = BM_CTA / CLUSTER;            // rows of A each cluster CTA fetches
+// K-fused loads: with 128-byte swizzle the host encodes A and B as
+// {64, rows, K/64 (, batch)} "atom" views (row stride K*2 bytes, atom stride
+// 128 bytes), so one box {64, rows, KATOMS} lands a whole stage of an operand
+// atom-major -- one TMA instruction per operand per stage instead of one per
+// 64-wide K atom (per-instruction TMA cost, not bytes, bounds small stages).
+// Multicast slices and conv taps keep per-atom boxes.
+constexpr bool FUSED_K = (SWZ == 128) && (CLUSTER == 1) && !OPEVO_CONV;
 constexpr int ACC = OPEVO_ACC;
 constexpr int TMEM_USED = MATOMS * BN * ACC;
 constexpr int TMEM_COLS = TMEM_USED <= 32 ? 32 : TMEM_USED <= 64 ? 64 :
                           TMEM_USED <= 128 ? 128 : TMEM_USED <= 256 ? 256 : 512;
 constexpr u32 LAYOUT = SWZ == 128 ? 2u : SWZ == 64 ? 4u : 6u;
-constexpr int EPI_COLS = (BN % 32 == 0) ? 32 : 16;
+constexpr int EPI_COLS = (BN % 32 == 0) ? 32 : 16;    // split-K / DSMEM reduction chunks
+// TMA-store epilogue chunk: 64 bf16 columns (one 128-byte swizzle row) when
+// BN allows, so each chunk is one TMEM load, one proxy fence and one store
+constexpr int STORE_COLS = (!OPEVO_OUT_F32 && BN % 64 == 0 && OPEVO_ACC == 1) ? 64 : EPI_COLS;
 constexpr int NUM_THREADS = 192;
 constexpr int SMEM_ALIGN = 1024;
 constexpr int TILE_H = OPEVO_TILE_H;
@@ -185,11 +199,16 @@ constexpr int PIPE_BYTES = (STAGES * STAGE_BYTES > RED_BYTES) ? STAGES * STAGE_B
 // (row bytes 32/64/128 -> SW32/64/128), so the warp's smem writes are
 // conflict-free and each chunk leaves as one cp.async.bulk.tensor store.
 constexpr int OUT_BYTES = OPEVO_OUT_F32 ? 4 : 2;
-constexpr int EPI_ROW_BYTES = EPI_COLS * OUT_BYTES;       // 32, 64 or 128
+constexpr int EPI_ROW_BYTES = STORE_COLS * OUT_BYTES;     // 32, 64 or 128
 constexpr int EPI_BUF = 32 * EPI_ROW_BYTES;               // one chunk of one warp
 constexpr int EPI_OFF = (PIPE_BYTES + 1023) / 1024 * 1024;
 constexpr int EPI_BYTES = 4 * 2 * EPI_BUF;
 constexpr int BAR_OFF = EPI_OFF + EPI_BYTES;
+// resident weight panel (B_RES): [K/64 atoms][BN rows][128 B], after a
+// 1 KB barrier block; its size (BN x K) is a launch-time quantity
+constexpr int BRES_OFF = BAR_OFF + 1024;
+static_assert(!B_RES || (OPEVO_CONV && SWZ == 128 && CG == 1 && SPLITCL == 0),
+              "resident weights: conv, 128-byte swizzle");
 static_assert(SPLITCL == 0 || ((SPLITCL == 2 || SPLITCL == 4 || SPLITCL == 8) && CG == 1 && CLUSTER == 1 &&
                            MATOMS == 1 && BM % (SPLITCL * 8) == 0),
               "DSMEM split-K: S in {2,4,8}, single-CTA 128-row tiles");
@@ -241,8 +260,13 @@ __device__ __forceinline__ void mbar_arrive(u32 bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(bar) : "memory");
 }
 
+// Arrive on a peer CTA's mbarrier (shared::cluster address).  Used only to
+// hand a drained TMEM buffer back to the pair leader: the TMEM reads are
+// ordered by tcgen05.wait::ld + tcgen05.fence::before_thread_sync, so the
+// arrive needs no cluster-scope release (which costs a full memory barrier,
+// ~0.5 us, on every epilogue).
 __device__ __forceinline__ void mbar_arrive_cluster(u32 cluster_bar) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];"
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];"
                  :: "r"(cluster_bar) : "memory");
 }
 
@@ -443,6 +467,13 @@ __device__ __forceinline__ void tma2_load_3d(u32 dst, const TmaDesc* d, u32 bar,
                  :: "r"(dst), "l"(d), "r"(bar), "r"(c0), "r"(c1), "r"(c2) : "memory");
 }
 
+__device__ __forceinline__ void tma2_load_4d(u32 dst, const TmaDesc* d, u32 bar, int c0, int c1, int c2,
+                                             int c3) {
+    asm volatile("{ .reg .pred e; elect.sync _|e, 0xffffffff; @e cp.async.bulk.tensor.4d.cta_group::2"
+                 ".shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2]; }"
+                 :: "r"(dst), "l"(d), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3) : "memory");
+}
+
 __device__ __forceinline__ u32 mapa_cta(u32 addr, u32 rank) {
     u32 r;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
@@ -481,6 +512,15 @@ __device__ __forceinline__ void tmem_load<32>(u32 taddr, u32 (&v)[32]) {
                    "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
                    "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
                    "=r"(v[30]), "=r"(v[31])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <>
+__device__ __forceinline__ void tmem_load<64>(u32 taddr, u32 (&v)[64]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x64.b32 "
+                 "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31]), "=r"(v[32]), "=r"(v[33]), "=r"(v[34]), "=r"(v[35]), "=r"(v[36]), "=r"(v[37]), "=r"(v[38]), "=r"(v[39]), "=r"(v[40]), "=r"(v[41]), "=r"(v[42]), "=r"(v[43]), "=r"(v[44]), "=r"(v[45]), "=r"(v[46]), "=r"(v[47]), "=r"(v[48]), "=r"(v[49]), "=r"(v[50]), "=r"(v[51]), "=r"(v[52]), "=r"(v[53]), "=r"(v[54]), "=r"(v[55]), "=r"(v[56]), "=r"(v[57]), "=r"(v[58]), "=r"(v[59]), "=r"(v[60]), "=r"(v[61]), "=r"(v[62]), "=r"(v[63])
                  : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -525,23 +565,24 @@ __device__ __forceinline__ float4 ld_cg_f4(const float* p) {
 }
 
 // Sum the ACC interleaved accumulators of one row segment (fixed order).
-__device__ __forceinline__ void gather_acc(u32 taddr, float (&out)[EPI_COLS]) {
-    u32 v[EPI_COLS];
-    tmem_load<EPI_COLS>(taddr, v);
+template <int N = EPI_COLS>
+__device__ __forceinline__ void gather_acc(u32 taddr, float (&out)[N]) {
+    u32 v[N];
+    tmem_load<N>(taddr, v);
 #pragma unroll
-    for (int j = 0; j < EPI_COLS; ++j) out[j] = __uint_as_float(v[j]);
+    for (int j = 0; j < N; ++j) out[j] = __uint_as_float(v[j]);
 #pragma unroll
     for (int a = 1; a < ACC; ++a) {
-        tmem_load<EPI_COLS>(taddr + a * MATOMS * BN, v);
+        tmem_load<N>(taddr + a * MATOMS * BN, v);
 #pragma unroll
-        for (int j = 0; j < EPI_COLS; ++j) out[j] += __uint_as_float(v[j]);
+        for (int j = 0; j < N; ++j) out[j] += __uint_as_float(v[j]);
     }
 }
 
 // Stage one thread's row (EPI_COLS outputs) of a 32-row epilogue chunk in the
 // TMA swizzle of the C map: 16-byte unit j of row r lands at unit
 // j ^ ((r * EPI_ROW_BYTES / 128) mod units), i.e. SW128/SW64/SW32 for 128/64/32-byte rows.
-__device__ __forceinline__ void stage_row(u32 buf, int r, const float* acc) {
+__device__ __forceinline__ void stage_row(u32 buf, int r, const float (&acc)[STORE_COLS]) {
     constexpr int UNITS = EPI_ROW_BYTES / 16;
     const u32 row = buf + (u32)(r * EPI_ROW_BYTES);
     const int x = ((r * EPI_ROW_BYTES) >> 7) & (UNITS - 1);
@@ -598,7 +639,8 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
     u64* tfull_bar = empty_bar + STAGES;      // MMA -> epilogue, per TMEM buffer
     u64* tempty_bar = tfull_bar + NBUF;       // epilogue -> MMA, per TMEM buffer
     u64* red_bar = tempty_bar + NBUF;         // DSMEM split-K: peers' partial rows landed
-    u32* tmem_slot = reinterpret_cast<u32*>(red_bar + 1);
+    u64* bres_bar = red_bar + 1;              // weight panel landed (B_RES)
+    u32* tmem_slot = reinterpret_cast<u32*>(bres_bar + 1);
     u32* last_flag = tmem_slot + 1;
 
     const int warp = threadIdx.x >> 5;
@@ -651,6 +693,50 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
         return t;
     };
 
+    // Incremental walk over this CTA's units u_first, u_first + u_step, ...:
+    // the mixed-radix digits (K slice, column group, row tile, batch) of the
+    // step are computed once, so advancing costs adds and compares instead
+    // of decode()'s divisions on every unit in three warps (decode remains
+    // for the K-split tail of grid mode 2).
+    struct UnitWalk { int u, kz, colg, row, batch; };
+    const int klen0 = depth / sched.split;
+    const int num_kb0 = OPEVO_ABLATE == 2 ? 0 : klen0 / BK;
+    auto digits = [&](int q) -> UnitWalk {
+        UnitWalk w;
+        w.u = q;
+        w.kz = q % sched.split; q /= sched.split;
+        w.colg = q % sched.col_groups; q /= sched.col_groups;
+        w.row = q % sched.row_tiles;
+        w.batch = q / sched.row_tiles;
+        return w;
+    };
+    const UnitWalk step = digits(u_step);
+    auto walk_next = [&](UnitWalk& w) {
+        w.u += u_step;
+        w.kz += step.kz;
+        int c = w.kz >= sched.split;
+        if (c) w.kz -= sched.split;
+        w.colg += step.colg + c;
+        c = w.colg >= sched.col_groups;
+        if (c) w.colg -= sched.col_groups;
+        w.row += step.row + c;
+        c = w.row >= sched.row_tiles;
+        if (c) w.row -= sched.row_tiles;
+        w.batch += step.batch + c;
+    };
+    auto unit_of = [&](const UnitWalk& w) -> Unit {
+        if (w.u >= head_items) return decode(w.u);
+        Unit t;
+        t.split = sched.split;
+        t.kz = w.kz;
+        t.k0 = w.kz * klen0;
+        t.num_kb = num_kb0;
+        t.row_tile = w.row;
+        t.batch = w.batch;
+        t.col_tile = w.colg * CLUSTER + (int)mrank;
+        return t;
+    };
+
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tma_a);
         tma_prefetch(&tma_b);
@@ -671,11 +757,16 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
             // one phase per launch: expect the (SPLITCL-1) row blocks the peers push
             mbar_init(smem_u32(red_bar), 1);
         }
+        if (B_RES) mbar_init(smem_u32(bres_bar), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         if (SPLITCL > 1)
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
                          :: "r"(smem_u32(red_bar)), "r"((u32)((SPLITCL - 1) * RED_BLOCK_BYTES)) : "memory");
     }
+    __syncwarp();
+    // Publish the barrier inits cluster-wide now (every warp arrives before
+    // its own setup work); each role waits at the end of setup.
+    if (CLSZ > 1) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     if (warp == 1) {
         if (CG == 2) {
             asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
@@ -687,11 +778,16 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
             asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
         }
     }
+    // The producer only needs its own warp's barrier inits (and, in a
+    // cluster, the peers'): it arrives on named barrier 2 without waiting,
+    // so its first TMA does not wait for the TMEM allocation; the MMA and
+    // epilogue warps wait for both the inits and the allocation.
     tc_fence_before();
-    __syncthreads();
-    if (CLSZ > 1) cluster_sync();
+    if (warp == 0) asm volatile("bar.arrive 2, %0;" :: "n"(NUM_THREADS) : "memory");
+    else           asm volatile("bar.sync 2, %0;" :: "n"(NUM_THREADS) : "memory");
+    if (CLSZ > 1) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     tc_fence_after();
-    const u32 tmem_base = __shfl_sync(0xffffffffu, *tmem_slot, 0);   // warp-uniform
+    const u32 tmem_base = (warp == 0) ? 0u : __shfl_sync(0xffffffffu, *tmem_slot, 0);   // warp-uniform
     if (threadIdx.x == 0) TRACE(2);
 
     if (warp == 0) {
@@ -702,11 +798,21 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
         int issued = 0;                 // k-blocks issued; the first STAGES slots start free
         bool first = true;
         // everything up to the first global read happens before the PDL wait
-        const Unit t_first = decode(u_first < sched.units ? u_first : 0);
+        UnitWalk w = digits(u_first);
+        const Unit t_first = unit_of(w);
         pdl_wait();                     // operands may be the previous launch's output
         if (lane == 0) TRACE(9);
-        for (int u = u_first; u < sched.units; u += u_step) {
-            const Unit t = (u == u_first) ? t_first : decode(u);
+#if OPEVO_CONV
+        if (B_RES && w.u < sched.units) {
+            // the whole weight panel of this CTA's column tile, once: one box
+            // {64, BN, K/64} of the atom view lands it atom-major
+            const u32 bytes = (u32)BN * (u32)depth * 2u;
+            mbar_expect_tx(smem_u32(bres_bar), bytes);
+            tma_load_3d(smem_u32(smem + BRES_OFF), &tma_b, smem_u32(bres_bar), 0, t_first.col_tile * BN, 0);
+        }
+#endif
+        for (; w.u < sched.units; walk_next(w)) {
+            const Unit t = (w.u == u_first) ? t_first : unit_of(w);
             const int k0 = t.k0;
             const int num_kb = t.num_kb;
             const int col0 = t.col_tile * BN;
@@ -743,9 +849,30 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                 for (int ka = 0; ka < KATOMS; ++ka) {
                     tma_load_4d(a_dst + ka * (BM_CTA * SWZ), &tma_a, fb, cbase + ka * ATOM_K,
                                 w0 + dj, h0 + di, n0);
-                    tma_load_2d(b_dst + ka * (BN_LOAD * SWZ), &tma_b, fb, kk + ka * ATOM_K, col0);
+                    if (!B_RES)
+                        tma_load_2d(b_dst + ka * (BN_LOAD * SWZ), &tma_b, fb, kk + ka * ATOM_K, col0);
                 }
 #else
+                if (FUSED_K) {
+                    const int katom = kk / ATOM_K;
+#if OPEVO_CTA_GROUP == 2
+#if OPEVO_BATCHED
+                    tma2_load_4d(a_dst, &tma_a, fb, 0, row0, katom, t.batch);
+                    tma2_load_4d(b_dst, &tma_b, fb, 0, b_row0, katom, t.batch);
+#else
+                    tma2_load_3d(a_dst, &tma_a, fb, 0, row0, katom);
+                    tma2_load_3d(b_dst, &tma_b, fb, 0, b_row0, katom);
+#endif
+#else
+#if OPEVO_BATCHED
+                    tma_load_4d(a_dst, &tma_a, fb, 0, row0, katom, t.batch);
+                    tma_load_4d(b_dst, &tma_b, fb, 0, b_row0, katom, t.batch);
+#else
+                    tma_load_3d(a_dst, &tma_a, fb, 0, row0, katom);
+                    tma_load_3d(b_dst, &tma_b, fb, 0, b_row0, katom);
+#endif
+#endif
+                } else
 #pragma unroll
                 for (int ka = 0; ka < KATOMS; ++ka) {
                     const int kc = kk + ka * ATOM_K;
@@ -803,8 +930,11 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
             // rather than a rebuild from the address.
             const u64 desc_a0 = DESC_HI | (u64)((smem_u32(smem) >> 4) & 0x3FFF);
             const u64 desc_b0 = desc_a0 + (u64)(A_TILE >> 4);
-            for (int u = u_first; u < sched.units; u += u_step) {
-                const int num_kb = decode(u).num_kb;
+            const u64 desc_bres = DESC_HI | (u64)((smem_u32(smem + BRES_OFF) >> 4) & 0x3FFF);
+            if (B_RES) mbar_wait(smem_u32(bres_bar), 0);     // the resident weight panel
+            for (UnitWalk w = digits(u_first); w.u < sched.units; walk_next(w)) {
+                const Unit tu = unit_of(w);
+                const int num_kb = tu.num_kb;
                 // the epilogue must have drained this accumulator buffer
                 mbar_wait(smem_u32(tempty_bar + buf), bph ^ 1);
                 tc_fence_after();
@@ -819,7 +949,10 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                         continue;
                     }
                     const u64 sdesc = (u64)((u32)(s * STAGE_BYTES) >> 4);
-                    const u64 da = desc_a0 + sdesc, db = desc_b0 + sdesc;
+                    // B: this stage's slot, or the resident panel's atoms of this K block
+                    const u64 da = desc_a0 + sdesc;
+                    const u64 db = B_RES ? desc_bres + (u64)(((tu.k0 / BK + kb) * KATOMS * (BN * SWZ)) >> 4)
+                                         : desc_b0 + sdesc;
                     if (MATOMS == 1 && ACC == 1) {
                         // one accumulator: each swizzle atom's K16 steps in one asm block
 #pragma unroll
@@ -881,8 +1014,8 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
         bool first = true;
         const u32 epi_stage = smem_u32(smem + EPI_OFF) + (u32)(quarter * 2 * EPI_BUF);
         int nchunk = 0;                            // TMA-store chunks issued by this warp
-        for (int u = u_first; u < sched.units; u += u_step) {
-            const Unit t = decode(u);
+        for (UnitWalk w = digits(u_first); w.u < sched.units; walk_next(w)) {
+            const Unit t = unit_of(w);
             const int col0 = t.col_tile * BN;
 #if OPEVO_CONV
             const int w_tiles = geom.wo / TILE_W, h_tiles = geom.ho / TILE_H;
@@ -926,11 +1059,11 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                 for (int ma = 0; ma < MATOMS; ++ma) {
                     const int lr0 = ma * 128 + quarter * 32;           // first tile row of the chunk
 #pragma unroll 1
-                    for (int c = 0; c < BN; c += EPI_COLS) {
-                        float acc[EPI_COLS];
-                        gather_acc(lane_addr + ma * BN + c, acc);
+                    for (int c = 0; c < BN; c += STORE_COLS) {
+                        float acc[STORE_COLS];
+                        gather_acc<STORE_COLS>(lane_addr + ma * BN + c, acc);
                         if (first && c == 0 && epi_tid == 0) TRACE(12);
-                        if (ma == MATOMS - 1 && c + EPI_COLS >= BN) release();
+                        if (ma == MATOMS - 1 && c + STORE_COLS >= BN) release();
                         const u32 buf = epi_stage + (u32)((nchunk & 1) * EPI_BUF);
                         if (nchunk >= 2) {             // this buffer's previous store has read it
                             if (lane == 0) bulk_wait_read<1>();

@@ -188,13 +188,13 @@ void load_nvrtc() {
 
 // ------------------------------------------------------------- knobs
 struct Knobs {
-    int bm, bn, bk, stages, split, cluster, tile_h, tile_w, acc, cg, grid_mode;
+    int bm, bn, bk, stages, split, cluster, tile_h, tile_w, acc, cg, grid_mode, b_res;
 };
 
 Knobs read_knobs(const int32_t* k, int n) {
-    int32_t v[OPEVO_NUM_KNOBS] = {128, 128, 64, 4, 1, 1, 1, 1, 1, 1, 0};
+    int32_t v[OPEVO_NUM_KNOBS] = {128, 128, 64, 4, 1, 1, 1, 1, 1, 1, 0, 0};
     for (int i = 0; i < n && i < OPEVO_NUM_KNOBS; ++i) v[i] = k[i];
-    return Knobs{v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8], v[9], v[10]};
+    return Knobs{v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8], v[9], v[10], v[11]};
 }
 
 // TMEM columns the kernel allocates (two accumulator buffers when they fit).
@@ -207,6 +207,18 @@ int tmem_alloc_cols(const Knobs& k) {
 }
 
 int swizzle_bytes(int bk) { return bk * 2 >= 128 ? 128 : bk * 2; }
+
+// Weight-resident conv (knob b_res): the whole BN x K weight panel is loaded
+// once per CTA into shared memory (one TMA box of the atom view), so the
+// pipeline stages carry only the activation tile.  128-byte swizzle (BK a
+// multiple of 64) and no split over taps.
+bool b_resident(const Knobs& k, int family) {
+    return family == 1 && k.b_res && k.bk % 64 == 0 && k.split == 1;
+}
+
+// K-fused operand loads (GEMM family, 128-byte swizzle, no multicast slices):
+// mirrors FUSED_K in gemm_sm100.cuh.
+bool fused_k(const Knobs& k) { return swizzle_bytes(k.bk) == 128 && k.cluster == 1; }
 
 // DSMEM split-K (the split slices of a tile form a cluster and reduce in
 // shared memory) when the shape allows it; split is then compiled in.
@@ -223,12 +235,14 @@ bool dsmem_split(const Knobs& k, int family) {
            (dsmem_red_bytes(k) + 1023) / 1024 * 1024 + epi_stage_bytes(k, 0) + 1024 + 256 <= 232448;
 }
 
-// Epilogue chunk width (mirrors EPI_COLS in gemm_sm100.cuh).
-int epi_cols(const Knobs& k) { return k.bn % 32 == 0 ? 32 : 16; }
+// TMA-store epilogue chunk width (mirrors STORE_COLS in gemm_sm100.cuh).
+int epi_cols(const Knobs& k, int out_f32 = 0) {
+    return (!out_f32 && k.bn % 64 == 0 && k.acc == 1) ? 64 : k.bn % 32 == 0 ? 32 : 16;
+}
 
-// TMA-store staging: 4 epilogue warps x 2 buffers x 32 rows x EPI_COLS outputs.
+// TMA-store staging: 4 epilogue warps x 2 buffers x 32 rows x STORE_COLS outputs.
 size_t epi_stage_bytes(const Knobs& k, int out_f32) {
-    return (size_t)4 * 2 * 32 * epi_cols(k) * (out_f32 ? 4 : 2);
+    return (size_t)4 * 2 * 32 * epi_cols(k, out_f32) * (out_f32 ? 4 : 2);
 }
 
 // per-CTA: a CTA pair stages 128 rows of A and BN/2 rows of B each; then the
@@ -236,7 +250,7 @@ size_t epi_stage_bytes(const Knobs& k, int out_f32) {
 size_t smem_bytes(const Knobs& k, int family = 0, int out_f32 = 0) {
     if (family == 2) return 0;
     const int a_rows = k.cg == 2 ? 128 : k.bm;
-    const int b_rows = k.bn / (k.cg == 2 ? 2 : 1);
+    const int b_rows = b_resident(k, family) ? 0 : k.bn / (k.cg == 2 ? 2 : 1);
     size_t pipe = (size_t)k.stages * (size_t)(a_rows + b_rows) * (size_t)k.bk * 2;
     if (dsmem_split(k, family)) pipe = std::max(pipe, dsmem_red_bytes(k));
     pipe = (pipe + 1023) / 1024 * 1024;
@@ -281,9 +295,10 @@ std::string make_key(int family, const Knobs& k, int batched, int out_f32) {
                  want_lineinfo() ? "L" : "", (unsigned long long)(h & 0xffffffffffffull));
         return buf;
     }
-    snprintf(buf, sizeof buf, "f%d_m%d_n%d_k%d_s%d_b%d_o%d_c%d_h%d_w%d_a%d_g%d_%s%012llx", family,
+    snprintf(buf, sizeof buf, "f%d_m%d_n%d_k%d_s%d_b%d_o%d_c%d_h%d_w%d_a%d_g%d%s_%s%012llx", family,
              k.bm, k.bn, k.bk, k.stages, batched, out_f32, k.cluster, family == 1 ? k.tile_h : 1,
              family == 1 ? k.tile_w : 1, k.acc, k.cg * 100 + (dsmem_split(k, family) ? k.split : 0),
+             b_resident(k, family) ? "_r" : "",
              want_lineinfo() ? "L" : "",
              (unsigned long long)(h & 0xffffffffffffull));
     return buf;
@@ -448,7 +463,8 @@ int nvrtc_build(int family, const Knobs& k, int batched, int out_f32, std::vecto
         "-DOPEVO_TILE_W=" + std::to_string(family == 1 ? k.tile_w : 1),
         "-DOPEVO_ACC=" + std::to_string(k.acc),
         "-DOPEVO_CTA_GROUP=" + std::to_string(k.cg),
-        "-DOPEVO_SPLIT_CLUSTER=" + std::to_string(dsmem_split(k, family) ? k.split : 0)};
+        "-DOPEVO_SPLIT_CLUSTER=" + std::to_string(dsmem_split(k, family) ? k.split : 0),
+        "-DOPEVO_B_RES=" + std::to_string(b_resident(k, family) ? 1 : 0)};
     if (want_lineinfo()) opts.push_back("-lineinfo");
     {
         std::istringstream extra(extra_flags());
@@ -1227,14 +1243,30 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
         uint64_t strides[3] = {(uint64_t)C * 2, (uint64_t)C * W * 2, (uint64_t)C * W * H * 2};
         uint32_t box[4] = {atom_k, (uint32_t)k.tile_w, (uint32_t)k.tile_h, (uint32_t)tile_n};
         st = encode_map(&kr->tma_a, op->a, 4, dims, strides, box, swz, err, errlen);
-        uint64_t bd[2] = {(uint64_t)op->depth, (uint64_t)op->cols};
-        uint64_t bs[1] = {(uint64_t)op->depth * 2};
-        uint32_t bb[2] = {atom_k, (uint32_t)k.bn};
-        if (!st) st = encode_map(&kr->tma_b, op->b, 2, bd, bs, bb, swz, err, errlen);
+        if (b_resident(k, family)) {
+            // resident weight panel: atom view {64, Cout, K/64}, one box {64, BN, K/64}
+            const uint64_t d = (uint64_t)op->depth;
+            const size_t panel = (size_t)k.bn * d * 2;
+            if (!st && (op->cols != k.bn || d / 64 > 256 || kr->smem + 768 + panel > (size_t)ctx->smem_optin)) {
+                put_err(err, errlen, "resident weights need BN = Cout (%lld) and a %zu B panel that fits",
+                        (long long)op->cols, panel);
+                st = OPEVO_INVALID_CONFIG;
+            }
+            uint64_t bd[3] = {64, (uint64_t)op->cols, d / 64};
+            uint64_t bs[2] = {d * 2, 128};
+            uint32_t bb[3] = {64, (uint32_t)k.bn, (uint32_t)(d / 64)};
+            if (!st) st = encode_map(&kr->tma_b, op->b, 3, bd, bs, bb, 128, err, errlen);
+            kr->smem += 768 + panel;    // 1 KB barrier block before the panel (BRES_OFF)
+        } else {
+            uint64_t bd[2] = {(uint64_t)op->depth, (uint64_t)op->cols};
+            uint64_t bs[1] = {(uint64_t)op->depth * 2};
+            uint32_t bb[2] = {atom_k, (uint32_t)k.bn};
+            if (!st) st = encode_map(&kr->tma_b, op->b, 2, bd, bs, bb, swz, err, errlen);
+        }
         if (!st) {
             // output NHWC {Cout, Wo, Ho, N}; a 32-pixel epilogue chunk of the
             // TILE_N x TILE_H x TILE_W tile is the box {EPI_COLS, bw, bh, bn}
-            const int ob = op->out_f32 ? 4 : 2, ec = epi_cols(k);
+            const int ob = op->out_f32 ? 4 : 2, ec = epi_cols(k, op->out_f32);
             const int bw = std::min(k.tile_w, 32);
             const int bh = k.tile_w >= 32 ? 1 : std::min(k.tile_h, 32 / k.tile_w);
             const int bn = k.tile_w * k.tile_h >= 32 ? 1 : 32 / (k.tile_w * k.tile_h);
@@ -1252,18 +1284,35 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
         kr->sched = SchedHost{(N / tile_n) * (HO / k.tile_h) * (WO / k.tile_w), (int)col_tiles, 1,
                               k.split, 0, 1, 0};
     } else {
-        const int rank = batched ? 3 : 2;
-        uint64_t ad[3] = {(uint64_t)op->depth, (uint64_t)op->rows, (uint64_t)op->batch};
-        uint64_t as[2] = {(uint64_t)op->depth * 2, (uint64_t)op->depth * op->rows * 2};
         const uint32_t a_rows = (uint32_t)((k.cg == 2 ? 128 : k.bm) / k.cluster);
-        uint32_t ab[3] = {atom_k, a_rows, 1};
-        uint64_t bd[3] = {(uint64_t)op->depth, (uint64_t)op->cols, (uint64_t)op->batch};
-        uint64_t bs[2] = {(uint64_t)op->depth * 2, (uint64_t)op->depth * op->cols * 2};
-        uint32_t bb[3] = {atom_k, (uint32_t)(k.bn / k.cg), 1};
-        st = encode_map(&kr->tma_a, op->a, rank, ad, as, ab, swz, err, errlen);
-        if (!st) st = encode_map(&kr->tma_b, op->b, rank, bd, bs, bb, swz, err, errlen);
+        const uint32_t b_rows = (uint32_t)(k.bn / k.cg);
+        if (fused_k(k)) {
+            // "atom" views {64, rows, K/64 (, batch)}: one box per operand per
+            // stage (mirrors FUSED_K in gemm_sm100.cuh)
+            const int rank = batched ? 4 : 3;
+            const uint64_t d = (uint64_t)op->depth;
+            uint64_t ad[4] = {64, (uint64_t)op->rows, d / 64, (uint64_t)op->batch};
+            uint64_t as[3] = {d * 2, 128, d * op->rows * 2};
+            uint32_t ab[4] = {64, a_rows, (uint32_t)(k.bk / 64), 1};
+            uint64_t bd[4] = {64, (uint64_t)op->cols, d / 64, (uint64_t)op->batch};
+            uint64_t bs[3] = {d * 2, 128, d * op->cols * 2};
+            uint32_t bb[4] = {64, b_rows, (uint32_t)(k.bk / 64), 1};
+            st = encode_map(&kr->tma_a, op->a, rank, ad, as, ab, 128, err, errlen);
+            if (!st) st = encode_map(&kr->tma_b, op->b, rank, bd, bs, bb, 128, err, errlen);
+        } else {
+            const int rank = batched ? 3 : 2;
+            uint64_t ad[3] = {(uint64_t)op->depth, (uint64_t)op->rows, (uint64_t)op->batch};
+            uint64_t as[2] = {(uint64_t)op->depth * 2, (uint64_t)op->depth * op->rows * 2};
+            uint32_t ab[3] = {atom_k, a_rows, 1};
+            uint64_t bd[3] = {(uint64_t)op->depth, (uint64_t)op->cols, (uint64_t)op->batch};
+            uint64_t bs[2] = {(uint64_t)op->depth * 2, (uint64_t)op->depth * op->cols * 2};
+            uint32_t bb[3] = {atom_k, b_rows, 1};
+            st = encode_map(&kr->tma_a, op->a, rank, ad, as, ab, swz, err, errlen);
+            if (!st) st = encode_map(&kr->tma_b, op->b, rank, bd, bs, bb, swz, err, errlen);
+        }
+        const int rank = batched ? 3 : 2;
         if (!st) {
-            const int ob = op->out_f32 ? 4 : 2, ec = epi_cols(k);
+            const int ob = op->out_f32 ? 4 : 2, ec = epi_cols(k, op->out_f32);
             uint64_t cd[3] = {(uint64_t)op->cols, (uint64_t)op->rows, (uint64_t)op->batch};
             uint64_t cs[2] = {(uint64_t)op->cols * ob, (uint64_t)op->cols * op->rows * ob};
             uint32_t cb[3] = {(uint32_t)ec, 32, 1};

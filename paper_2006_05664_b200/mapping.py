@@ -29,8 +29,10 @@ Cout / co[0]; ``ho[0]``, ``wo[0]`` -> the output tile TILE_H = Ho / ho[0],
 TILE_W = Wo / wo[0] (BM = 128 pixels = TILE_N x TILE_H x TILE_W); ``ci[0]`` ->
 BK = Cin / ci[0] channels per stage; ``kh[0] * kw[0]`` -> split-K over filter
 taps; ``unroll_step`` -> pipeline stages {0:2, 16:3, 64:4, 512:6, 1500:8};
-``unroll_explicit`` has no counterpart (the MMA issue loop is always
-unrolled).
+``unroll_explicit`` = on selects the weight-resident variant when it applies
+(BN = Cout, BK a multiple of 64, no split over taps): the whole BN x K weight
+panel is loaded once per CTA and stays in shared memory -- the K loop is
+"unrolled" over resident weights -- so the stages carry activations only.
 
 A configuration whose mapping is infeasible is *invalid* and scores 0, as an
 un-compilable TVM configuration does in the paper.
@@ -41,6 +43,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 from .operators import (
+    UNROLL_ON,
     BatchMatMulSpec,
     Conv2dSpec,
     MatMulSpec,
@@ -75,10 +78,13 @@ class Knobs:
     tile_w: int = 1
     acc: int = 1
     cta_group: int = 1
+    grid: int = 0
+    b_res: int = 0           # conv: weight panel resident in shared memory
+    panel_bytes: int = 0     # its size (BN x K x 2; not a code knob)
 
     def as_tuple(self) -> tuple[int, ...]:
         return (self.bm, self.bn, self.bk, self.stages, self.split, self.cluster,
-                self.tile_h, self.tile_w, self.acc, self.cta_group)
+                self.tile_h, self.tile_w, self.acc, self.cta_group, self.grid, self.b_res)
 
     def dsmem_split(self) -> int:
         """Split factor compiled in when the K slices reduce through DSMEM
@@ -94,10 +100,12 @@ class Knobs:
         """Fields that change the generated code (split-K is a launch arg
         except for DSMEM-reduced splits)."""
         return (self.bm, self.bn, self.bk, self.stages, self.cluster, self.tile_h, self.tile_w,
-                self.acc, self.cta_group, self.dsmem_split())
+                self.acc, self.cta_group, self.dsmem_split(), self.b_res)
 
     def smem_bytes(self) -> int:
         """Mirrors ``smem_bytes`` in csrc/opevo.cpp (bf16 output)."""
+        if self.b_res:
+            return _align1k(self.bm * self.bk * 2 * self.stages) + epi_bytes(self.bn) + 2048 + self.panel_bytes
         pipe = stage_bytes(self.bm, self.bn, self.bk, self.cta_group) * self.stages
         if self.dsmem_split():
             ld = self.bn + 4
@@ -125,8 +133,8 @@ def _align1k(n: int) -> int:
 
 def epi_bytes(bn: int) -> int:
     """TMA-store staging of the epilogue (bf16 output): 4 warps x 2 buffers
-    x 32 rows x EPI_COLS (32, or 16 when BN is not a multiple of 32)."""
-    return 4 * 2 * 32 * (32 if bn % 32 == 0 else 16) * 2
+    x 32 rows x STORE_COLS (64, 32 or 16: the widest dividing BN)."""
+    return 4 * 2 * 32 * (64 if bn % 64 == 0 else 32 if bn % 32 == 0 else 16) * 2
 
 
 def stage_bytes(bm: int, bn: int, bk: int, cta_group: int = 1) -> int:
@@ -219,10 +227,31 @@ def _conv_knobs(spec: Conv2dSpec, vals: dict) -> tuple[Knobs | None, str]:
     if not _bk_ok(bk):
         return None, f"BK={bk} channels is not a TMA/UMMA K stage"
     split = kh[0] * kw[0]
-    stages = _fit_stages(UNROLL_TO_STAGES[vals["unroll_step"]], bm, bn, bk)
+    want = UNROLL_TO_STAGES[vals["unroll_step"]]
+    if vals.get("unroll_explicit") == UNROLL_ON:
+        stages, panel = _conv_resident_fit(spec, bn, bk, split, want)
+        if stages:
+            return Knobs(bm, bn, bk, stages, split, 1, th, tw, b_res=1, panel_bytes=panel), ""
+    stages = _fit_stages(want, bm, bn, bk)
     if stages < 1:
         return None, "one stage does not fit in shared memory"
     return Knobs(bm, bn, bk, stages, split, 1, th, tw), ""
+
+
+def _conv_resident_fit(spec: Conv2dSpec, bn: int, bk: int, split: int, want: int) -> tuple[int, int]:
+    """(stages, panel bytes) of the weight-resident conv variant -- the whole
+    BN x K weight panel loaded once per CTA, stages carry activations only --
+    or (0, 0) when it does not apply (needs BN = Cout, BK a multiple of 64, no
+    split over taps, the panel plus two stages within 227 KB).  Mirrors
+    ``b_resident`` / the panel check in csrc/opevo.cpp."""
+    depth = spec.kernel_h * spec.kernel_w * spec.in_channels
+    if bn != spec.out_channels or bk % 64 or split != 1 or depth // 64 > 256:
+        return 0, 0
+    panel = bn * depth * 2
+    s = want
+    while s > 0 and _align1k(s * 128 * bk * 2) + epi_bytes(bn) + 2048 + panel > SMEM_LIMIT:
+        s -= 1
+    return (s, panel) if s >= 2 else (0, 0)
 
 
 def _simt_knobs(vals: dict) -> tuple[Knobs | None, str]:

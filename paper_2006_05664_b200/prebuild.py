@@ -14,7 +14,7 @@ import time
 from concurrent.futures import ThreadPoolExecutor
 
 from . import capi
-from .mapping import STAGE_VALUES, UNROLL_TO_STAGES, Knobs, _bk_ok, _fit_stages
+from .mapping import _conv_resident_fit, STAGE_VALUES, UNROLL_TO_STAGES, Knobs, _bk_ok, _fit_stages
 from .operators import BatchMatMulSpec, Conv2dSpec, MatMulSpec, parse_operator
 
 
@@ -72,6 +72,11 @@ def family_instances(spec) -> set[tuple[int, bool, tuple]]:
                         s = _fit_stages(st, 128, bn, bk)
                         if s >= 1:
                             out.add((1, False, Knobs(128, bn, bk, s, 1, 1, th, tw).as_tuple()))
+                        # weight-resident variant (unroll_explicit = 1)
+                        rs, panel = _conv_resident_fit(spec, bn, bk, 1, st)
+                        if rs:
+                            out.add((1, False, Knobs(128, bn, bk, rs, 1, 1, th, tw, b_res=1,
+                                                     panel_bytes=panel).as_tuple()))
     return out
 
 

@@ -134,6 +134,10 @@ def test_batchmatmul_parity(dev, knobs):
     (128, 32, 64, 3, 1, 1, 4, 8),
     (128, 64, 32, 6, 3, 1, 2, 8),
     (128, 64, 64, 4, 1, 1, 1, 8),
+    # weight-resident panel (knob 11): stages carry activations only
+    (128, 64, 64, 4, 1, 1, 8, 8, 1, 1, 0, 1),
+    (128, 64, 64, 3, 1, 1, 4, 2, 1, 1, 0, 1),
+    (128, 64, 64, 6, 1, 1, 8, 8, 1, 1, 0, 1),
 ])
 def test_conv2d_parity(dev, knobs):
     import oracle

@@ -70,6 +70,71 @@ __global__ void __launch_bounds__(64, 1) tma_ingress(const __grid_constant__ CUt
     }
 }
 
+// Same loads, one box per operand per stage: 3-D maps {64, rows, K/64}
+// (strides: K*2 bytes per row, 128 bytes per 64-element K atom) with box
+// {64, rows, bk/64} land the stage's K atoms atom-major in one instruction.
+__global__ void __launch_bounds__(64, 1) tma_ingress3d(const __grid_constant__ CUtensorMap ma,
+                                                       const __grid_constant__ CUtensorMap mb, int a_rows,
+                                                       int b_rows, int K, int bk, int stages, int row_tiles,
+                                                       u64* out) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    __shared__ __align__(8) u64 full[16];
+    unsigned char* smem = (unsigned char*)(((u64)smem_raw + 1023) & ~1023ull);
+    const int stage_bytes = (a_rows + b_rows) * bk * 2;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&full[s])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int arow0 = (blockIdx.x % row_tiles) * a_rows;
+    const int brow0 = (blockIdx.x / row_tiles) * b_rows;
+    const int nkb = K / bk;
+    u64 c0 = clock64(), t0 = gtimer();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < nkb + stages; ++i) {
+            if (i >= stages) {
+                const int s = (i - stages) % stages;
+                const u32 par = ((i - stages) / stages) & 1;
+                asm volatile("{ .reg .pred p; W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra W; }"
+                             :: "r"(smem_u32(&full[s])), "r"(par) : "memory");
+            }
+            if (i < nkb) {
+                const int s = i % stages;
+                const u32 bar = smem_u32(&full[s]);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(stage_bytes) : "memory");
+                const u32 a_dst = smem_u32(smem + s * stage_bytes);
+                const u32 b_dst = a_dst + a_rows * bk * 2;
+                const int katom = i * bk / 64;
+                asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+                             :: "r"(a_dst), "l"(&ma), "r"(bar), "r"(0), "r"(arow0), "r"(katom) : "memory");
+                if (b_rows > 0)
+                    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+                                 :: "r"(b_dst), "l"(&mb), "r"(bar), "r"(0), "r"(brow0), "r"(katom) : "memory");
+            }
+        }
+    }
+    __syncthreads();
+    u64 c1 = clock64(), t1 = gtimer();
+    if (threadIdx.x == 0) {
+        out[blockIdx.x * 2] = c1 - c0;
+        out[blockIdx.x * 2 + 1] = t1 - t0;
+    }
+}
+
+static CUtensorMap make_map3(void* base, int rows, int K, int box_rows, int box_atoms) {
+    CUtensorMap m;
+    cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)(K / 64)};
+    cuuint64_t strides[2] = {(cuuint64_t)K * 2, 128};
+    cuuint32_t box[3] = {64, (cuuint32_t)box_rows, (cuuint32_t)box_atoms};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = cuTensorMapEncodeTiled(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, es,
+                                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) { printf("encode3 failed %d\n", (int)r); exit(1); }
+    return m;
+}
+
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); exit(1); } } while (0)
 
 static CUtensorMap make_map(void* base, int rows, int K, int box_rows) {
@@ -98,14 +163,23 @@ int main() {
     struct Cfg { int a_rows, b_rows, bk, stages; } cfgs[] = {
         {128, 64, 128, 3}, {128, 64, 128, 4}, {128, 64, 64, 6}, {128, 128, 128, 3}, {128, 32, 128, 4},
         {128, 32, 256, 2}, {256, 0, 128, 3}, {128, 0, 128, 4}, {128, 0, 256, 3}};
+    CK(cudaFuncSetAttribute(tma_ingress3d, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    for (int mode = 0; mode < 2; ++mode)
     for (auto c : cfgs) {
+        if (mode == 1 && c.b_rows == 0) continue;
         CUtensorMap ma = make_map(a, N, K, c.a_rows);
         CUtensorMap mb = make_map(b, N, K, c.b_rows > 0 ? c.b_rows : 8);
         const int row_tiles = N / c.a_rows;
         const int smem = (c.a_rows + c.b_rows) * c.bk * 2 * c.stages + 1024;
-        for (int grid : {1, 16, 64, 128, 148}) {
-            for (int rep = 0; rep < 3; ++rep)
-                tma_ingress<<<grid, 64, smem>>>(ma, mb, c.a_rows, c.b_rows, K, c.bk, c.stages, row_tiles, d_out);
+        for (int grid : {1, 128}) {
+            CUtensorMap ma3 = make_map3(a, N, K, c.a_rows, c.bk / 64);
+            CUtensorMap mb3 = make_map3(b, N, K, c.b_rows > 0 ? c.b_rows : 8, c.bk / 64);
+            for (int rep = 0; rep < 3; ++rep) {
+                if (mode == 0)
+                    tma_ingress<<<grid, 64, smem>>>(ma, mb, c.a_rows, c.b_rows, K, c.bk, c.stages, row_tiles, d_out);
+                else
+                    tma_ingress3d<<<grid, 64, smem>>>(ma3, mb3, c.a_rows, c.b_rows, K, c.bk, c.stages, row_tiles, d_out);
+            }
             CK(cudaDeviceSynchronize());
             u64 h[2 * 148];
             CK(cudaMemcpy(h, d_out, sizeof(u64) * 2 * grid, cudaMemcpyDeviceToHost));
@@ -113,6 +187,7 @@ int main() {
             for (int i = 0; i < grid; ++i) { cyc += h[2 * i]; ns += h[2 * i + 1]; if (h[2 * i + 1] > mx) mx = h[2 * i + 1]; }
             cyc /= grid; ns /= grid;
             const double bytes = (double)(c.a_rows + c.b_rows) * K * 2;
+            printf(mode ? "3D " : "2D ");
             printf("tile A%3d+B%3d BK%3d st%d grid=%3d: %6.1f B/clk/SM  %6.1f GB/s/SM  loop %.2f us (slowest %.2f)  chip %.1f TB/s\n",
                    c.a_rows, c.b_rows, c.bk, c.stages, grid, bytes / cyc, bytes / ns, ns / 1e3, mx / 1e3,
                    grid * bytes / mx / 1e3);

@@ -37,7 +37,12 @@ def main():
     t0 = tr[:, 1].min()
     print(f"{spec.id()} knobs={knobs} ctas={ctas} distinct SMs={len(set(tr[:, 0]))}")
     for name, a, b in PHASES:
-        d = (tr[:, b] - (t0 if a is None else tr[:, a])) / 1e3
+        # stamps a CTA never writes (e.g. MMA stamps of a CTA-pair follower) are 0
+        ok = (tr[:, b] != 0) & ((tr[:, a] != 0) if a is not None else True)
+        if not ok.any():
+            print(f"  {name:20s} (no stamps)")
+            continue
+        d = (tr[ok, b] - (t0 if a is None else tr[ok, a])) / 1e3
         print(f"  {name:20s} min {d.min():7.2f}  med {np.median(d):7.2f}  max {d.max():7.2f} us")
     print(f"  kernel span (first entry -> last exit): {(tr[:, 8].max() - t0) / 1e3:.2f} us")
     if nl > 1:
@@ -48,10 +53,14 @@ def main():
         print(f"  back-to-back x{nl} (us from launch 0 first entry):")
         print("    launch  first-entry  med-entry  med-post-wait  med-first-MMA  med-MMA-done  "
               "med-epi-done  last-exit")
+        def med(col):
+            v = col[col != 0]
+            return np.median((v - z) / 1e3) if v.size else float("nan")
+
         for i in range(nl):
             t = (tl[i] - z) / 1e3
-            print(f"    {i:6d}  {t[:, 1].min():11.2f}  {np.median(t[:, 1]):9.2f}  {np.median(t[:, 9]):13.2f}"
-                  f"  {np.median(t[:, 4]):13.2f}  {np.median(t[:, 5]):12.2f}  {np.median(t[:, 7]):12.2f}"
+            print(f"    {i:6d}  {t[:, 1].min():11.2f}  {med(tl[i][:, 1]):9.2f}  {med(tl[i][:, 9]):13.2f}"
+                  f"  {med(tl[i][:, 4]):13.2f}  {med(tl[i][:, 5]):12.2f}  {med(tl[i][:, 7]):12.2f}"
                   f"  {t[:, 8].max():9.2f}")
         span = (tl[-1, :, 8].max() - tl[0, :, 1].min()) / 1e3
         print(f"  steady state: {span / nl:.2f} us per launch over {nl} launches")
