@@ -216,11 +216,16 @@ def _conv_knobs(spec: Conv2dSpec, vals: dict) -> tuple[Knobs | None, str]:
     bn = spec.out_channels // co[0]
     th, tw = spec.out_height // ho[0], spec.out_width // wo[0]
     bk = spec.in_channels // ci[0]
-    bm = 128
+    # an even Cout virtual-thread split runs two M=128 atoms per K step:
+    # 256-pixel tiles, so each tap's activation box is twice as large (a TMA
+    # box costs about the same whatever its size, so this halves the boxes)
+    bm = 256 if co[1] % 2 == 0 else 128
     if bn % 16 or not 16 <= bn <= 256:
         return None, f"BN={bn} is not a UMMA column tile"
+    if bm == 256 and 2 * bn > 512:
+        return None, "accumulator exceeds TMEM"
     if th * tw > bm or bm % (th * tw):
-        return None, f"output tile {th}x{tw} does not divide 128 pixels"
+        return None, f"output tile {th}x{tw} does not divide {bm} pixels"
     tn = bm // (th * tw)
     if spec.batch % tn or tn > 256 or th > 256 or tw > 256:
         return None, f"image tile {tn} does not divide the batch {spec.batch}"
@@ -229,7 +234,7 @@ def _conv_knobs(spec: Conv2dSpec, vals: dict) -> tuple[Knobs | None, str]:
     split = kh[0] * kw[0]
     want = UNROLL_TO_STAGES[vals["unroll_step"]]
     if vals.get("unroll_explicit") == UNROLL_ON:
-        stages, panel = _conv_resident_fit(spec, bn, bk, split, want)
+        stages, panel = _conv_resident_fit(spec, bn, bk, split, want, bm)
         if stages:
             return Knobs(bm, bn, bk, stages, split, 1, th, tw, b_res=1, panel_bytes=panel), ""
     stages = _fit_stages(want, bm, bn, bk)
@@ -238,7 +243,8 @@ def _conv_knobs(spec: Conv2dSpec, vals: dict) -> tuple[Knobs | None, str]:
     return Knobs(bm, bn, bk, stages, split, 1, th, tw), ""
 
 
-def _conv_resident_fit(spec: Conv2dSpec, bn: int, bk: int, split: int, want: int) -> tuple[int, int]:
+def _conv_resident_fit(spec: Conv2dSpec, bn: int, bk: int, split: int, want: int,
+                       bm: int = 128) -> tuple[int, int]:
     """(stages, panel bytes) of the weight-resident conv variant -- the whole
     BN x K weight panel loaded once per CTA, stages carry activations only --
     or (0, 0) when it does not apply (needs BN = Cout, BK a multiple of 64, no
@@ -249,7 +255,7 @@ def _conv_resident_fit(spec: Conv2dSpec, bn: int, bk: int, split: int, want: int
         return 0, 0
     panel = bn * depth * 2
     s = want
-    while s > 0 and _align1k(s * 128 * bk * 2) + epi_bytes(bn) + 2048 + panel > SMEM_LIMIT:
+    while s > 0 and _align1k(s * bm * bk * 2) + epi_bytes(bn) + 2048 + panel > SMEM_LIMIT:
         s -= 1
     return (s, panel) if s >= 2 else (0, 0)
 

@@ -59,23 +59,23 @@ def family_instances(spec) -> set[tuple[int, bool, tuple]]:
             return out
         ths = [t for t in _divisors(spec.out_height) if 128 % t == 0]
         tws = [t for t in _divisors(spec.out_width) if 128 % t == 0]
-        for th, tw in itertools.product(ths, tws):
-            if th * tw > 128 or spec.batch % (128 // (th * tw)):
+        for bm, th, tw in itertools.product((128, 256), ths, tws):
+            if th * tw > bm or bm % (th * tw) or spec.batch % (bm // (th * tw)):
                 continue
             for bn in range(16, 257, 16):
-                if spec.out_channels % bn:
+                if spec.out_channels % bn or (bm == 256 and 2 * bn > 512):
                     continue
                 for bk in _divisors(spec.in_channels):
                     if not _bk_ok(bk):
                         continue
                     for st in set(UNROLL_TO_STAGES.values()):
-                        s = _fit_stages(st, 128, bn, bk)
+                        s = _fit_stages(st, bm, bn, bk)
                         if s >= 1:
-                            out.add((1, False, Knobs(128, bn, bk, s, 1, 1, th, tw).as_tuple()))
-                        # weight-resident variant (unroll_explicit = 1)
-                        rs, panel = _conv_resident_fit(spec, bn, bk, 1, st)
+                            out.add((1, False, Knobs(bm, bn, bk, s, 1, 1, th, tw).as_tuple()))
+                        # weight-resident variant (unroll_explicit = on)
+                        rs, panel = _conv_resident_fit(spec, bn, bk, 1, st, bm)
                         if rs:
-                            out.add((1, False, Knobs(128, bn, bk, rs, 1, 1, th, tw, b_res=1,
+                            out.add((1, False, Knobs(bm, bn, bk, rs, 1, 1, th, tw, b_res=1,
                                                      panel_bytes=panel).as_tuple()))
     return out
 

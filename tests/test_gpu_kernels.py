@@ -138,6 +138,10 @@ def test_batchmatmul_parity(dev, knobs):
     (128, 64, 64, 4, 1, 1, 8, 8, 1, 1, 0, 1),
     (128, 64, 64, 3, 1, 1, 4, 2, 1, 1, 0, 1),
     (128, 64, 64, 6, 1, 1, 8, 8, 1, 1, 0, 1),
+    # 256-pixel tiles (two M=128 atoms per K step), streaming and resident
+    (256, 64, 64, 4, 1, 1, 8, 8),
+    (256, 64, 64, 3, 1, 1, 8, 8, 1, 1, 0, 1),
+    (256, 32, 64, 4, 3, 1, 4, 8),
 ])
 def test_conv2d_parity(dev, knobs):
     import oracle

@@ -135,6 +135,54 @@ static CUtensorMap make_map3(void* base, int rows, int K, int box_rows, int box_
     return m;
 }
 
+// Conv-like activation loads: a 4-D NHWC map {C=64, W, H, N} with box
+// {64, tw, th, tn} (128 pixels x 128 B), shifted per filter tap like the
+// implicit-GEMM producer; `taps` boxes per tile, tiles walked like the
+// persistent conv kernel.
+__global__ void __launch_bounds__(64, 1) tma_conv4d(const __grid_constant__ CUtensorMap mx, int tw, int th, int tn,
+                                                    int W, int H, int N, int tiles_per_cta, int stages, u64* out) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    __shared__ __align__(8) u64 full[16];
+    unsigned char* smem = (unsigned char*)(((u64)smem_raw + 1023) & ~1023ull);
+    const int stage_bytes = 128 * 128;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&full[s])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int wt = W / tw, ht = H / th;
+    const int n_it = tiles_per_cta * 9;
+    u64 c0 = clock64(), t0 = gtimer();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < n_it + stages; ++i) {
+            if (i >= stages) {
+                const int s = (i - stages) % stages;
+                const u32 par = ((i - stages) / stages) & 1;
+                asm volatile("{ .reg .pred p; W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra W; }"
+                             :: "r"(smem_u32(&full[s])), "r"(par) : "memory");
+            }
+            if (i < n_it) {
+                const int s = i % stages;
+                const u32 bar = smem_u32(&full[s]);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(stage_bytes) : "memory");
+                const int tile = blockIdx.x + (i / 9) * gridDim.x, tap = i % 9;
+                const int w0 = (tile % wt) * tw, h0 = ((tile / wt) % ht) * th, n0 = (tile / (wt * ht)) * tn;
+                const int dj = tap % 3 - 1, di = tap / 3 - 1;
+                asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];"
+                             :: "r"(smem_u32(smem + s * stage_bytes)), "l"(&mx), "r"(bar), "r"(0), "r"(w0 + dj),
+                                "r"(h0 + di), "r"(n0 % N) : "memory");
+            }
+        }
+    }
+    __syncthreads();
+    u64 c1 = clock64(), t1 = gtimer();
+    if (threadIdx.x == 0) {
+        out[blockIdx.x * 2] = c1 - c0;
+        out[blockIdx.x * 2 + 1] = t1 - t0;
+    }
+}
+
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); exit(1); } } while (0)
 
 static CUtensorMap make_map(void* base, int rows, int K, int box_rows) {
@@ -191,6 +239,40 @@ int main() {
             printf("tile A%3d+B%3d BK%3d st%d grid=%3d: %6.1f B/clk/SM  %6.1f GB/s/SM  loop %.2f us (slowest %.2f)  chip %.1f TB/s\n",
                    c.a_rows, c.b_rows, c.bk, c.stages, grid, bytes / cyc, bytes / ns, ns / 1e3, mx / 1e3,
                    grid * bytes / mx / 1e3);
+        }
+    }
+    {
+        // conv activations NHWC 32x56x56x64 bf16
+        const int N = 32, H = 56, W = 56, C = 64;
+        void* x;
+        CK(cudaMalloc(&x, (size_t)N * H * W * C * 2));
+        CK(cudaMemset(x, 0, (size_t)N * H * W * C * 2));
+        CK(cudaFuncSetAttribute(tma_conv4d, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        int shapes[][3] = {{8, 8, 2}, {8, 4, 4}, {4, 8, 4}, {8, 2, 8}, {2, 8, 8}, {8, 1, 16}};
+        for (auto& sh : shapes) {
+            CUtensorMap m;
+            cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+            cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)C * W * 2, (cuuint64_t)C * W * H * 2};
+            cuuint32_t box[4] = {64, (cuuint32_t)sh[0], (cuuint32_t)sh[1], (cuuint32_t)sh[2]};
+            cuuint32_t es[4] = {1, 1, 1, 1};
+            CUresult r = cuTensorMapEncodeTiled(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, x, dims, strides, box, es,
+                                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) { printf("encode4 failed %d\n", (int)r); continue; }
+            for (int stages : {4, 8}) {
+                const int grid = 148, tiles = 5;
+                for (int rep = 0; rep < 3; ++rep)
+                    tma_conv4d<<<grid, 64, stages * 16384 + 1024>>>(m, sh[0], sh[1], sh[2], W, H, N, tiles, stages, d_out);
+                CK(cudaDeviceSynchronize());
+                u64 h[2 * 148];
+                CK(cudaMemcpy(h, d_out, sizeof(u64) * 2 * grid, cudaMemcpyDeviceToHost));
+                double ns = 0, cyc = 0;
+                for (int i = 0; i < grid; ++i) { cyc += h[2 * i]; ns += h[2 * i + 1]; }
+                cyc /= grid; ns /= grid;
+                const double bytes = tiles * 9.0 * 16384;
+                printf("conv4d box w%d h%d n%d st%d: %6.1f B/clk/SM %6.1f GB/s/SM  %.0f ns per box\n", sh[0], sh[1], sh[2],
+                       stages, bytes / cyc, bytes / ns, ns / (tiles * 9));
+            }
         }
     }
     return 0;
