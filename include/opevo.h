@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define OPEVO_ABI_VERSION 1
+#define OPEVO_ABI_VERSION 2   /* 2: 12-slot knob vector (b_res), trial batch, preload */
 
 enum opevo_status {
     OPEVO_OK = 0,
