@@ -1727,7 +1727,10 @@ int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nk
     std::vector<int> gst(count, OPEVO_OK);
     std::vector<std::string> gmsg(count);
     bool pooled = false;
-    if (!fatal && mode == 0) {
+    // OPEVO_NO_POOL=1: build the graphs on this thread (profilers that do not
+    // follow stream capture on other threads, e.g. an ncu launch list)
+    static const bool no_pool = getenv("OPEVO_NO_POOL") != nullptr;
+    if (!fatal && mode == 0 && !no_pool) {
         if (!ctx->pool) {
             const int nw = 6;
             for (int w = 0; w < nw; ++w) {
