@@ -45,6 +45,20 @@ def test_nvrtc_compiles_instances_without_gpu(tmp_path):
     assert len(files) == 4 and all(f.endswith(".cubin") for f in files)
 
 
+def test_conv_variants_compile_without_gpu(tmp_path):
+    """The weight-resident (knob 11) and 256-pixel conv variants are distinct
+    compile keys and build with NVRTC; the resident flag only applies to
+    un-split, 128-byte-swizzle instances."""
+    cache = str(tmp_path)
+    capi.compile_kernel(1, (256, 64, 64, 3, 1, 1, 8, 8, 1, 1, 0, 1), False, False, cache)
+    capi.compile_kernel(1, (256, 64, 64, 4, 1, 1, 8, 8), False, False, cache)
+    k0 = capi.kernel_key(1, (128, 64, 64, 4, 1, 1, 8, 8), False, False)
+    k1 = capi.kernel_key(1, (128, 64, 64, 4, 1, 1, 8, 8, 1, 1, 0, 1), False, False)
+    k2 = capi.kernel_key(1, (128, 64, 32, 4, 1, 1, 8, 8, 1, 1, 0, 1), False, False)   # SW64: not resident
+    k3 = capi.kernel_key(1, (128, 64, 32, 4, 1, 1, 8, 8), False, False)
+    assert k0 != k1 and "_r_" in k1 and k2 == k3
+
+
 def test_split_is_a_launch_argument_unless_reduced_in_dsmem():
     k1 = capi.kernel_key(0, (128, 64, 64, 4, 1, 1), False, False)
     k16 = capi.kernel_key(0, (128, 64, 64, 4, 16, 1), False, False)   # global reduction

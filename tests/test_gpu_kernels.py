@@ -275,3 +275,33 @@ def test_trial_batch_matches_single_trials(dev):
         assert _rel(op.output(), _oracle_gemm(1, rows, cols, depth, 1234)) < BF16_TOL
     finally:
         op.close()
+
+
+@pytest.mark.parametrize("op_id", ["matmul:1024,1024,1024", "batchmatmul:960,128,64,128",
+                                   "conv2d:32,64,56,56,64,3,3,1,1"])
+def test_mapping_smem_matches_library(dev, op_id):
+    """The mapping's shared-memory accounting (stage fitting) equals what the
+    library requests at launch for every sampled valid configuration."""
+    from paper_2006_05664_b200.evaluator import _op_args
+    from paper_2006_05664_b200.mapping import config_to_knobs, gpu_operator_space
+    from paper_2006_05664_b200.operators import parse_operator
+
+    spec = parse_operator(op_id)
+    space = gpu_operator_space(spec)
+    op = dev.prepare(**_op_args(spec))
+    rng = np.random.default_rng(3)
+    seen = 0
+    try:
+        for _ in range(3000):
+            m = config_to_knobs(spec, space, space.sample_uniform(rng))
+            if not m.valid:
+                continue
+            k = dev.kernel(op, m.knobs.as_tuple())
+            assert k.info.smem_bytes == m.knobs.smem_bytes(), (m.knobs, k.info.smem_bytes)
+            k.close()
+            seen += 1
+            if seen >= 40:
+                break
+        assert seen >= 10
+    finally:
+        op.close()
