@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define OPEVO_ABI_VERSION 2   /* 2: 12-slot knob vector (b_res), trial batch, preload */
+#define OPEVO_ABI_VERSION 3   /* 3: 13-slot knob vector (b_res, bpu), trial batch, preload */
 
 enum opevo_status {
     OPEVO_OK = 0,
@@ -86,7 +86,10 @@ enum opevo_knob {
     OPEVO_KNOB_B_RES = 11,    /* conv: 1 = the whole weight panel (BN = Cout
                                  x K) is loaded once into shared memory and
                                  stays resident across the CTA's tiles     */
-    OPEVO_NUM_KNOBS = 12
+    OPEVO_KNOB_BPU = 12,      /* BatchMatMul: consecutive batches per CTA
+                                 work unit (1, 2, 4), loaded by one TMA box
+                                 per operand and stage                    */
+    OPEVO_NUM_KNOBS = 13
 };
 
 /* Result of one trial (opevo_trial). */

@@ -94,6 +94,10 @@
 #ifndef OPEVO_B_RES
 #define OPEVO_B_RES 0      // conv: the BN x K weight panel stays resident in shared memory
 #endif
+#ifndef OPEVO_BPU
+#define OPEVO_BPU 1        // BatchMatMul: consecutive batches per work unit (one TMA box per
+                           // operand and stage covers all of them; accumulators side by side)
+#endif
 #ifndef OPEVO_ACC
 #define OPEVO_ACC 1        // K-interleaved TMEM accumulators (1, 2, 4)
 #endif
@@ -126,9 +130,12 @@ constexpr int BM_CTA = (CG == 2) ? 128 : BM;             // A rows resident in t
 constexpr int BN_LOAD = BN / CG;                          // B rows this CTA stages
 constexpr int MATOMS = (CG == 1 && BM == 256) ? 2 : 1;    // M=128 MMAs per k-step
 constexpr int UMMA_M = (CG == 2) ? 256 : ((BM == 256) ? 128 : BM);
-constexpr int A_TILE = BM_CTA * BK * 2;
+constexpr int BPU = OPEVO_BPU;
+constexpr int A_SUB = BM_CTA * BK * 2;                    // one batch's A tile of a stage
+constexpr int A_TILE = BPU * A_SUB;
 constexpr bool B_RES = OPEVO_B_RES != 0;
-constexpr int B_TILE = B_RES ? 0 : BN_LOAD * BK * 2;          // per stage (0: panel resident)
+constexpr int B_SUB = BN_LOAD * BK * 2;
+constexpr int B_TILE = B_RES ? 0 : BPU * B_SUB;               // per stage (0: panel resident)
 constexpr int STAGE_BYTES = A_TILE + B_TILE;
 constexpr int TX_BYTES = STAGE_BYTES * CG;                // bytes landing per stage (pair)
 constexpr int A_SLICE_ROWS = BM_CTA / CLUSTER;            // rows of A each cluster CTA fetches
@@ -140,7 +147,7 @@ constexpr int A_SLICE_ROWS = BM_CTA / CLUSTER;            // rows of A each clus
 // Multicast slices and conv taps keep per-atom boxes.
 constexpr bool FUSED_K = (SWZ == 128) && (CLUSTER == 1) && !OPEVO_CONV;
 constexpr int ACC = OPEVO_ACC;
-constexpr int TMEM_USED = MATOMS * BN * ACC;
+constexpr int TMEM_USED = MATOMS * BN * ACC * BPU;
 constexpr int TMEM_COLS = TMEM_USED <= 32 ? 32 : TMEM_USED <= 64 ? 64 :
                           TMEM_USED <= 128 ? 128 : TMEM_USED <= 256 ? 256 : 512;
 constexpr u32 LAYOUT = SWZ == 128 ? 2u : SWZ == 64 ? 4u : 6u;
@@ -183,6 +190,9 @@ constexpr int NBUF = (2 * TMEM_USED <= 512) ? 2 : 1;
 constexpr int TMEM_ALLOC = (NBUF * TMEM_USED <= 32) ? 32 : (NBUF * TMEM_USED <= 64) ? 64 :
                            (NBUF * TMEM_USED <= 128) ? 128 : (NBUF * TMEM_USED <= 256) ? 256 : 512;
 constexpr int SPLITCL = OPEVO_SPLIT_CLUSTER;   // DSMEM split-K cluster size (0: off)
+static_assert(BPU == 1 || (OPEVO_BATCHED && CG == 1 && CLUSTER == 1 && MATOMS == 1 && ACC == 1 &&
+                           SPLITCL == 0 && (FUSED_K || KATOMS == 1)),
+              "batches per unit: single-CTA 128-row BatchMatMul tiles");
 constexpr int CLSZ = CLUSTER * CG * (SPLITCL > 1 ? SPLITCL : 1);   // CTAs per cluster (launch dim x)
 // DSMEM reduction buffers (reusing the pipeline smem after the mainloop):
 // OWN [BM][RED_LD] fp32, then RECV [SPLITCL-1][BM/SPLITCL][RED_LD] fp32.  Rows
@@ -865,8 +875,8 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
 #endif
 #else
 #if OPEVO_BATCHED
-                    tma_load_4d(a_dst, &tma_a, fb, 0, row0, katom, t.batch);
-                    tma_load_4d(b_dst, &tma_b, fb, 0, b_row0, katom, t.batch);
+                    tma_load_4d(a_dst, &tma_a, fb, 0, row0, katom, t.batch * BPU);
+                    tma_load_4d(b_dst, &tma_b, fb, 0, b_row0, katom, t.batch * BPU);
 #else
                     tma_load_3d(a_dst, &tma_a, fb, 0, row0, katom);
                     tma_load_3d(b_dst, &tma_b, fb, 0, b_row0, katom);
@@ -899,13 +909,13 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
 #endif
 #else
 #if OPEVO_BATCHED
-                    tma_load_3d(a_sub, &tma_a, fb, kc, row0, t.batch);
+                    tma_load_3d(a_sub, &tma_a, fb, kc, row0, t.batch * BPU);
 #else
                     tma_load_2d(a_sub, &tma_a, fb, kc, row0);
 #endif
 #endif
 #if OPEVO_BATCHED
-                    tma_load_3d(b_sub, &tma_b, fb, kc, b_row0, t.batch);
+                    tma_load_3d(b_sub, &tma_b, fb, kc, b_row0, t.batch * BPU);
 #else
                     tma_load_2d(b_sub, &tma_b, fb, kc, b_row0);
 #endif
@@ -954,14 +964,19 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                     const u64 db = B_RES ? desc_bres + (u64)(((tu.k0 / BK + kb) * KATOMS * (BN * SWZ)) >> 4)
                                          : desc_b0 + sdesc;
                     if (MATOMS == 1 && ACC == 1) {
-                        // one accumulator: each swizzle atom's K16 steps in one asm block
+                        // one accumulator per batch of the unit: each swizzle
+                        // atom's K16 steps in one asm block
+#pragma unroll
+                        for (int j = 0; j < BPU; ++j) {
 #pragma unroll
                         for (int ka = 0; ka < KATOMS; ++ka) {
-                            const u64 adesc = da + (u64)((ka * (BM_CTA * SWZ)) >> 4);
-                            const u64 bdesc = db + (u64)((ka * (BN_LOAD * SWZ)) >> 4);
+                            const u64 adesc = da + (u64)((j * A_SUB + ka * (BM_CTA * SWZ)) >> 4);
+                            const u64 bdesc = db + (u64)((j * B_SUB + ka * (BN_LOAD * SWZ)) >> 4);
                             const u32 accumulate = (kb != 0 || ka != 0) ? 1u : 0u;
-                            if (CG == 2) umma2_atom<ATOM_K / 16>(acc_base, adesc, bdesc, accumulate);
-                            else         umma1_atom<ATOM_K / 16>(acc_base, adesc, bdesc, accumulate);
+                            const u32 d = acc_base + (u32)(j * BN);
+                            if (CG == 2) umma2_atom<ATOM_K / 16>(d, adesc, bdesc, accumulate);
+                            else         umma1_atom<ATOM_K / 16>(d, adesc, bdesc, accumulate);
+                        }
                         }
                     } else {
 #pragma unroll
@@ -1056,14 +1071,17 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                 // TMEM -> registers -> swizzled smem chunk -> TMA store (one
                 // bulk store per 32 x EPI_COLS chunk; two buffers per warp)
 #pragma unroll 1
-                for (int ma = 0; ma < MATOMS; ++ma) {
+                for (int jm = 0; jm < MATOMS * BPU; ++jm) {
+                    // jm: M atom (MATOMS > 1) or batch of the unit (BPU > 1)
+                    const int ma = MATOMS > 1 ? jm : 0;
+                    const int jb = BPU > 1 ? jm : 0;
                     const int lr0 = ma * 128 + quarter * 32;           // first tile row of the chunk
 #pragma unroll 1
                     for (int c = 0; c < BN; c += STORE_COLS) {
                         float acc[STORE_COLS];
-                        gather_acc<STORE_COLS>(lane_addr + ma * BN + c, acc);
+                        gather_acc<STORE_COLS>(lane_addr + jm * BN + c, acc);
                         if (first && c == 0 && epi_tid == 0) TRACE(12);
-                        if (ma == MATOMS - 1 && c + STORE_COLS >= BN) release();
+                        if (jm == MATOMS * BPU - 1 && c + STORE_COLS >= BN) release();
                         const u32 buf = epi_stage + (u32)((nchunk & 1) * EPI_BUF);
                         if (nchunk >= 2) {             // this buffer's previous store has read it
                             if (lane == 0) bulk_wait_read<1>();
@@ -1079,7 +1097,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                             const int w_l = lr0 % TILE_W;
                             tma_store_4d(&tma_c, buf, col0 + c, w0 + w_l, h0 + h_l, n0 + n_l);
 #elif OPEVO_BATCHED
-                            tma_store_3d(&tma_c, buf, col0 + c, out_row(lr0), t.batch);
+                            tma_store_3d(&tma_c, buf, col0 + c, out_row(lr0), t.batch * BPU + jb);
 #else
                             tma_store_2d(&tma_c, buf, col0 + c, out_row(lr0));
 #endif

@@ -188,18 +188,18 @@ void load_nvrtc() {
 
 // ------------------------------------------------------------- knobs
 struct Knobs {
-    int bm, bn, bk, stages, split, cluster, tile_h, tile_w, acc, cg, grid_mode, b_res;
+    int bm, bn, bk, stages, split, cluster, tile_h, tile_w, acc, cg, grid_mode, b_res, bpu;
 };
 
 Knobs read_knobs(const int32_t* k, int n) {
-    int32_t v[OPEVO_NUM_KNOBS] = {128, 128, 64, 4, 1, 1, 1, 1, 1, 1, 0, 0};
+    int32_t v[OPEVO_NUM_KNOBS] = {128, 128, 64, 4, 1, 1, 1, 1, 1, 1, 0, 0, 1};
     for (int i = 0; i < n && i < OPEVO_NUM_KNOBS; ++i) v[i] = k[i];
-    return Knobs{v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8], v[9], v[10], v[11]};
+    return Knobs{v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8], v[9], v[10], v[11], v[12]};
 }
 
 // TMEM columns the kernel allocates (two accumulator buffers when they fit).
 int tmem_alloc_cols(const Knobs& k) {
-    const int used = (k.cg == 1 && k.bm == 256 ? 2 : 1) * k.bn * k.acc;
+    const int used = (k.cg == 1 && k.bm == 256 ? 2 : 1) * k.bn * k.acc * std::max(1, k.bpu);
     const int want = (2 * used <= 512 ? 2 : 1) * used;
     int cols = 32;
     while (cols < want) cols *= 2;
@@ -251,7 +251,7 @@ size_t smem_bytes(const Knobs& k, int family = 0, int out_f32 = 0) {
     if (family == 2) return 0;
     const int a_rows = k.cg == 2 ? 128 : k.bm;
     const int b_rows = b_resident(k, family) ? 0 : k.bn / (k.cg == 2 ? 2 : 1);
-    size_t pipe = (size_t)k.stages * (size_t)(a_rows + b_rows) * (size_t)k.bk * 2;
+    size_t pipe = (size_t)k.stages * (size_t)(a_rows + b_rows) * (size_t)k.bk * 2 * (size_t)std::max(1, k.bpu);
     if (dsmem_split(k, family)) pipe = std::max(pipe, dsmem_red_bytes(k));
     pipe = (pipe + 1023) / 1024 * 1024;
     return pipe + epi_stage_bytes(k, out_f32) + 1024 + 256;
@@ -298,7 +298,7 @@ std::string make_key(int family, const Knobs& k, int batched, int out_f32) {
     snprintf(buf, sizeof buf, "f%d_m%d_n%d_k%d_s%d_b%d_o%d_c%d_h%d_w%d_a%d_g%d%s_%s%012llx", family,
              k.bm, k.bn, k.bk, k.stages, batched, out_f32, k.cluster, family == 1 ? k.tile_h : 1,
              family == 1 ? k.tile_w : 1, k.acc, k.cg * 100 + (dsmem_split(k, family) ? k.split : 0),
-             b_resident(k, family) ? "_r" : "",
+             b_resident(k, family) ? "_r" : k.bpu > 1 ? (k.bpu == 2 ? "_u2" : "_u4") : "",
              want_lineinfo() ? "L" : "",
              (unsigned long long)(h & 0xffffffffffffull));
     return buf;
@@ -369,7 +369,13 @@ bool knobs_compilable(int family, const Knobs& k, char* err, size_t len) {
         put_err(err, len, "cta_group=%d needs BM=256, no multicast cluster, GEMM family", k.cg);
         return false;
     }
-    if ((k.cg == 1 && k.bm == 256 ? 2 : 1) * k.bn * k.acc > 512) {
+    if (!(k.bpu == 1 || k.bpu == 2 || k.bpu == 4) ||
+        (k.bpu > 1 && (family != 0 || k.cg != 1 || k.cluster != 1 || k.bm != 128 || k.acc != 1 || k.split != 1 ||
+                       (k.bk > 32 && k.bk % 64) || dsmem_split(k, family)))) {
+        put_err(err, len, "bpu=%d needs a single-CTA 128-row GEMM tile, no multicast or DSMEM split", k.bpu);
+        return false;
+    }
+    if ((k.cg == 1 && k.bm == 256 ? 2 : 1) * k.bn * k.acc * std::max(1, k.bpu) > 512) {
         put_err(err, len, "accumulators %dx%d x%d exceed 512 TMEM columns", k.bm, k.bn, k.acc);
         return false;
     }
@@ -464,7 +470,8 @@ int nvrtc_build(int family, const Knobs& k, int batched, int out_f32, std::vecto
         "-DOPEVO_ACC=" + std::to_string(k.acc),
         "-DOPEVO_CTA_GROUP=" + std::to_string(k.cg),
         "-DOPEVO_SPLIT_CLUSTER=" + std::to_string(dsmem_split(k, family) ? k.split : 0),
-        "-DOPEVO_B_RES=" + std::to_string(b_resident(k, family) ? 1 : 0)};
+        "-DOPEVO_B_RES=" + std::to_string(b_resident(k, family) ? 1 : 0),
+        "-DOPEVO_BPU=" + std::to_string(family == 0 ? std::max(1, k.bpu) : 1)};
     if (want_lineinfo()) opts.push_back("-lineinfo");
     {
         std::istringstream extra(extra_flags());
@@ -1286,6 +1293,13 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
     } else {
         const uint32_t a_rows = (uint32_t)((k.cg == 2 ? 128 : k.bm) / k.cluster);
         const uint32_t b_rows = (uint32_t)(k.bn / k.cg);
+        const uint32_t bpu = (uint32_t)std::max(1, k.bpu);     // batches per work unit
+        if (bpu > 1 && (!batched || op->batch % bpu)) {
+            put_err(err, errlen, "bpu=%u needs a BatchMatMul whose batch (%lld) it divides", bpu,
+                    (long long)op->batch);
+            delete kr;
+            return OPEVO_INVALID_CONFIG;
+        }
         if (fused_k(k)) {
             // "atom" views {64, rows, K/64 (, batch)}: one box per operand per
             // stage (mirrors FUSED_K in gemm_sm100.cuh)
@@ -1293,20 +1307,20 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
             const uint64_t d = (uint64_t)op->depth;
             uint64_t ad[4] = {64, (uint64_t)op->rows, d / 64, (uint64_t)op->batch};
             uint64_t as[3] = {d * 2, 128, d * op->rows * 2};
-            uint32_t ab[4] = {64, a_rows, (uint32_t)(k.bk / 64), 1};
+            uint32_t ab[4] = {64, a_rows, (uint32_t)(k.bk / 64), bpu};
             uint64_t bd[4] = {64, (uint64_t)op->cols, d / 64, (uint64_t)op->batch};
             uint64_t bs[3] = {d * 2, 128, d * op->cols * 2};
-            uint32_t bb[4] = {64, b_rows, (uint32_t)(k.bk / 64), 1};
+            uint32_t bb[4] = {64, b_rows, (uint32_t)(k.bk / 64), bpu};
             st = encode_map(&kr->tma_a, op->a, rank, ad, as, ab, 128, err, errlen);
             if (!st) st = encode_map(&kr->tma_b, op->b, rank, bd, bs, bb, 128, err, errlen);
         } else {
             const int rank = batched ? 3 : 2;
             uint64_t ad[3] = {(uint64_t)op->depth, (uint64_t)op->rows, (uint64_t)op->batch};
             uint64_t as[2] = {(uint64_t)op->depth * 2, (uint64_t)op->depth * op->rows * 2};
-            uint32_t ab[3] = {atom_k, a_rows, 1};
+            uint32_t ab[3] = {atom_k, a_rows, bpu};
             uint64_t bd[3] = {(uint64_t)op->depth, (uint64_t)op->cols, (uint64_t)op->batch};
             uint64_t bs[2] = {(uint64_t)op->depth * 2, (uint64_t)op->depth * op->cols * 2};
-            uint32_t bb[3] = {atom_k, b_rows, 1};
+            uint32_t bb[3] = {atom_k, b_rows, bpu};
             st = encode_map(&kr->tma_a, op->a, rank, ad, as, ab, swz, err, errlen);
             if (!st) st = encode_map(&kr->tma_b, op->b, rank, bd, bs, bb, swz, err, errlen);
         }
@@ -1318,7 +1332,7 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
             uint32_t cb[3] = {(uint32_t)ec, 32, 1};
             st = encode_map(&kr->tma_c, op->c, rank, cd, cs, cb, ec * ob, err, errlen, op->out_f32);
         }
-        kr->sched = SchedHost{(int)row_tiles, (int)(col_tiles / k.cluster), (int)op->batch, k.split,
+        kr->sched = SchedHost{(int)row_tiles, (int)(col_tiles / k.cluster), (int)(op->batch / bpu), k.split,
                               0, 1, 0};
     }
     const bool dsm = dsmem_split(k, family);

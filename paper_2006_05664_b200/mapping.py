@@ -80,11 +80,12 @@ class Knobs:
     cta_group: int = 1
     grid: int = 0
     b_res: int = 0           # conv: weight panel resident in shared memory
-    panel_bytes: int = 0     # its size (BN x K x 2; not a code knob)
+    bpu: int = 1             # BatchMatMul: batches per work unit
+    panel_bytes: int = 0     # size of the resident panel (BN x K x 2; not a code knob)
 
     def as_tuple(self) -> tuple[int, ...]:
         return (self.bm, self.bn, self.bk, self.stages, self.split, self.cluster,
-                self.tile_h, self.tile_w, self.acc, self.cta_group, self.grid, self.b_res)
+                self.tile_h, self.tile_w, self.acc, self.cta_group, self.grid, self.b_res, self.bpu)
 
     def dsmem_split(self) -> int:
         """Split factor compiled in when the K slices reduce through DSMEM
@@ -100,13 +101,13 @@ class Knobs:
         """Fields that change the generated code (split-K is a launch arg
         except for DSMEM-reduced splits)."""
         return (self.bm, self.bn, self.bk, self.stages, self.cluster, self.tile_h, self.tile_w,
-                self.acc, self.cta_group, self.dsmem_split(), self.b_res)
+                self.acc, self.cta_group, self.dsmem_split(), self.b_res, self.bpu)
 
     def smem_bytes(self) -> int:
         """Mirrors ``smem_bytes`` in csrc/opevo.cpp (bf16 output)."""
         if self.b_res:
             return _align1k(self.bm * self.bk * 2 * self.stages) + epi_bytes(self.bn) + 2048 + self.panel_bytes
-        pipe = stage_bytes(self.bm, self.bn, self.bk, self.cta_group) * self.stages
+        pipe = stage_bytes(self.bm, self.bn, self.bk, self.cta_group) * self.stages * self.bpu
         if self.dsmem_split():
             ld = self.bn + 4
             pipe = max(pipe, self.bm * ld * 4 + (self.split - 1) * (self.bm // self.split) * ld * 4)
@@ -149,10 +150,10 @@ def _bk_ok(bk: int) -> bool:
     return bk in (16, 32) or (64 <= bk <= 256 and bk % 64 == 0)
 
 
-def _fit_stages(want: int, bm: int, bn: int, bk: int, cta_group: int = 1) -> int:
+def _fit_stages(want: int, bm: int, bn: int, bk: int, cta_group: int = 1, bpu: int = 1) -> int:
     """Largest ring depth <= want whose shared memory (pipeline, epilogue
     staging, barriers) fits in 227 KB; 0 when not even one stage fits."""
-    sb = stage_bytes(bm, bn, bk, cta_group)
+    sb = stage_bytes(bm, bn, bk, cta_group) * bpu
     s = want
     while s > 0 and _align1k(s * sb) + epi_bytes(bn) + SMEM_EXTRA > SMEM_LIMIT:
         s -= 1
@@ -186,7 +187,8 @@ def gpu_operator_space(spec: OperatorSpec, dtype: str = "bf16") -> SearchSpace:
     return SearchSpace(list(zip(base.names, base.spaces)) + [("stages", Discrete(STAGE_VALUES))])
 
 
-def _gemm_knobs(rows: int, cols: int, depth: int, vals: dict) -> tuple[Knobs | None, str]:
+def _gemm_knobs(rows: int, cols: int, depth: int, vals: dict,
+                batch: int = 0) -> tuple[Knobs | None, str]:
     n, m, k = vals["n"], vals["m"], vals["k"]
     bm, bn = rows // n[0], cols // m[0]
     split, bk = k[0], k[2]
@@ -201,11 +203,30 @@ def _gemm_knobs(rows: int, cols: int, depth: int, vals: dict) -> tuple[Knobs | N
     cta_group = 2 if (bm == 256 and n[1] % 2 == 0) else 1
     if (2 if (bm == 256 and cta_group == 1) else 1) * bn > 512:
         return None, "accumulator exceeds TMEM"
-    stages = _fit_stages(int(vals.get("stages", 4)), bm, bn, bk, cta_group)
+    bpu = _batches_per_unit(vals, batch, bm, bn, bk, split, cta_group)
+    stages = _fit_stages(int(vals.get("stages", 4)), bm, bn, bk, cta_group, bpu)
     if stages < 1:
         return None, "one stage does not fit in shared memory"
-    cluster = 1 if cta_group == 2 else _largest_pow2_divisor(m[1], m[0])
-    return Knobs(bm, bn, bk, stages, split, cluster, cta_group=cta_group), ""
+    cluster = 1 if (cta_group == 2 or bpu > 1) else _largest_pow2_divisor(m[1], m[0])
+    return Knobs(bm, bn, bk, stages, split, cluster, cta_group=cta_group, bpu=bpu), ""
+
+
+def _batches_per_unit(vals: dict, batch: int, bm: int, bn: int, bk: int, split: int,
+                      cta_group: int) -> int:
+    """BatchMatMul: the batch factor's inner level ``b[1]`` (batches handled by
+    one block in the paper's schedule) -> consecutive batches per CTA work
+    unit, the largest of {4, 2, 1} dividing it: one TMA box per operand and
+    stage then carries all of them (a box costs about the same whatever its
+    size) and their accumulators sit side by side in TMEM.  Single-CTA
+    128-row tiles without a K split only (mirrors ``bpu`` in csrc/opevo.cpp)."""
+    if not batch or "b" not in vals or bm != 128 or cta_group != 1 or split != 1:
+        return 1
+    if bk > 32 and bk % 64:
+        return 1
+    u = _largest_pow2_divisor(vals["b"][1], batch)
+    while u > 1 and 2 * u * bn > 512:        # two TMEM buffers of u x BN columns
+        u //= 2
+    return u
 
 
 def _conv_knobs(spec: Conv2dSpec, vals: dict) -> tuple[Knobs | None, str]:
@@ -287,7 +308,7 @@ def config_to_knobs(spec: OperatorSpec, space: SearchSpace, config: tuple,
         kn, why = _gemm_knobs(spec.n, spec.m, spec.k, vals)
         return Mapped(kn, why, FAMILY_GEMM, False)
     if isinstance(spec, BatchMatMulSpec):
-        kn, why = _gemm_knobs(spec.n, spec.m, spec.k, vals)
+        kn, why = _gemm_knobs(spec.n, spec.m, spec.k, vals, batch=spec.b)
         return Mapped(kn, why, FAMILY_GEMM, True)
     if isinstance(spec, Conv2dSpec):
         kn, why = _conv_knobs(spec, vals)

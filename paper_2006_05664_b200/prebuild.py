@@ -48,6 +48,14 @@ def family_instances(spec) -> set[tuple[int, bool, tuple]]:
                             for c in (clusters if cg == 1 else {1}):
                                 out.add((0, batched, Knobs(bm, bn, bk, s, 1, c,
                                                            cta_group=cg).as_tuple()))
+                            # BatchMatMul units of several batches (bpu)
+                            if batched and cg == 1 and bm == 128 and not (bk > 32 and bk % 64):
+                                for u in (2, 4):
+                                    if spec.b % u or 2 * u * bn > 512:
+                                        continue
+                                    su = _fit_stages(st, bm, bn, bk, 1, u)
+                                    if su >= 1:
+                                        out.add((0, batched, Knobs(bm, bn, bk, su, 1, 1, bpu=u).as_tuple()))
                             # DSMEM split-K instances compile the split in
                             if cg == 1 and bm == 128:
                                 for sp in (2, 4, 8):

@@ -114,7 +114,11 @@ def test_matmul_parity(dev, rows, cols, depth, knobs):
 
 
 @pytest.mark.parametrize("knobs", [(128, 64, 64, 2, 1, 1), (128, 64, 64, 2, 2, 1), (128, 64, 32, 4, 4, 1),
-                                   (128, 32, 64, 4, 1, 2), (256, 64, 64, 3, 1, 1, 1, 1, 1, 2)])
+                                   (128, 32, 64, 4, 1, 2), (256, 64, 64, 3, 1, 1, 1, 1, 1, 2),
+                                   # several batches per work unit (knob 12)
+                                   (128, 64, 128, 2, 1, 1, 1, 1, 1, 1, 0, 0, 2),
+                                   (128, 64, 64, 2, 1, 1, 1, 1, 1, 1, 0, 0, 4),
+                                   (128, 32, 32, 4, 1, 1, 1, 1, 1, 1, 0, 0, 4)])
 def test_batchmatmul_parity(dev, knobs):
     from paper_2006_05664_b200 import capi
 
