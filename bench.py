@@ -54,18 +54,46 @@ def peaks() -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons sampled during the timed region.
 
+    In-process NVML (nvidia-ml-py) polled every 100 ms: a handful of fields
+    per sample.  A looping ``nvidia-smi`` (the fallback) queries many fields
+    per sample and was seen to stall concurrent driver calls (module loads,
+    graph instantiation) by tens of milliseconds, which shows up as noise in
+    the trials/s of this short timed region."""
+
+    # NVML clocks-event reason bits
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
     FIELDS = ("index,clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu: int):
+    def __init__(self, gpu: int, period_s: float = 0.1):
         self.gpu = gpu
+        self.period = period_s
         self.proc = None
-        self.lines: list[str] = []
+        self.nvml = None
+        self.rows: list[tuple] = []      # (sm_mhz, max_mhz, util, reason_bits)
+        self.lines: list[str] = []       # nvidia-smi fallback
+        self.stop = threading.Event()
 
     def __enter__(self):
+        if os.environ.get("OPEVO_NO_CLOCKS") == "1":      # diagnostics only
+            return self
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.sample()
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:   # noqa: BLE001 - NVML unavailable: nvidia-smi
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
@@ -77,16 +105,43 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def sample(self):
+        n = self.nvml
+        try:
+            sm = n.nvmlDeviceGetClockInfo(self.h, n.NVML_CLOCK_SM)
+            util = n.nvmlDeviceGetUtilizationRates(self.h).gpu
+            try:
+                bits = n.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except AttributeError:
+                bits = n.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+            self.rows.append((float(sm), float(self.max_mhz), float(util), int(bits)))
+        except Exception:   # noqa: BLE001
+            pass
+
+    def _poll(self):
+        while not self.stop.wait(self.period):
+            self.sample()
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        if self.nvml is not None:
+            self.stop.set()
+            self.t.join(timeout=2)
+            self.sample()
         if self.proc is not None:
             self.proc.terminate()
             self.proc.wait(timeout=5)
 
     def summary(self) -> dict:
+        if self.rows:
+            sm = [r[0] for r in self.rows]
+            loaded = [r[0] for r in self.rows if r[2] > 0] or sm
+            reasons = sorted({name for r in self.rows for name, bit in self.REASONS.items() if r[3] & bit})
+            return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": self.rows[0][1],
+                    "reasons": reasons, "samples": len(self.rows), "source": "nvml"}
         rows = []
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
@@ -101,7 +156,7 @@ class ClockSampler:
         reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v == "Active"})
         return {"sm_mhz": statistics.median(loaded) if loaded else None,
                 "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples": len(rows), "source": "nvidia-smi"}
 
 
 def dist_env():
@@ -174,6 +229,9 @@ def main() -> None:
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--reps", type=int, default=20, help="timed launches per trial")
     ap.add_argument("--l2", default="warm", choices=("warm", "cold"))
+    ap.add_argument("--timing", default="stream", choices=("graph", "stream"),
+                    help="fitness launches: stream launches released together by a device gate "
+                         "(default) or one CUDA graph")
     ap.add_argument("--dtype", default="bf16", choices=("bf16", "f32"),
                     help="f32: the SIMT family on the reference space (cfg1)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -203,7 +261,8 @@ def main() -> None:
 
     spec = parse_operator(args.op)
     space = gpu_operator_space(spec, args.dtype)
-    settings = EvalSettings(reps=args.reps, flush_l2=(args.l2 == "cold"),
+    settings = EvalSettings(reps=args.reps,
+                            flush_l2=1 if args.l2 == "cold" else (2 if args.timing == "stream" else 0),
                             dtype=capi.F32 if args.dtype == "f32" else capi.BF16)
     local_ev = GpuEvaluator(spec, space, local, settings)
     if world > 1:
@@ -349,10 +408,14 @@ def main() -> None:
                        "seed": args.seed, "trials_timed": trials,
                        "space": ("reference operator space (fp32 SIMT family)" if args.dtype == "f32"
                                  else "reference operator space + stages (mapping.py)"),
-                       "fitness_timing": f"{settings.reps} back-to-back launches in one CUDA "
-                                         f"graph (fewer for candidates slower than 15 us: "
-                                         f"0.3 ms device budget, min 5) after {settings.warmup} "
-                                         f"warm-up launches incl. the verified one, L2 "
+                       "fitness_timing": (f"{settings.reps} back-to-back launches in one CUDA graph"
+                                          if args.timing == "graph" else
+                                          f"{settings.reps} back-to-back stream launches released "
+                                          f"by a device gate")
+                                         + f" after {settings.warmup} warm-up launches incl. "
+                                         f"the verified one (a 0.3 ms device budget per trial "
+                                         f"caps the repetitions; a candidate whose verified "
+                                         f"launch alone exceeds it is timed by that launch), L2 "
                                          f"{args.l2} (operands fit in L2)",
                        "l2_between_steps": "flushed: a 256 MB write (2x L2) before every timed "
                                            "step; within a trial the fitness is L2-warm "

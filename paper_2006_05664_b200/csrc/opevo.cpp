@@ -69,6 +69,7 @@ struct Driver {
     X(ModuleLoadData, cuModuleLoadData)                           \
     X(ModuleUnload, cuModuleUnload)                               \
     X(ModuleGetFunction, cuModuleGetFunction)                     \
+    X(FuncLoad, cuFuncLoad)                                       \
     X(FuncSetAttribute, cuFuncSetAttribute)                       \
     X(LaunchKernel, cuLaunchKernel)                               \
     X(LaunchKernelEx, cuLaunchKernelEx)                           \
@@ -614,7 +615,28 @@ struct opevo_op {
     size_t ws_bytes = 0, counter_bytes = 0;
     size_t a_bytes = 0, b_bytes = 0, c_bytes = 0;
     int in_f32 = 0, out_f32 = 0;
+    // Timed graphs by (knobs, repetitions).  Many configurations map to one
+    // kernel instance (the thread-level factors have no tcgen05 counterpart),
+    // so a generation often re-times an instance an earlier trial captured;
+    // the graph's kernel arguments (tensor maps, pointers) are copied at
+    // capture and stay valid until the split-K workspace is reallocated.
+    std::unordered_map<std::string, CUgraphExec> graphs;
 };
+
+namespace {
+void drop_graphs(opevo_op* op) {
+    for (auto& kv : op->graphs)
+        if (kv.second) g_cu.GraphExecDestroy(kv.second);
+    op->graphs.clear();
+}
+
+std::string graph_key(const Knobs& k, int reps) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "%d_%d_%d_%d_%d_%d_%d_%d_%d_%d_%d_%d_%d_r%d", k.bm, k.bn, k.bk, k.stages, k.split,
+             k.cluster, k.tile_h, k.tile_w, k.acc, k.cg, k.grid_mode, k.b_res, k.bpu, reps);
+    return buf;
+}
+}  // namespace
 
 struct ConvGeomHost {
     int cin, ho, wo, kw, pad, taps_cchunks;
@@ -701,6 +723,7 @@ int compute_reference(opevo_op* op, char* err, size_t errlen) {
 
 int ensure_ws(opevo_op* op, size_t ws_need, size_t cnt_need, char* err, size_t errlen) {
     opevo_ctx* ctx = op->ctx;
+    if (ws_need > op->ws_bytes || cnt_need > op->counter_bytes) drop_graphs(op);   // captured pointers go stale
     if (ws_need > op->ws_bytes) {
         if (op->ws) g_cu.MemFree(op->ws);
         op->ws = 0;
@@ -764,7 +787,7 @@ int launch_kernel(opevo_kernel* kr, char* err, size_t errlen, CUstream on = null
             cfg.numAttrs = 1;
         }
         CUresult r = g_cu.LaunchKernelEx(&cfg, kr->fn, args, nullptr);
-        ++kr->launches;
+        if (strm == ctx->stream) ++kr->launches;   // captured launches count when the graph runs
         if (r != CUDA_SUCCESS) {
             int st = fail_cu(ctx, r, "kernel launch", err, errlen);
             return st == OPEVO_ERR_STICKY ? st : OPEVO_LAUNCH_ERROR;
@@ -809,7 +832,7 @@ int launch_kernel(opevo_kernel* kr, char* err, size_t errlen, CUstream on = null
     cfg.attrs = na ? attr : nullptr;
     cfg.numAttrs = na;
     CUresult r = g_cu.LaunchKernelEx(&cfg, kr->fn, args, nullptr);
-    ++kr->launches;
+    if (strm == ctx->stream) ++kr->launches;       // captured launches count when the graph runs
     if (r != CUDA_SUCCESS) {
         int st = fail_cu(ctx, r, "kernel launch", err, errlen);
         return st == OPEVO_ERR_STICKY ? st : OPEVO_LAUNCH_ERROR;
@@ -843,6 +866,11 @@ int get_function(opevo_ctx* ctx, int family, const Knobs& k, int batched, int ou
         LoadedModule lm;
         CUresult r = g_cu.ModuleLoadData(&lm.mod, cubin.data());
         if (r == CUDA_SUCCESS) r = g_cu.ModuleGetFunction(&lm.fn, lm.mod, name);
+        // Under lazy module loading (the CUDA 12 default) the code would reach
+        // the device at its first launch or graph instantiation -- on the
+        // trial's critical path, holding the driver lock for milliseconds.
+        // Load it here, on the preload thread.
+        if (r == CUDA_SUCCESS) r = g_cu.FuncLoad(lm.fn);
         if (r != CUDA_SUCCESS) {
             st = fail_cu(ctx, r, "load module", err, errlen);
             return st == OPEVO_ERR_STICKY ? st : OPEVO_LAUNCH_ERROR;
@@ -1040,6 +1068,8 @@ int opevo_ctx_info(opevo_ctx* ctx, int* sm_count, int* max_smem_optin, int* cc_m
 void opevo_op_destroy(opevo_op* op) {
     if (!op) return;
     if (g_cu.ok && op->ctx && !op->ctx->poisoned) {
+        g_cu.CtxSetCurrent(op->ctx->cu);
+        drop_graphs(op);
         CUdeviceptr ps[] = {op->a, op->b, op->c, op->ref, op->conv_x, op->conv_w, op->ws, op->counters};
         for (CUdeviceptr p : ps)
             if (p) g_cu.MemFree(p);
@@ -1128,6 +1158,14 @@ int opevo_op_prepare(opevo_ctx* ctx, const opevo_op_desc* desc, opevo_op** out, 
         return OPEVO_ERR_ARG;
     }
     if (!st) st = compute_reference(op, err, errlen);
+    if (!st) {
+        // split-K workspace for up to 16 slices and tile counters, up front:
+        // growing them during a search reallocates (and drops the timed
+        // graphs that captured the old pointers) on the trial's critical path
+        const size_t slice = (size_t)op->batch * op->rows * op->cols * 4;
+        const size_t tiles = (size_t)op->batch * ((op->rows + 127) / 128) * ((op->cols + 15) / 16);
+        st = ensure_ws(op, slice * 16, tiles * 16 * 4, err, errlen);
+    }
     if (st) {
         opevo_op_destroy(op);
         return st;
@@ -1423,12 +1461,15 @@ namespace {
 // that skips tiles fails), launch, compare against the reference into
 // compare slot `slot` of ctx->cmp_buf (16 bytes each).  No synchronisation;
 // see finish_check.
-int enqueue_check(opevo_kernel* k, char* err, size_t errlen, int slot = 0) {
+int enqueue_check(opevo_kernel* k, char* err, size_t errlen, int slot = 0, CUevent e0 = nullptr,
+                  CUevent e1 = nullptr) {
     opevo_op* op = k->op;
     opevo_ctx* ctx = op->ctx;
     CU_TRY(ctx, g_cu.MemsetD8Async(op->c, 0xFF, op->c_bytes, ctx->stream), "poison C");
+    if (e0) CU_TRY(ctx, g_cu.EventRecord(e0, ctx->stream), "event");
     int st = launch_kernel(k, err, errlen);
     if (st) return st;
+    if (e1) CU_TRY(ctx, g_cu.EventRecord(e1, ctx->stream), "event");
     CUdeviceptr out = ctx->cmp_buf + 16 * (CUdeviceptr)slot;
     CU_TRY(ctx, g_cu.MemsetD8Async(out, 0, 16, ctx->stream), "zero compare");
     uint64_t n = (uint64_t)op->batch * op->rows * op->cols;
@@ -1465,10 +1506,25 @@ int finish_check(opevo_kernel* k, double tol, double* rel_err, char* err, size_t
 // 20 and a 10 ms one 5; the fast instances that decide the search keep all
 // `reps`.  Once the measured time is device-bound (the trial pipeline's
 // host work is overlapped), this budget sets the trial rate.
+// A candidate whose single timed launch exceeds the whole per-trial budget.
+bool slow_candidate(float est_ms) {
+    double budget = 0.3;
+    if (const char* b = getenv("OPEVO_TIME_BUDGET_MS")) budget = atof(b);
+    return budget > 0 && est_ms > budget;
+}
+
 int capped_reps(int reps, float est_ms) {
     double budget = 0.3;
     if (const char* b = getenv("OPEVO_TIME_BUDGET_MS")) budget = atof(b);
-    if (budget > 0 && est_ms > 0 && est_ms * reps > budget) reps = std::max(std::min(reps, 5), (int)(budget / est_ms));
+    if (budget > 0 && est_ms > 0 && est_ms * reps > budget) {
+        // quantised to {reps, 16, 8, 5} so an instance has few distinct timed graphs
+        const int want = std::max(std::min(reps, 5), (int)(budget / est_ms));
+        const int steps[] = {16, 8, 5};
+        int q = std::min(reps, 5);
+        for (int v : steps)
+            if (v <= want && v < reps) { q = v; break; }
+        reps = q;
+    }
     return reps;
 }
 
@@ -1618,30 +1674,34 @@ int enqueue_warmup_estimate(opevo_kernel* k, int warmup, CUevent e0, CUevent e1,
 //   0  R back-to-back launches in one CUDA graph (L2 warm) -- the fitness
 //   1  a 2x-L2 write before every launch, each launch timed (cold L2)
 //   2  R back-to-back stream launches behind a device gate (no graph)
-// check (optional, tol >= 0) + warm-up + estimate with ONE synchronisation,
-// then the timed launches.  In mode 0 the graph is captured and
-// instantiated while the check runs on the device.
+//
+// One trial = phase A (the verified launch, timed by events, + the compare;
+// one synchronisation) then, for candidates faster than the device budget,
+// phase B: warm-up launches and the timed launches.  A candidate whose
+// verified launch already exceeds the budget is measured by that launch
+// alone: it is far from competitive, and on a large operator a bad tile can
+// take milliseconds per launch -- with several GPUs evaluating one trial
+// each per generation such a straggler would set the generation time.
+// Without a check (tol < 0) an untimed-check estimate launch plays the same
+// role.  In mode 0 the graph is captured and instantiated while phase A runs
+// on the device.
 int check_and_time(opevo_kernel* k, double tol, double* rel_err, int warmup, int reps, int mode,
                    double* ms_per_launch, char* err, size_t errlen) {
     opevo_ctx* ctx = k->op->ctx;
     int st = OPEVO_OK;
     CUgraphExec ge = nullptr;
     int graph_reps = 0;
-    if (tol >= 0) {
-        st = enqueue_check(k, err, errlen);
-        if (st) return st;
-        warmup = std::max(0, warmup - 1);        // the checked launch warms up too
-    }
     CUevent e0, e1;
     CU_TRY(ctx, g_cu.EventCreate(&e0, CU_EVENT_DEFAULT), "event");
     CU_TRY(ctx, g_cu.EventCreate(&e1, CU_EVENT_DEFAULT), "event");
     float est = 0.f;
-    st = enqueue_warmup_estimate(k, warmup, e0, e1, err, errlen);
+    if (tol >= 0) st = enqueue_check(k, err, errlen, 0, e0, e1);
+    else          st = enqueue_warmup_estimate(k, 0, e0, e1, err, errlen);
     if (!st && mode == 0 && ms_per_launch) {
         st = build_graph(k, reps, &ge, err, errlen);
         graph_reps = reps;
     }
-    if (!st) st = sync_checked(ctx, "check/warm-up", err, errlen);
+    if (!st) st = sync_checked(ctx, "check", err, errlen);
     if (!st) {
         CUresult r = g_cu.EventElapsedTime(&est, e0, e1);
         if (r != CUDA_SUCCESS) st = fail_cu(ctx, r, "estimate", err, errlen);
@@ -1653,21 +1713,28 @@ int check_and_time(opevo_kernel* k, double tol, double* rel_err, int warmup, int
         if (ge) g_cu.GraphExecDestroy(ge);
         return st;
     }
+    if (slow_candidate(est)) {
+        if (ge) g_cu.GraphExecDestroy(ge);
+        *ms_per_launch = est;
+        return OPEVO_OK;
+    }
     reps = capped_reps(reps, est);
+    for (int i = 0; i + 1 < warmup && !st; ++i) st = launch_kernel(k, err, errlen);
     double total = 0.0;
-    if (mode == 0) {
-        if (reps != graph_reps) {            // a slow candidate: fewer launches
+    if (!st && mode == 0) {
+        if (reps != graph_reps) {
             g_cu.GraphExecDestroy(ge);
             ge = nullptr;
             st = build_graph(k, reps, &ge, err, errlen);
         }
         if (!st) st = time_graph(k, ge, &total, err, errlen);
-        if (ge) g_cu.GraphExecDestroy(ge);
-    } else if (mode == 1) {
+        if (!st) k->launches += reps;
+    } else if (!st && mode == 1) {
         st = time_flushed(k, reps, &total, err, errlen);
-    } else {
+    } else if (!st) {
         st = time_gated(k, reps, &total, err, errlen);
     }
+    if (ge) g_cu.GraphExecDestroy(ge);
     if (st) return st;
     *ms_per_launch = total / reps;
     return OPEVO_OK;
@@ -1725,6 +1792,20 @@ int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nk
     std::vector<opevo_kernel*> ks(count, nullptr);
     std::vector<CUgraphExec> ge(count, nullptr);
     std::vector<int> greps(count, 0);
+    // every graph built here joins the operand's cache (bounded: past 2048
+    // entries new graphs are destroyed instead; destroying executable graphs
+    // costs device round trips, so the cache is never flushed wholesale)
+    auto remember = [&](int i) {
+        if (!ge[i] || !ks[i]) return;
+        const std::string key = graph_key(ks[i]->k, greps[i]);
+        auto it = op->graphs.find(key);
+        if (it == op->graphs.end() && op->graphs.size() < 2048) {
+            op->graphs.emplace(key, ge[i]);
+        } else if (it == op->graphs.end() || it->second != ge[i]) {
+            g_cu.GraphExecDestroy(ge[i]);
+        }
+        ge[i] = nullptr;
+    };
     std::vector<CUevent> ev(4 * (size_t)count, nullptr);   // per trial: est0, est1, t0, t1
     auto msg = [&](int i) -> char* { return msgs ? msgs + (size_t)i * msg_stride : nullptr; };
     auto mlen = [&]() -> size_t { return msgs ? msg_stride : 0; };
@@ -1762,6 +1843,11 @@ int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nk
             for (int i = 0; i < count; ++i) {
                 if (status[i] != OPEVO_OK) continue;
                 greps[i] = reps;
+                auto hit = op->graphs.find(graph_key(ks[i]->k, reps));
+                if (hit != op->graphs.end()) {          // captured by an earlier trial
+                    ge[i] = hit->second;
+                    continue;
+                }
                 tasks.push_back([&, i](int w) {
                     char e[512] = {0};
                     gst[i] = build_graph(ks[i], reps, &ge[i], e, sizeof e, ctx->pool_streams[w]);
@@ -1779,11 +1865,13 @@ int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nk
         int st = OPEVO_OK;
         for (int e = 0; e < 4 && !st; ++e)
             if (g_cu.EventCreate(&ev[4 * i + e], CU_EVENT_DEFAULT) != CUDA_SUCCESS) st = OPEVO_ERR_CUDA;
-        if (!st) st = enqueue_check(ks[i], msg(i), mlen(), i);
-        if (!st) st = enqueue_warmup_estimate(ks[i], std::max(0, warmup - 1), ev[4 * i], ev[4 * i + 1], msg(i), mlen());
+        // the verified launch is bracketed by events: it is also the estimate
+        if (!st) st = enqueue_check(ks[i], msg(i), mlen(), i, ev[4 * i], ev[4 * i + 1]);
         if (!st && mode == 0 && !pooled) {
-            st = build_graph(ks[i], reps, &ge[i], msg(i), mlen());
             greps[i] = reps;
+            auto hit = op->graphs.find(graph_key(ks[i]->k, reps));
+            if (hit != op->graphs.end()) ge[i] = hit->second;
+            else st = build_graph(ks[i], reps, &ge[i], msg(i), mlen());
         }
         status[i] = st;
         if (st < 0) fatal = st;
@@ -1806,8 +1894,10 @@ int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nk
     }
     if (!fatal && count && g_cu.MemcpyDtoH(cmp.data(), ctx->cmp_buf, 16 * (size_t)count) != CUDA_SUCCESS)
         fatal = OPEVO_ERR_CUDA;
-    // judge, cap repetitions of slow instances
+    // judge; candidates slower than the whole budget keep their verified
+    // launch's time (no phase B); cap the repetitions of the rest
     std::vector<int> nreps(count, reps);
+    std::vector<char> timed(count, 0);
     for (int i = 0; i < count && !fatal; ++i) {
         if (status[i] != OPEVO_OK) continue;
         double rel = 0.0;
@@ -1816,12 +1906,22 @@ int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nk
         if (status[i] != OPEVO_OK) continue;
         float est = 0.f;
         g_cu.EventElapsedTime(&est, ev[4 * i], ev[4 * i + 1]);
+        if (slow_candidate(est)) {
+            res[i].ms = est;
+            timed[i] = 1;
+            continue;
+        }
         nreps[i] = capped_reps(reps, est);
         if (mode == 0 && nreps[i] != greps[i]) {
-            g_cu.GraphExecDestroy(ge[i]);
-            ge[i] = nullptr;
-            status[i] = build_graph(ks[i], nreps[i], &ge[i], msg(i), mlen());
-            if (status[i] < 0) fatal = status[i];
+            remember(i);                                 // keep the full-length graph too
+            greps[i] = nreps[i];
+            auto hit = op->graphs.find(graph_key(ks[i]->k, nreps[i]));
+            if (hit != op->graphs.end()) {
+                ge[i] = hit->second;
+            } else {
+                status[i] = build_graph(ks[i], nreps[i], &ge[i], msg(i), mlen());
+                if (status[i] < 0) fatal = status[i];
+            }
         }
     }
     tp[4] = now_ms();
@@ -1830,10 +1930,18 @@ int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nk
     if (!fatal && mode == 0) {
         int last = -1;
         for (int i = 0; i < count; ++i) {
-            if (status[i] != OPEVO_OK) continue;
+            if (status[i] != OPEVO_OK || timed[i]) continue;
+            int wst = OPEVO_OK;
+            for (int w = 0; w + 1 < warmup && !wst; ++w) wst = launch_kernel(ks[i], msg(i), mlen());
+            if (wst) {
+                status[i] = wst;
+                if (wst < 0) { fatal = wst; break; }
+                continue;
+            }
             CUresult r = g_cu.GraphUpload(ge[i], ctx->stream);
             if (r == CUDA_SUCCESS) r = g_cu.EventRecord(ev[4 * i + 2], ctx->stream);
             if (r == CUDA_SUCCESS) r = g_cu.GraphLaunch(ge[i], ctx->stream);
+            if (r == CUDA_SUCCESS) ks[i]->launches += nreps[i];
             if (r == CUDA_SUCCESS) r = g_cu.EventRecord(ev[4 * i + 3], ctx->stream);
             if (r != CUDA_SUCCESS) {
                 status[i] = fail_cu(ctx, r, "timed graph", msg(i), mlen());
@@ -1848,14 +1956,71 @@ int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nk
             if (fatal == OPEVO_LAUNCH_ERROR) fatal = OPEVO_ERR_CUDA;
         }
         for (int i = 0; i < count && !fatal; ++i) {
-            if (status[i] != OPEVO_OK) continue;
+            if (status[i] != OPEVO_OK || timed[i]) continue;
+            float ms = 0.f;
+            g_cu.EventElapsedTime(&ms, ev[4 * i + 2], ev[4 * i + 3]);
+            res[i].ms = ms / nreps[i];
+        }
+    } else if (!fatal && mode == 2) {
+        // every verified instance's warm-ups and timed launches (between its
+        // own events) behind device gates of at most 64 launches each, so the
+        // launch queue never fills while a gate holds the stream; one
+        // synchronisation at the end
+        bool gate_open = false;
+        int in_gate = 0;
+        uint32_t seq = 0;
+        auto open_gate = [&]() -> int {
+            seq = ++ctx->gate_seq;
+            uint64_t timeout_ns = 2000000000ull;
+            void* ga[] = {&ctx->gate_dev, &seq, &timeout_ns};
+            int gst2 = launch_simple(ctx, ctx->k_gate, 1, 32, ga, err, errlen);
+            gate_open = gst2 == OPEVO_OK;
+            in_gate = 0;
+            return gst2;
+        };
+        auto release = [&]() {
+            if (gate_open) __atomic_store_n(const_cast<uint32_t*>(ctx->gate_host), seq, __ATOMIC_SEQ_CST);
+            gate_open = false;
+        };
+        int last = -1;
+        for (int i = 0; i < count && !fatal; ++i) {
+            if (status[i] != OPEVO_OK || timed[i]) continue;
+            const int need = std::max(0, warmup - 1) + nreps[i];
+            if (gate_open && in_gate + need > 64) release();
+            if (!gate_open) {
+                const int gst2 = open_gate();
+                if (gst2) { fatal = gst2 < 0 ? gst2 : OPEVO_ERR_CUDA; break; }
+            }
+            int st2 = OPEVO_OK;
+            for (int w = 0; w + 1 < warmup && !st2; ++w) st2 = launch_kernel(ks[i], msg(i), mlen());
+            if (!st2 && g_cu.EventRecord(ev[4 * i + 2], ctx->stream) != CUDA_SUCCESS) st2 = OPEVO_ERR_CUDA;
+            for (int r = 0; r < nreps[i] && !st2; ++r) st2 = launch_kernel(ks[i], msg(i), mlen());
+            if (!st2 && g_cu.EventRecord(ev[4 * i + 3], ctx->stream) != CUDA_SUCCESS) st2 = OPEVO_ERR_CUDA;
+            in_gate += need;
+            status[i] = st2;
+            if (st2 < 0) fatal = st2;
+            else if (!st2) last = i;
+        }
+        release();
+        if (last >= 0 || fatal) {
+            const int sst = sync_checked(ctx, "batch timing", err, errlen);
+            if (!fatal && sst) fatal = sst == OPEVO_LAUNCH_ERROR ? OPEVO_ERR_CUDA : sst;
+        }
+        for (int i = 0; i < count && !fatal; ++i) {
+            if (status[i] != OPEVO_OK || timed[i]) continue;
             float ms = 0.f;
             g_cu.EventElapsedTime(&ms, ev[4 * i + 2], ev[4 * i + 3]);
             res[i].ms = ms / nreps[i];
         }
     } else if (!fatal) {
         for (int i = 0; i < count && !fatal; ++i) {
-            if (status[i] != OPEVO_OK) continue;
+            if (status[i] != OPEVO_OK || timed[i]) continue;
+            for (int w = 0; w + 1 < warmup && status[i] == OPEVO_OK; ++w)
+                status[i] = launch_kernel(ks[i], msg(i), mlen());
+            if (status[i] != OPEVO_OK) {
+                if (status[i] < 0) fatal = status[i];
+                continue;
+            }
             double total = 0.0;
             status[i] = mode == 1 ? time_flushed(ks[i], nreps[i], &total, msg(i), mlen())
                                   : time_gated(ks[i], nreps[i], &total, msg(i), mlen());
@@ -1866,11 +2031,17 @@ int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nk
     for (int i = 0; i < count; ++i) {
         if (fatal && status[i] == OPEVO_OK) status[i] = fatal;
         if (status[i] == OPEVO_OK && res[i].ms > 0) res[i].tflops = ks[i]->flops / (res[i].ms * 1e-3) / 1e12;
+        if (fatal) {                                     // nothing from a failed batch is kept
+            if (ge[i] && !op->graphs.count(graph_key(ks[i]->k, greps[i]))) g_cu.GraphExecDestroy(ge[i]);
+            ge[i] = nullptr;
+        } else {
+            remember(i);                                 // needs ks[i]: before the release
+        }
         if (ks[i]) {
             res[i].launches = ks[i]->launches;
             opevo_kernel_release(ks[i]);
+            ks[i] = nullptr;
         }
-        if (ge[i]) g_cu.GraphExecDestroy(ge[i]);
         for (int e = 0; e < 4; ++e)
             if (ev[4 * i + e]) g_cu.EventDestroy(ev[4 * i + e]);
     }

@@ -41,7 +41,7 @@ class WorkerFault(FatalEvaluationError):
 class EvalSettings:
     warmup: int = 3
     reps: int = 20
-    flush_l2: bool = False
+    flush_l2: int = 2             # timing mode: 0 graph, 1 cold L2, 2 gated stream (capi)
     seed: int = 1234
     compile_threads: int = 0          # 0 -> min(8, cpu count)
     cache_dir: str = capi.DEFAULT_CACHE

@@ -309,3 +309,41 @@ def test_mapping_smem_matches_library(dev, op_id):
         assert seen >= 10
     finally:
         op.close()
+
+
+def test_slow_candidate_is_timed_by_its_verified_launch(dev):
+    """A candidate whose verified launch alone exceeds the per-trial device
+    budget (0.3 ms) gets no further launches: one launch, positive time."""
+    from paper_2006_05664_b200 import capi
+
+    op = dev.prepare(capi.MATMUL, rows=4096, cols=4096, depth=4096)
+    try:
+        t = dev.trial(op, (128, 16, 32, 2, 1, 1))
+        assert t.ok, t.message
+        assert t.launches == 1 and t.ms > 0.3
+        fast = dev.trial(op, (256, 256, 64, 4, 1, 1, 1, 1, 1, 2))
+        assert fast.ok and fast.launches > 3 and fast.ms < 0.3
+        b = dev.trial_batch(op, [(128, 16, 32, 2, 1, 1), (256, 256, 64, 4, 1, 1, 1, 1, 1, 2)])
+        assert [x.launches == 1 for x in b] == [True, False]
+    finally:
+        op.close()
+
+
+def test_trial_batch_gated_stream_mode(dev):
+    """Mode 2 (the default fitness timing): every verified instance timed
+    behind shared device gates with one synchronisation; statuses as in
+    mode 0 and times within 2x of the graph timing."""
+    from paper_2006_05664_b200 import capi
+
+    op = dev.prepare(capi.MATMUL, rows=1024, cols=1024, depth=1024, seed=1234)
+    try:
+        kl = [(128, 64, 128, 3, 1, 1), (128, 128, 64, 4, 1, 1), (96, 128, 64, 4, 1, 1),
+              (256, 64, 128, 4, 1, 1, 1, 1, 1, 2)] * 4          # > 64 launches: several gates
+        s = dev.trial_batch(op, kl, warmup=3, reps=20, flush_l2=2)
+        g = dev.trial_batch(op, kl, warmup=3, reps=20, flush_l2=0)
+        assert [t.status for t in s] == [t.status for t in g]
+        for a, b in zip(s, g):
+            if a.ok:
+                assert 0.5 < a.ms / b.ms < 2.0 and a.rel_err < BF16_TOL
+    finally:
+        op.close()

@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+for i in 1 2 3; do
+OPEVO_NO_CLOCKS=1 OPEVO_PROFILE_BATCH=1 timeout 600 python bench.py --no-cpu --no-e2e > gpurun_out/g31_bench$i.json 2> gpurun_out/g31_err$i.txt; python -c "import json;d=json.loads(open('gpurun_out/g31_bench$i.json').read().strip().splitlines()[-1]);print('noclk', d['value'], d['ms_per_step'], d['best_tflops'])"
+done
+for i in 1 2; do
+timeout 600 python bench.py --no-cpu --no-e2e > gpurun_out/g31_cbench$i.json 2>/dev/null; python -c "import json;d=json.loads(open('gpurun_out/g31_cbench$i.json').read().strip().splitlines()[-1]);print('clk', d['value'], d['ms_per_step'], d['best_tflops'], d['clocks'])"
+done

@@ -1,0 +1,8 @@
+mkdir -p gpurun_out
+make -s -C paper_2006_05664_b200/csrc
+timeout 900 python -m pytest tests/ -q -m gpu -x -p no:cacheprovider > gpurun_out/g35_pytest.txt 2>&1; tail -2 gpurun_out/g35_pytest.txt
+for i in 1 2 3; do
+timeout 600 python bench.py --no-cpu > gpurun_out/g35_bench$i.json 2>/dev/null; python -c "import json;d=json.loads(open('gpurun_out/g35_bench$i.json').read().strip().splitlines()[-1]);print(round(d['value']), round(d['ms_per_step'],2), round(d['best_tflops'],1), round(d['roofline']['achieved'],1), round(d['e2e']['value']), d['gpu_launches'])"
+done
+timeout 900 python tools/scaling_projection.py matmul:1024,1024,1024 40 > gpurun_out/g35_scaling_mm1024.txt 2>&1; grep "N=" gpurun_out/g35_scaling_mm1024.txt
+timeout 900 python tools/scaling_projection.py matmul:4096,4096,4096 20 > gpurun_out/g35_scaling_mm4096.txt 2>&1; grep "N=" gpurun_out/g35_scaling_mm4096.txt

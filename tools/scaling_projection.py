@@ -1,0 +1,98 @@
+"""Project 1/2/4/8-GPU trial throughput from one GPU (a measurement aid for a
+box with one GPU; the real multi-GPU run is ``torchrun ... bench.py --gpus N``).
+
+Under ``scheduler.ShardedEvaluator`` every rank runs the same engine replica
+and evaluates ask indices i = rank (mod N); a generation ends when the slowest
+rank has its shard and one small all-reduce has gathered the rows.  Here:
+
+1. a reference run measures every trial of K generations on this GPU and
+   records its fitness;
+2. for each N, the same trajectory is replayed (recorded fitness told, so the
+   asks are identical) and, generation by generation, each rank's shard is
+   measured on this GPU in turn (real compile-cache lookups, checks and
+   timed graphs) together with the host ask/tell of that generation;
+3. the projected generation time is the max over ranks plus a fixed
+   all-reduce latency (``--allreduce-us``, an NVLink small-message figure).
+
+Usage: python tools/scaling_projection.py [op] [generations]
+"""
+import argparse
+import json
+import sys
+import time
+
+sys.path.insert(0, ".")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("op", nargs="?", default="matmul:1024,1024,1024")
+    ap.add_argument("generations", nargs="?", type=int, default=40)
+    ap.add_argument("--allreduce-us", type=float, default=30.0)
+    args = ap.parse_args()
+
+    from paper_2006_05664_b200 import EngineConfig, OpEvo, parse_operator
+    from paper_2006_05664_b200.evaluator import GpuEvaluator
+    from paper_2006_05664_b200.mapping import gpu_operator_space
+    from paper_2006_05664_b200.scheduler import shard_indices
+
+    spec = parse_operator(args.op)
+    space = gpu_operator_space(spec)
+    ev = GpuEvaluator(spec, space, 0)
+    warm = 3
+    budget = 8 * (args.generations + warm)
+
+    # 1. reference run: fitness of every asked configuration
+    fitness = {}
+    eng = OpEvo(space, EngineConfig(seed=0, budget=budget))
+    while True:
+        a = eng.ask()
+        if not a.configs:
+            break
+        fits = ev.evaluate(a.configs)
+        for c, f in zip(a.configs, fits):
+            fitness[c] = f
+        eng.tell(list(zip(a.configs, fits)))
+
+    out = {"op": args.op, "generations": args.generations, "allreduce_us": args.allreduce_us,
+           "per_n": {}}
+    for n in (1, 2, 4, 8):
+        eng = OpEvo(space, EngineConfig(seed=0, budget=budget))
+        gen_ms = []
+        trials = 0
+        g = 0
+        while True:
+            ev.dev.flush_l2()
+            t0 = time.perf_counter()
+            a = eng.ask()
+            t_ask = time.perf_counter() - t0
+            if not a.configs:
+                break
+            rank_s = []
+            for r in range(n):
+                idx = shard_indices(len(a.configs), n, r)
+                t1 = time.perf_counter()
+                if idx:
+                    ev.evaluate([a.configs[i] for i in idx])
+                rank_s.append(time.perf_counter() - t1)
+            t2 = time.perf_counter()
+            eng.tell([(c, fitness[c]) for c in a.configs])   # recorded: identical trajectory
+            t_tell = time.perf_counter() - t2
+            if g >= warm:
+                gen_ms.append(1e3 * (t_ask + max(rank_s) + t_tell) + (args.allreduce_us / 1e3 if n > 1 else 0))
+                trials += len(a.configs)
+            g += 1
+        tot = sum(gen_ms)
+        out["per_n"][n] = {"trials": trials, "ms_per_generation": tot / max(1, len(gen_ms)),
+                           "trials_per_s": trials / (tot / 1e3) if tot else 0.0}
+        print(f"N={n}: {out['per_n'][n]['ms_per_generation']:.3f} ms/generation, "
+              f"{out['per_n'][n]['trials_per_s']:.0f} trials/s", flush=True)
+    base = out["per_n"][1]["trials_per_s"]
+    for n in (2, 4, 8):
+        out["per_n"][n]["speedup_vs_1"] = out["per_n"][n]["trials_per_s"] / base if base else 0.0
+    print(json.dumps(out))
+    ev.close()
+
+
+if __name__ == "__main__":
+    main()
