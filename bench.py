@@ -179,7 +179,7 @@ def cpu_reference_arm(op: str, steps: int, warmup: int, seed: int) -> dict:
         total_s += time.perf_counter() - t0
         trials += len(log)
         reps += 1
-        if time.perf_counter() > t_end or reps >= 200:
+        if time.perf_counter() > t_end or reps >= 2000:
             break
     return {"value": trials / total_s, "unit": "trials/s", "cores": 1, "kind": "port",
             "sample": f"{reps} OpEvo runs x {budget} trials of {op} with the reference's "
