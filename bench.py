@@ -235,6 +235,8 @@ def main() -> None:
     ap.add_argument("--dtype", default="bf16", choices=("bf16", "f32"),
                     help="f32: the SIMT family on the reference space (cfg1)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-preload", action="store_true",
+                    help="do not load the cached kernel family into the context before timing")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--log", default="")
     args = ap.parse_args()
@@ -261,7 +263,7 @@ def main() -> None:
 
     spec = parse_operator(args.op)
     space = gpu_operator_space(spec, args.dtype)
-    settings = EvalSettings(reps=args.reps,
+    settings = EvalSettings(reps=args.reps, preload_family=not args.no_preload,
                             flush_l2=1 if args.l2 == "cold" else (2 if args.timing == "stream" else 0),
                             dtype=capi.F32 if args.dtype == "f32" else capi.BF16)
     local_ev = GpuEvaluator(spec, space, local, settings)
@@ -421,7 +423,10 @@ def main() -> None:
                                            "step; within a trial the fitness is L2-warm "
                                            "back-to-back launches (use --l2 cold to flush "
                                            "before every timed launch)",
-                       "parallelism": f"trial sharding x{world}"},
+                       "parallelism": f"trial sharding x{world}",
+                       "kernel_cache": ("prebuilt cubins (build()); the operator's cached family "
+                                        "loaded into the context before timing" if not args.no_preload
+                                        else "prebuilt cubins (build()), loaded on first use")},
             "best_tflops": best.fitness,
             "best_frac_of_peak": best.fitness / (pk["tflops"] if args.dtype == "bf16" else FP32_PEAK),
             "best_knobs": best_knobs, "best_config": space.config_to_json(best.config),

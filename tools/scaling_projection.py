@@ -32,13 +32,13 @@ def main():
     args = ap.parse_args()
 
     from paper_2006_05664_b200 import EngineConfig, OpEvo, parse_operator
-    from paper_2006_05664_b200.evaluator import GpuEvaluator
+    from paper_2006_05664_b200.evaluator import EvalSettings, GpuEvaluator
     from paper_2006_05664_b200.mapping import gpu_operator_space
     from paper_2006_05664_b200.scheduler import shard_indices
 
     spec = parse_operator(args.op)
     space = gpu_operator_space(spec)
-    ev = GpuEvaluator(spec, space, 0)
+    ev = GpuEvaluator(spec, space, 0, EvalSettings(preload_family=True))
     warm = 3
     budget = 8 * (args.generations + warm)
 
