@@ -43,8 +43,20 @@ def _objective(args):
     from .evaluator import EvalSettings, GpuEvaluator
 
     ev = GpuEvaluator(spec, None, args.device,
-                      EvalSettings(reps=args.reps, dtype=capi.F32 if args.dtype == "f32" else capi.BF16))
+                      EvalSettings(reps=args.reps, dtype=capi.F32 if args.dtype == "f32" else capi.BF16,
+                                   preload_family=True))
     return ev.space, ev
+
+
+def _peak_tflops() -> float:
+    """Measured bf16 peak (MEASURED_PEAKS.json at the repo root), else the
+    profiling guide's fallback."""
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["bf16_tflops"])
+    except (OSError, KeyError, ValueError):
+        return 1590.0
 
 
 def _run(algo, space, objective, seed, budget):
@@ -68,7 +80,7 @@ def cmd_tune(args) -> int:
     os.makedirs(args.out, exist_ok=True)
     path = os.path.join(args.out, f"trials_{args.algo}_seed{args.seed}.jsonl")
     write_trial_log(path, recs)
-    rep = tuning_report(recs, wall, 1639.1)
+    rep = tuning_report(recs, wall, _peak_tflops())
     print(json.dumps({"operator": args.operator, "algorithm": args.algo, "seed": args.seed,
                       "best_fitness": best.fitness, "best_config": space.config_to_json(best.config),
                       "log": path, **rep}))
