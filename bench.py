@@ -256,9 +256,18 @@ def main() -> None:
     from paper_2006_05664_b200.reporting import trials_to_fraction, wallclock_to_fraction
     from paper_2006_05664_b200.scheduler import ShardedEvaluator
 
+    # OPEVO_DIST_BACKEND=gloo (test mode): ranks may share GPUs and the
+    # per-generation exchange goes through host memory; default NCCL
+    backend = os.environ.get("OPEVO_DIST_BACKEND", "nccl")
+    if backend == "gloo":
+        local %= max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    coll_device = torch.device("cuda", local) if backend == "nccl" else None
     from paper_2006_05664_b200 import capi
 
     spec = parse_operator(args.op)
@@ -268,7 +277,7 @@ def main() -> None:
                             dtype=capi.F32 if args.dtype == "f32" else capi.BF16)
     local_ev = GpuEvaluator(spec, space, local, settings)
     if world > 1:
-        evaluator = ShardedEvaluator(local_ev, rank, world, device=torch.device("cuda", local))
+        evaluator = ShardedEvaluator(local_ev, rank, world, device=coll_device)
     else:
         evaluator = local_ev.evaluate
 
@@ -280,7 +289,7 @@ def main() -> None:
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=coll_device or "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
