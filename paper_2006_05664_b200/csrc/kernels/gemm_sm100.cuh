@@ -94,6 +94,10 @@
 #ifndef OPEVO_B_RES
 #define OPEVO_B_RES 0      // conv: the BN x K weight panel stays resident in shared memory
 #endif
+#ifndef OPEVO_SPLIT_TMA
+#define OPEVO_SPLIT_TMA 0  // S > 1: split-K in one wave; slices 1..S-1 publish fp32 partials
+                           // with TMA stores, slice 0 TMA-loads them and reduces
+#endif
 #ifndef OPEVO_BPU
 #define OPEVO_BPU 1        // BatchMatMul: consecutive batches per work unit (one TMA box per
                            // operand and stage covers all of them; accumulators side by side)
@@ -203,7 +207,13 @@ constexpr int RED_ROWS = (SPLITCL > 1) ? BM / SPLITCL : BM;
 constexpr int RED_OWN_BYTES = BM * RED_LD * 4;
 constexpr int RED_BLOCK_BYTES = RED_ROWS * RED_LD * 4;
 constexpr int RED_BYTES = (SPLITCL > 1) ? RED_OWN_BYTES + (SPLITCL - 1) * RED_BLOCK_BYTES : 0;
-constexpr int PIPE_BYTES = (STAGES * STAGE_BYTES > RED_BYTES) ? STAGES * STAGE_BYTES : RED_BYTES;
+constexpr int SPLITT = OPEVO_SPLIT_TMA;        // TMA split-K slices (0: off)
+// TMA split-K staging in the (then idle) pipeline smem: a slice's fp32 tile
+// [BN/32 chunks][BM rows][32] for publishing, or the S-1 peers' tiles for
+// reducing
+constexpr int SPLITT_BYTES = SPLITT > 1 ? ((SPLITT - 1 > 1 ? SPLITT - 1 : 1) * BM * BN * 4) : 0;
+constexpr int PIPE_BYTES0 = (STAGES * STAGE_BYTES > RED_BYTES) ? STAGES * STAGE_BYTES : RED_BYTES;
+constexpr int PIPE_BYTES = PIPE_BYTES0 > SPLITT_BYTES ? PIPE_BYTES0 : SPLITT_BYTES;
 // Epilogue staging for TMA stores: per epilogue warp two buffers of
 // 32 rows x EPI_COLS outputs, laid out in the swizzle the C tensor map uses
 // (row bytes 32/64/128 -> SW32/64/128), so the warp's smem writes are
@@ -219,6 +229,10 @@ constexpr int BAR_OFF = EPI_OFF + EPI_BYTES;
 constexpr int BRES_OFF = BAR_OFF + 1024;
 static_assert(!B_RES || (OPEVO_CONV && SWZ == 128 && CG == 1 && SPLITCL == 0),
               "resident weights: conv, 128-byte swizzle");
+static_assert(SPLITT == 0 || ((SPLITT == 2 || SPLITT == 4) && SPLITCL == 0 && CG == 1 && CLUSTER == 1 &&
+                           BM == 128 && ACC == 1 && !OPEVO_BATCHED && !OPEVO_CONV && BN % 32 == 0 &&
+                           OPEVO_BPU == 1 && !OPEVO_OUT_F32),
+              "TMA split-K: S in {2,4}, single-CTA 128-row bf16 GEMM tiles");
 static_assert(SPLITCL == 0 || ((SPLITCL == 2 || SPLITCL == 4 || SPLITCL == 8) && CG == 1 && CLUSTER == 1 &&
                            MATOMS == 1 && BM % (SPLITCL * 8) == 0),
               "DSMEM split-K: S in {2,4,8}, single-CTA 128-row tiles");
@@ -609,6 +623,32 @@ __device__ __forceinline__ void stage_row(u32 buf, int r, const float (&acc)[STO
     }
 }
 
+// fp32 row of a 32-column chunk (128 bytes) in the SW128 layout of tma_w.
+__device__ __forceinline__ void stage_row_f32(u32 buf, int r, const float* acc) {
+    const u32 row = buf + (u32)(r * 128);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        st_shared_v4(row + (u32)((j ^ (r & 7)) << 4), __float_as_uint(acc[4 * j]), __float_as_uint(acc[4 * j + 1]),
+                     __float_as_uint(acc[4 * j + 2]), __float_as_uint(acc[4 * j + 3]));
+}
+
+__device__ __forceinline__ void add_row_f32(u32 buf, int r, float* acc) {
+    const u32 row = buf + (u32)(r * 128);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        float4 v;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(row + (u32)((j ^ (r & 7)) << 4)));
+        acc[4 * j] += v.x; acc[4 * j + 1] += v.y; acc[4 * j + 2] += v.z; acc[4 * j + 3] += v.w;
+    }
+}
+
+__device__ __forceinline__ u32 ld_acquire_gpu(const u32* p) {
+    u32 v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 // Write EPI_COLS fp32 accumulator values (one row segment) as the output type.
 __device__ __forceinline__ void store_row(void* c_out, u64 off, const float* acc) {
 #if OPEVO_OUT_F32
@@ -634,6 +674,7 @@ extern "C" __global__ void __launch_bounds__(NUM_THREADS, 2)   // 2: keep <= 168
 opevo_gemm(const __grid_constant__ TmaDesc tma_a,
            const __grid_constant__ TmaDesc tma_b,
            const __grid_constant__ TmaDesc tma_c,   // C, box = 32 rows x EPI_COLS (TMA-store epilogue)
+           const __grid_constant__ TmaDesc tma_w,   // split-K partials {cols, rows, split} fp32, box 32 x 32
            void* __restrict__ c_out,
            float* __restrict__ ws,            // split-K partials [split][batch*rows][cols]
            u32* __restrict__ counters,        // per-tile arrival counters (self-resetting)
@@ -650,7 +691,8 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
     u64* tempty_bar = tfull_bar + NBUF;       // epilogue -> MMA, per TMEM buffer
     u64* red_bar = tempty_bar + NBUF;         // DSMEM split-K: peers' partial rows landed
     u64* bres_bar = red_bar + 1;              // weight panel landed (B_RES)
-    u32* tmem_slot = reinterpret_cast<u32*>(bres_bar + 1);
+    u64* part_bar = bres_bar + 1;             // TMA split-K: peers' partials landed, per epilogue warp
+    u32* tmem_slot = reinterpret_cast<u32*>(part_bar + 4);
     u32* last_flag = tmem_slot + 1;
 
     const int warp = threadIdx.x >> 5;
@@ -768,6 +810,8 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
             mbar_init(smem_u32(red_bar), 1);
         }
         if (B_RES) mbar_init(smem_u32(bres_bar), 1);
+        if (SPLITT > 1)
+            for (int q = 0; q < 4; ++q) mbar_init(smem_u32(part_bar + q), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         if (SPLITCL > 1)
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
@@ -1108,6 +1152,87 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                     }
                 }
                 if (first && epi_tid == 0) TRACE(7);
+#if OPEVO_SPLIT_TMA > 1 && !OPEVO_CONV
+            } else if (SPLITT > 1) {
+                // ---- TMA split-K in one wave (the host guarantees every slice
+                // of every tile is resident, so slice 0 may wait for the rest):
+                // slices 1..S-1 publish their fp32 partial with TMA stores and
+                // count in; slice 0 waits for S-1 arrivals, TMA-loads the
+                // partials into its idle pipeline smem and sums them in z order
+                // onto its own accumulator, then stores bf16 C.
+                const int band0 = row0 + quarter * 32;          // first row of this warp's band
+                u32* cnt = counters + (t.row_tile * sched.col_groups + t.col_tile);
+                constexpr int CH = BN / 32;                      // 32-column fp32 chunks
+                if (t.kz != 0) {
+                    const u32 wst = smem_u32(smem) + (u32)(quarter * CH * 4096);
+#pragma unroll 1
+                    for (int c = 0; c < CH; ++c) {
+                        float acc[32];
+                        gather_acc<32>(lane_addr + c * 32, acc);
+                        stage_row_f32(wst + (u32)(c * 4096), lane, acc);
+                    }
+                    release();
+                    fence_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        for (int c = 0; c < CH; ++c) tma_store_3d(&tma_w, wst + (u32)(c * 4096), col0 + c * 32, band0, t.kz);
+                        bulk_commit();
+                        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // written, not just read
+                        asm volatile("fence.proxy.async.global;" ::: "memory");
+                    }
+                    epi_bar();
+                    if (epi_tid == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" :: "l"(cnt) : "memory");
+                } else {
+                    if (lane == 0) {
+                        const u64 t0 = global_ns();
+                        while (ld_acquire_gpu(cnt) < (u32)(SPLITT - 1)) {
+                            __nanosleep(64);
+                            if (global_ns() - t0 > 4000000000ull) asm volatile("trap;");
+                        }
+                        asm volatile("fence.proxy.async.global;" ::: "memory");
+                        const u32 pb = smem_u32(smem) + (u32)(quarter * (SPLITT - 1) * CH * 4096);
+                        // single lane: the plain arrive (mbar_expect_tx elects within a full warp)
+                        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                                     :: "r"(smem_u32(part_bar + quarter)), "r"((u32)((SPLITT - 1) * CH * 4096))
+                                     : "memory");
+                        for (int z = 1; z < SPLITT; ++z)
+                            for (int c = 0; c < CH; ++c)
+                                asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+                                             "[%0], [%1, {%3, %4, %5}], [%2];"
+                                             :: "r"(pb + (u32)(((z - 1) * CH + c) * 4096)), "l"(&tma_w),
+                                                "r"(smem_u32(part_bar + quarter)), "r"(col0 + c * 32), "r"(band0), "r"(z)
+                                             : "memory");
+                    }
+                    __syncwarp();
+                    mbar_wait(smem_u32(part_bar + quarter), 0);
+                    epi_bar();
+                    if (epi_tid == 0) *cnt = 0u;                     // ready for the next launch
+                    const u32 pb = smem_u32(smem) + (u32)(quarter * (SPLITT - 1) * CH * 4096);
+#pragma unroll 1
+                    for (int c = 0; c < BN; c += STORE_COLS) {
+                        float acc[STORE_COLS];
+                        gather_acc<STORE_COLS>(lane_addr + c, acc);
+                        if (c + STORE_COLS >= BN) release();
+#pragma unroll
+                        for (int h = 0; h < STORE_COLS / 32; ++h)
+                            for (int z = 1; z < SPLITT; ++z)
+                                add_row_f32(pb + (u32)(((z - 1) * CH + c / 32 + h) * 4096), lane, acc + 32 * h);
+                        const u32 buf = epi_stage + (u32)((nchunk & 1) * EPI_BUF);
+                        if (nchunk >= 2) {
+                            if (lane == 0) bulk_wait_read<1>();
+                            __syncwarp();
+                        }
+                        stage_row(buf, lane, acc);
+                        fence_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tma_store_2d(&tma_c, buf, col0 + c, band0);
+                            bulk_commit();
+                        }
+                        ++nchunk;
+                    }
+                }
+#endif
             } else if (SPLITCL > 1) {
                 // ---- DSMEM split-K: this CTA is slice kz == cluster rank
                 float* own = reinterpret_cast<float*>(smem);
@@ -1127,9 +1252,9 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 epi_bar();
             }
-            if (SPLITCL > 1) {
-                // steps 2-4 (DSMEM exchange + reduction) run after the role
-                // loops with every thread of the CTA, see below
+            if (SPLITCL > 1 || SPLITT > 1) {
+                // DSMEM: steps 2-4 (exchange + reduction) run after the role
+                // loops with every thread of the CTA, see below; TMA: done above
             } else if (split > 1) {
                 // split-K: publish this slice's fp32 partial, count arrivals; the
                 // last CTA of the tile sums all slices in z order (its own from

@@ -230,9 +230,20 @@ size_t dsmem_red_bytes(const Knobs& k) {
 
 size_t epi_stage_bytes(const Knobs& k, int out_f32);
 
-bool dsmem_split(const Knobs& k, int family) {
+// TMA split-K (split 2 or 4 on single-CTA 128-row bf16 GEMM tiles): the
+// slices of a tile reduce through fp32 partials in global memory written
+// and read by TMA, slice 0 waiting for the others -- one wave only (checked
+// at bind time).  Mirrors SPLITT in gemm_sm100.cuh and tma_split in mapping.py.
+int tma_split(const Knobs& k, int family, int batched) {
+    return (family == 0 && !batched && (k.split == 2 || k.split == 4) && k.cg == 1 && k.cluster == 1 &&
+            k.bm == 128 && k.acc == 1 && k.bpu <= 1 && k.bn % 32 == 0 &&
+            (size_t)(k.split - 1) * 128 * k.bn * 4 <= 196608)
+               ? k.split : 0;
+}
+
+bool dsmem_split(const Knobs& k, int family, int batched = 0) {
     return family != 2 && (k.split == 2 || k.split == 4 || k.split == 8) && k.cg == 1 &&
-           k.cluster == 1 && k.bm == 128 &&
+           k.cluster == 1 && k.bm == 128 && !tma_split(k, family, batched) &&
            (dsmem_red_bytes(k) + 1023) / 1024 * 1024 + epi_stage_bytes(k, 0) + 1024 + 256 <= 232448;
 }
 
@@ -248,12 +259,14 @@ size_t epi_stage_bytes(const Knobs& k, int out_f32) {
 
 // per-CTA: a CTA pair stages 128 rows of A and BN/2 rows of B each; then the
 // epilogue staging (1024-aligned) and the barriers (mirrors EPI_OFF/BAR_OFF)
-size_t smem_bytes(const Knobs& k, int family = 0, int out_f32 = 0) {
+size_t smem_bytes(const Knobs& k, int family = 0, int out_f32 = 0, int batched = 0) {
     if (family == 2) return 0;
     const int a_rows = k.cg == 2 ? 128 : k.bm;
     const int b_rows = b_resident(k, family) ? 0 : k.bn / (k.cg == 2 ? 2 : 1);
     size_t pipe = (size_t)k.stages * (size_t)(a_rows + b_rows) * (size_t)k.bk * 2 * (size_t)std::max(1, k.bpu);
-    if (dsmem_split(k, family)) pipe = std::max(pipe, dsmem_red_bytes(k));
+    if (dsmem_split(k, family, batched)) pipe = std::max(pipe, dsmem_red_bytes(k));
+    if (const int ts = tma_split(k, family, batched))
+        pipe = std::max(pipe, (size_t)std::max(ts - 1, 1) * 128 * k.bn * 4);   // SPLITT_BYTES
     pipe = (pipe + 1023) / 1024 * 1024;
     return pipe + epi_stage_bytes(k, out_f32) + 1024 + 256;
 }
@@ -298,7 +311,8 @@ std::string make_key(int family, const Knobs& k, int batched, int out_f32) {
     }
     snprintf(buf, sizeof buf, "f%d_m%d_n%d_k%d_s%d_b%d_o%d_c%d_h%d_w%d_a%d_g%d%s_%s%012llx", family,
              k.bm, k.bn, k.bk, k.stages, batched, out_f32, k.cluster, family == 1 ? k.tile_h : 1,
-             family == 1 ? k.tile_w : 1, k.acc, k.cg * 100 + (dsmem_split(k, family) ? k.split : 0),
+             family == 1 ? k.tile_w : 1, k.acc,
+             k.cg * 100 + (dsmem_split(k, family, batched) ? k.split : 0) + 10 * tma_split(k, family, batched),
              b_resident(k, family) ? "_r" : k.bpu > 1 ? (k.bpu == 2 ? "_u2" : "_u4") : "",
              want_lineinfo() ? "L" : "",
              (unsigned long long)(h & 0xffffffffffffull));
@@ -470,7 +484,8 @@ int nvrtc_build(int family, const Knobs& k, int batched, int out_f32, std::vecto
         "-DOPEVO_TILE_W=" + std::to_string(family == 1 ? k.tile_w : 1),
         "-DOPEVO_ACC=" + std::to_string(k.acc),
         "-DOPEVO_CTA_GROUP=" + std::to_string(k.cg),
-        "-DOPEVO_SPLIT_CLUSTER=" + std::to_string(dsmem_split(k, family) ? k.split : 0),
+        "-DOPEVO_SPLIT_CLUSTER=" + std::to_string(dsmem_split(k, family, batched) ? k.split : 0),
+        "-DOPEVO_SPLIT_TMA=" + std::to_string(tma_split(k, family, batched)),
         "-DOPEVO_B_RES=" + std::to_string(b_resident(k, family) ? 1 : 0),
         "-DOPEVO_BPU=" + std::to_string(family == 0 ? std::max(1, k.bpu) : 1)};
     if (want_lineinfo()) opts.push_back("-lineinfo");
@@ -655,6 +670,7 @@ struct opevo_kernel {
     alignas(64) CUtensorMap tma_a;
     alignas(64) CUtensorMap tma_b;
     alignas(64) CUtensorMap tma_c;      // output, box = one 32-row epilogue chunk
+    alignas(64) CUtensorMap tma_w{};    // TMA split-K partials {cols, rows, split} fp32 (else unused)
     unsigned grid[3] = {1, 1, 1};
     size_t smem = 0;
     int k_per_split = 0;
@@ -800,7 +816,7 @@ int launch_kernel(opevo_kernel* kr, char* err, size_t errlen, CUstream on = null
     void* cptr = (void*)op->c;
     float* ws = (float*)op->ws;
     unsigned* cnt = (unsigned*)op->counters;
-    void* args[] = {&kr->tma_a, &kr->tma_b, &kr->tma_c, &cptr, &ws, &cnt, &rows, &cols, &depth, &kr->sched,
+    void* args[] = {&kr->tma_a, &kr->tma_b, &kr->tma_c, &kr->tma_w, &cptr, &ws, &cnt, &rows, &cols, &depth, &kr->sched,
                     &kr->geom};
     CUlaunchConfig cfg{};
     cfg.gridDimX = kr->grid[0];
@@ -813,7 +829,9 @@ int launch_kernel(opevo_kernel* kr, char* err, size_t errlen, CUstream on = null
     cfg.hStream = strm;
     CUlaunchAttribute attr[2];
     unsigned na = 0;
-    const unsigned clx = (unsigned)(kr->k.cluster * kr->k.cg * (dsmem_split(kr->k, kr->family) ? kr->k.split : 1));
+    const int batched = op->d.kind == OPEVO_BATCHMATMUL ? 1 : 0;
+    const unsigned clx = (unsigned)(kr->k.cluster * kr->k.cg *
+                                    (dsmem_split(kr->k, kr->family, batched) ? kr->k.split : 1));
     if (clx > 1) {
         attr[na].id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
         attr[na].value.clusterDim.x = clx;
@@ -1242,8 +1260,8 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
     const int batched = op->d.kind == OPEVO_BATCHMATMUL ? 1 : 0;
     if (!knobs_compilable(family, k, err, errlen)) return OPEVO_INVALID_CONFIG;
     if (family == 2) return simt_kernel_get(ctx, op, k, out, info, t0, err, errlen);
-    if ((int)smem_bytes(k, family, op->out_f32) > ctx->smem_optin) {
-        put_err(err, errlen, "shared memory %zu B exceeds the device limit %d", smem_bytes(k, family, op->out_f32),
+    if ((int)smem_bytes(k, family, op->out_f32, batched) > ctx->smem_optin) {
+        put_err(err, errlen, "shared memory %zu B exceeds the device limit %d", smem_bytes(k, family, op->out_f32, batched),
                 ctx->smem_optin);
         return OPEVO_INVALID_CONFIG;
     }
@@ -1267,7 +1285,7 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
     kr->k = k;
     kr->family = family;
     kr->k_per_split = (int)(op->depth / k.split);
-    kr->smem = smem_bytes(k, family, op->out_f32);
+    kr->smem = smem_bytes(k, family, op->out_f32, batched);
     kr->flops = 2.0 * (double)op->batch * (double)op->rows * (double)op->cols * (double)op->depth;
     int st = OPEVO_OK;
     const int swz = swizzle_bytes(k.bk);
@@ -1373,7 +1391,8 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
         kr->sched = SchedHost{(int)row_tiles, (int)(col_tiles / k.cluster), (int)(op->batch / bpu), k.split,
                               0, 1, 0};
     }
-    const bool dsm = dsmem_split(k, family);
+    const bool dsm = dsmem_split(k, family, batched);
+    const int tsplit = tma_split(k, family, batched);
     const int clsz = k.cluster * k.cg * (dsm ? k.split : 1);
     if (st) {
         delete kr;
@@ -1418,15 +1437,28 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
             }
         }
         sc.units = sc.head_tiles * sc.split + (tiles - sc.head_tiles) * sc.split * sc.tail_split;
-        // DSMEM split-K clusters each own exactly one unit (no persistence)
-        const int clusters = (k.grid_mode == 1 || dsm) ? sc.units / (dsm ? k.split : 1)
-                                                      : std::min(sc.units, capacity);
+        // DSMEM split-K clusters each own exactly one unit (no persistence);
+        // TMA split-K needs every slice resident at once (slice 0 waits for
+        // the others): one wave or the configuration is infeasible
+        if (tsplit && sc.units > capacity) {
+            put_err(err, errlen, "TMA split-K needs one wave: %d units > %d resident CTAs", sc.units, capacity);
+            delete kr;
+            return OPEVO_INVALID_CONFIG;
+        }
+        const int clusters = (k.grid_mode == 1 || dsm || tsplit) ? sc.units / (dsm ? k.split : 1)
+                                                                 : std::min(sc.units, capacity);
         kr->grid[0] = (unsigned)(clusters * clsz);
         kr->grid[1] = kr->grid[2] = 1;
         const int max_split = sc.split * sc.tail_split;
         if (max_split > 1 && !dsm) {
             const size_t slice = (size_t)op->batch * op->rows * op->cols * 4;
             st = ensure_ws(op, slice * max_split, (size_t)tiles * clsz * 4, err, errlen);
+            if (!st && tsplit) {
+                uint64_t wd[3] = {(uint64_t)op->cols, (uint64_t)op->rows, (uint64_t)tsplit};
+                uint64_t wstr[2] = {(uint64_t)op->cols * 4, (uint64_t)op->cols * op->rows * 4};
+                uint32_t wb[3] = {32, 32, 1};
+                st = encode_map(&kr->tma_w, op->ws, 3, wd, wstr, wb, 128, err, errlen, 1);
+            }
             if (st) {
                 delete kr;
                 return st;

@@ -55,6 +55,7 @@ from .operators import (
 from .spaces import Discrete, SearchSpace
 
 SMEM_LIMIT = 232448          # 227 KB opt-in per CTA on B200
+B200_SMS = 148
 SMEM_EXTRA = 1024 + 256      # alignment slack + barriers
 STAGE_VALUES = (2, 3, 4, 5, 6, 7, 8)
 UNROLL_TO_STAGES = {0: 2, 16: 3, 64: 4, 512: 6, 1500: 8}
@@ -82,10 +83,22 @@ class Knobs:
     b_res: int = 0           # conv: weight panel resident in shared memory
     bpu: int = 1             # BatchMatMul: batches per work unit
     panel_bytes: int = 0     # size of the resident panel (BN x K x 2; not a code knob)
+    family: int = 0          # kernel family / batched operator (set by the mapping; decide
+    batched: int = 0         # which split-K reduction is compiled in)
 
     def as_tuple(self) -> tuple[int, ...]:
         return (self.bm, self.bn, self.bk, self.stages, self.split, self.cluster,
                 self.tile_h, self.tile_w, self.acc, self.cta_group, self.grid, self.b_res, self.bpu)
+
+    def tma_split(self) -> int:
+        """Split factor compiled in when the K slices reduce through fp32
+        partials moved by TMA in one wave (mirrors ``tma_split`` in
+        csrc/opevo.cpp), else 0."""
+        s = self.split
+        ok = (self.family == FAMILY_GEMM and not self.batched and s in (2, 4) and self.cta_group == 1
+              and self.cluster == 1 and self.bm == 128 and self.acc == 1 and self.bpu <= 1
+              and self.bn % 32 == 0 and (s - 1) * 128 * self.bn * 4 <= 196608)
+        return s if ok else 0
 
     def dsmem_split(self) -> int:
         """Split factor compiled in when the K slices reduce through DSMEM
@@ -94,6 +107,7 @@ class Knobs:
         ld = self.bn + 4
         red = self.bm * ld * 4 + (s - 1) * (self.bm // max(s, 1)) * ld * 4
         ok = (s in (2, 4, 8) and self.cta_group == 1 and self.cluster == 1 and self.bm == 128
+              and not self.tma_split()
               and _align1k(red) + epi_bytes(self.bn) + SMEM_EXTRA <= SMEM_LIMIT)
         return s if ok else 0
 
@@ -101,7 +115,7 @@ class Knobs:
         """Fields that change the generated code (split-K is a launch arg
         except for DSMEM-reduced splits)."""
         return (self.bm, self.bn, self.bk, self.stages, self.cluster, self.tile_h, self.tile_w,
-                self.acc, self.cta_group, self.dsmem_split(), self.b_res, self.bpu)
+                self.acc, self.cta_group, self.dsmem_split(), self.tma_split(), self.b_res, self.bpu)
 
     def smem_bytes(self) -> int:
         """Mirrors ``smem_bytes`` in csrc/opevo.cpp (bf16 output)."""
@@ -111,6 +125,8 @@ class Knobs:
         if self.dsmem_split():
             ld = self.bn + 4
             pipe = max(pipe, self.bm * ld * 4 + (self.split - 1) * (self.bm // self.split) * ld * 4)
+        if self.tma_split():
+            pipe = max(pipe, max(self.split - 1, 1) * 128 * self.bn * 4)
         return _align1k(pipe) + epi_bytes(self.bn) + SMEM_EXTRA
 
 
@@ -208,7 +224,12 @@ def _gemm_knobs(rows: int, cols: int, depth: int, vals: dict,
     if stages < 1:
         return None, "one stage does not fit in shared memory"
     cluster = 1 if (cta_group == 2 or bpu > 1) else _largest_pow2_divisor(m[1], m[0])
-    return Knobs(bm, bn, bk, stages, split, cluster, cta_group=cta_group, bpu=bpu), ""
+    kn = Knobs(bm, bn, bk, stages, split, cluster, cta_group=cta_group, bpu=bpu,
+               batched=int(bool(batch)))
+    if kn.tma_split() and (rows // bm) * (cols // bn) * split > B200_SMS:
+        # slice 0 of a tile waits for the others: every slice must be resident
+        return None, "TMA split-K needs one wave of CTAs"
+    return kn, ""
 
 
 def _batches_per_unit(vals: dict, batch: int, bm: int, bn: int, bk: int, split: int,
@@ -257,11 +278,12 @@ def _conv_knobs(spec: Conv2dSpec, vals: dict) -> tuple[Knobs | None, str]:
     if vals.get("unroll_explicit") == UNROLL_ON:
         stages, panel = _conv_resident_fit(spec, bn, bk, split, want, bm)
         if stages:
-            return Knobs(bm, bn, bk, stages, split, 1, th, tw, b_res=1, panel_bytes=panel), ""
+            return Knobs(bm, bn, bk, stages, split, 1, th, tw, b_res=1, panel_bytes=panel,
+                         family=FAMILY_CONV), ""
     stages = _fit_stages(want, bm, bn, bk)
     if stages < 1:
         return None, "one stage does not fit in shared memory"
-    return Knobs(bm, bn, bk, stages, split, 1, th, tw), ""
+    return Knobs(bm, bn, bk, stages, split, 1, th, tw, family=FAMILY_CONV), ""
 
 
 def _conv_resident_fit(spec: Conv2dSpec, bn: int, bk: int, split: int, want: int,

@@ -57,10 +57,11 @@ def family_instances(spec) -> set[tuple[int, bool, tuple]]:
                                     if su >= 1:
                                         out.add((0, batched, Knobs(bm, bn, bk, su, 1, 1, bpu=u).as_tuple()))
                             # DSMEM split-K instances compile the split in
+                            # (TMA split-K for non-batched 2/4 slices) compile the split in
                             if cg == 1 and bm == 128:
                                 for sp in (2, 4, 8):
-                                    kn = Knobs(bm, bn, bk, s, sp, 1)
-                                    if kn.dsmem_split() and spec.k % (sp * bk) == 0:
+                                    kn = Knobs(bm, bn, bk, s, sp, 1, batched=int(batched))
+                                    if (kn.dsmem_split() or kn.tma_split()) and spec.k % (sp * bk) == 0:
                                         out.add((0, batched, kn.as_tuple()))
     elif isinstance(spec, Conv2dSpec):
         if spec.stride != 1:

@@ -83,9 +83,12 @@ GEMM_CASES = [
     (2048, 4096, 256, (256, 128, 64, 4, 1, 1, 1, 1, 1, 2)),
     (2048, 2048, 512, (128, 64, 64, 4, 1, 1, 1, 1, 1, 1, 1)),
     (2048, 2048, 512, (256, 256, 64, 3, 1, 1, 1, 1, 1, 1, 0)),
-    # DSMEM split-K (the K slices of a tile form a cluster, reduce in smem)
+    # TMA split-K (2 or 4 slices, one wave: fp32 partials through TMA)
     (512, 1024, 1024, (128, 128, 64, 4, 2)),
-    (512, 1024, 1024, (128, 64, 128, 3, 4)),
+    (512, 1024, 1024, (128, 128, 64, 4, 4)),
+    (1024, 1024, 1024, (128, 128, 128, 3, 2)),
+    (512, 1024, 1024, (128, 256, 64, 3, 2)),
+    # DSMEM split-K (the K slices of a tile form a cluster, reduce in smem)
     (512, 1024, 1024, (128, 32, 64, 4, 8)),
     (512, 960, 1024, (128, 48, 64, 4, 2)),
     # split 16 falls back to the global-memory reduction

@@ -77,10 +77,10 @@ def test_conv_mapping():
     m = config_to_knobs(spec, sp, cfg)
     assert m.valid and m.family == 1
     # co[1] = 2 (even): two M=128 atoms per K step -> 256-pixel tiles (8x8x4)
-    assert m.knobs == Knobs(256, 64, 64, 4, 3, 1, 8, 8)
+    assert m.knobs == Knobs(256, 64, 64, 4, 3, 1, 8, 8, family=1)
     # co[1] odd: 128-pixel tiles (8x8x2)
     m = config_to_knobs(spec, sp, ((1, 1, 8, 8),) + cfg[1:])
-    assert m.valid and m.knobs == Knobs(128, 64, 64, 4, 3, 1, 8, 8)
+    assert m.valid and m.knobs == Knobs(128, 64, 64, 4, 3, 1, 8, 8, family=1)
     # explicit unroll without a tap split: the weight panel stays resident
     m = config_to_knobs(spec, sp, ((1, 1, 8, 8), (7, 1, 2, 4), (7, 2, 2, 2), (1, 64), (1, 3), (1, 3),
                                    "explicit_unroll_on", 512))

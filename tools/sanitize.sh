@@ -16,6 +16,8 @@ run gemm_pair          matmul:512,512,512            256,64,128,4,1,1,1,1,1,2
 run gemm_multicast     matmul:256,512,512            128,64,64,4,1,2
 run gemm_split_dsmem   matmul:256,512,512            128,64,64,4,2,1
 run gemm_split_global  matmul:256,512,1024           128,64,64,2,16,1
+run gemm_split_tma2    matmul:256,512,1024           128,128,64,4,2,1
+run gemm_split_tma4    matmul:256,512,1024           128,64,64,4,4,1
 run gemm_persistent    matmul:2048,2048,256          128,64,64,4,1,1
 run gemm_sw32          matmul:256,480,512            128,48,16,8,1,1
 run bmm_bpu4           batchmatmul:8,128,64,128      128,64,64,2,1,1,1,1,1,1,0,0,4
