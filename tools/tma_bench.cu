@@ -183,6 +183,54 @@ __global__ void __launch_bounds__(64, 1) tma_conv4d(const __grid_constant__ CUte
     }
 }
 
+// Conv activation loads in TMA im2col mode: a run of `pixels` consecutive
+// output pixels (linear over N x H x W), 64 channels each, one instruction
+// per filter tap (the tap is the im2col offset).
+__global__ void __launch_bounds__(64, 1) tma_conv_im2col(const __grid_constant__ CUtensorMap mx, int pixels, int W,
+                                                         int H, int N, int tiles_per_cta, int stages, u64* out) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    __shared__ __align__(8) u64 full[16];
+    unsigned char* smem = (unsigned char*)(((u64)smem_raw + 1023) & ~1023ull);
+    const int stage_bytes = pixels * 128;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(&full[s])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int n_it = tiles_per_cta * 9;
+    u64 c0 = clock64(), t0 = gtimer();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < n_it + stages; ++i) {
+            if (i >= stages) {
+                const int s = (i - stages) % stages;
+                const u32 par = ((i - stages) / stages) & 1;
+                asm volatile("{ .reg .pred p; W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra W; }"
+                             :: "r"(smem_u32(&full[s])), "r"(par) : "memory");
+            }
+            if (i < n_it) {
+                const int s = i % stages;
+                const u32 bar = smem_u32(&full[s]);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(stage_bytes) : "memory");
+                const int tile = blockIdx.x + (i / 9) * gridDim.x, tap = i % 9;
+                const int m0 = (tile * pixels) % (N * H * W);
+                const int q0 = m0 % W, p0 = (m0 / W) % H, n0 = m0 / (W * H);
+                const unsigned short ow = (unsigned short)(tap % 3), oh = (unsigned short)(tap / 3);
+                asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+                             " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};"
+                             :: "r"(smem_u32(smem + s * stage_bytes)), "l"(&mx), "r"(bar), "r"(0), "r"(q0 - 1),
+                                "r"(p0 - 1), "r"(n0), "h"(ow), "h"(oh) : "memory");
+            }
+        }
+    }
+    __syncthreads();
+    u64 c1 = clock64(), t1 = gtimer();
+    if (threadIdx.x == 0) {
+        out[blockIdx.x * 2] = c1 - c0;
+        out[blockIdx.x * 2 + 1] = t1 - t0;
+    }
+}
+
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); exit(1); } } while (0)
 
 static CUtensorMap make_map(void* base, int rows, int K, int box_rows) {
@@ -272,6 +320,39 @@ int main() {
                 const double bytes = tiles * 9.0 * 16384;
                 printf("conv4d box w%d h%d n%d st%d: %6.1f B/clk/SM %6.1f GB/s/SM  %.0f ns per box\n", sh[0], sh[1], sh[2],
                        stages, bytes / cyc, bytes / ns, ns / (tiles * 9));
+            }
+        }
+    }
+    {
+        const int N = 32, H = 56, W = 56, C = 64;
+        void* x;
+        CK(cudaMalloc(&x, (size_t)N * H * W * C * 2));
+        CK(cudaMemset(x, 0, (size_t)N * H * W * C * 2));
+        CK(cudaFuncSetAttribute(tma_conv_im2col, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        for (int pixels : {128, 256}) {
+            CUtensorMap m;
+            cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+            cuuint64_t strides[3] = {(cuuint64_t)C * 2, (cuuint64_t)C * W * 2, (cuuint64_t)C * W * H * 2};
+            int lo[2] = {-1, -1}, hi[2] = {-1, -1};
+            cuuint32_t es[4] = {1, 1, 1, 1};
+            CUresult r = cuTensorMapEncodeIm2col(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, x, dims, strides, lo, hi, 64,
+                                                 (cuuint32_t)pixels, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) { printf("encode im2col failed %d\n", (int)r); continue; }
+            for (int stages : {4, 8}) {
+                const int grid = 148, tiles = 5;
+                for (int rep = 0; rep < 3; ++rep)
+                    tma_conv_im2col<<<grid, 64, stages * pixels * 128 + 1024>>>(m, pixels, W, H, N, tiles, stages, d_out);
+                CK(cudaDeviceSynchronize());
+                u64 h[2 * 148];
+                CK(cudaMemcpy(h, d_out, sizeof(u64) * 2 * grid, cudaMemcpyDeviceToHost));
+                double ns = 0, cyc = 0;
+                for (int i = 0; i < grid; ++i) { cyc += h[2 * i]; ns += h[2 * i + 1]; }
+                cyc /= grid; ns /= grid;
+                const double bytes = tiles * 9.0 * pixels * 128;
+                printf("im2col pixels %d st%d: %6.1f B/clk/SM %6.1f GB/s/SM  %.0f ns per box\n", pixels, stages,
+                       bytes / cyc, bytes / ns, ns / (tiles * 9));
             }
         }
     }
