@@ -390,12 +390,22 @@ def main() -> None:
         k.close()
         ach = spec.flops() / (ms * 1e-3) / 1e12
         peak = pk["tflops"] if args.dtype == "bf16" else FP32_PEAK
-        roof = {"bound": "tensor" if args.dtype == "bf16" else "fp32-fma", "achieved": ach,
-                "peak": peak, "unit": "TFLOP/s",
-                "frac": ach / peak, "traffic": _ncu_traffic(best_knobs),
-                "peak_source": (f"{pk['source']} burst bf16 (MEASURED_PEAKS.json)" if args.dtype == "bf16"
-                                else "nominal fp32 FMA peak at 1965 MHz (no measured figure)"),
-                "kernel_ms": ms, "per_launch_flops": spec.flops()}
+        nbytes = algo_bytes(spec, 2 if args.dtype == "bf16" else 4)
+        if args.dtype == "bf16" and spec.flops() / nbytes < pk["tflops"] * 1e3 / pk["hbm_gbs"]:
+            # below the ridge (BMM 960x128x64x128: AI 32): HBM-bound roofline
+            gbs = nbytes / (ms * 1e-3) / 1e9
+            roof = {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                    "frac": gbs / pk["hbm_gbs"], "traffic": _ncu_traffic(args.op, best_knobs),
+                    "peak_source": f"{pk['source']} HBM copy bandwidth (MEASURED_PEAKS.json)",
+                    "note": "fitness is L2-warm (operands fit in L2), so frac can exceed 1",
+                    "kernel_ms": ms, "per_launch_bytes": nbytes, "achieved_tflops": ach}
+        else:
+            roof = {"bound": "tensor" if args.dtype == "bf16" else "fp32-fma", "achieved": ach,
+                    "peak": peak, "unit": "TFLOP/s",
+                    "frac": ach / peak, "traffic": _ncu_traffic(args.op, best_knobs),
+                    "peak_source": (f"{pk['source']} burst bf16 (MEASURED_PEAKS.json)" if args.dtype == "bf16"
+                                    else "nominal fp32 FMA peak at 1965 MHz (no measured figure)"),
+                    "kernel_ms": ms, "per_launch_flops": spec.flops(), "per_launch_bytes": nbytes}
 
     if rank == 0:
         cpu = None if (args.no_cpu or world > 1) else cpu_reference_arm(
@@ -453,16 +463,30 @@ def main() -> None:
         dist.destroy_process_group()
 
 
-def _ncu_traffic(knobs) -> float | None:
-    """DRAM read+write bytes per launch of this exact instance from the
-    committed ncu capture (profiles/ncu_summary.json), else None."""
+def algo_bytes(spec, elem: int) -> int:
+    """Algorithmic bytes of one launch: every input read once, the output
+    written once."""
+    from paper_2006_05664_b200.operators import BatchMatMulSpec, MatMulSpec
+    if isinstance(spec, MatMulSpec):
+        return elem * (spec.n * spec.k + spec.m * spec.k + spec.n * spec.m)
+    if isinstance(spec, BatchMatMulSpec):
+        return elem * spec.b * (spec.n * spec.k + spec.m * spec.k + spec.n * spec.m)
+    return elem * (spec.batch * spec.in_channels * spec.in_height * spec.in_width
+                   + spec.out_channels * spec.in_channels * spec.kernel_h * spec.kernel_w
+                   + spec.batch * spec.out_channels * spec.out_height * spec.out_width)
+
+
+def _ncu_traffic(op: str, knobs) -> float | None:
+    """DRAM read+write bytes per launch of this exact instance on this
+    operator from the committed ncu capture (profiles/ncu_summary.json,
+    keyed "operator|knobs"), else None."""
     path = os.path.join(REPO, "profiles", "ncu_summary.json")
     try:
         with open(path) as fh:
             d = json.load(fh)
     except (OSError, ValueError):
         return None
-    entry = d.get("kernels", {}).get(",".join(map(str, knobs)))
+    entry = d.get("kernels", {}).get(op + "|" + ",".join(map(str, knobs)))
     return entry.get("dram_bytes") if entry else None
 
 
