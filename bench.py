@@ -232,8 +232,9 @@ def main() -> None:
     ap.add_argument("--timing", default="stream", choices=("graph", "stream"),
                     help="fitness launches: stream launches released together by a device gate "
                          "(default) or one CUDA graph")
-    ap.add_argument("--dtype", default="bf16", choices=("bf16", "f32"),
-                    help="f32: the SIMT family on the reference space (cfg1)")
+    ap.add_argument("--dtype", default="bf16", choices=("bf16", "f32", "tf32x3"),
+                    help="f32: the SIMT family on the reference space (cfg1); tf32x3: fp32 "
+                         "operands on the tensor cores (three kind::tf32 MMAs per K step)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-preload", action="store_true",
                     help="do not load the cached kernel family into the context before timing")
@@ -250,7 +251,7 @@ def main() -> None:
     import torch.distributed as dist
 
     from paper_2006_05664_b200 import EngineConfig, OpEvo, parse_operator
-    from paper_2006_05664_b200.evaluator import EvalSettings, GpuEvaluator
+    from paper_2006_05664_b200.evaluator import DTYPES, EvalSettings, GpuEvaluator
     from paper_2006_05664_b200.logs import TrialRecorder
     from paper_2006_05664_b200.mapping import config_to_knobs, gpu_operator_space
     from paper_2006_05664_b200.reporting import trials_to_fraction, wallclock_to_fraction
@@ -274,7 +275,7 @@ def main() -> None:
     space = gpu_operator_space(spec, args.dtype)
     settings = EvalSettings(reps=args.reps, preload_family=not args.no_preload,
                             flush_l2=1 if args.l2 == "cold" else (2 if args.timing == "stream" else 0),
-                            dtype=capi.F32 if args.dtype == "f32" else capi.BF16)
+                            dtype=DTYPES[args.dtype])
     local_ev = GpuEvaluator(spec, space, local, settings)
     if world > 1:
         evaluator = ShardedEvaluator(local_ev, rank, world, device=coll_device)
@@ -389,7 +390,7 @@ def main() -> None:
         best_cold = spec.flops() / (k.time(warmup=2, reps=20, flush_l2=True) * 1e-3) / 1e12
         k.close()
         ach = spec.flops() / (ms * 1e-3) / 1e12
-        peak = pk["tflops"] if args.dtype == "bf16" else FP32_PEAK
+        peak = _dtype_peak(args.dtype, pk)
         nbytes = algo_bytes(spec, 2 if args.dtype == "bf16" else 4)
         if args.dtype == "bf16" and spec.flops() / nbytes < pk["tflops"] * 1e3 / pk["hbm_gbs"]:
             # below the ridge (BMM 960x128x64x128: AI 32): HBM-bound roofline
@@ -400,11 +401,10 @@ def main() -> None:
                     "note": "fitness is L2-warm (operands fit in L2), so frac can exceed 1",
                     "kernel_ms": ms, "per_launch_bytes": nbytes, "achieved_tflops": ach}
         else:
-            roof = {"bound": "tensor" if args.dtype == "bf16" else "fp32-fma", "achieved": ach,
+            roof = {"bound": "fp32-fma" if args.dtype == "f32" else "tensor", "achieved": ach,
                     "peak": peak, "unit": "TFLOP/s",
                     "frac": ach / peak, "traffic": _ncu_traffic(args.op, best_knobs),
-                    "peak_source": (f"{pk['source']} burst bf16 (MEASURED_PEAKS.json)" if args.dtype == "bf16"
-                                    else "nominal fp32 FMA peak at 1965 MHz (no measured figure)"),
+                    "peak_source": _dtype_peak_source(args.dtype, pk),
                     "kernel_ms": ms, "per_launch_flops": spec.flops(), "per_launch_bytes": nbytes}
 
     if rank == 0:
@@ -421,6 +421,8 @@ def main() -> None:
             "dtype": args.dtype, "data": "synthetic",
             "config": {"workload": (f"OpEvo tuning of the sm_100a tcgen05 kernel family on {args.op} "
                                     f"bf16" if args.dtype == "bf16" else
+                                    f"OpEvo tuning of the sm_100a tcgen05 3xTF32 family on {args.op} "
+                                    f"fp32" if args.dtype == "tf32x3" else
                                     f"OpEvo tuning of the sm_100a fp32 SIMT family (paper TVM dense "
                                     f"schedule) on {args.op} fp32")
                                    + (" (BASELINE configs[1])" if args.op == DEFAULT_OP
@@ -447,7 +449,7 @@ def main() -> None:
                                         "loaded into the context before timing" if not args.no_preload
                                         else "prebuilt cubins (build()), loaded on first use")},
             "best_tflops": best.fitness,
-            "best_frac_of_peak": best.fitness / (pk["tflops"] if args.dtype == "bf16" else FP32_PEAK),
+            "best_frac_of_peak": best.fitness / _dtype_peak(args.dtype, pk),
             "best_knobs": best_knobs, "best_config": space.config_to_json(best.config),
             "best_tflops_cold_l2": best_cold,
             "trials_to_95pct": trials_to_fraction(records),
@@ -461,6 +463,25 @@ def main() -> None:
     local_ev.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def _dtype_peak(dtype: str, pk: dict) -> float:
+    """Roofline denominator (TFLOP/s of useful work) for a compute dtype."""
+    if dtype == "bf16":
+        return pk["tflops"]
+    if dtype == "tf32x3":
+        # kind::tf32 runs at half the bf16 rate and every K step issues three
+        return pk["tflops"] / 2 / 3
+    return FP32_PEAK
+
+
+def _dtype_peak_source(dtype: str, pk: dict) -> str:
+    if dtype == "bf16":
+        return f"{pk['source']} burst bf16 (MEASURED_PEAKS.json)"
+    if dtype == "tf32x3":
+        return (f"{pk['source']} burst bf16 (MEASURED_PEAKS.json) / 2 (tf32 rate) / 3 (MMAs per "
+                f"K step): the 3xTF32 ceiling in useful fp32 FLOP/s")
+    return "nominal fp32 FMA peak at 1965 MHz (no measured figure)"
 
 
 def algo_bytes(spec, elem: int) -> int:

@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define OPEVO_ABI_VERSION 3   /* 3: 13-slot knob vector (b_res, bpu), trial batch, preload */
+#define OPEVO_ABI_VERSION 4   /* 4: OPEVO_F32_TF32X3; 3: 13-slot knobs, trial batch, preload */
 
 enum opevo_status {
     OPEVO_OK = 0,
@@ -50,7 +50,12 @@ enum opevo_status {
 
 /* operator kinds (reference benchmarks.py:36-107) */
 enum opevo_op_kind { OPEVO_MATMUL = 0, OPEVO_BATCHMATMUL = 1, OPEVO_CONV2D = 2 };
-enum opevo_dtype { OPEVO_BF16 = 0, OPEVO_F32 = 1 };
+/* OPEVO_F32: fp32 in/out on the CUDA cores (the paper's SIMT schedule, knob
+ * slots 0..7 = n2 n3 n4 m2 m3 m4 k2 k3).  OPEVO_F32_TF32X3: fp32 in/out on
+ * the tensor cores as three kind::tf32 MMAs per K step (hi*hi + hi*lo +
+ * lo*hi), the tcgen05 knob layout with BK in fp32 elements (a multiple of 8;
+ * 8, 16 or a multiple of 32 up to 128). */
+enum opevo_dtype { OPEVO_BF16 = 0, OPEVO_F32 = 1, OPEVO_F32_TF32X3 = 2 };
 
 /*
  * Operator descriptor.  MatMul / BatchMatMul use GEMM naming:
@@ -112,7 +117,8 @@ typedef struct opevo_kernel opevo_kernel;
 int opevo_abi_version(void);
 
 /* NVRTC compile of one instance into the on-disk cubin cache; no device
- * needed.  family: 0 = GEMM, 1 = implicit-GEMM conv.  Thread-safe. */
+ * needed.  family: 0 = GEMM, 1 = implicit-GEMM conv, 2 = fp32 SIMT,
+ * 3 = fp32 3xTF32 GEMM (out_f32 = 1).  Thread-safe. */
 int opevo_compile(int family, const int32_t* knobs, int nknobs, int batched, int out_f32,
                   const char* cache_dir, double* compile_ms, char* err, size_t errlen);
 

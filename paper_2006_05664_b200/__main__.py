@@ -39,11 +39,10 @@ def _objective(args):
     spec = parse_operator(args.operator)
     if args.evaluator == "synthetic":
         return make_objective(spec)
-    from . import capi
-    from .evaluator import EvalSettings, GpuEvaluator
+    from .evaluator import DTYPES, EvalSettings, GpuEvaluator
 
     ev = GpuEvaluator(spec, None, args.device,
-                      EvalSettings(reps=args.reps, dtype=capi.F32 if args.dtype == "f32" else capi.BF16,
+                      EvalSettings(reps=args.reps, dtype=DTYPES[args.dtype],
                                    preload_family=True))
     return ev.space, ev
 
@@ -115,7 +114,7 @@ def main(argv=None) -> int:
         p = sub.add_parser(name)
         p.add_argument("--operator", required=True)
         p.add_argument("--evaluator", default="gpu", choices=("gpu", "synthetic"))
-        p.add_argument("--dtype", default="bf16", choices=("bf16", "f32"))
+        p.add_argument("--dtype", default="bf16", choices=("bf16", "f32", "tf32x3"))
         p.add_argument("--device", type=int, default=0)
         p.add_argument("--reps", type=int, default=20)
         p.add_argument("--budget", type=int, default=500)

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libopevo.so")
 DEFAULT_CACHE = os.path.join(HERE, "kernel_cache")
 
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 # status codes (opevo.h)
 OK = 0
@@ -36,7 +36,8 @@ STATUS_NAMES = {OK: "ok", INVALID_CONFIG: "invalid_config", COMPILE_ERROR: "comp
                 ERR_ARG: "bad_argument", ERR_CUDA: "cuda_error"}
 
 MATMUL, BATCHMATMUL, CONV2D = 0, 1, 2
-BF16, F32 = 0, 1
+BF16, F32, F32_TF32X3 = 0, 1, 2
+FP32_OUT = (F32, F32_TF32X3)
 NUM_KNOBS = 13
 KNOB_NAMES = ("bm", "bn", "bk", "stages", "split", "cluster", "tile_h", "tile_w", "acc",
               "cta_group", "grid")
@@ -329,7 +330,7 @@ class Operand:
     def reference(self):
         import numpy as np
 
-        n = self.c_bytes // (4 if self.desc.dtype == F32 else 2)
+        n = self.c_bytes // (4 if self.desc.dtype in FP32_OUT else 2)
         out = np.empty(n, dtype=np.float32)
         err = _errbuf()
         _check(self.dev.lib.opevo_op_reference(
@@ -340,7 +341,7 @@ class Operand:
         """Kernel output as float32 numpy (bf16 widened)."""
         import numpy as np
 
-        if self.desc.dtype == F32:
+        if self.desc.dtype in FP32_OUT:
             out = np.empty(self.c_bytes // 4, dtype=np.float32)
             self.download(out.ctypes.data, self.c_bytes)
             return out

@@ -27,6 +27,12 @@
 //                 (cp.async.bulk shared::cluster, DSMEM); every CTA then sums
 //                 its own row block in z order and writes it.  No partials
 //                 touch global memory.
+//   OPEVO_TF32X3  1: fp32 operands on the tensor cores, three kind::tf32 MMAs
+//                 per K step (hi*hi + hi*lo + lo*hi, fp32-level accuracy).
+//                 The host views each fp32 operand as bf16 pairs -- BK, depth
+//                 and every byte offset keep the bf16 meaning, so K8 of tf32
+//                 is one 32-byte K16 step -- and the epilogue warps write the
+//                 lo part of each landed stage into a second area.
 //   OPEVO_ACC     independent TMEM accumulators the K loop round-robins over
 //                 (summed in the epilogue).  Consecutive MMAs into one
 //                 accumulator form a dependent chain; for small N the chain
@@ -102,6 +108,9 @@
 #define OPEVO_BPU 1        // BatchMatMul: consecutive batches per work unit (one TMA box per
                            // operand and stage covers all of them; accumulators side by side)
 #endif
+#ifndef OPEVO_TF32X3
+#define OPEVO_TF32X3 0     // fp32 GEMM as 3xTF32 on tcgen05 (fp32 in/out)
+#endif
 #ifndef OPEVO_ACC
 #define OPEVO_ACC 1        // K-interleaved TMEM accumulators (1, 2, 4)
 #endif
@@ -140,8 +149,11 @@ constexpr int A_TILE = BPU * A_SUB;
 constexpr bool B_RES = OPEVO_B_RES != 0;
 constexpr int B_SUB = BN_LOAD * BK * 2;
 constexpr int B_TILE = B_RES ? 0 : BPU * B_SUB;               // per stage (0: panel resident)
-constexpr int STAGE_BYTES = A_TILE + B_TILE;
-constexpr int TX_BYTES = STAGE_BYTES * CG;                // bytes landing per stage (pair)
+constexpr bool X3 = OPEVO_TF32X3 != 0;
+constexpr int LOAD_BYTES = A_TILE + B_TILE;               // what TMA lands per stage
+constexpr int LO_OFF = LOAD_BYTES;                        // X3: lo parts, same layout
+constexpr int STAGE_BYTES = X3 ? 2 * LOAD_BYTES : LOAD_BYTES;
+constexpr int TX_BYTES = LOAD_BYTES * CG;                 // bytes landing per stage (pair)
 constexpr int A_SLICE_ROWS = BM_CTA / CLUSTER;            // rows of A each cluster CTA fetches
 // K-fused loads: with 128-byte swizzle the host encodes A and B as
 // {64, rows, K/64 (, batch)} "atom" views (row stride K*2 bytes, atom stride
@@ -178,9 +190,14 @@ static_assert(CG == 1 || (CG == 2 && BM == 256 && CLUSTER == 1 && !OPEVO_CONV &&
 static_assert(!OPEVO_CONV || (TILE_N * TILE_H * TILE_W == BM && CLUSTER == 1),
               "conv tile must cover BM pixels, no multicast");
 
-// UMMA instruction descriptor, kind::f16: D=f32, A=B=bf16, both K-major.
-constexpr u32 IDESC = (1u << 4) | (1u << 7) | (1u << 10) |
+// UMMA instruction descriptor, kind::f16: D=f32, A=B=bf16, both K-major
+// (kind::tf32 for X3: A=B=tf32, format code 2).
+constexpr u32 AB_FMT = X3 ? 2u : 1u;
+constexpr u32 IDESC = (1u << 4) | (AB_FMT << 7) | (AB_FMT << 10) |
                       ((u32)(BN >> 3) << 17) | ((u32)(UMMA_M >> 4) << 24);
+static_assert(!X3 || (CG == 1 && CLUSTER == 1 && !OPEVO_CONV && BPU == 1 && OPEVO_ACC == 1 &&
+                      OPEVO_TF32X3 > 0 && OPEVO_OUT_F32 && !B_RES),
+              "3xTF32: single-CTA GEMM tiles, fp32 output");
 
 // Shared-memory matrix descriptor minus the start address.
 constexpr u64 DESC_HI = ((u64)1 << 16)                          // LBO (unused for swizzled K-major)
@@ -418,6 +435,21 @@ __device__ __forceinline__ void umma_bf16(u32 tmem_d, u64 adesc, u64 bdesc, u32 
     asm volatile("{ .reg .pred e, p; elect.sync _|e, 0xffffffff; setp.ne.b32 p, %4, 0; "
                  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }"
                  :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
+}
+
+// One 3xTF32 K step (K8 of fp32 = one 32-byte step): D += A.B_lo + A_lo.B +
+// A.B, the small terms first.  kind::tf32 reads the top 19 bits of each fp32
+// container (truncation: hi = x & ~0x1fff); the epilogue warps wrote the
+// exact remainders lo = x - hi at +LO_OFF, so the
+// three products are hi*lo, lo*hi and hi*hi and only lo*lo (~2^-22
+// relative) and the tf32 truncation of the lo parts are lost.
+__device__ __forceinline__ void umma_x3(u32 d, u64 a, u64 b, u64 alo, u64 blo, u32 accumulate) {
+    asm volatile("{ .reg .pred e, p, t; elect.sync _|e, 0xffffffff; setp.ne.b32 p, %5, 0; "
+                 "setp.eq.b32 t, 0, 0; "
+                 "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %4, %6, p; "
+                 "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %3, %2, %6, t; "
+                 "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %6, t; }"
+                 :: "r"(d), "l"(a), "l"(b), "l"(alo), "l"(blo), "r"(accumulate), "r"(IDESC));
 }
 
 // All K16 steps of one swizzle atom (NK = ATOM_K / 16 MMAs into one
@@ -692,7 +724,8 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
     u64* red_bar = tempty_bar + NBUF;         // DSMEM split-K: peers' partial rows landed
     u64* bres_bar = red_bar + 1;              // weight panel landed (B_RES)
     u64* part_bar = bres_bar + 1;             // TMA split-K: peers' partials landed, per epilogue warp
-    u32* tmem_slot = reinterpret_cast<u32*>(part_bar + 4);
+    u64* lo_bar = part_bar + 4;               // X3: stage split into hi/lo (epilogue warps -> MMA)
+    u32* tmem_slot = reinterpret_cast<u32*>(lo_bar + (X3 ? STAGES : 0));
     u32* last_flag = tmem_slot + 1;
 
     const int warp = threadIdx.x >> 5;
@@ -812,6 +845,8 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
         if (B_RES) mbar_init(smem_u32(bres_bar), 1);
         if (SPLITT > 1)
             for (int q = 0; q < 4; ++q) mbar_init(smem_u32(part_bar + q), 1);
+        if (X3)
+            for (int q = 0; q < STAGES; ++q) mbar_init(smem_u32(lo_bar + q), 4);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         if (SPLITCL > 1)
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
@@ -995,6 +1030,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                 const u32 acc_base = tmem_base + (u32)(buf * TMEM_USED);
                 for (int kb = 0; kb < num_kb; ++kb) {
                     mbar_wait(smem_u32(full_bar + s), ph);
+                    if (X3) mbar_wait(smem_u32(lo_bar + s), ph);
                     tc_fence_after();
                     if (first && lane == 0) { TRACE(4); first = false; }
                     if (OPEVO_ABLATE == 4) {
@@ -1007,7 +1043,23 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                     const u64 da = desc_a0 + sdesc;
                     const u64 db = B_RES ? desc_bres + (u64)(((tu.k0 / BK + kb) * KATOMS * (BN * SWZ)) >> 4)
                                          : desc_b0 + sdesc;
-                    if (MATOMS == 1 && ACC == 1) {
+                    if (X3) {
+#pragma unroll
+                        for (int ka = 0; ka < KATOMS; ++ka) {
+#pragma unroll
+                            for (int k16 = 0; k16 < ATOM_K / 16; ++k16) {
+                                const u32 koff = k16 * 32;
+                                const u64 bdesc = db + (u64)((ka * (BN_LOAD * SWZ) + koff) >> 4);
+#pragma unroll
+                                for (int ma = 0; ma < MATOMS; ++ma) {
+                                    const u64 adesc = da + (u64)((ka * (BM_CTA * SWZ) + ma * (128 * SWZ) + koff) >> 4);
+                                    const u32 accumulate = (kb != 0 || ka != 0 || k16 != 0) ? 1u : 0u;
+                                    umma_x3(acc_base + (u32)(ma * BN), adesc, bdesc, adesc + (u64)(LO_OFF >> 4),
+                                            bdesc + (u64)(LO_OFF >> 4), accumulate);
+                                }
+                            }
+                        }
+                    } else if (MATOMS == 1 && ACC == 1) {
                         // one accumulator per batch of the unit: each swizzle
                         // atom's K16 steps in one asm block
 #pragma unroll
@@ -1073,9 +1125,46 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
         bool first = true;
         const u32 epi_stage = smem_u32(smem + EPI_OFF) + (u32)(quarter * 2 * EPI_BUF);
         int nchunk = 0;                            // TMA-store chunks issued by this warp
+#if OPEVO_TF32X3
+        int xs = 0;                                // ring slot / phase of the hi/lo split
+        u32 xph = 0;
+#endif
         for (UnitWalk w = digits(u_first); w.u < sched.units; walk_next(w)) {
             const Unit t = unit_of(w);
             const int col0 = t.col_tile * BN;
+#if OPEVO_TF32X3
+            // Split every landed stage of this unit: lo = x - hi (exact in
+            // fp32) at +LO_OFF, where hi = x with the low 13 mantissa bits
+            // cleared -- exactly what kind::tf32 reads from the landed x, so
+            // x itself serves as hi (writing hi back in place gave identical
+            // results and cost 14 %, profiles/round1_c/tf32x3_probe.txt).
+            // Same byte offset, same swizzled position, so one descriptor
+            // offset addresses either.
+            for (int kb = 0; kb < t.num_kb; ++kb) {
+                mbar_wait(smem_u32(full_bar + xs), xph);
+                const u32 base = smem_u32(smem + xs * STAGE_BYTES);
+#pragma unroll 4
+                for (int v = epi_tid; v < LOAD_BYTES / 16; v += 128) {
+                    const u32 at = base + (u32)v * 16u;
+                    u32 x[4], h[4], l[4];
+                    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]) : "r"(at) : "memory");
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        h[q] = x[q] & 0xffffe000u;
+                        l[q] = __float_as_uint(__uint_as_float(x[q]) - __uint_as_float(h[q]));
+                    }
+#ifdef OPEVO_X3_HI_INPLACE    // debug: write hi explicitly (the tensor core's own truncation
+                    st_shared_v4(at, h[0], h[1], h[2], h[3]);   // gives the same results)
+#endif
+                    st_shared_v4(at + (u32)LO_OFF, l[0], l[1], l[2], l[3]);
+                }
+                fence_async_smem();                // generic smem writes -> the MMA (async proxy)
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(lo_bar + xs));
+                if (++xs == STAGES) { xs = 0; xph ^= 1; }
+            }
+#endif
 #if OPEVO_CONV
             const int w_tiles = geom.wo / TILE_W, h_tiles = geom.ho / TILE_H;
             const int w0 = (t.row_tile % w_tiles) * TILE_W;

@@ -198,6 +198,23 @@ Knobs read_knobs(const int32_t* k, int n) {
     return Knobs{v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8], v[9], v[10], v[11], v[12]};
 }
 
+// Family 3 (fp32 GEMM as 3xTF32 on tcgen05) takes BK in fp32 elements at the
+// ABI; inside the library -- cache key, NVRTC macros, shared-memory sizing,
+// tensor maps -- each fp32 operand is viewed as bf16 pairs, so BK and K are
+// counted in bf16 units (twice the fp32 count).
+constexpr int FAMILY_X3 = 3;
+Knobs lib_knobs(int family, const int32_t* k, int n) {
+    Knobs kn = read_knobs(k, n);
+    if (family == FAMILY_X3) kn.bk *= 2;
+    return kn;
+}
+
+// Kernel family of an operator: 0 bf16 GEMM, 1 conv, 2 fp32 SIMT, 3 fp32 3xTF32.
+int family_of(const opevo_op_desc& d) {
+    if (d.kind == OPEVO_CONV2D) return 1;
+    return d.dtype == OPEVO_F32 ? 2 : d.dtype == OPEVO_F32_TF32X3 ? FAMILY_X3 : 0;
+}
+
 // TMEM columns the kernel allocates (two accumulator buffers when they fit).
 int tmem_alloc_cols(const Knobs& k) {
     const int used = (k.cg == 1 && k.bm == 256 ? 2 : 1) * k.bn * k.acc * std::max(1, k.bpu);
@@ -244,7 +261,8 @@ int tma_split(const Knobs& k, int family, int batched) {
 bool dsmem_split(const Knobs& k, int family, int batched = 0) {
     return family != 2 && (k.split == 2 || k.split == 4 || k.split == 8) && k.cg == 1 &&
            k.cluster == 1 && k.bm == 128 && !tma_split(k, family, batched) &&
-           (dsmem_red_bytes(k) + 1023) / 1024 * 1024 + epi_stage_bytes(k, 0) + 1024 + 256 <= 232448;
+           (dsmem_red_bytes(k) + 1023) / 1024 * 1024 + epi_stage_bytes(k, family == FAMILY_X3) + 1024 + 256 <=
+               232448;
 }
 
 // TMA-store epilogue chunk width (mirrors STORE_COLS in gemm_sm100.cuh).
@@ -264,6 +282,7 @@ size_t smem_bytes(const Knobs& k, int family = 0, int out_f32 = 0, int batched =
     const int a_rows = k.cg == 2 ? 128 : k.bm;
     const int b_rows = b_resident(k, family) ? 0 : k.bn / (k.cg == 2 ? 2 : 1);
     size_t pipe = (size_t)k.stages * (size_t)(a_rows + b_rows) * (size_t)k.bk * 2 * (size_t)std::max(1, k.bpu);
+    if (family == FAMILY_X3) pipe *= 2;       // hi (as landed) + lo parts per stage
     if (dsmem_split(k, family, batched)) pipe = std::max(pipe, dsmem_red_bytes(k));
     if (const int ts = tma_split(k, family, batched))
         pipe = std::max(pipe, (size_t)std::max(ts - 1, 1) * 128 * k.bn * 4);   // SPLITT_BYTES
@@ -390,6 +409,10 @@ bool knobs_compilable(int family, const Knobs& k, char* err, size_t len) {
         put_err(err, len, "bpu=%d needs a single-CTA 128-row GEMM tile, no multicast or DSMEM split", k.bpu);
         return false;
     }
+    if (family == FAMILY_X3 && (k.cg != 1 || k.cluster != 1 || k.bpu > 1 || k.acc != 1 || k.b_res)) {
+        put_err(err, len, "3xTF32: single-CTA tiles without multicast, bpu or acc");
+        return false;
+    }
     if ((k.cg == 1 && k.bm == 256 ? 2 : 1) * k.bn * k.acc * std::max(1, k.bpu) > 512) {
         put_err(err, len, "accumulators %dx%d x%d exceed 512 TMEM columns", k.bm, k.bn, k.acc);
         return false;
@@ -487,7 +510,8 @@ int nvrtc_build(int family, const Knobs& k, int batched, int out_f32, std::vecto
         "-DOPEVO_SPLIT_CLUSTER=" + std::to_string(dsmem_split(k, family, batched) ? k.split : 0),
         "-DOPEVO_SPLIT_TMA=" + std::to_string(tma_split(k, family, batched)),
         "-DOPEVO_B_RES=" + std::to_string(b_resident(k, family) ? 1 : 0),
-        "-DOPEVO_BPU=" + std::to_string(family == 0 ? std::max(1, k.bpu) : 1)};
+        "-DOPEVO_BPU=" + std::to_string(family == 0 ? std::max(1, k.bpu) : 1),
+        "-DOPEVO_TF32X3=" + std::to_string(family == FAMILY_X3 ? 1 : 0)};
     if (want_lineinfo()) opts.push_back("-lineinfo");
     {
         std::istringstream extra(extra_flags());
@@ -812,7 +836,7 @@ int launch_kernel(opevo_kernel* kr, char* err, size_t errlen, CUstream on = null
     }
     int rows = (int)op->rows;
     int cols = (int)op->cols;
-    int depth = (int)op->depth;
+    int depth = (int)(op->depth * (kr->family == FAMILY_X3 ? 2 : 1));   // bf16 units
     void* cptr = (void*)op->c;
     float* ws = (float*)op->ws;
     unsigned* cnt = (unsigned*)op->counters;
@@ -963,7 +987,7 @@ int opevo_abi_version(void) { return OPEVO_ABI_VERSION; }
 int opevo_kernel_key(int family, const int32_t* knobs, int nknobs, int batched, int out_f32, char* key,
                      size_t keylen) {
     if (!knobs || !key) return OPEVO_ERR_ARG;
-    std::string s = make_key(family, read_knobs(knobs, nknobs), batched, out_f32);
+    std::string s = make_key(family, lib_knobs(family, knobs, nknobs), batched, out_f32);
     snprintf(key, keylen, "%s", s.c_str());
     return OPEVO_OK;
 }
@@ -971,7 +995,7 @@ int opevo_kernel_key(int family, const int32_t* knobs, int nknobs, int batched, 
 int opevo_compile(int family, const int32_t* knobs, int nknobs, int batched, int out_f32,
                   const char* cache_dir, double* compile_ms, char* err, size_t errlen) {
     if (!knobs) return OPEVO_ERR_ARG;
-    Knobs k = read_knobs(knobs, nknobs);
+    Knobs k = lib_knobs(family, knobs, nknobs);
     if (!knobs_compilable(family, k, err, errlen)) return OPEVO_INVALID_CONFIG;
     std::vector<char> cubin;
     int hit = 0;
@@ -1106,7 +1130,12 @@ int opevo_op_prepare(opevo_ctx* ctx, const opevo_op_desc* desc, opevo_op** out, 
     opevo_op* op = new opevo_op();
     op->ctx = ctx;
     op->d = *desc;
-    op->in_f32 = op->out_f32 = desc->dtype == OPEVO_F32 ? 1 : 0;
+    if (desc->dtype == OPEVO_F32_TF32X3 && desc->kind == OPEVO_CONV2D) {
+        put_err(err, errlen, "3xTF32 is served for MatMul / BatchMatMul");
+        delete op;
+        return OPEVO_ERR_ARG;
+    }
+    op->in_f32 = op->out_f32 = (desc->dtype == OPEVO_F32 || desc->dtype == OPEVO_F32_TF32X3) ? 1 : 0;
     const size_t esz = op->in_f32 ? 4 : 2;
     int st = OPEVO_OK;
     auto alloc = [&](CUdeviceptr* p, size_t bytes, const char* what) -> bool {
@@ -1254,9 +1283,11 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
     }
     g_cu.CtxSetCurrent(ctx->cu);
     const double t0 = now_ms();
-    Knobs k = read_knobs(knobs, nknobs);
-    // fp32 operands are served by the SIMT family (the tcgen05 family is bf16)
-    const int family = op->d.kind == OPEVO_CONV2D ? 1 : (op->in_f32 ? 2 : 0);
+    // fp32 operands: the SIMT family (OPEVO_F32) or 3xTF32 on tcgen05 (OPEVO_F32_TF32X3)
+    const int family = family_of(op->d);
+    Knobs k = lib_knobs(family, knobs, nknobs);
+    // K as the kernel sees it (bf16 units: doubled for the 3xTF32 family)
+    const int64_t depth = op->depth * (family == FAMILY_X3 ? 2 : 1);
     const int batched = op->d.kind == OPEVO_BATCHMATMUL ? 1 : 0;
     if (!knobs_compilable(family, k, err, errlen)) return OPEVO_INVALID_CONFIG;
     if (family == 2) return simt_kernel_get(ctx, op, k, out, info, t0, err, errlen);
@@ -1271,8 +1302,8 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
                 (long long)op->cols);
         return OPEVO_INVALID_CONFIG;
     }
-    if (k.split < 1 || op->depth % ((int64_t)k.split * k.bk)) {
-        put_err(err, errlen, "split %d x BK %d does not divide K=%lld", k.split, k.bk, (long long)op->depth);
+    if (k.split < 1 || depth % ((int64_t)k.split * k.bk)) {
+        put_err(err, errlen, "split %d x BK %d does not divide K=%lld", k.split, k.bk, (long long)depth);
         return OPEVO_INVALID_CONFIG;
     }
     const int64_t col_tiles = op->cols / k.bn, row_tiles = op->rows / k.bm;
@@ -1284,7 +1315,7 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
     kr->op = op;
     kr->k = k;
     kr->family = family;
-    kr->k_per_split = (int)(op->depth / k.split);
+    kr->k_per_split = (int)(depth / k.split);
     kr->smem = smem_bytes(k, family, op->out_f32, batched);
     kr->flops = 2.0 * (double)op->batch * (double)op->rows * (double)op->cols * (double)op->depth;
     int st = OPEVO_OK;
@@ -1308,7 +1339,7 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
         st = encode_map(&kr->tma_a, op->a, 4, dims, strides, box, swz, err, errlen);
         if (b_resident(k, family)) {
             // resident weight panel: atom view {64, Cout, K/64}, one box {64, BN, K/64}
-            const uint64_t d = (uint64_t)op->depth;
+            const uint64_t d = (uint64_t)depth;
             const size_t panel = (size_t)k.bn * d * 2;
             if (!st && (op->cols != k.bn || d / 64 > 256 || kr->smem + 768 + panel > (size_t)ctx->smem_optin)) {
                 put_err(err, errlen, "resident weights need BN = Cout (%lld) and a %zu B panel that fits",
@@ -1321,8 +1352,8 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
             if (!st) st = encode_map(&kr->tma_b, op->b, 3, bd, bs, bb, 128, err, errlen);
             kr->smem += 768 + panel;    // 1 KB barrier block before the panel (BRES_OFF)
         } else {
-            uint64_t bd[2] = {(uint64_t)op->depth, (uint64_t)op->cols};
-            uint64_t bs[1] = {(uint64_t)op->depth * 2};
+            uint64_t bd[2] = {(uint64_t)depth, (uint64_t)op->cols};
+            uint64_t bs[1] = {(uint64_t)depth * 2};
             uint32_t bb[2] = {atom_k, (uint32_t)k.bn};
             if (!st) st = encode_map(&kr->tma_b, op->b, 2, bd, bs, bb, swz, err, errlen);
         }
@@ -1360,7 +1391,7 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
             // "atom" views {64, rows, K/64 (, batch)}: one box per operand per
             // stage (mirrors FUSED_K in gemm_sm100.cuh)
             const int rank = batched ? 4 : 3;
-            const uint64_t d = (uint64_t)op->depth;
+            const uint64_t d = (uint64_t)depth;
             uint64_t ad[4] = {64, (uint64_t)op->rows, d / 64, (uint64_t)op->batch};
             uint64_t as[3] = {d * 2, 128, d * op->rows * 2};
             uint32_t ab[4] = {64, a_rows, (uint32_t)(k.bk / 64), bpu};
@@ -1371,11 +1402,11 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
             if (!st) st = encode_map(&kr->tma_b, op->b, rank, bd, bs, bb, 128, err, errlen);
         } else {
             const int rank = batched ? 3 : 2;
-            uint64_t ad[3] = {(uint64_t)op->depth, (uint64_t)op->rows, (uint64_t)op->batch};
-            uint64_t as[2] = {(uint64_t)op->depth * 2, (uint64_t)op->depth * op->rows * 2};
+            uint64_t ad[3] = {(uint64_t)depth, (uint64_t)op->rows, (uint64_t)op->batch};
+            uint64_t as[2] = {(uint64_t)depth * 2, (uint64_t)depth * op->rows * 2};
             uint32_t ab[3] = {atom_k, a_rows, bpu};
-            uint64_t bd[3] = {(uint64_t)op->depth, (uint64_t)op->cols, (uint64_t)op->batch};
-            uint64_t bs[2] = {(uint64_t)op->depth * 2, (uint64_t)op->depth * op->cols * 2};
+            uint64_t bd[3] = {(uint64_t)depth, (uint64_t)op->cols, (uint64_t)op->batch};
+            uint64_t bs[2] = {(uint64_t)depth * 2, (uint64_t)depth * op->cols * 2};
             uint32_t bb[3] = {atom_k, b_rows, bpu};
             st = encode_map(&kr->tma_a, op->a, rank, ad, as, ab, swz, err, errlen);
             if (!st) st = encode_map(&kr->tma_b, op->b, rank, bd, bs, bb, swz, err, errlen);
@@ -1430,7 +1461,7 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
         if (k.grid_mode == 2 && k.split == 1 && tiles > capacity && tiles % capacity) {
             const int rem = tiles % capacity;
             int ts = 1;
-            while (ts < 8 && 2 * ts * rem <= capacity && op->depth % ((int64_t)2 * ts * k.bk) == 0) ts *= 2;
+            while (ts < 8 && 2 * ts * rem <= capacity && depth % ((int64_t)2 * ts * k.bk) == 0) ts *= 2;
             if (ts > 1) {
                 sc.head_tiles = tiles - rem;
                 sc.tail_split = ts;
@@ -2094,8 +2125,8 @@ int opevo_op_preload(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
         return OPEVO_ERR_STICKY;
     }
     g_cu.CtxSetCurrent(ctx->cu);
-    Knobs k = read_knobs(knobs, nknobs);
-    const int family = op->d.kind == OPEVO_CONV2D ? 1 : (op->in_f32 ? 2 : 0);
+    const int family = family_of(op->d);
+    Knobs k = lib_knobs(family, knobs, nknobs);
     const int batched = op->d.kind == OPEVO_BATCHMATMUL ? 1 : 0;
     if (!knobs_compilable(family, k, err, errlen)) return OPEVO_INVALID_CONFIG;
     CUfunction fn = nullptr;

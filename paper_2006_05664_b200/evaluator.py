@@ -31,6 +31,9 @@ from .spaces import SearchSpace
 
 BF16_TOL = 1e-2
 F32_TOL = 1e-4
+# ABI dtype -> the name the mapping / space use
+DTYPE_NAMES = {capi.BF16: "bf16", capi.F32: "f32", capi.F32_TF32X3: "tf32x3"}
+DTYPES = {v: k for k, v in DTYPE_NAMES.items()}
 
 
 class WorkerFault(FatalEvaluationError):
@@ -97,10 +100,10 @@ class GpuEvaluator:
                  settings: EvalSettings | None = None):
         self.spec = spec
         self.settings = settings or EvalSettings()
-        self.dtype = "f32" if self.settings.dtype == capi.F32 else "bf16"
+        self.dtype = DTYPE_NAMES[self.settings.dtype]
         self.space = space if space is not None else gpu_operator_space(spec, self.dtype)
         self.device_index = device
-        self.tol = F32_TOL if self.settings.dtype == capi.F32 else BF16_TOL
+        self.tol = F32_TOL if self.settings.dtype in capi.FP32_OUT else BF16_TOL
         try:
             self.dev = capi.Device(device, self.settings.cache_dir)
             self.op = self.dev.prepare(dtype=self.settings.dtype, seed=self.settings.seed,
@@ -113,7 +116,7 @@ class GpuEvaluator:
         nthreads = self.settings.compile_threads or min(8, os.cpu_count() or 1)
         self._pool = ThreadPoolExecutor(max_workers=nthreads)
         self._staged: set = set()          # kernels already loaded in this context
-        if self.settings.preload_family and self.dtype == "bf16":
+        if self.settings.preload_family and self.dtype in ("bf16", "tf32x3"):
             self.preload_family()
 
     def close(self) -> None:
@@ -163,8 +166,8 @@ class GpuEvaluator:
 
         todo = []
         have = set(os.listdir(self.settings.cache_dir)) if os.path.isdir(self.settings.cache_dir) else set()
-        for fam, batched, kn in family_instances(self.spec):
-            if capi.kernel_key(fam, kn, batched, False) + ".cubin" in have:
+        for fam, batched, kn in family_instances(self.spec, self.dtype):
+            if capi.kernel_key(fam, kn, batched, self.dtype == "tf32x3") + ".cubin" in have:
                 todo.append(kn)
 
         def load(kn):

@@ -63,6 +63,7 @@ UNROLL_TO_STAGES = {0: 2, 16: 3, 64: 4, 512: 6, 1500: 8}
 FAMILY_GEMM = 0
 FAMILY_CONV = 1
 FAMILY_SIMT = 2            # fp32 MatMul: the paper's TVM dense schedule on CUDA cores
+FAMILY_TF32X3 = 3          # fp32 MatMul / BMM on tcgen05: three kind::tf32 MMAs per K step
 
 
 @dataclass(frozen=True)
@@ -108,7 +109,8 @@ class Knobs:
         red = self.bm * ld * 4 + (s - 1) * (self.bm // max(s, 1)) * ld * 4
         ok = (s in (2, 4, 8) and self.cta_group == 1 and self.cluster == 1 and self.bm == 128
               and not self.tma_split()
-              and _align1k(red) + epi_bytes(self.bn) + SMEM_EXTRA <= SMEM_LIMIT)
+              and _align1k(red) + epi_bytes(self.bn, self.family == FAMILY_TF32X3) + SMEM_EXTRA
+              <= SMEM_LIMIT)
         return s if ok else 0
 
     def compile_key(self) -> tuple[int, ...]:
@@ -121,13 +123,17 @@ class Knobs:
         """Mirrors ``smem_bytes`` in csrc/opevo.cpp (bf16 output)."""
         if self.b_res:
             return _align1k(self.bm * self.bk * 2 * self.stages) + epi_bytes(self.bn) + 2048 + self.panel_bytes
-        pipe = stage_bytes(self.bm, self.bn, self.bk, self.cta_group) * self.stages * self.bpu
+        x3 = self.family == FAMILY_TF32X3
+        if x3:   # fp32 operands (bf16 pairs) staged twice: hi as landed + lo
+            pipe = 2 * stage_bytes(self.bm, self.bn, 2 * self.bk) * self.stages
+        else:
+            pipe = stage_bytes(self.bm, self.bn, self.bk, self.cta_group) * self.stages * self.bpu
         if self.dsmem_split():
             ld = self.bn + 4
             pipe = max(pipe, self.bm * ld * 4 + (self.split - 1) * (self.bm // self.split) * ld * 4)
         if self.tma_split():
             pipe = max(pipe, max(self.split - 1, 1) * 128 * self.bn * 4)
-        return _align1k(pipe) + epi_bytes(self.bn) + SMEM_EXTRA
+        return _align1k(pipe) + epi_bytes(self.bn, x3) + SMEM_EXTRA
 
 
 @dataclass(frozen=True)
@@ -148,9 +154,12 @@ def _align1k(n: int) -> int:
     return (n + 1023) // 1024 * 1024
 
 
-def epi_bytes(bn: int) -> int:
-    """TMA-store staging of the epilogue (bf16 output): 4 warps x 2 buffers
-    x 32 rows x STORE_COLS (64, 32 or 16: the widest dividing BN)."""
+def epi_bytes(bn: int, out_f32: bool = False) -> int:
+    """TMA-store staging of the epilogue: 4 warps x 2 buffers x 32 rows x
+    STORE_COLS (bf16 output: 64, 32 or 16, the widest dividing BN; fp32
+    output: 32 or 16)."""
+    if out_f32:
+        return 4 * 2 * 32 * (32 if bn % 32 == 0 else 16) * 4
     return 4 * 2 * 32 * (64 if bn % 64 == 0 else 32 if bn % 32 == 0 else 16) * 2
 
 
@@ -166,12 +175,14 @@ def _bk_ok(bk: int) -> bool:
     return bk in (16, 32) or (64 <= bk <= 256 and bk % 64 == 0)
 
 
-def _fit_stages(want: int, bm: int, bn: int, bk: int, cta_group: int = 1, bpu: int = 1) -> int:
+def _fit_stages(want: int, bm: int, bn: int, bk: int, cta_group: int = 1, bpu: int = 1,
+                x3: bool = False) -> int:
     """Largest ring depth <= want whose shared memory (pipeline, epilogue
-    staging, barriers) fits in 227 KB; 0 when not even one stage fits."""
-    sb = stage_bytes(bm, bn, bk, cta_group) * bpu
+    staging, barriers) fits in 227 KB; 0 when not even one stage fits.
+    ``x3``: 3xTF32 (fp32 BK, hi + lo areas per stage, fp32 output)."""
+    sb = 2 * stage_bytes(bm, bn, 2 * bk) if x3 else stage_bytes(bm, bn, bk, cta_group) * bpu
     s = want
-    while s > 0 and _align1k(s * sb) + epi_bytes(bn) + SMEM_EXTRA > SMEM_LIMIT:
+    while s > 0 and _align1k(s * sb) + epi_bytes(bn, x3) + SMEM_EXTRA > SMEM_LIMIT:
         s -= 1
     return s
 
@@ -192,6 +203,8 @@ def gpu_operator_space(spec: OperatorSpec, dtype: str = "bf16") -> SearchSpace:
         if not isinstance(spec, (MatMulSpec, BatchMatMulSpec)):
             raise TypeError("fp32 is served for MatMul / BatchMatMul only")
         return matmul_space(spec) if isinstance(spec, MatMulSpec) else batchmatmul_space(spec)
+    if dtype == "tf32x3" and not isinstance(spec, (MatMulSpec, BatchMatMulSpec)):
+        raise TypeError("3xTF32 is served for MatMul / BatchMatMul only")
     if isinstance(spec, MatMulSpec):
         base = matmul_space(spec)
     elif isinstance(spec, BatchMatMulSpec):
@@ -230,6 +243,27 @@ def _gemm_knobs(rows: int, cols: int, depth: int, vals: dict,
         # slice 0 of a tile waits for the others: every slice must be resident
         return None, "TMA split-K needs one wave of CTAs"
     return kn, ""
+
+
+def _x3_knobs(rows: int, cols: int, vals: dict, batch: int = 0) -> tuple[Knobs | None, str]:
+    """3xTF32 family: the bf16 GEMM mapping with BK = k[2] fp32 elements (a
+    stage of 2*BK bf16-unit bytes per row, landed once and split into hi and
+    lo areas), single-CTA tiles (BM 256 = two M=128 atoms), no multicast."""
+    n, m, k = vals["n"], vals["m"], vals["k"]
+    bm, bn = rows // n[0], cols // m[0]
+    split, bk = k[0], k[2]
+    if bm not in (128, 256):
+        return None, f"BM={bm} is not a UMMA row tile (128 or 256)"
+    if bn % 16 or not 16 <= bn <= 256:
+        return None, f"BN={bn} is not a UMMA column tile (16..256, step 16)"
+    if not _bk_ok(2 * bk):
+        return None, f"BK={bk} fp32 is not a TMA/UMMA K stage (8, 16, 32k)"
+    if (2 if bm == 256 else 1) * bn > 512:
+        return None, "accumulator exceeds TMEM"
+    stages = _fit_stages(int(vals.get("stages", 4)), bm, bn, bk, x3=True)
+    if stages < 1:
+        return None, "one stage does not fit in shared memory"
+    return Knobs(bm, bn, bk, stages, split, 1, family=FAMILY_TF32X3, batched=int(bool(batch))), ""
 
 
 def _batches_per_unit(vals: dict, batch: int, bm: int, bn: int, bk: int, split: int,
@@ -326,6 +360,14 @@ def config_to_knobs(spec: OperatorSpec, space: SearchSpace, config: tuple,
     if dtype == "f32":
         kn, why = _simt_knobs(vals)
         return Mapped(kn, why, FAMILY_SIMT, isinstance(spec, BatchMatMulSpec))
+    if dtype == "tf32x3":
+        if isinstance(spec, MatMulSpec):
+            kn, why = _x3_knobs(spec.n, spec.m, vals)
+            return Mapped(kn, why, FAMILY_TF32X3, False)
+        if isinstance(spec, BatchMatMulSpec):
+            kn, why = _x3_knobs(spec.n, spec.m, vals, batch=spec.b)
+            return Mapped(kn, why, FAMILY_TF32X3, True)
+        raise TypeError("3xTF32 is served for MatMul / BatchMatMul only")
     if isinstance(spec, MatMulSpec):
         kn, why = _gemm_knobs(spec.n, spec.m, spec.k, vals)
         return Mapped(kn, why, FAMILY_GEMM, False)

@@ -14,7 +14,15 @@ import time
 from concurrent.futures import ThreadPoolExecutor
 
 from . import capi
-from .mapping import _conv_resident_fit, STAGE_VALUES, UNROLL_TO_STAGES, Knobs, _bk_ok, _fit_stages
+from .mapping import (
+    FAMILY_TF32X3,
+    STAGE_VALUES,
+    UNROLL_TO_STAGES,
+    Knobs,
+    _bk_ok,
+    _conv_resident_fit,
+    _fit_stages,
+)
 from .operators import BatchMatMulSpec, Conv2dSpec, MatMulSpec, parse_operator
 
 
@@ -22,9 +30,37 @@ def _divisors(n: int) -> list[int]:
     return [d for d in range(1, n + 1) if n % d == 0]
 
 
-def family_instances(spec) -> set[tuple[int, bool, tuple]]:
+def _x3_instances(spec) -> set[tuple[int, bool, tuple]]:
+    """3xTF32 family (fp32 MatMul / BMM on tcgen05): mirrors mapping._x3_knobs."""
+    out = set()
+    batched = isinstance(spec, BatchMatMulSpec)
+    for bm in (128, 256):
+        if spec.n % bm:
+            continue
+        for bn in range(16, 257, 16):
+            if spec.m % bn or (2 if bm == 256 else 1) * bn > 512:
+                continue
+            for bk in _divisors(spec.k):
+                if not _bk_ok(2 * bk):
+                    continue
+                for st in STAGE_VALUES:
+                    s = _fit_stages(st, bm, bn, bk, x3=True)
+                    if s < 1:
+                        continue
+                    out.add((FAMILY_TF32X3, batched, Knobs(bm, bn, bk, s, family=FAMILY_TF32X3).as_tuple()))
+                    if bm == 128:
+                        for sp in (2, 4, 8):
+                            kn = Knobs(bm, bn, bk, s, sp, family=FAMILY_TF32X3, batched=int(batched))
+                            if kn.dsmem_split() and spec.k % (sp * bk) == 0:
+                                out.add((FAMILY_TF32X3, batched, kn.as_tuple()))
+    return out
+
+
+def family_instances(spec, dtype: str = "bf16") -> set[tuple[int, bool, tuple]]:
     """All (family, batched, knobs) reachable from the operator's space."""
     out = set()
+    if dtype == "tf32x3":
+        return _x3_instances(spec)
     if isinstance(spec, (MatMulSpec, BatchMatMulSpec)):
         batched = isinstance(spec, BatchMatMulSpec)
         for bm in (128, 256):
@@ -93,11 +129,13 @@ def prebuild_ops(ops, cache_dir: str = capi.DEFAULT_CACHE, threads: int | None =
                  verbose: bool = True) -> dict:
     todo = set()
     for op in ops:
-        todo |= family_instances(parse_operator(op))
+        # "tf32x3:<operator>" selects the fp32 3xTF32 family of that operator
+        dtype, name = ("tf32x3", op[len("tf32x3:"):]) if op.startswith("tf32x3:") else ("bf16", op)
+        todo |= family_instances(parse_operator(name), dtype)
     # dedupe by compile key (split is a launch argument)
     keyed = {}
     for fam, batched, kn in todo:
-        keyed[capi.kernel_key(fam, kn, batched, False)] = (fam, batched, kn)
+        keyed[capi.kernel_key(fam, kn, batched, fam == FAMILY_TF32X3)] = (fam, batched, kn)
     os.makedirs(cache_dir, exist_ok=True)
     have = set(os.listdir(cache_dir))
     pending = [v for k, v in keyed.items() if k + ".cubin" not in have]
@@ -107,7 +145,7 @@ def prebuild_ops(ops, cache_dir: str = capi.DEFAULT_CACHE, threads: int | None =
     def one(item):
         fam, batched, kn = item
         try:
-            return capi.compile_kernel(fam, kn, batched, False, cache_dir)
+            return capi.compile_kernel(fam, kn, batched, fam == FAMILY_TF32X3, cache_dir)
         except capi.OpevoError as err:
             failures.append((item, str(err)[:200]))
             return 0.0

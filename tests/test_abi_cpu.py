@@ -59,6 +59,24 @@ def test_conv_variants_compile_without_gpu(tmp_path):
     assert k0 != k1 and "_r_" in k1 and k2 == k3
 
 
+def test_tf32x3_family_compiles_without_gpu(tmp_path):
+    """Family 3 (fp32 on tcgen05, three kind::tf32 MMAs per K step): BK is in
+    fp32 elements at the ABI, distinct keys from the bf16 family, and the
+    bf16-only knobs (CTA pair, multicast) are rejected before NVRTC."""
+    cache = str(tmp_path)
+    assert capi.compile_kernel(3, (128, 64, 32, 4), False, True, cache) > 0
+    capi.compile_kernel(3, (128, 64, 8, 8), True, True, cache)              # batched, SW32
+    k3 = capi.kernel_key(3, (128, 64, 32, 4), False, True)
+    k0 = capi.kernel_key(0, (128, 64, 64, 4), False, True)
+    assert k3.startswith("f3_") and k3 != k0
+    assert "_k64_" in k3          # 32 fp32 = 64 bf16 units inside the library
+    for bad in [(256, 64, 32, 2, 1, 1, 1, 1, 1, 2), (128, 64, 32, 2, 1, 2),
+                (128, 64, 12, 4)]:
+        with pytest.raises(capi.OpevoError) as e:
+            capi.compile_kernel(3, bad, False, True, cache)
+        assert e.value.status == capi.INVALID_CONFIG
+
+
 def test_split_is_a_launch_argument_unless_reduced_in_dsmem():
     k1 = capi.kernel_key(0, (128, 64, 64, 4, 1, 1), False, False)
     k16 = capi.kernel_key(0, (128, 64, 64, 4, 16, 1), False, False)   # global reduction

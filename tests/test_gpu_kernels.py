@@ -213,6 +213,73 @@ def test_fp32_simt_batched(dev):
         op.close()
 
 
+X3_CASES = [
+    # fp32 on the tensor cores (3xTF32); knobs as the tcgen05 family, BK in
+    # fp32 elements: (rows, cols, depth, (bm, bn, bk, stages, split, ...))
+    (512, 1024, 1024, (128, 64, 32, 4)),
+    (512, 1024, 1024, (128, 128, 32, 3)),
+    (512, 1024, 1024, (256, 64, 32, 2)),          # two M=128 atoms per K step
+    (512, 1024, 1024, (128, 64, 16, 6)),          # 64-byte swizzle
+    (512, 1024, 1024, (128, 64, 8, 8)),           # 32-byte swizzle
+    (512, 1024, 1024, (128, 32, 64, 2)),          # two swizzle atoms per stage
+    (512, 1024, 1024, (128, 64, 32, 4, 2)),       # DSMEM split-K
+    (512, 1024, 1024, (128, 64, 32, 3, 4)),
+    (512, 1024, 1024, (128, 64, 32, 3, 16)),      # global split-K reduction
+    (2048, 2048, 512, (128, 64, 32, 4, 1, 1, 1, 1, 1, 1, 0)),   # persistent: 512 tiles
+    (1024, 1024, 1024, (128, 128, 32, 3, 1, 1, 1, 1, 1, 1, 1)),
+]
+
+
+@pytest.mark.parametrize("rows,cols,depth,knobs", X3_CASES)
+def test_fp32_tf32x3_matmul_parity(dev, rows, cols, depth, knobs):
+    """fp32 MatMul on tcgen05 (kind::tf32 x3) within the fp32 tolerance of
+    the north star, against the fp64 oracle on the same fp32 operands."""
+    import oracle
+    from paper_2006_05664_b200 import capi
+
+    op = dev.prepare(capi.MATMUL, dtype=capi.F32_TF32X3, rows=rows, cols=cols, depth=depth, seed=31)
+    try:
+        t = dev.trial(op, knobs, warmup=1, reps=3, tol=F32_TOL)
+        assert t.ok, t.message
+        assert t.rel_err < F32_TOL
+        a = oracle.operand(rows * depth, 31, bf16=False)
+        b = oracle.operand(cols * depth, 32, bf16=False)
+        ref = oracle.gemm(a, b, 1, rows, cols, depth)
+        assert _rel(op.output(), ref) < F32_TOL
+    finally:
+        op.close()
+
+
+def test_fp32_tf32x3_batched(dev):
+    import oracle
+    from paper_2006_05664_b200 import capi
+
+    b_, n, m, k = 12, 256, 64, 128
+    op = dev.prepare(capi.BATCHMATMUL, dtype=capi.F32_TF32X3, batch=b_, rows=n, cols=m, depth=k, seed=41)
+    try:
+        for knobs in [(128, 64, 32, 4), (128, 32, 16, 4, 2)]:
+            t = dev.trial(op, knobs, warmup=1, reps=3, tol=F32_TOL)
+            assert t.ok, t.message
+            ref = oracle.gemm(oracle.operand(b_ * n * k, 41, bf16=False),
+                              oracle.operand(b_ * m * k, 42, bf16=False), b_, n, m, k)
+            assert _rel(op.output(), ref) < F32_TOL
+    finally:
+        op.close()
+
+
+def test_fp32_tf32x3_rejects_bf16_only_knobs(dev):
+    """CTA pairs, multicast clusters and batches per unit are bf16-only."""
+    from paper_2006_05664_b200 import capi
+
+    op = dev.prepare(capi.MATMUL, dtype=capi.F32_TF32X3, rows=512, cols=1024, depth=1024, seed=31)
+    try:
+        for knobs in [(256, 64, 32, 2, 1, 1, 1, 1, 1, 2), (128, 64, 32, 2, 1, 2)]:
+            t = dev.trial(op, knobs, warmup=1, reps=3, tol=F32_TOL)
+            assert t.status == capi.INVALID_CONFIG, (knobs, t.message)
+    finally:
+        op.close()
+
+
 def test_invalid_knobs_score_invalid(dev):
     from paper_2006_05664_b200 import capi
 

@@ -95,6 +95,29 @@ def test_bmm_mapping_is_batched():
     assert m.valid and m.batched and m.knobs.bm == 128 and m.knobs.bn == 64
 
 
+def test_tf32x3_mapping():
+    """fp32 on the tensor cores: the tcgen05 mapping with BK = k[2] fp32
+    elements, single-CTA tiles, the stage ring sized for hi + lo areas."""
+    from paper_2006_05664_b200.mapping import FAMILY_TF32X3, SMEM_LIMIT
+
+    spec = MatMulSpec(512, 1024, 1024)
+    sp = gpu_operator_space(spec, "tf32x3")
+    assert sp.names == gpu_operator_space(spec).names
+    m = config_to_knobs(spec, sp, ((4, 2, 4, 4), (16, 1, 8, 8), (1, 32, 32), 8), "tf32x3")
+    assert m.valid and m.family == FAMILY_TF32X3
+    k = m.knobs
+    assert (k.bm, k.bn, k.bk, k.cta_group, k.cluster) == (128, 64, 32, 1, 1)
+    assert k.stages == 4 and k.smem_bytes() <= SMEM_LIMIT      # 8 wanted, 4 fit
+    # an even row vthread split stays on one CTA (two M=128 atoms)
+    m2 = config_to_knobs(spec, sp, ((2, 2, 8, 8), (16, 1, 8, 8), (1, 32, 32), 2), "tf32x3")
+    assert m2.valid and m2.knobs.bm == 256 and m2.knobs.cta_group == 1
+    # BK 4 fp32 is not a K stage
+    m3 = config_to_knobs(spec, sp, ((4, 2, 4, 4), (16, 1, 8, 8), (1, 256, 4), 2), "tf32x3")
+    assert not m3.valid
+    with pytest.raises(TypeError):
+        gpu_operator_space(parse_operator("conv2d:32,64,56,56,64,3,3,1,1"), "tf32x3")
+
+
 def test_every_valid_mapping_is_prebuilt():
     """Uniform samples that map must land in the enumerated (prebuilt) family."""
     for op in ("matmul:1024,1024,1024", "batchmatmul:960,128,64,128",
@@ -112,6 +135,21 @@ def test_every_valid_mapping_is_prebuilt():
                 k = m.knobs.as_tuple()
                 assert (m.family, m.batched, tuple(k[:4]) + tuple(k[5:])) in fam, (op, k)
         assert hits > 0
+
+
+def test_every_valid_tf32x3_mapping_is_prebuilt():
+    spec = parse_operator("matmul:512,1024,1024")
+    sp = gpu_operator_space(spec, "tf32x3")
+    fam = {(f, b, tuple(k[:4]) + tuple(k[5:])) for f, b, k in family_instances(spec, "tf32x3")}
+    rng = np.random.default_rng(0)
+    hits = 0
+    for _ in range(3000):
+        m = config_to_knobs(spec, sp, sp.sample_uniform(rng), "tf32x3")
+        if m.valid:
+            hits += 1
+            k = m.knobs.as_tuple()
+            assert (m.family, m.batched, tuple(k[:4]) + tuple(k[5:])) in fam, k
+    assert hits > 0
 
 
 def test_valid_fractions_recorded():
