@@ -188,6 +188,63 @@ def cpu_reference_arm(op: str, steps: int, warmup: int, seed: int) -> dict:
             "cpu": _cpu_model(), "host_cpus": os.cpu_count()}
 
 
+_CPU_OP_SCRIPT = r"""
+import json, os, sys, time
+import torch
+kind, dims, dtype, reps = sys.argv[1], [int(x) for x in sys.argv[2].split(",")], sys.argv[3], int(sys.argv[4])
+threads = os.cpu_count() or 1
+torch.set_num_threads(threads)
+tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+g = torch.Generator().manual_seed(1234)
+r = lambda *s: torch.rand(*s, generator=g).to(tdt)
+if kind == "matmul":
+    n, m, k = dims; a, b = r(n, k), r(m, k); fn = lambda: torch.matmul(a, b.t())
+elif kind == "batchmatmul":
+    bb, n, m, k = dims; a, b = r(bb, n, k), r(bb, m, k); fn = lambda: torch.bmm(a, b.transpose(1, 2))
+else:
+    n, c, h, w, co, kh, kw, st, pd = dims
+    x, f = r(n, c, h, w), r(co, c, kh, kw)
+    fn = lambda: torch.nn.functional.conv2d(x, f, stride=st, padding=pd)
+fn()
+best, t_end = float("inf"), time.perf_counter() + 15.0
+for _ in range(reps):
+    t0 = time.perf_counter(); fn(); best = min(best, time.perf_counter() - t0)
+    if time.perf_counter() > t_end:
+        break
+print(json.dumps({"best_s": best, "threads": threads}))
+"""
+
+
+def cpu_operator_throughput(op: str, dtype: str = "bf16", reps: int = 30) -> dict | None:
+    """SURVEY.md §8d CPU baseline (2): the operator itself on this host's
+    cores (torch.matmul / bmm / conv2d with every thread, in a separate
+    process), best of `reps`.  A reported baseline for best_tflops, not a
+    target."""
+    from paper_2006_05664_b200 import parse_operator
+
+    spec = parse_operator(op)
+    kind, dims = op.split(":")
+    # Best of three processes: on the build container torch's CPU bf16 GEMM
+    # ran either ~2.4 or ~0.065 TFLOP/s per process at random (the oneDNN
+    # AMX path is picked up or not), so one process can understate the host.
+    runs = []
+    for _ in range(3):
+        try:
+            out = subprocess.run([sys.executable, "-c", _CPU_OP_SCRIPT, kind, dims, dtype, str(reps)],
+                                 capture_output=True, text=True, timeout=300, check=True)
+            runs.append(json.loads(out.stdout.strip().splitlines()[-1]))
+        except (subprocess.SubprocessError, ValueError, IndexError):
+            continue
+    if not runs:
+        return None
+    r = min(runs, key=lambda x: x["best_s"])
+    fn = {"matmul": "matmul", "batchmatmul": "bmm", "conv2d": "conv2d"}[kind]
+    return {"value": spec.flops() / r["best_s"] / 1e12, "unit": "TFLOP/s", "cores": r["threads"],
+            "impl": f"torch.{fn} {'bf16' if dtype == 'bf16' else 'fp32'} on the host CPU",
+            "sample": f"best of {reps} calls of {op}, best of {len(runs)} processes",
+            "per_process_tflops": [spec.flops() / x["best_s"] / 1e12 for x in runs]}
+
+
 def _cpu_model() -> str:
     try:
         with open("/proc/cpuinfo") as fh:
@@ -204,6 +261,7 @@ def run_reference(args) -> None:
     if rank != 0:
         return
     cb = cpu_reference_arm(args.op, args.steps, args.warmup, args.seed)
+    cb["operator"] = cpu_operator_throughput(args.op)
     ms = 1e3 * RHO / cb["value"]
     line = {"metric": METRIC, "value": cb["value"], "unit": "trials/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -410,6 +468,9 @@ def main() -> None:
     if rank == 0:
         cpu = None if (args.no_cpu or world > 1) else cpu_reference_arm(
             args.op, args.steps, args.warmup, args.seed)
+        if cpu is not None:
+            # §8d (2): the operator itself on the host cores, beside best_tflops
+            cpu["operator"] = cpu_operator_throughput(args.op, "bf16" if args.dtype == "bf16" else "f32")
         if args.log:
             from paper_2006_05664_b200.logs import write_trial_log
 

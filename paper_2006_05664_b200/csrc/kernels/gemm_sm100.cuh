@@ -437,8 +437,10 @@ __device__ __forceinline__ void umma_bf16(u32 tmem_d, u64 adesc, u64 bdesc, u32 
                  :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
 }
 
-// One 3xTF32 K step (K8 of fp32 = one 32-byte step): D += A.B_lo + A_lo.B +
-// A.B, the small terms first.  kind::tf32 reads the top 19 bits of each fp32
+// One 3xTF32 K step (K8 of fp32 = one 32-byte step): D += A.B_lo + A.B +
+// A_lo.B.  The first two share A: the first MMA fills the tensor core's A
+// collector buffer and the second reads A from it (lastuse), saving one A
+// read from shared memory per step.  kind::tf32 reads the top 19 bits of each fp32
 // container (truncation: hi = x & ~0x1fff); the epilogue warps wrote the
 // exact remainders lo = x - hi at +LO_OFF, so the
 // three products are hi*lo, lo*hi and hi*hi and only lo*lo (~2^-22
@@ -446,9 +448,9 @@ __device__ __forceinline__ void umma_bf16(u32 tmem_d, u64 adesc, u64 bdesc, u32 
 __device__ __forceinline__ void umma_x3(u32 d, u64 a, u64 b, u64 alo, u64 blo, u32 accumulate) {
     asm volatile("{ .reg .pred e, p, t; elect.sync _|e, 0xffffffff; setp.ne.b32 p, %5, 0; "
                  "setp.eq.b32 t, 0, 0; "
-                 "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %4, %6, p; "
-                 "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %3, %2, %6, t; "
-                 "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %6, t; }"
+                 "@e tcgen05.mma.cta_group::1.kind::tf32.collector::a::fill [%0], %1, %4, %6, p; "
+                 "@e tcgen05.mma.cta_group::1.kind::tf32.collector::a::lastuse [%0], %1, %2, %6, t; "
+                 "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %3, %2, %6, t; }"
                  :: "r"(d), "l"(a), "l"(b), "l"(alo), "l"(blo), "r"(accumulate), "r"(IDESC));
 }
 
