@@ -125,6 +125,22 @@ def family_instances(spec, dtype: str = "bf16") -> set[tuple[int, bool, tuple]]:
     return out
 
 
+def prune_stale(cache_dir: str = capi.DEFAULT_CACHE) -> int:
+    """Delete cubins built from an earlier kernel source (their key ends in a
+    different source hash), so the cache that travels with the repo holds
+    only loadable instances.  Returns how many were removed."""
+    if not os.path.isdir(cache_dir):
+        return 0
+    live = {capi.kernel_key(0, (128, 128, 64, 4), False, False).rsplit("_", 1)[1],
+            capi.kernel_key(2, (1, 16, 4, 1, 16, 4, 4, 4), False, True).rsplit("_", 1)[1]}
+    n = 0
+    for f in os.listdir(cache_dir):
+        if f.endswith(".cubin") and f[:-len(".cubin")].rsplit("_", 1)[-1] not in live:
+            os.remove(os.path.join(cache_dir, f))
+            n += 1
+    return n
+
+
 def prebuild_ops(ops, cache_dir: str = capi.DEFAULT_CACHE, threads: int | None = None,
                  verbose: bool = True) -> dict:
     todo = set()
@@ -137,6 +153,7 @@ def prebuild_ops(ops, cache_dir: str = capi.DEFAULT_CACHE, threads: int | None =
     for fam, batched, kn in todo:
         keyed[capi.kernel_key(fam, kn, batched, fam == FAMILY_TF32X3)] = (fam, batched, kn)
     os.makedirs(cache_dir, exist_ok=True)
+    pruned = prune_stale(cache_dir)
     have = set(os.listdir(cache_dir))
     pending = [v for k, v in keyed.items() if k + ".cubin" not in have]
     t0 = time.perf_counter()
@@ -153,7 +170,7 @@ def prebuild_ops(ops, cache_dir: str = capi.DEFAULT_CACHE, threads: int | None =
     nthreads = threads or min(16, os.cpu_count() or 1)
     with ThreadPoolExecutor(nthreads) as pool:
         ms = list(pool.map(one, pending))
-    stats = {"instances": len(keyed), "compiled": len(pending) - len(failures),
+    stats = {"instances": len(keyed), "compiled": len(pending) - len(failures), "pruned": pruned,
              "failed": len(failures), "compile_s_total": sum(ms) / 1e3,
              "wall_s": time.perf_counter() - t0}
     if verbose:
