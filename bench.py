@@ -454,14 +454,14 @@ def main() -> None:
             # below the ridge (BMM 960x128x64x128: AI 32): HBM-bound roofline
             gbs = nbytes / (ms * 1e-3) / 1e9
             roof = {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                    "frac": gbs / pk["hbm_gbs"], "traffic": _ncu_traffic(args.op, best_knobs),
+                    "frac": gbs / pk["hbm_gbs"], "traffic": _ncu_traffic(("" if args.dtype == "bf16" else args.dtype + ":") + args.op, best_knobs),
                     "peak_source": f"{pk['source']} HBM copy bandwidth (MEASURED_PEAKS.json)",
                     "note": "fitness is L2-warm (operands fit in L2), so frac can exceed 1",
                     "kernel_ms": ms, "per_launch_bytes": nbytes, "achieved_tflops": ach}
         else:
             roof = {"bound": "fp32-fma" if args.dtype == "f32" else "tensor", "achieved": ach,
                     "peak": peak, "unit": "TFLOP/s",
-                    "frac": ach / peak, "traffic": _ncu_traffic(args.op, best_knobs),
+                    "frac": ach / peak, "traffic": _ncu_traffic(("" if args.dtype == "bf16" else args.dtype + ":") + args.op, best_knobs),
                     "peak_source": _dtype_peak_source(args.dtype, pk),
                     "kernel_ms": ms, "per_launch_flops": spec.flops(), "per_launch_bytes": nbytes}
 
@@ -561,7 +561,8 @@ def algo_bytes(spec, elem: int) -> int:
 def _ncu_traffic(op: str, knobs) -> float | None:
     """DRAM read+write bytes per launch of this exact instance on this
     operator from the committed ncu capture (profiles/ncu_summary.json,
-    keyed "operator|knobs"), else None."""
+    keyed "operator|knobs", the operator prefixed "tf32x3:" / "f32:" for the
+    fp32 families), else None."""
     path = os.path.join(REPO, "profiles", "ncu_summary.json")
     try:
         with open(path) as fh:

@@ -1851,7 +1851,7 @@ int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nk
     const int mode = flush_l2;
     g_cu.CtxSetCurrent(ctx->cu);
     static const bool prof = getenv("OPEVO_PROFILE_BATCH") != nullptr;
-    double tp[8] = {now_ms()};
+    double tp[8] = {now_ms(), 0, 0, 0, 0, 0, 0, 0};
     std::vector<opevo_kernel*> ks(count, nullptr);
     std::vector<CUgraphExec> ge(count, nullptr);
     std::vector<int> greps(count, 0);
@@ -1987,7 +1987,7 @@ int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nk
             }
         }
     }
-    tp[4] = now_ms();
+    tp[4] = tp[5] = now_ms();
     // phase B: the timed launches of every verified instance, back to back,
     // each bracketed by its own events; one synchronisation at the end
     if (!fatal && mode == 0) {
@@ -2064,6 +2064,7 @@ int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nk
             if (st2 < 0) fatal = st2;
             else if (!st2) last = i;
         }
+        tp[5] = now_ms();
         release();
         if (last >= 0 || fatal) {
             const int sst = sync_checked(ctx, "batch timing", err, errlen);
