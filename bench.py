@@ -354,9 +354,10 @@ def main() -> None:
 
     def launches_of(extras) -> int:
         # tuned-kernel launches reported by the C ABI, plus one compare
-        # kernel per verified trial
+        # kernel per trial that ran its check (not for re-timed instances
+        # verified earlier on the same operands)
         return sum(int(e.get("launches", 0)) + (1 if e.get("status") in ("ok", "verify_failed")
-                                                else 0) for e in extras)
+                                                and not e.get("verify_cached") else 0) for e in extras)
 
     budget = RHO * (args.steps + args.warmup)
     engine = OpEvo(space, EngineConfig(seed=args.seed, budget=budget, parents=RHO, offspring=RHO))

@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define OPEVO_ABI_VERSION 4   /* 4: OPEVO_F32_TF32X3; 3: 13-slot knobs, trial batch, preload */
+#define OPEVO_ABI_VERSION 4   /* 4: OPEVO_F32_TF32X3, verification cache; 3: 13-slot knobs, trial batch */
 
 enum opevo_status {
     OPEVO_OK = 0,
@@ -108,6 +108,9 @@ typedef struct opevo_trial_result {
     int32_t grid_ctas;
     int32_t smem_bytes;
     int32_t launches;         /* tuned-kernel launches this trial made    */
+    int32_t verify_cached;    /* 1: instance verified on these operands by an
+                                 earlier trial of the batch API; re-timed,
+                                 not re-checked (rel_err is that check's)  */
 } opevo_trial_result;
 
 typedef struct opevo_ctx opevo_ctx;

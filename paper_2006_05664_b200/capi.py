@@ -64,7 +64,8 @@ class OpDesc(C.Structure):
 class TrialResult(C.Structure):
     _fields_ = [("tflops", C.c_double), ("ms", C.c_double), ("rel_err", C.c_double),
                 ("compile_ms", C.c_double), ("load_ms", C.c_double), ("cache_hit", C.c_int32),
-                ("grid_ctas", C.c_int32), ("smem_bytes", C.c_int32), ("launches", C.c_int32)]
+                ("grid_ctas", C.c_int32), ("smem_bytes", C.c_int32), ("launches", C.c_int32),
+                ("verify_cached", C.c_int32)]
 
 
 class OpevoError(RuntimeError):
@@ -186,6 +187,7 @@ class Trial:
     smem_bytes: int
     message: str
     launches: int = 0
+    verify_cached: int = 0
 
     @property
     def ok(self) -> bool:
@@ -271,7 +273,7 @@ class Device:
                 m = msgs.raw[i * stride:(i + 1) * stride].split(b"\0", 1)[0].decode(errors="replace")
                 trials.append(Trial(status[i], r.tflops, r.ms, r.rel_err, r.compile_ms, r.load_ms,
                                     r.cache_hit, r.grid_ctas, r.smem_bytes,
-                                    m if status[i] != OK else "", r.launches))
+                                    m if status[i] != OK else "", r.launches, r.verify_cached))
             out.extend(trials)
             if st != OK:
                 e = OpevoError(st, err.value.decode(errors="replace"))

@@ -67,12 +67,13 @@ class TrialInfo:
     cache_hit: int = 0
     message: str = ""
     launches: int = 0
+    verify_cached: int = 0        # 1: instance verified by an earlier trial on these operands
     extra: dict = field(default_factory=dict)
 
     def as_extra(self, gpu: int) -> dict:
         d = {"status": self.status, "device_ms": self.ms, "compile_ms": self.compile_ms,
              "rel_err": self.rel_err, "gpu_id": gpu, "cache_hit": self.cache_hit,
-             "launches": self.launches}
+             "launches": self.launches, "verify_cached": self.verify_cached}
         if self.knobs is not None:
             d["knobs"] = list(self.knobs)
         if self.message:
@@ -223,7 +224,7 @@ class GpuEvaluator:
         if not math.isfinite(fit):
             fit = 0.0
         return TrialInfo(fit, "ok", knobs, ms=t.ms, rel_err=t.rel_err, compile_ms=t.compile_ms,
-                         cache_hit=t.cache_hit, launches=t.launches)
+                         cache_hit=t.cache_hit, launches=t.launches, verify_cached=t.verify_cached)
 
 
 def make_gpu_objective(spec: OperatorSpec, space: SearchSpace | None = None, device: int = 0,

@@ -351,6 +351,37 @@ def test_trial_batch_matches_single_trials(dev):
         op.close()
 
 
+def test_trial_batch_verification_cache(dev):
+    """A trial of an instance already verified on the same operands is
+    re-timed without re-running the check (verify_cached = 1, the earlier
+    rel_err, one fewer compare kernel); new operands clear the cache."""
+    import ctypes
+
+    from paper_2006_05664_b200 import capi
+
+    rows, cols, depth = 512, 1024, 1024
+    kn = [(128, 64, 128, 3, 1, 1), (128, 128, 64, 4, 2, 1)]
+    op = dev.prepare(capi.MATMUL, rows=rows, cols=cols, depth=depth, seed=1234)
+    try:
+        first = dev.trial_batch(op, kn, warmup=3, reps=5, flush_l2=2)
+        again = dev.trial_batch(op, kn, warmup=3, reps=5, flush_l2=2)
+        assert all(t.ok and not t.verify_cached for t in first)
+        assert all(t.ok and t.verify_cached for t in again)
+        assert [t.rel_err for t in again] == [t.rel_err for t in first]
+        # the re-timed launches still produce the verified output
+        assert _rel(op.output(), _oracle_gemm(1, rows, cols, depth, 1234)) < BF16_TOL
+        # the same number of tuned-kernel launches (the check launch becomes a warm-up)
+        assert [t.launches for t in again] == [t.launches for t in first]
+        a = (ctypes.c_char * op.a_bytes)()
+        b = (ctypes.c_char * op.b_bytes)()
+        op.read_inputs(ctypes.addressof(a), ctypes.addressof(b))
+        op.upload(ctypes.addressof(a), ctypes.addressof(b))
+        fresh = dev.trial_batch(op, kn, warmup=3, reps=5, flush_l2=2)
+        assert all(t.ok and not t.verify_cached for t in fresh)
+    finally:
+        op.close()
+
+
 @pytest.mark.parametrize("op_id", ["matmul:1024,1024,1024", "batchmatmul:960,128,64,128",
                                    "conv2d:32,64,56,56,64,3,3,1,1"])
 def test_mapping_smem_matches_library(dev, op_id):
