@@ -1935,6 +1935,47 @@ int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nk
     // (`op->verified`); such a trial skips the check and is re-timed only
     std::vector<char> cached(count, 0);
     std::vector<std::string> vkey(count);
+    std::vector<int> nreps(count, reps);
+    // Gated stream timing (mode 2): each trial's warm-ups and timed launches
+    // (between its own events) are queued behind a device gate of at most 64
+    // launches, so the launch queue never fills while a gate holds the
+    // stream and no host gap falls inside a measurement.
+    bool gate_open = false;
+    int in_gate = 0, gated_trials = 0;
+    uint32_t seq = 0;
+    auto open_gate = [&]() -> int {
+        seq = ++ctx->gate_seq;
+        uint64_t timeout_ns = 2000000000ull;
+        void* ga[] = {&ctx->gate_dev, &seq, &timeout_ns};
+        int gst2 = launch_simple(ctx, ctx->k_gate, 1, 32, ga, err, errlen);
+        gate_open = gst2 == OPEVO_OK;
+        in_gate = 0;
+        return gst2;
+    };
+    auto release = [&]() {
+        if (gate_open) __atomic_store_n(const_cast<uint32_t*>(ctx->gate_host), seq, __ATOMIC_SEQ_CST);
+        gate_open = false;
+    };
+    auto enqueue_timed = [&](int i) -> int {
+        const int need = std::max(0, warmup - 1 + cached[i]) + nreps[i];
+        // the first gate holds one trial, so the device starts while the
+        // host queues the rest (queueing a trial takes less host time than
+        // running it); a trial never straddles two gates
+        if (gate_open && (in_gate + need > 64 || gated_trials == 1)) release();
+        if (!gate_open) {
+            const int gst2 = open_gate();
+            if (gst2) return gst2 < 0 ? gst2 : OPEVO_ERR_CUDA;
+        }
+        int st2 = OPEVO_OK;
+        for (int w = 0; w + 1 < warmup + cached[i] && !st2; ++w) st2 = launch_kernel(ks[i], msg(i), mlen());
+        if (!st2 && g_cu.EventRecord(ev[4 * i + 2], ctx->stream) != CUDA_SUCCESS) st2 = OPEVO_ERR_CUDA;
+        for (int r = 0; r < nreps[i] && !st2; ++r) st2 = launch_kernel(ks[i], msg(i), mlen());
+        if (!st2 && g_cu.EventRecord(ev[4 * i + 3], ctx->stream) != CUDA_SUCCESS) st2 = OPEVO_ERR_CUDA;
+        in_gate += need;
+        ++gated_trials;
+        return st2;
+    };
+    std::vector<char> early(count, 0);
     for (int i = 0; i < count && !fatal; ++i) {
         if (status[i] != OPEVO_OK) continue;
         int st = OPEVO_OK;
@@ -1952,6 +1993,21 @@ int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nk
         }
         status[i] = st;
         if (st < 0) fatal = st;
+    }
+    // Instances verified by an earlier trial need no judging: in mode 2 their
+    // timed launches are queued right behind the checks, so the device keeps
+    // working through the check synchronisation and the judging below.
+    if (!fatal && mode == 2) {
+        for (int i = 0; i < count && !fatal; ++i) {
+            if (status[i] != OPEVO_OK || !cached[i]) continue;
+            const opevo_op::Verified& v = op->verified[vkey[i]];
+            if (tol >= 0 && !(v.rel_err <= tol)) continue;       // judged (and failed) below
+            nreps[i] = capped_reps(reps, v.est_ms);
+            status[i] = enqueue_timed(i);
+            early[i] = 1;
+            if (status[i] < 0) fatal = status[i];
+        }
+        release();
     }
     tp[2] = now_ms();
     if (pooled) {
@@ -1973,7 +2029,6 @@ int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nk
         fatal = OPEVO_ERR_CUDA;
     // judge; candidates slower than the whole budget keep their verified
     // launch's time (no phase B); cap the repetitions of the rest
-    std::vector<int> nreps(count, reps);
     std::vector<char> timed(count, 0);
     for (int i = 0; i < count && !fatal; ++i) {
         if (status[i] != OPEVO_OK) continue;
@@ -2054,45 +2109,18 @@ int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nk
             res[i].ms = ms / nreps[i];
         }
     } else if (!fatal && mode == 2) {
-        // every verified instance's warm-ups and timed launches (between its
-        // own events) behind device gates of at most 64 launches each, so the
-        // launch queue never fills while a gate holds the stream; one
-        // synchronisation at the end
-        bool gate_open = false;
-        int in_gate = 0;
-        uint32_t seq = 0;
-        auto open_gate = [&]() -> int {
-            seq = ++ctx->gate_seq;
-            uint64_t timeout_ns = 2000000000ull;
-            void* ga[] = {&ctx->gate_dev, &seq, &timeout_ns};
-            int gst2 = launch_simple(ctx, ctx->k_gate, 1, 32, ga, err, errlen);
-            gate_open = gst2 == OPEVO_OK;
-            in_gate = 0;
-            return gst2;
-        };
-        auto release = [&]() {
-            if (gate_open) __atomic_store_n(const_cast<uint32_t*>(ctx->gate_host), seq, __ATOMIC_SEQ_CST);
-            gate_open = false;
-        };
+        // every other verified instance's warm-ups and timed launches behind
+        // the gates (the early ones are already queued); one synchronisation
         int last = -1;
         for (int i = 0; i < count && !fatal; ++i) {
-            if (status[i] != OPEVO_OK || timed[i]) continue;
-            const int need = std::max(0, warmup - 1 + cached[i]) + nreps[i];
-            if (gate_open && in_gate + need > 64) release();
-            if (!gate_open) {
-                const int gst2 = open_gate();
-                if (gst2) { fatal = gst2 < 0 ? gst2 : OPEVO_ERR_CUDA; break; }
-            }
-            int st2 = OPEVO_OK;
-            for (int w = 0; w + 1 < warmup + cached[i] && !st2; ++w) st2 = launch_kernel(ks[i], msg(i), mlen());
-            if (!st2 && g_cu.EventRecord(ev[4 * i + 2], ctx->stream) != CUDA_SUCCESS) st2 = OPEVO_ERR_CUDA;
-            for (int r = 0; r < nreps[i] && !st2; ++r) st2 = launch_kernel(ks[i], msg(i), mlen());
-            if (!st2 && g_cu.EventRecord(ev[4 * i + 3], ctx->stream) != CUDA_SUCCESS) st2 = OPEVO_ERR_CUDA;
-            in_gate += need;
+            if (status[i] != OPEVO_OK || timed[i] || early[i]) continue;
+            const int st2 = enqueue_timed(i);
             status[i] = st2;
             if (st2 < 0) fatal = st2;
             else if (!st2) last = i;
         }
+        for (int i = 0; i < count; ++i)
+            if (early[i] && status[i] == OPEVO_OK) last = i;
         tp[5] = now_ms();
         release();
         if (last >= 0 || fatal) {

@@ -165,17 +165,24 @@ class GpuEvaluator:
         Returns how many were loaded."""
         from .prebuild import family_instances
 
+        from .mapping import Knobs
+
         todo = []
         have = set(os.listdir(self.settings.cache_dir)) if os.path.isdir(self.settings.cache_dir) else set()
         for fam, batched, kn in family_instances(self.spec, self.dtype):
             if capi.kernel_key(fam, kn, batched, self.dtype == "tf32x3") + ".cubin" in have:
-                todo.append(kn)
+                todo.append((fam, batched, kn))
 
-        def load(kn):
-            return self.dev.preload(self.op, kn)[0] == capi.OK
+        def load(item):
+            return self.dev.preload(self.op, item[2])[0] == capi.OK
 
-        n = sum(self._pool.map(load, todo))
-        return n
+        oks = list(self._pool.map(load, todo))
+        # loaded modules need no staging when a batch first maps to them
+        for (fam, batched, kn), ok in zip(todo, oks):
+            if ok:
+                self._staged.add((fam, bool(batched),
+                                  Knobs(*kn, family=fam, batched=int(batched)).compile_key()))
+        return sum(oks)
 
     def evaluate_infos(self, configs: list[tuple]) -> list[TrialInfo]:
         """Map, stage (compile/load on the host pool) and measure a batch.
