@@ -26,6 +26,8 @@ def main(argv=None) -> int:
     ap.add_argument("--operator", required=True, help="e.g. matmul:1024,1024,1024")
     ap.add_argument("--device", type=int, default=0)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--dtype", default="bf16", choices=("bf16", "f32", "tf32x3"),
+                    help="f32: the SIMT family; tf32x3: fp32 on the tensor cores")
     ap.add_argument("--dump-space", action="store_true",
                     help="print the B200 search space (reference JSON format) and exit")
     args = ap.parse_args(argv)
@@ -34,7 +36,7 @@ def main(argv=None) -> int:
     from .operators import parse_operator
 
     spec = parse_operator(args.operator)
-    space = gpu_operator_space(spec)
+    space = gpu_operator_space(spec, args.dtype)
     if args.dump_space:
         print(json.dumps(space.to_json()))
         return 0
@@ -46,10 +48,10 @@ def main(argv=None) -> int:
         return 2
 
     from .engine import FatalEvaluationError
-    from .evaluator import EvalSettings, GpuEvaluator
+    from .evaluator import DTYPES, EvalSettings, GpuEvaluator
 
     try:
-        ev = GpuEvaluator(spec, space, args.device, EvalSettings(reps=args.reps))
+        ev = GpuEvaluator(spec, space, args.device, EvalSettings(reps=args.reps, dtype=DTYPES[args.dtype]))
         info = ev.evaluate_infos([config])[0]
         ev.close()
     except FatalEvaluationError as err:
