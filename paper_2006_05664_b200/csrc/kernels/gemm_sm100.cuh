@@ -15,6 +15,15 @@
 //                 tap; padding comes from TMA out-of-bounds zero fill.  B is
 //                 the O(HW)I weight matrix [Cout][Kh*Kw*Cin].
 //   OPEVO_TILE_H / OPEVO_TILE_W  conv output tile (BM = TILE_N*TILE_H*TILE_W)
+//   OPEVO_HALO    KW > 0: conv "halo lines".  The tile is TILE_N*TILE_H lines of
+//                 TILE_W = 17 - KW output pixels, each line padded to 16 tile
+//                 rows (the last KW - 1 rows are junk and never stored).  One
+//                 4-D box {C, 16, TILE_H, TILE_N} per filter row (di) holds the
+//                 input pixels of all KW taps of that row: tap dj's A operand
+//                 is the same box with the descriptor start moved dj rows (128 B;
+//                 the SW128 pattern is keyed on the absolute shared address, so
+//                 any whole-row shift stays canonical -- tools/swizzle_probe.cu).
+//                 KW times fewer TMA boxes for (16 - TILE_W)/16 more MMA rows.
 //   OPEVO_CTA_GROUP 2: a cluster of two CTAs on neighbouring SMs computes a
 //                 256 x BN tile with tcgen05.mma.cta_group::2 (M=256); each
 //                 CTA stages 128 rows of A and BN/2 rows of B, so per-SM
@@ -85,6 +94,9 @@
 #ifndef OPEVO_CONV
 #define OPEVO_CONV 0
 #endif
+#ifndef OPEVO_HALO
+#define OPEVO_HALO 0       // conv: KW taps per halo box (0: one box per tap)
+#endif
 #ifndef OPEVO_TILE_H
 #define OPEVO_TILE_H 1
 #endif
@@ -146,9 +158,11 @@ constexpr int UMMA_M = (CG == 2) ? 256 : ((BM == 256) ? 128 : BM);
 constexpr int BPU = OPEVO_BPU;
 constexpr int A_SUB = BM_CTA * BK * 2;                    // one batch's A tile of a stage
 constexpr int A_TILE = BPU * A_SUB;
+constexpr int HKW = OPEVO_HALO;                          // conv taps served per halo box
+constexpr bool HALO = HKW > 0;
 constexpr bool B_RES = OPEVO_B_RES != 0;
 constexpr int B_SUB = BN_LOAD * BK * 2;
-constexpr int B_TILE = B_RES ? 0 : BPU * B_SUB;               // per stage (0: panel resident)
+constexpr int B_TILE = B_RES ? 0 : (HALO ? HKW : BPU) * B_SUB;   // per stage (0: panel resident)
 constexpr bool X3 = OPEVO_TF32X3 != 0;
 constexpr int LOAD_BYTES = A_TILE + B_TILE;               // what TMA lands per stage
 constexpr int LO_OFF = LOAD_BYTES;                        // X3: lo parts, same layout
@@ -175,7 +189,8 @@ constexpr int NUM_THREADS = 192;
 constexpr int SMEM_ALIGN = 1024;
 constexpr int TILE_H = OPEVO_TILE_H;
 constexpr int TILE_W = OPEVO_TILE_W;
-constexpr int TILE_N = BM / (TILE_H * TILE_W);
+constexpr int LINE_ROWS = HALO ? 16 : TILE_W;            // tile rows per output line
+constexpr int TILE_N = BM / (TILE_H * LINE_ROWS);
 
 static_assert(BM == 64 || BM == 128 || BM == 256, "BM must be 64, 128 or 256");
 static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "BN must be a multiple of 16 in [16, 256]");
@@ -187,7 +202,9 @@ static_assert((BK / 16) % ACC == 0, "each stage must feed every accumulator");
 static_assert(BM % (8 * CLUSTER) == 0, "multicast slice must be whole 8-row groups");
 static_assert(CG == 1 || (CG == 2 && BM == 256 && CLUSTER == 1 && !OPEVO_CONV && BN % 16 == 0),
               "CTA pairs: 256-row tiles, no extra multicast, GEMM only");
-static_assert(!OPEVO_CONV || (TILE_N * TILE_H * TILE_W == BM && CLUSTER == 1),
+static_assert(!HALO || (OPEVO_CONV && TILE_W + HKW - 1 == 16 && SWZ == 128 && CG == 1),
+              "halo lines: 3x3-style conv, TILE_W = 17 - KW, 128-byte swizzle");
+static_assert(!OPEVO_CONV || (TILE_N * TILE_H * LINE_ROWS == BM && CLUSTER == 1),
               "conv tile must cover BM pixels, no multicast");
 
 // UMMA instruction descriptor, kind::f16: D=f32, A=B=bf16, both K-major
@@ -897,7 +914,9 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
         if (B_RES && w.u < sched.units) {
             // the whole weight panel of this CTA's column tile, once: one box
             // {64, BN, K/64} of the atom view lands it atom-major
-            const u32 bytes = (u32)BN * (u32)depth * 2u;
+            // (halo lines: the kernel's K loop runs over filter rows only,
+            // depth = KH * Cin, while the panel holds all KH * KW taps)
+            const u32 bytes = (u32)BN * (u32)depth * (HALO ? (u32)HKW : 1u) * 2u;
             mbar_expect_tx(smem_u32(bres_bar), bytes);
             tma_load_3d(smem_u32(smem + BRES_OFF), &tma_b, smem_u32(bres_bar), 0, t_first.col_tile * BN, 0);
         }
@@ -933,8 +952,24 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                 const int kk = k0 + kb * BK;
 #if OPEVO_CONV
                 const int kblk = kk / BK;                    // global K block
-                const int tap = kblk / geom.taps_cchunks;
+                const int tap = kblk / geom.taps_cchunks;    // halo lines: the filter row
                 const int cbase = (kblk - tap * geom.taps_cchunks) * BK;
+                if (HALO) {
+                    // one box of 16-pixel lines (the KW taps of filter row `tap`
+                    // read it at row offsets 0..KW-1) plus, streamed, the KW
+                    // weight tiles of that filter row
+                    const int di = tap - geom.pad;
+#pragma unroll
+                    for (int ka = 0; ka < KATOMS; ++ka) {
+                        tma_load_4d(a_dst + ka * (BM_CTA * SWZ), &tma_a, fb, cbase + ka * ATOM_K,
+                                    w0 - geom.pad, h0 + di, n0);
+                        if (!B_RES)
+#pragma unroll
+                            for (int dj = 0; dj < HKW; ++dj)
+                                tma_load_2d(b_dst + dj * B_SUB + ka * (BN_LOAD * SWZ), &tma_b, fb,
+                                            (tap * HKW + dj) * geom.cin + cbase + ka * ATOM_K, col0);
+                    }
+                } else {
                 const int di = tap / geom.kw - geom.pad, dj = tap % geom.kw - geom.pad;
 #pragma unroll
                 for (int ka = 0; ka < KATOMS; ++ka) {
@@ -942,6 +977,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                                 w0 + dj, h0 + di, n0);
                     if (!B_RES)
                         tma_load_2d(b_dst + ka * (BN_LOAD * SWZ), &tma_b, fb, kk + ka * ATOM_K, col0);
+                }
                 }
 #else
                 if (FUSED_K) {
@@ -1045,7 +1081,32 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                     const u64 da = desc_a0 + sdesc;
                     const u64 db = B_RES ? desc_bres + (u64)(((tu.k0 / BK + kb) * KATOMS * (BN * SWZ)) >> 4)
                                          : desc_b0 + sdesc;
-                    if (X3) {
+                    if (HALO) {
+                        // filter row `tap` of this K block: tap dj reads the
+                        // halo box dj rows further on
+                        const int kblk = tu.k0 / BK + kb;
+                        const int tap = kblk / geom.taps_cchunks;
+                        const int cbase = (kblk - tap * geom.taps_cchunks) * BK;
+#pragma unroll
+                        for (int dj = 0; dj < HKW; ++dj) {
+#pragma unroll
+                            for (int ka = 0; ka < KATOMS; ++ka) {
+                                const u64 bdesc = B_RES
+                                    ? desc_bres + (u64)(((((tap * HKW + dj) * geom.cin + cbase) / 64 + ka) * (BN * SWZ)) >> 4)
+                                    : db + (u64)((dj * B_SUB + ka * (BN_LOAD * SWZ)) >> 4);
+                                // (tap, atom) steps round-robin over ACC accumulators
+                                const int step = dj * KATOMS + ka;
+                                const int acc = step % ACC;
+#pragma unroll
+                                for (int ma = 0; ma < MATOMS; ++ma) {
+                                    const u64 adesc = da + (u64)((ka * (BM_CTA * SWZ) + ma * (128 * SWZ) + dj * 128) >> 4);
+                                    const u32 accumulate = (kb != 0 || step >= ACC) ? 1u : 0u;
+                                    umma1_atom<ATOM_K / 16>(acc_base + (u32)((acc * MATOMS + ma) * BN), adesc, bdesc,
+                                                            accumulate);
+                                }
+                            }
+                        }
+                    } else if (X3) {
 #pragma unroll
                         for (int ka = 0; ka < KATOMS; ++ka) {
 #pragma unroll
@@ -1227,10 +1288,22 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                         __syncwarp();
                         if (lane == 0) {
 #if OPEVO_CONV
-                            const int n_l = lr0 / (TILE_H * TILE_W);
-                            const int h_l = (lr0 / TILE_W) % TILE_H;
-                            const int w_l = lr0 % TILE_W;
-                            tma_store_4d(&tma_c, buf, col0 + c, w0 + w_l, h0 + h_l, n0 + n_l);
+                            if (HALO) {
+                                // the chunk's 32 rows are two 16-row lines: store
+                                // their TILE_W valid pixels, skip the junk rows
+                                // (direct st.global per lane measured no faster)
+#pragma unroll
+                                for (int q = 0; q < 2; ++q) {
+                                    const int line = lr0 / 16 + q;
+                                    tma_store_4d(&tma_c, buf + (u32)(q * 16 * EPI_ROW_BYTES), col0 + c, w0,
+                                                 h0 + line % TILE_H, n0 + line / TILE_H);
+                                }
+                            } else {
+                                const int n_l = lr0 / (TILE_H * TILE_W);
+                                const int h_l = (lr0 / TILE_W) % TILE_H;
+                                const int w_l = lr0 % TILE_W;
+                                tma_store_4d(&tma_c, buf, col0 + c, w0 + w_l, h0 + h_l, n0 + n_l);
+                            }
 #elif OPEVO_BATCHED
                             tma_store_3d(&tma_c, buf, col0 + c, out_row(lr0), t.batch * BPU + jb);
 #else

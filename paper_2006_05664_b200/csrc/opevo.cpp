@@ -234,6 +234,15 @@ bool b_resident(const Knobs& k, int family) {
     return family == 1 && k.b_res && k.bk % 64 == 0 && k.split == 1;
 }
 
+// Conv "halo lines" (OPEVO_HALO in gemm_sm100.cuh): a conv tile whose width
+// does not divide BM is read as lines of TILE_W = 17 - KW output pixels padded
+// to 16 tile rows; one TMA box per filter row serves its KW taps.  Returns KW,
+// or 0 for the one-box-per-tap layout.
+int halo_kw(const Knobs& k, int family) {
+    return (family == 1 && k.tile_w >= 1 && k.tile_w < 16 && k.tile_h >= 1 && k.bm % (k.tile_h * k.tile_w) != 0)
+               ? 17 - k.tile_w : 0;
+}
+
 // K-fused operand loads (GEMM family, 128-byte swizzle, no multicast slices):
 // mirrors FUSED_K in gemm_sm100.cuh.
 bool fused_k(const Knobs& k) { return swizzle_bytes(k.bk) == 128 && k.cluster == 1; }
@@ -280,7 +289,7 @@ size_t epi_stage_bytes(const Knobs& k, int out_f32) {
 size_t smem_bytes(const Knobs& k, int family = 0, int out_f32 = 0, int batched = 0) {
     if (family == 2) return 0;
     const int a_rows = k.cg == 2 ? 128 : k.bm;
-    const int b_rows = b_resident(k, family) ? 0 : k.bn / (k.cg == 2 ? 2 : 1);
+    const int b_rows = b_resident(k, family) ? 0 : k.bn / (k.cg == 2 ? 2 : 1) * std::max(1, halo_kw(k, family));
     size_t pipe = (size_t)k.stages * (size_t)(a_rows + b_rows) * (size_t)k.bk * 2 * (size_t)std::max(1, k.bpu);
     if (family == FAMILY_X3) pipe *= 2;       // hi (as landed) + lo parts per stage
     if (dsmem_split(k, family, batched)) pipe = std::max(pipe, dsmem_red_bytes(k));
@@ -431,8 +440,14 @@ bool knobs_compilable(int family, const Knobs& k, char* err, size_t len) {
             put_err(err, len, "conv instances do not multicast");
             return false;
         }
-        if (k.tile_h < 1 || k.tile_w < 1 || k.bm % (k.tile_h * k.tile_w) || k.tile_w > 256 ||
-            k.tile_h > 256 || k.bm / (k.tile_h * k.tile_w) > 256) {
+        if (halo_kw(k, family)) {
+            if (k.bm % (16 * k.tile_h) || k.bk % 64 || k.split != 1 || k.cg != 1) {
+                put_err(err, len, "halo lines: BM=%d must hold 16-row lines of %d rows, BK a multiple of 64, "
+                        "no split", k.bm, k.tile_h);
+                return false;
+            }
+        } else if (k.tile_h < 1 || k.tile_w < 1 || k.bm % (k.tile_h * k.tile_w) || k.tile_w > 256 ||
+                   k.tile_h > 256 || k.bm / (k.tile_h * k.tile_w) > 256) {
             put_err(err, len, "conv tile %dx%d does not divide BM=%d", k.tile_h, k.tile_w, k.bm);
             return false;
         }
@@ -511,7 +526,8 @@ int nvrtc_build(int family, const Knobs& k, int batched, int out_f32, std::vecto
         "-DOPEVO_SPLIT_TMA=" + std::to_string(tma_split(k, family, batched)),
         "-DOPEVO_B_RES=" + std::to_string(b_resident(k, family) ? 1 : 0),
         "-DOPEVO_BPU=" + std::to_string(family == 0 ? std::max(1, k.bpu) : 1),
-        "-DOPEVO_TF32X3=" + std::to_string(family == FAMILY_X3 ? 1 : 0)};
+        "-DOPEVO_TF32X3=" + std::to_string(family == FAMILY_X3 ? 1 : 0),
+        "-DOPEVO_HALO=" + std::to_string(halo_kw(k, family))};
     if (want_lineinfo()) opts.push_back("-lineinfo");
     {
         std::istringstream extra(extra_flags());
@@ -704,6 +720,7 @@ struct opevo_kernel {
     unsigned grid[3] = {1, 1, 1};
     size_t smem = 0;
     int k_per_split = 0;
+    int kdepth = 0;                     // the kernel's `depth` argument (its K-loop extent)
     ConvGeomHost geom{};
     SchedHost sched{};
     std::atomic<int> launches{0};       // launches of this instance (all paths; graph
@@ -842,7 +859,7 @@ int launch_kernel(opevo_kernel* kr, char* err, size_t errlen, CUstream on = null
     }
     int rows = (int)op->rows;
     int cols = (int)op->cols;
-    int depth = (int)(op->depth * (kr->family == FAMILY_X3 ? 2 : 1));   // bf16 units
+    int depth = kr->kdepth;                        // K-loop extent (bf16 units for 3xTF32)
     void* cptr = (void*)op->c;
     float* ws = (float*)op->ws;
     unsigned* cnt = (unsigned*)op->counters;
@@ -1305,7 +1322,9 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
         return OPEVO_INVALID_CONFIG;
     }
     // operator-dependent feasibility (divisibility: no tail handling by design)
-    if (op->rows % k.bm || op->cols % k.bn) {
+    // (halo-line conv tiles hold 16 * lines rows for TILE_W * lines pixels;
+    // the conv branch checks their tiling)
+    if ((op->rows % k.bm && !halo_kw(k, family)) || op->cols % k.bn) {
         put_err(err, errlen, "tile %dx%d does not divide %lldx%lld", k.bm, k.bn, (long long)op->rows,
                 (long long)op->cols);
         return OPEVO_INVALID_CONFIG;
@@ -1324,6 +1343,7 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
     kr->k = k;
     kr->family = family;
     kr->k_per_split = (int)(depth / k.split);
+    kr->kdepth = (int)depth;
     kr->smem = smem_bytes(k, family, op->out_f32, batched);
     kr->flops = 2.0 * (double)op->batch * (double)op->rows * (double)op->cols * (double)op->depth;
     int st = OPEVO_OK;
@@ -1333,7 +1353,14 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
         const int32_t* c = op->d.conv;
         int N = c[0], C = c[1], H = c[2], W = c[3], KH = c[5], KW = c[6], S = c[7], P = c[8];
         int HO = (H + 2 * P - KH) / S + 1, WO = (W + 2 * P - KW) / S + 1;
-        const int tile_n = k.bm / (k.tile_h * k.tile_w);
+        const int hkw = halo_kw(k, family);
+        const int tile_n = k.bm / (k.tile_h * (hkw ? 16 : k.tile_w));
+        if (hkw && (hkw != KW || k.split != 1 || P >= KW)) {
+            put_err(err, errlen, "halo lines of %d pixels need a %d-wide filter (this one is %d wide)",
+                    k.tile_w, hkw, KW);
+            delete kr;
+            return OPEVO_INVALID_CONFIG;
+        }
         if (S != 1 || C % k.bk || HO % k.tile_h || WO % k.tile_w || N % tile_n) {
             put_err(err, errlen, "conv tiling (n%d h%d w%d, BK %d, stride %d) does not divide the problem",
                     tile_n, k.tile_h, k.tile_w, k.bk, S);
@@ -1343,7 +1370,8 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
         kr->geom = ConvGeomHost{C, HO, WO, KW, P, C / k.bk};
         uint64_t dims[4] = {(uint64_t)C, (uint64_t)W, (uint64_t)H, (uint64_t)N};
         uint64_t strides[3] = {(uint64_t)C * 2, (uint64_t)C * W * 2, (uint64_t)C * W * H * 2};
-        uint32_t box[4] = {atom_k, (uint32_t)k.tile_w, (uint32_t)k.tile_h, (uint32_t)tile_n};
+        // halo lines: 16 input pixels per line (TILE_W outputs + KW - 1 halo)
+        uint32_t box[4] = {atom_k, (uint32_t)(hkw ? 16 : k.tile_w), (uint32_t)k.tile_h, (uint32_t)tile_n};
         st = encode_map(&kr->tma_a, op->a, 4, dims, strides, box, swz, err, errlen);
         if (b_resident(k, family)) {
             // resident weight panel: atom view {64, Cout, K/64}, one box {64, BN, K/64}
@@ -1368,11 +1396,13 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
         if (!st) {
             // output NHWC {Cout, Wo, Ho, N}; a 32-pixel epilogue chunk of the
             // TILE_N x TILE_H x TILE_W tile is the box {EPI_COLS, bw, bh, bn}
+            // (halo lines: one box per line, {EPI_COLS, TILE_W, 1, 1}; the
+            // chunk's junk rows are never stored)
             const int ob = op->out_f32 ? 4 : 2, ec = epi_cols(k, op->out_f32);
-            const int bw = std::min(k.tile_w, 32);
-            const int bh = k.tile_w >= 32 ? 1 : std::min(k.tile_h, 32 / k.tile_w);
-            const int bn = k.tile_w * k.tile_h >= 32 ? 1 : 32 / (k.tile_w * k.tile_h);
-            if (bw * bh * bn != 32 || k.tile_w % bw || k.tile_h % bh || tile_n % bn) {
+            const int bw = hkw ? k.tile_w : std::min(k.tile_w, 32);
+            const int bh = hkw ? 1 : k.tile_w >= 32 ? 1 : std::min(k.tile_h, 32 / k.tile_w);
+            const int bn = hkw ? 1 : k.tile_w * k.tile_h >= 32 ? 1 : 32 / (k.tile_w * k.tile_h);
+            if (!hkw && (bw * bh * bn != 32 || k.tile_w % bw || k.tile_h % bh || tile_n % bn)) {
                 put_err(err, errlen, "conv tile %dx%d cannot be stored in 32-pixel boxes", k.tile_h, k.tile_w);
                 st = OPEVO_INVALID_CONFIG;
             } else {
@@ -1385,6 +1415,7 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
         }
         kr->sched = SchedHost{(N / tile_n) * (HO / k.tile_h) * (WO / k.tile_w), (int)col_tiles, 1,
                               k.split, 0, 1, 0};
+        if (hkw) kr->kdepth = KH * C;       // the K loop runs over filter rows x channel blocks
     } else {
         const uint32_t a_rows = (uint32_t)((k.cg == 2 ? 128 : k.bm) / k.cluster);
         const uint32_t b_rows = (uint32_t)(k.bn / k.cg);

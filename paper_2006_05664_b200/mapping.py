@@ -113,6 +113,15 @@ class Knobs:
               <= SMEM_LIMIT)
         return s if ok else 0
 
+    def halo_kw(self) -> int:
+        """Conv "halo lines" (mirrors ``halo_kw`` in csrc/opevo.cpp): a tile
+        width that does not divide BM marks lines of 17 - KW pixels padded to
+        16 rows, one TMA box per filter row; returns KW, else 0."""
+        if (self.family == FAMILY_CONV and 1 <= self.tile_w < 16 and self.tile_h >= 1
+                and self.bm % (self.tile_h * self.tile_w)):
+            return 17 - self.tile_w
+        return 0
+
     def compile_key(self) -> tuple[int, ...]:
         """Fields that change the generated code (split-K is a launch arg
         except for DSMEM-reduced splits)."""
@@ -123,6 +132,9 @@ class Knobs:
         """Mirrors ``smem_bytes`` in csrc/opevo.cpp (bf16 output)."""
         if self.b_res:
             return _align1k(self.bm * self.bk * 2 * self.stages) + epi_bytes(self.bn) + 2048 + self.panel_bytes
+        if self.halo_kw():
+            return (_align1k((self.bm + self.halo_kw() * self.bn) * self.bk * 2 * self.stages)
+                    + epi_bytes(self.bn) + SMEM_EXTRA)
         x3 = self.family == FAMILY_TF32X3
         if x3:   # fp32 operands (bf16 pairs) staged twice: hi as landed + lo
             pipe = 2 * stage_bytes(self.bm, self.bn, 2 * self.bk) * self.stages
@@ -300,6 +312,8 @@ def _conv_knobs(spec: Conv2dSpec, vals: dict) -> tuple[Knobs | None, str]:
         return None, f"BN={bn} is not a UMMA column tile"
     if bm == 256 and 2 * bn > 512:
         return None, "accumulator exceeds TMEM"
+    if tw + spec.kernel_w - 1 == 16 and bm % (th * tw):
+        return _conv_halo_knobs(spec, vals, bm, bn, bk, th, tw)
     if th * tw > bm or bm % (th * tw):
         return None, f"output tile {th}x{tw} does not divide {bm} pixels"
     tn = bm // (th * tw)
@@ -318,6 +332,40 @@ def _conv_knobs(spec: Conv2dSpec, vals: dict) -> tuple[Knobs | None, str]:
     if stages < 1:
         return None, "one stage does not fit in shared memory"
     return Knobs(bm, bn, bk, stages, split, 1, th, tw, family=FAMILY_CONV), ""
+
+
+def _conv_halo_knobs(spec: Conv2dSpec, vals: dict, bm: int, bn: int, bk: int, th: int,
+                     tw: int) -> tuple[Knobs | None, str]:
+    """Halo lines: output lines of TILE_W = 17 - KW pixels, each padded to 16
+    tile rows, so one TMA box {Cin block, 16, TILE_H, TILE_N} per filter row
+    serves all KW taps of that row (mirrors OPEVO_HALO in gemm_sm100.cuh)."""
+    kh, kw = vals["kh"], vals["kw"]
+    if bm % (16 * th):
+        return None, f"BM={bm} does not hold 16-row lines x {th} rows"
+    tn = bm // (16 * th)
+    if spec.batch % tn or spec.padding >= spec.kernel_w:
+        return None, f"image tile {tn} does not divide the batch {spec.batch}"
+    if bk % 64 or kh[0] * kw[0] != 1:
+        return None, "halo lines need BK a multiple of 64 and no split over taps"
+    want = UNROLL_TO_STAGES[vals["unroll_step"]]
+    if vals.get("unroll_explicit") == UNROLL_ON:
+        stages, panel = _conv_resident_fit(spec, bn, bk, 1, want, bm)
+        if stages:
+            return Knobs(bm, bn, bk, stages, 1, 1, th, tw, b_res=1, panel_bytes=panel,
+                         family=FAMILY_CONV), ""
+    stages = _fit_halo_stages(want, bm, bn, bk, spec.kernel_w)
+    if stages < 1:
+        return None, "one stage does not fit in shared memory"
+    return Knobs(bm, bn, bk, stages, 1, 1, th, tw, family=FAMILY_CONV), ""
+
+
+def _fit_halo_stages(want: int, bm: int, bn: int, bk: int, kw: int) -> int:
+    """Stages of a streaming halo-lines conv: each holds the activation box
+    and the KW weight tiles of one filter row."""
+    s = want
+    while s > 0 and _align1k(s * (bm + kw * bn) * bk * 2) + epi_bytes(bn) + SMEM_EXTRA > SMEM_LIMIT:
+        s -= 1
+    return s
 
 
 def _conv_resident_fit(spec: Conv2dSpec, bn: int, bk: int, split: int, want: int,

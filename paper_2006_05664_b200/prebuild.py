@@ -21,6 +21,7 @@ from .mapping import (
     Knobs,
     _bk_ok,
     _conv_resident_fit,
+    _fit_halo_stages,
     _fit_stages,
 )
 from .operators import BatchMatMulSpec, Conv2dSpec, MatMulSpec, parse_operator
@@ -122,6 +123,27 @@ def family_instances(spec, dtype: str = "bf16") -> set[tuple[int, bool, tuple]]:
                         if rs:
                             out.add((1, False, Knobs(bm, bn, bk, rs, 1, 1, th, tw, b_res=1,
                                                      panel_bytes=panel).as_tuple()))
+        # halo lines: 17 - KW output pixels per 16-row line (mapping._conv_halo_knobs)
+        tw = 17 - spec.kernel_w
+        if 1 <= tw < 16 and spec.out_width % tw == 0 and spec.padding < spec.kernel_w:
+            for bm in (128, 256):
+                for th in _divisors(spec.out_height):
+                    if bm % (16 * th) or spec.batch % (bm // (16 * th)) or bm % (th * tw) == 0:
+                        continue
+                    for bn in range(16, 257, 16):
+                        if spec.out_channels % bn or (bm == 256 and 2 * bn > 512):
+                            continue
+                        for bk in _divisors(spec.in_channels):
+                            if bk % 64 or not _bk_ok(bk):
+                                continue
+                            for st in set(UNROLL_TO_STAGES.values()):
+                                s = _fit_halo_stages(st, bm, bn, bk, spec.kernel_w)
+                                if s >= 1:
+                                    out.add((1, False, Knobs(bm, bn, bk, s, 1, 1, th, tw).as_tuple()))
+                                rs, panel = _conv_resident_fit(spec, bn, bk, 1, st, bm)
+                                if rs:
+                                    out.add((1, False, Knobs(bm, bn, bk, rs, 1, 1, th, tw, b_res=1,
+                                                             panel_bytes=panel).as_tuple()))
     return out
 
 

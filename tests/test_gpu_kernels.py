@@ -168,6 +168,46 @@ def test_conv2d_parity(dev, knobs):
         op.close()
 
 
+@pytest.mark.parametrize("knobs", [
+    # halo lines (TILE_W = 17 - KW = 14 pixels per 16-row line, one TMA box
+    # per filter row serving its three taps): streaming and resident weights,
+    # 128- and 256-row tiles, 2-row line blocks, BN 32
+    (128, 64, 64, 4, 1, 1, 4, 14),
+    (128, 64, 64, 4, 1, 1, 4, 14, 1, 1, 0, 1),
+    (256, 64, 64, 3, 1, 1, 4, 14),
+    (256, 64, 64, 3, 1, 1, 2, 14, 1, 1, 0, 1),
+    (128, 64, 64, 4, 1, 1, 2, 14),
+    (128, 32, 64, 4, 1, 1, 4, 14),
+])
+def test_conv2d_halo_lines_parity(dev, knobs):
+    import oracle
+    from paper_2006_05664_b200 import capi
+
+    n, c, h, w, k, kh, kw, s, p = 8, 64, 28, 28, 64, 3, 3, 1, 1
+    op = dev.prepare(capi.CONV2D, conv=[n, c, h, w, k, kh, kw, s, p], seed=5)
+    try:
+        t = dev.trial(op, knobs, warmup=1, reps=3)
+        assert t.ok, t.message
+        x = oracle.operand(n * c * h * w, 5)
+        f = oracle.operand(k * c * kh * kw, 6)
+        ref = oracle.conv(x, f, n, c, h, w, k, kh, kw, s, p)
+        assert _rel(op.output(), ref) < BF16_TOL
+    finally:
+        op.close()
+
+
+def test_conv2d_halo_lines_need_matching_filter(dev):
+    """A 14-pixel halo line is a 3-wide filter's; other filters reject it."""
+    from paper_2006_05664_b200 import capi
+
+    op = dev.prepare(capi.CONV2D, conv=[8, 64, 28, 28, 64, 5, 5, 1, 2], seed=5)
+    try:
+        t = dev.trial(op, (128, 64, 64, 4, 1, 1, 4, 14), warmup=1, reps=3)
+        assert t.status == capi.INVALID_CONFIG, t.message
+    finally:
+        op.close()
+
+
 F32_TOL = 1e-4   # north star: fp32 within 1e-4 relative
 
 
