@@ -224,7 +224,10 @@ constexpr u64 DESC_HI = ((u64)1 << 16)                          // LBO (unused f
 
 // TMEM accumulator buffers: two when they fit, so the epilogue of one tile
 // overlaps the mainloop of the next (persistent schedule).
-constexpr int NBUF = (2 * TMEM_USED <= 512) ? 2 : 1;
+// Four when they fit in half of TMEM: a persistent CTA's epilogue then
+// trails the MMA by up to three units (the commit -> epilogue -> release
+// round trip is long next to a small unit's mainloop).
+constexpr int NBUF = (4 * TMEM_USED <= 256) ? 4 : (2 * TMEM_USED <= 512) ? 2 : 1;
 constexpr int TMEM_ALLOC = (NBUF * TMEM_USED <= 32) ? 32 : (NBUF * TMEM_USED <= 64) ? 64 :
                            (NBUF * TMEM_USED <= 128) ? 128 : (NBUF * TMEM_USED <= 256) ? 256 : 512;
 constexpr int SPLITCL = OPEVO_SPLIT_CLUSTER;   // DSMEM split-K cluster size (0: off)

@@ -218,7 +218,7 @@ int family_of(const opevo_op_desc& d) {
 // TMEM columns the kernel allocates (two accumulator buffers when they fit).
 int tmem_alloc_cols(const Knobs& k) {
     const int used = (k.cg == 1 && k.bm == 256 ? 2 : 1) * k.bn * k.acc * std::max(1, k.bpu);
-    const int want = (2 * used <= 512 ? 2 : 1) * used;
+    const int want = (4 * used <= 256 ? 4 : 2 * used <= 512 ? 2 : 1) * used;   // mirrors NBUF
     int cols = 32;
     while (cols < want) cols *= 2;
     return cols;
