@@ -29,3 +29,6 @@ run x3_split_dsmem     matmul:256,512,512            128,64,32,3,2              
 run x3_256rows         matmul:256,512,512            256,64,16,3                   --tf32x3
 run x3_persistent      matmul:2048,2048,256          128,64,32,3                   --tf32x3
 run x3_bmm             batchmatmul:8,128,64,128      128,64,32,3                   --tf32x3
+run conv_halo          conv2d:4,64,28,28,64,3,3,1,1  128,64,64,4,1,1,4,14
+run conv_halo_resident conv2d:4,64,28,28,64,3,3,1,1  256,64,64,3,1,1,4,14,1,1,0,1
+run bmm_nbuf4          batchmatmul:64,128,64,128     128,64,64,4,1,1
