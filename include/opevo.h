@@ -81,7 +81,10 @@ enum opevo_knob {
     OPEVO_KNOB_SPLIT = 4,     /* split-K factor (runtime)                 */
     OPEVO_KNOB_CLUSTER = 5,   /* CTAs per cluster sharing A (multicast)   */
     OPEVO_KNOB_TILE_H = 6,    /* conv: output rows per CTA tile           */
-    OPEVO_KNOB_TILE_W = 7,    /* conv: output cols per CTA tile           */
+    OPEVO_KNOB_TILE_W = 7,    /* conv: output cols per CTA tile; 17 - KW
+                                 (a width not dividing BM) selects "halo
+                                 lines": 16-row lines, one TMA box per
+                                 filter row serving its KW taps           */
     OPEVO_KNOB_ACC = 8,       /* K-interleaved TMEM accumulators (1,2,4)  */
     OPEVO_KNOB_CTA_GROUP = 9, /* 2: CTA-pair MMA (cta_group::2), BM=256   */
     OPEVO_KNOB_GRID = 10,     /* 0: persistent when work > residency
