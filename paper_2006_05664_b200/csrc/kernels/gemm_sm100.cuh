@@ -123,9 +123,6 @@
 #ifndef OPEVO_TF32X3
 #define OPEVO_TF32X3 0     // fp32 GEMM as 3xTF32 on tcgen05 (fp32 in/out)
 #endif
-#ifndef OPEVO_EPI_GROUPS
-#define OPEVO_EPI_GROUPS 1 // 2: two groups of four epilogue warps take alternate units
-#endif
 #ifndef OPEVO_ACC
 #define OPEVO_ACC 1        // K-interleaved TMEM accumulators (1, 2, 4)
 #endif
@@ -188,8 +185,7 @@ constexpr int EPI_COLS = (BN % 32 == 0) ? 32 : 16;    // split-K / DSMEM reducti
 // TMA-store epilogue chunk: 64 bf16 columns (one 128-byte swizzle row) when
 // BN allows, so each chunk is one TMEM load, one proxy fence and one store
 constexpr int STORE_COLS = (!OPEVO_OUT_F32 && BN % 64 == 0 && OPEVO_ACC == 1) ? 64 : EPI_COLS;
-constexpr int EPI_GROUPS = OPEVO_EPI_GROUPS;
-constexpr int NUM_THREADS = 64 + 128 * EPI_GROUPS;
+constexpr int NUM_THREADS = 192;
 constexpr int SMEM_ALIGN = 1024;
 constexpr int TILE_H = OPEVO_TILE_H;
 constexpr int TILE_W = OPEVO_TILE_W;
@@ -206,9 +202,6 @@ static_assert((BK / 16) % ACC == 0, "each stage must feed every accumulator");
 static_assert(BM % (8 * CLUSTER) == 0, "multicast slice must be whole 8-row groups");
 static_assert(CG == 1 || (CG == 2 && BM == 256 && CLUSTER == 1 && !OPEVO_CONV && BN % 16 == 0),
               "CTA pairs: 256-row tiles, no extra multicast, GEMM only");
-static_assert(EPI_GROUPS == 1 || (EPI_GROUPS == 2 && CG == 1 && OPEVO_SPLIT_CLUSTER == 0 && OPEVO_SPLIT_TMA == 0 &&
-                                  !OPEVO_TF32X3),
-              "two epilogue groups: single-CTA tiles, no compiled-in split, no 3xTF32");
 static_assert(!HALO || (OPEVO_CONV && TILE_W + HKW - 1 == 16 && SWZ == 128 && CG == 1),
               "halo lines: 3x3-style conv, TILE_W = 17 - KW, 128-byte swizzle");
 static_assert(!OPEVO_CONV || (TILE_N * TILE_H * LINE_ROWS == BM && CLUSTER == 1),
@@ -266,8 +259,7 @@ constexpr int OUT_BYTES = OPEVO_OUT_F32 ? 4 : 2;
 constexpr int EPI_ROW_BYTES = STORE_COLS * OUT_BYTES;     // 32, 64 or 128
 constexpr int EPI_BUF = 32 * EPI_ROW_BYTES;               // one chunk of one warp
 constexpr int EPI_OFF = (PIPE_BYTES + 1023) / 1024 * 1024;
-constexpr int EPI_WBUF = EPI_GROUPS == 2 ? 1 : 2;          // staging buffers per epilogue warp
-constexpr int EPI_BYTES = 4 * EPI_GROUPS * EPI_WBUF * EPI_BUF;
+constexpr int EPI_BYTES = 4 * 2 * EPI_BUF;
 constexpr int BAR_OFF = EPI_OFF + EPI_BYTES;
 // resident weight panel (B_RES): [K/64 atoms][BN rows][128 B], after a
 // 1 KB barrier block; its size (BN x K) is a launch-time quantity
@@ -732,7 +724,7 @@ __device__ __forceinline__ void store_row(void* c_out, u64 off, const float* acc
 
 using namespace opevo;
 
-extern "C" __global__ void __launch_bounds__(NUM_THREADS, EPI_GROUPS == 1 ? 2 : 1)   // 2: keep <= 168 regs so two CTAs can co-reside
+extern "C" __global__ void __launch_bounds__(NUM_THREADS, 2)   // 2: keep <= 168 regs so two CTAs can co-reside
 opevo_gemm(const __grid_constant__ TmaDesc tma_a,
            const __grid_constant__ TmaDesc tma_b,
            const __grid_constant__ TmaDesc tma_c,   // C, box = 32 rows x EPI_COLS (TMA-store epilogue)
@@ -1197,20 +1189,13 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
         int buf = 0;
         u32 bph = 0;
         bool first = true;
-        const int egroup = (warp - 2) >> 2;        // EPI_GROUPS == 2: this group takes units ui % 2 == egroup
-        const u32 epi_stage = smem_u32(smem + EPI_OFF) +
-                              (u32)((EPI_GROUPS == 2 ? warp - 2 : quarter) * EPI_WBUF * EPI_BUF);
+        const u32 epi_stage = smem_u32(smem + EPI_OFF) + (u32)(quarter * 2 * EPI_BUF);
         int nchunk = 0;                            // TMA-store chunks issued by this warp
-        int ui = 0;                                // this CTA's unit counter
 #if OPEVO_TF32X3
         int xs = 0;                                // ring slot / phase of the hi/lo split
         u32 xph = 0;
 #endif
         for (UnitWalk w = digits(u_first); w.u < sched.units; walk_next(w)) {
-            if (EPI_GROUPS > 1 && (ui++ & 1) != egroup) {      // the other group's unit
-                if (++buf == NBUF) { buf = 0; bph ^= 1; }
-                continue;
-            }
             const Unit t = unit_of(w);
             const int col0 = t.col_tile * BN;
 #if OPEVO_TF32X3
@@ -1296,9 +1281,9 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                         gather_acc<STORE_COLS>(lane_addr + jm * BN + c, acc);
                         if (first && c == 0 && epi_tid == 0) TRACE(12);
                         if (jm == MATOMS * BPU - 1 && c + STORE_COLS >= BN) release();
-                        const u32 buf = epi_stage + (u32)((nchunk % EPI_WBUF) * EPI_BUF);
-                        if (nchunk >= EPI_WBUF) {      // this buffer's previous store has read it
-                            if (lane == 0) bulk_wait_read<EPI_WBUF - 1>();
+                        const u32 buf = epi_stage + (u32)((nchunk & 1) * EPI_BUF);
+                        if (nchunk >= 2) {             // this buffer's previous store has read it
+                            if (lane == 0) bulk_wait_read<1>();
                             __syncwarp();
                         }
                         stage_row(buf, lane, acc);

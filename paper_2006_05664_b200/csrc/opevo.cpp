@@ -243,18 +243,6 @@ int halo_kw(const Knobs& k, int family) {
                ? 17 - k.tile_w : 0;
 }
 
-// Two groups of four epilogue warps taking alternate units (OPEVO_EPI_GROUPS
-// in gemm_sm100.cuh) for single-CTA bf16 GEMM / conv instances without a K
-// split: a persistent CTA then drains two units' accumulators at once.
-// Experimental: on when OPEVO_EPI_GROUPS=2 is set in the environment.
-int epi_groups(const Knobs& k, int family) {
-    static const bool on = [] {
-        const char* e = getenv("OPEVO_EPI_GROUPS");
-        return e && atoi(e) == 2;
-    }();
-    return (on && (family == 0 || family == 1) && k.cg == 1 && k.split == 1 && k.grid_mode != 2) ? 2 : 1;
-}
-
 // K-fused operand loads (GEMM family, 128-byte swizzle, no multicast slices):
 // mirrors FUSED_K in gemm_sm100.cuh.
 bool fused_k(const Knobs& k) { return swizzle_bytes(k.bk) == 128 && k.cluster == 1; }
@@ -353,8 +341,7 @@ std::string make_key(int family, const Knobs& k, int batched, int out_f32) {
              k.bm, k.bn, k.bk, k.stages, batched, out_f32, k.cluster, family == 1 ? k.tile_h : 1,
              family == 1 ? k.tile_w : 1, k.acc,
              k.cg * 100 + (dsmem_split(k, family, batched) ? k.split : 0) + 10 * tma_split(k, family, batched),
-             (std::string(b_resident(k, family) ? "_r" : k.bpu > 1 ? (k.bpu == 2 ? "_u2" : "_u4") : "") +
-              (epi_groups(k, family) == 2 ? "_e2" : "")).c_str(),
+             b_resident(k, family) ? "_r" : k.bpu > 1 ? (k.bpu == 2 ? "_u2" : "_u4") : "",
              want_lineinfo() ? "L" : "",
              (unsigned long long)(h & 0xffffffffffffull));
     return buf;
@@ -540,8 +527,7 @@ int nvrtc_build(int family, const Knobs& k, int batched, int out_f32, std::vecto
         "-DOPEVO_B_RES=" + std::to_string(b_resident(k, family) ? 1 : 0),
         "-DOPEVO_BPU=" + std::to_string(family == 0 ? std::max(1, k.bpu) : 1),
         "-DOPEVO_TF32X3=" + std::to_string(family == FAMILY_X3 ? 1 : 0),
-        "-DOPEVO_HALO=" + std::to_string(halo_kw(k, family)),
-        "-DOPEVO_EPI_GROUPS=" + std::to_string(family == 2 ? 1 : epi_groups(k, family))};
+        "-DOPEVO_HALO=" + std::to_string(halo_kw(k, family))};
     if (want_lineinfo()) opts.push_back("-lineinfo");
     {
         std::istringstream extra(extra_flags());
@@ -883,7 +869,7 @@ int launch_kernel(opevo_kernel* kr, char* err, size_t errlen, CUstream on = null
     cfg.gridDimX = kr->grid[0];
     cfg.gridDimY = kr->grid[1];
     cfg.gridDimZ = kr->grid[2];
-    cfg.blockDimX = kr->block;
+    cfg.blockDimX = 192;
     cfg.blockDimY = 1;
     cfg.blockDimZ = 1;
     cfg.sharedMemBytes = (unsigned)kr->smem;
@@ -1359,7 +1345,6 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
     kr->k_per_split = (int)(depth / k.split);
     kr->kdepth = (int)depth;
     kr->smem = smem_bytes(k, family, op->out_f32, batched);
-    kr->block = 64 + 128 * (unsigned)epi_groups(k, family);
     kr->flops = 2.0 * (double)op->batch * (double)op->rows * (double)op->cols * (double)op->depth;
     int st = OPEVO_OK;
     const int swz = swizzle_bytes(k.bk);
@@ -1501,7 +1486,7 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
     // once, in which case CTAs loop over units (persistent schedule)
     {
         int per_sm = 1;
-        if (g_cu.OccupancyMaxBlocks(&per_sm, kr->fn, (int)kr->block, kr->smem) != CUDA_SUCCESS || per_sm < 1) per_sm = 1;
+        if (g_cu.OccupancyMaxBlocks(&per_sm, kr->fn, 192, kr->smem) != CUDA_SUCCESS || per_sm < 1) per_sm = 1;
         per_sm = std::min(per_sm, 512 / tmem_alloc_cols(k));
         const int capacity = std::max(1, (ctx->sm_count / clsz) * per_sm);
         SchedHost& sc = kr->sched;
