@@ -88,6 +88,32 @@ def test_conv_mapping():
     assert m.knobs.panel_bytes == 64 * 9 * 64 * 2 and m.knobs.smem_bytes() <= 232448
 
 
+def test_conv_halo_lines_mapping():
+    """wo[0] giving 14-pixel tiles (17 - KW for a 3x3 filter) selects halo
+    lines: 16-row lines, TILE_N = BM / (16 * TILE_H), stages sized for the
+    activation box plus the KW weight tiles of one filter row."""
+    from paper_2006_05664_b200.mapping import SMEM_LIMIT
+
+    spec = parse_operator("conv2d:32,64,56,56,64,3,3,1,1")
+    sp = gpu_operator_space(spec)
+    cfg = ((1, 1, 8, 8), (14, 1, 4, 1), (4, 2, 7, 1), (1, 64), (1, 3), (1, 3), "explicit_unroll_off", 64)
+    m = config_to_knobs(spec, sp, cfg)
+    assert m.valid, m.reason
+    k = m.knobs
+    assert (k.bm, k.bn, k.bk, k.tile_h, k.tile_w, k.split) == (128, 64, 64, 4, 14, 1)
+    assert k.halo_kw() == 3 and k.stages == 4
+    assert k.smem_bytes() == 4 * (128 + 3 * 64) * 64 * 2 + 32768 + 1280 <= SMEM_LIMIT
+    # a split over taps cannot use halo lines
+    bad = config_to_knobs(spec, sp, ((1, 1, 8, 8), (14, 1, 4, 1), (4, 2, 7, 1), (1, 64), (3, 1), (1, 3),
+                                     "explicit_unroll_off", 64))
+    assert not bad.valid
+    # a 5x5 filter needs 12-pixel lines, so 14-pixel tiles stay invalid for it
+    spec5 = parse_operator("conv2d:32,64,56,56,64,5,5,1,2")
+    sp5 = gpu_operator_space(spec5)
+    cfg5 = ((1, 1, 8, 8), (14, 1, 4, 1), (4, 2, 7, 1), (1, 64), (1, 5), (1, 5), "explicit_unroll_off", 64)
+    assert not config_to_knobs(spec5, sp5, cfg5).valid
+
+
 def test_bmm_mapping_is_batched():
     spec = BatchMatMulSpec(960, 128, 64, 128)
     sp = gpu_operator_space(spec)
