@@ -128,7 +128,8 @@
 #endif
 #ifndef OPEVO_ABLATE
 #define OPEVO_ABLATE 0     // debug: 1 exit at entry, 2 no mainloop, 3 no TMA, 4 no MMA,
-                           // 5 trap (fault injection: poisons the context)
+                           // 5 trap (fault injection: poisons the context), 6 no C stores,
+                           // 7 no mainloop and no C stores
 #endif
 #ifndef OPEVO_TRACE
 #define OPEVO_TRACE 0      // 1: per-CTA %globaltimer phase stamps into `ws` (debug)
@@ -338,6 +339,11 @@ __device__ __forceinline__ void mbar_wait(u32 bar, u32 parity) {
     asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
                  "selp.u32 %0, 1, 0, p; }" : "=r"(done) : "r"(bar), "r"(parity) : "memory");
     if (done) return;
+#ifdef OPEVO_NO_WATCHDOG      // debug: plain spin
+    while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+                     "selp.u32 %0, 1, 0, p; }" : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+#else
     const u64 t0 = global_ns();
     while (true) {
         asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
@@ -345,6 +351,7 @@ __device__ __forceinline__ void mbar_wait(u32 bar, u32 parity) {
         if (done) return;
         if (global_ns() - t0 > 4000000000ull) asm volatile("trap;");
     }
+#endif
 }
 
 __device__ __forceinline__ void pdl_wait() {
@@ -791,7 +798,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
         }
         const int klen = depth / t.split;
         t.k0 = t.kz * klen;
-        t.num_kb = OPEVO_ABLATE == 2 ? 0 : klen / BK;
+        t.num_kb = (OPEVO_ABLATE == 2 || OPEVO_ABLATE == 7) ? 0 : klen / BK;
         const int colg = u % sched.col_groups;
         u /= sched.col_groups;
         t.row_tile = u % sched.row_tiles;
@@ -807,7 +814,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
     // for the K-split tail of grid mode 2).
     struct UnitWalk { int u, kz, colg, row, batch; };
     const int klen0 = depth / sched.split;
-    const int num_kb0 = OPEVO_ABLATE == 2 ? 0 : klen0 / BK;
+    const int num_kb0 = (OPEVO_ABLATE == 2 || OPEVO_ABLATE == 7) ? 0 : klen0 / BK;
     auto digits = [&](int q) -> UnitWalk {
         UnitWalk w;
         w.u = q;
@@ -1289,7 +1296,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                         stage_row(buf, lane, acc);
                         fence_async_smem();
                         __syncwarp();
-                        if (lane == 0) {
+                        if (lane == 0 && OPEVO_ABLATE != 6 && OPEVO_ABLATE != 7) {
 #if OPEVO_CONV
                             if (HALO) {
                                 // the chunk's 32 rows are two 16-row lines: store

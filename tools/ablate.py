@@ -15,11 +15,12 @@ dev = capi.Device(0, "/tmp/opevo_ablate_cache"); op = dev.prepare(**_op_args(spe
 k = dev.kernel(op, kn)
 print("%.3f" % (k.time(warmup=5, reps=100) * 1e3))
 '''
-NAMES = {0: "full kernel", 1: "exit at entry", 2: "no mainloop", 3: "no TMA (MMA only)", 4: "no MMA (TMA only)"}
+NAMES = {0: "full kernel", 1: "exit at entry", 2: "no mainloop", 3: "no TMA (MMA only)", 4: "no MMA (TMA only)",
+         6: "no C stores", 7: "no mainloop, no stores"}
 for op, kn in [(a.split("@")[0], a.split("@")[1]) for a in sys.argv[1:]]:
     print(f"{op} knobs {kn}")
     for pdl in ("1", "0"):
-        for ab in range(5):
+        for ab in (0, 1, 2, 3, 4, 6, 7):
             env = dict(os.environ, OPEVO_EXTRA_FLAGS=f"-DOPEVO_ABLATE={ab}", OPEVO_NO_PDL="0" if pdl == "1" else "1")
             r = subprocess.run([sys.executable, "-c", CODE, op, kn], env=env, capture_output=True, text=True)
             val = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else ("ERR " + r.stderr.strip()[-120:])
