@@ -2013,7 +2013,10 @@ int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nk
         for (int e = 0; e < 4 && !st; ++e)
             if (g_cu.EventCreate(&ev[4 * i + e], CU_EVENT_DEFAULT) != CUDA_SUCCESS) st = OPEVO_ERR_CUDA;
         vkey[i] = graph_key(ks[i]->k, 0);
-        cached[i] = op->verified.count(vkey[i]) ? 1 : 0;
+        // OPEVO_NO_VERIFY_CACHE=1: check every trial (e.g. to project
+        // per-rank costs, where each rank keeps its own record)
+        static const bool no_vcache = getenv("OPEVO_NO_VERIFY_CACHE") != nullptr;
+        cached[i] = (!no_vcache && op->verified.count(vkey[i])) ? 1 : 0;
         // the verified launch is bracketed by events: it is also the estimate
         if (!st && !cached[i]) st = enqueue_check(ks[i], msg(i), mlen(), i, ev[4 * i], ev[4 * i + 1]);
         if (!st && mode == 0 && !pooled) {

@@ -14,12 +14,21 @@ rank has its shard and one small all-reduce has gathered the rows.  Here:
 3. the projected generation time is the max over ranks plus a fixed
    all-reduce latency (``--allreduce-us``, an NVLink small-message figure).
 
+The library's per-operand verification record (repeats of an instance are
+re-timed, not re-checked) would be shared by all simulated ranks here, while
+each real rank keeps its own; the projection therefore runs with it off
+(OPEVO_NO_VERIFY_CACHE=1): every trial is checked at every N, a slightly
+conservative figure for all N alike.
+
 Usage: python tools/scaling_projection.py [op] [generations]
 """
 import argparse
 import json
+import os
 import sys
 import time
+
+os.environ.setdefault("OPEVO_NO_VERIFY_CACHE", "1")
 
 sys.path.insert(0, ".")
 
