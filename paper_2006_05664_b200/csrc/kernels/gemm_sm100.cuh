@@ -368,10 +368,18 @@ __device__ __forceinline__ u32 sm_id() {
     return r;
 }
 
-#if OPEVO_TRACE
+#if OPEVO_TRACE == 1
 #define TRACE(slot) do { trace[(slot)] = global_ns(); } while (0)
 #else
 #define TRACE(slot) do { } while (0)
+#endif
+// OPEVO_TRACE == 2: per-unit handshake stamps of the first five units instead
+// (slot 1 + 3u: MMA warp issued unit u's tfull commit; 2 + 3u: epilogue saw
+// it; 3 + 3u: epilogue finished unit u) -- tools/trace_units.py
+#if OPEVO_TRACE == 2
+#define UTRACE(slot) do { trace[(slot)] = global_ns(); } while (0)
+#else
+#define UTRACE(slot) do { } while (0)
 #endif
 
 __device__ __forceinline__ void tma_prefetch(const TmaDesc* d) {
@@ -1057,7 +1065,8 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
         if (CG == 1 || prank == 0) {
             // ------------------------------------------------ MMA issuer
             // (whole warp iterates; umma_* elect one lane to issue)
-            int s = 0, buf = 0;
+            int s = 0, buf = 0, mu = 0;   // mu: units committed (trace)
+            (void)mu;
             u32 ph = 0, bph = 0;
             bool first = true;
             // Shared-memory descriptors of stage 0; every other operand
@@ -1181,6 +1190,8 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                 }
                 if (CG == 2) umma2_commit_mc(smem_u32(tfull_bar + buf), (u16)3);   // both halves
                 else         umma_commit(smem_u32(tfull_bar + buf));
+                if (lane == 0 && mu < 5) UTRACE(1 + 3 * mu);
+                ++mu;
                 if (++buf == NBUF) { buf = 0; bph ^= 1; }
             }
             if (lane == 0) TRACE(5);
@@ -1198,6 +1209,8 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
         bool first = true;
         const u32 epi_stage = smem_u32(smem + EPI_OFF) + (u32)(quarter * 2 * EPI_BUF);
         int nchunk = 0;                            // TMA-store chunks issued by this warp
+        int eu = 0;                                // units drained (trace)
+        (void)eu;
 #if OPEVO_TF32X3
         int xs = 0;                                // ring slot / phase of the hi/lo split
         u32 xph = 0;
@@ -1257,6 +1270,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
             const u64 c_batch = (u64)t.batch * plane;
             mbar_wait(smem_u32(tfull_bar + buf), bph);
             tc_fence_after();
+            if (epi_tid == 0 && eu < 5) UTRACE(2 + 3 * eu);
             if (first) {
                 pdl_wait();                 // C may still be written by the previous launch
                 if (epi_tid == 0) TRACE(6);
@@ -1326,6 +1340,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                     }
                 }
                 if (first && epi_tid == 0) TRACE(7);
+                if (epi_tid == 0 && eu < 5) UTRACE(3 + 3 * eu);
 #if OPEVO_SPLIT_TMA > 1 && !OPEVO_CONV
             } else if (SPLITT > 1) {
                 // ---- TMA split-K in one wave (the host guarantees every slice
@@ -1517,6 +1532,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                 epi_bar();                  // last_flag is reused by the next unit
             }
             first = false;
+            ++eu;
             if (++buf == NBUF) { buf = 0; bph ^= 1; }
         }
         // staged chunks must be read out before the CTA's smem goes away
