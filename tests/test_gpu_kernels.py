@@ -196,6 +196,26 @@ def test_conv2d_halo_lines_parity(dev, knobs):
         op.close()
 
 
+def test_conv2d_halo_lines_wide_cin(dev):
+    """Cin = 128 > BK: two channel blocks per filter row, weight tiles loaded
+    one 2-D box per tap (the one-box-per-row load needs Cin = BK = 64)."""
+    import oracle
+    from paper_2006_05664_b200 import capi
+
+    n, c, h, w, k, kh, kw, s, p = 4, 128, 28, 28, 64, 3, 3, 1, 1
+    op = dev.prepare(capi.CONV2D, conv=[n, c, h, w, k, kh, kw, s, p], seed=5)
+    try:
+        for knobs in [(128, 64, 64, 4, 1, 1, 4, 14), (128, 64, 64, 2, 1, 1, 4, 14, 1, 1, 0, 1)]:
+            t = dev.trial(op, knobs, warmup=1, reps=3)
+            assert t.ok, t.message
+            x = oracle.operand(n * c * h * w, 5)
+            f = oracle.operand(k * c * kh * kw, 6)
+            ref = oracle.conv(x, f, n, c, h, w, k, kh, kw, s, p)
+            assert _rel(op.output(), ref) < BF16_TOL
+    finally:
+        op.close()
+
+
 def test_conv2d_halo_lines_need_matching_filter(dev):
     """A 14-pixel halo line is a 3-wide filter's; other filters reject it."""
     from paper_2006_05664_b200 import capi
