@@ -56,7 +56,7 @@ def peaks() -> dict:
 class ClockSampler:
     """SM clocks / throttle reasons sampled during the timed region.
 
-    In-process NVML (nvidia-ml-py) polled every 100 ms: a handful of fields
+    In-process NVML (nvidia-ml-py) polled every 20 ms: a handful of fields
     per sample.  A looping ``nvidia-smi`` (the fallback) queries many fields
     per sample and was seen to stall concurrent driver calls (module loads,
     graph instantiation) by tens of milliseconds, which shows up as noise in
@@ -69,7 +69,7 @@ class ClockSampler:
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu: int, period_s: float = 0.1):
+    def __init__(self, gpu: int, period_s: float = 0.02):
         self.gpu = gpu
         self.period = period_s
         self.proc = None
