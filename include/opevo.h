@@ -72,6 +72,10 @@ typedef struct opevo_op_desc {
     uint64_t seed;            /* synthetic-input seed */
 } opevo_op_desc;
 
+/* Deepest split-K (knob OPEVO_KNOB_SPLIT): the fp32 partial workspace is
+ * allocated for this many slices when the operator is prepared. */
+#define OPEVO_MAX_SPLIT 16
+
 /* Kernel knob vector: fixed order, OPEVO_NUM_KNOBS entries. */
 enum opevo_knob {
     OPEVO_KNOB_BM = 0,        /* CTA tile rows (UMMA M / atoms)          */
@@ -142,14 +146,19 @@ int opevo_op_prepare(opevo_ctx* ctx, const opevo_op_desc* desc, opevo_op** out,
 void opevo_op_destroy(opevo_op* op);
 /* Operand sizes in bytes (A, B in the kernel layout, C output). */
 int opevo_op_sizes(const opevo_op* op, size_t* a_bytes, size_t* b_bytes, size_t* c_bytes);
-/* Host <-> device copies for the end-to-end path (inputs in kernel layout). */
+/* Host <-> device copies for the end-to-end path (inputs in kernel layout:
+ * MatMul/BMM A [batch][rows][depth], B [batch][cols][depth]; Conv2d X NHWC,
+ * W [Cout][Kh][Kw][Cin]).  Uploading marks the reference stale: the next
+ * check recomputes it from the new operands (for Conv2d after converting
+ * them back to the paper's NCHW / OIHW layouts), and every instance is
+ * verified again. */
 int opevo_op_upload(opevo_op* op, const void* a_host, const void* b_host, char* err, size_t errlen);
 int opevo_op_download(opevo_op* op, void* c_host, size_t bytes, char* err, size_t errlen);
 /* Device operands (kernel layout) to host, e.g. to stage them in pinned memory. */
 int opevo_op_read_inputs(opevo_op* op, void* a_host, void* b_host, char* err, size_t errlen);
 /* Reference output (fp32, kernel output layout) to host. */
 int opevo_op_reference(opevo_op* op, float* host, size_t count, char* err, size_t errlen);
-/* Recompute the reference (after opevo_op_upload). */
+/* Recompute the reference now (opevo_op_upload otherwise defers it to the next check). */
 int opevo_op_refresh_reference(opevo_op* op, char* err, size_t errlen);
 
 /* Bind knobs to an operator: validate, fetch/compile the module, build the
@@ -164,7 +173,10 @@ int opevo_kernel_check(opevo_kernel* k, double tol, double* rel_err, char* err, 
  *               L2 warm; captured while the warm-up runs) -- the fitness;
  * flush_l2 = 1: an L2-sized write before every launch, each launch timed;
  * flush_l2 = 2: `reps` back-to-back stream launches released together from a
- *               device-side gate (no graph, no host gaps). */
+ *               device-side gate (no graph, no host gaps).
+ * Exactly `reps` timed launches: the per-trial device budget
+ * (OPEVO_TIME_BUDGET_MS) that caps repetitions of slow candidates applies to
+ * opevo_trial / opevo_trial_batch only. */
 int opevo_kernel_time(opevo_kernel* k, int warmup, int reps, int flush_l2, double* ms_per_launch,
                       char* err, size_t errlen);
 

@@ -30,7 +30,7 @@ _lib = None
 def build() -> str:
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
     if not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
-        subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-o", LIB, SRC, "-lm"])
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-o", LIB, SRC, "-lm"])
     return LIB
 
 
@@ -43,10 +43,12 @@ def load():
         lib.oracle_fill.argtypes = [fp, C.c_uint64, C.c_uint64, C.c_int]
         lib.oracle_fill_bf16_bits.argtypes = [C.POINTER(C.c_uint16), C.c_uint64, C.c_uint64]
         lib.oracle_gemm.argtypes = [fp, fp, dp, C.c_int64, C.c_int64, C.c_int64, C.c_int64]
+        lib.oracle_gemm_rows.argtypes = [fp, fp, dp, C.c_int64, C.c_int64, C.c_int64,
+                                         C.POINTER(C.c_int64), C.c_int64]
         lib.oracle_conv.argtypes = [fp, fp, dp] + [C.c_int] * 9
         lib.oracle_compare.argtypes = [fp, dp, C.c_uint64, dp, dp, C.POINTER(C.c_uint64)]
-        for f in (lib.oracle_fill, lib.oracle_fill_bf16_bits, lib.oracle_gemm, lib.oracle_conv,
-                  lib.oracle_compare):
+        for f in (lib.oracle_fill, lib.oracle_fill_bf16_bits, lib.oracle_gemm, lib.oracle_gemm_rows,
+                  lib.oracle_conv, lib.oracle_compare):
             f.restype = None
         _lib = lib
     return _lib
@@ -84,6 +86,18 @@ def gemm(a, b, batch: int, rows: int, cols: int, depth: int):
     out = np.empty(batch * rows * cols, dtype=np.float64)
     load().oracle_gemm(_fp(a), _fp(b), _dp(out), batch, rows, cols, depth)
     return out
+
+
+def gemm_rows(a, b, rows: int, cols: int, depth: int, row_idx):
+    """fp64 rows ``row_idx`` (counted over all batches, b * rows + r) of
+    :func:`gemm`: an array [len(row_idx)][cols]."""
+    import numpy as np
+
+    idx = np.ascontiguousarray(row_idx, dtype=np.int64)
+    out = np.empty(len(idx) * cols, dtype=np.float64)
+    load().oracle_gemm_rows(_fp(a), _fp(b), _dp(out), rows, cols, depth,
+                            idx.ctypes.data_as(C.POINTER(C.c_int64)), len(idx))
+    return out.reshape(len(idx), cols)
 
 
 def conv(x, w, n, c, h, wd, k, kh, kw, stride, pad):

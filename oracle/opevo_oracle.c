@@ -61,24 +61,38 @@ void oracle_fill_bf16_bits(uint16_t* out, uint64_t n, uint64_t seed) {
 }
 
 /* R[b][r][c] = sum_k A[b][r][k] * B[b][c][k] in fp64 */
+static void gemm_row(const float* A, const float* B, double* out, int64_t rows, int64_t cols,
+                     int64_t depth, int64_t br) {
+    const int64_t b = br / rows;
+    const float* a = A + br * depth;
+    for (int64_t c = 0; c < cols; ++c) {
+        const float* y = B + (b * cols + c) * depth;
+        double acc = 0.0;
+        for (int64_t k = 0; k < depth; ++k) acc += (double)a[k] * (double)y[k];
+        out[c] = acc;
+    }
+}
+
+/* R[b][r][c] = sum_k A[b][r][k] * B[b][c][k] in fp64 (rows in parallel) */
 void oracle_gemm(const float* A, const float* B, double* R, int64_t batch, int64_t rows,
                  int64_t cols, int64_t depth) {
-    for (int64_t b = 0; b < batch; ++b)
-        for (int64_t r = 0; r < rows; ++r) {
-            const float* a = A + (b * rows + r) * depth;
-            for (int64_t c = 0; c < cols; ++c) {
-                const float* y = B + (b * cols + c) * depth;
-                double acc = 0.0;
-                for (int64_t k = 0; k < depth; ++k) acc += (double)a[k] * (double)y[k];
-                R[(b * rows + r) * cols + c] = acc;
-            }
-        }
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t br = 0; br < batch * rows; ++br) gemm_row(A, B, R + br * cols, rows, cols, depth, br);
+}
+
+/* The same for a sample of output rows: out[i][c] = R[row_idx[i]][c], where
+ * row_idx counts rows over all batches (b * rows + r). */
+void oracle_gemm_rows(const float* A, const float* B, double* out, int64_t rows, int64_t cols,
+                      int64_t depth, const int64_t* row_idx, int64_t nidx) {
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t i = 0; i < nidx; ++i) gemm_row(A, B, out + i * cols, rows, cols, depth, row_idx[i]);
 }
 
 /* direct conv, X NCHW, W OIHW -> R NHWC (the implicit-GEMM output layout) */
 void oracle_conv(const float* X, const float* W, double* R, int N, int C, int H, int Wd, int K,
                  int KH, int KW, int stride, int pad) {
     const int HO = (H + 2 * pad - KH) / stride + 1, WO = (Wd + 2 * pad - KW) / stride + 1;
+#pragma omp parallel for collapse(2) schedule(dynamic, 1)
     for (int n = 0; n < N; ++n)
         for (int ho = 0; ho < HO; ++ho)
             for (int wo = 0; wo < WO; ++wo)

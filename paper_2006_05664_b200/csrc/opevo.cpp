@@ -403,6 +403,13 @@ bool knobs_compilable(int family, const Knobs& k, char* err, size_t len) {
         put_err(err, len, "stages=%d out of range", k.stages);
         return false;
     }
+    // the split-K workspace is allocated for OPEVO_MAX_SPLIT slices when the
+    // operator is prepared; a deeper split would have to reallocate it under
+    // kernels already bound in the same trial batch
+    if (k.split < 1 || k.split > OPEVO_MAX_SPLIT) {
+        put_err(err, len, "split=%d out of range (1..%d)", k.split, OPEVO_MAX_SPLIT);
+        return false;
+    }
     if (!(k.acc == 1 || k.acc == 2 || k.acc == 4) || (k.bk / 16) % k.acc) {
         put_err(err, len, "acc=%d unsupported for BK=%d (1, 2 or 4 dividing BK/16)", k.acc, k.bk);
         return false;
@@ -668,6 +675,8 @@ struct opevo_op {
     CUdeviceptr conv_x = 0, conv_w = 0;                 // paper layouts (NCHW / OIHW)
     CUdeviceptr ws = 0, counters = 0;
     size_t ws_bytes = 0, counter_bytes = 0;
+    unsigned ws_gen = 0;                                // bumped when `ws` moves
+    bool ref_stale = false;                             // operands uploaded since the reference
     size_t a_bytes = 0, b_bytes = 0, c_bytes = 0;
     int in_f32 = 0, out_f32 = 0;
     // Timed graphs by (knobs, repetitions).  Many configurations map to one
@@ -717,6 +726,7 @@ struct opevo_kernel {
     alignas(64) CUtensorMap tma_b;
     alignas(64) CUtensorMap tma_c;      // output, box = one 32-row epilogue chunk
     alignas(64) CUtensorMap tma_w{};    // TMA split-K partials {cols, rows, split} fp32 (else unused)
+    unsigned ws_gen = 0;                // op->ws_gen tma_w was encoded against
     unsigned grid[3] = {1, 1, 1};
     size_t smem = 0;
     int k_per_split = 0;
@@ -784,10 +794,20 @@ int compute_reference(opevo_op* op, char* err, size_t errlen) {
     return OPEVO_OK;
 }
 
+// Before any check: a reference made stale by opevo_op_upload is recomputed
+// from the uploaded operands.
+int fresh_reference(opevo_op* op, char* err, size_t errlen) {
+    if (!op->ref_stale) return OPEVO_OK;
+    op->ref_stale = false;
+    op->verified.clear();
+    return compute_reference(op, err, errlen);
+}
+
 int ensure_ws(opevo_op* op, size_t ws_need, size_t cnt_need, char* err, size_t errlen) {
     opevo_ctx* ctx = op->ctx;
     if (ws_need > op->ws_bytes || cnt_need > op->counter_bytes) drop_graphs(op);   // captured pointers go stale
     if (ws_need > op->ws_bytes) {
+        ++op->ws_gen;                                   // bound TMA split maps re-encode
         if (op->ws) g_cu.MemFree(op->ws);
         op->ws = 0;
         op->ws_bytes = 0;
@@ -827,6 +847,18 @@ int encode_map(CUtensorMap* map, CUdeviceptr base, int rank, const uint64_t* dim
     return OPEVO_OK;
 }
 
+// TMA split-K partials {cols, rows, split} fp32 in op->ws.  Recorded against
+// op->ws_gen, so a kernel bound before the workspace moved re-encodes it at
+// its next launch instead of storing into freed memory.
+int encode_split_map(opevo_kernel* kr, int tsplit, char* err, size_t errlen) {
+    opevo_op* op = kr->op;
+    uint64_t wd[3] = {(uint64_t)op->cols, (uint64_t)op->rows, (uint64_t)tsplit};
+    uint64_t wstr[2] = {(uint64_t)op->cols * 4, (uint64_t)op->cols * op->rows * 4};
+    uint32_t wb[3] = {32, 32, 1};
+    kr->ws_gen = op->ws_gen;
+    return encode_map(&kr->tma_w, op->ws, 3, wd, wstr, wb, 128, err, errlen, 1);
+}
+
 int launch_kernel(opevo_kernel* kr, char* err, size_t errlen, CUstream on = nullptr) {
     opevo_op* op = kr->op;
     opevo_ctx* ctx = op->ctx;
@@ -857,6 +889,14 @@ int launch_kernel(opevo_kernel* kr, char* err, size_t errlen, CUstream on = null
         }
         return OPEVO_OK;
     }
+    const int batched = op->d.kind == OPEVO_BATCHMATMUL ? 1 : 0;
+    if (kr->ws_gen != op->ws_gen) {
+        if (const int ts = tma_split(kr->k, kr->family, batched)) {
+            const int est = encode_split_map(kr, ts, err, errlen);
+            if (est) return est;
+        }
+        kr->ws_gen = op->ws_gen;
+    }
     int rows = (int)op->rows;
     int cols = (int)op->cols;
     int depth = kr->kdepth;                        // K-loop extent (bf16 units for 3xTF32)
@@ -876,7 +916,6 @@ int launch_kernel(opevo_kernel* kr, char* err, size_t errlen, CUstream on = null
     cfg.hStream = strm;
     CUlaunchAttribute attr[2];
     unsigned na = 0;
-    const int batched = op->d.kind == OPEVO_BATCHMATMUL ? 1 : 0;
     const unsigned clx = (unsigned)(kr->k.cluster * kr->k.cg *
                                     (dsmem_split(kr->k, kr->family, batched) ? kr->k.split : 1));
     if (clx > 1) {
@@ -1229,12 +1268,12 @@ int opevo_op_prepare(opevo_ctx* ctx, const opevo_op_desc* desc, opevo_op** out, 
     }
     if (!st) st = compute_reference(op, err, errlen);
     if (!st) {
-        // split-K workspace for up to 16 slices and tile counters, up front:
+        // split-K workspace for OPEVO_MAX_SPLIT slices and tile counters, up front:
         // growing them during a search reallocates (and drops the timed
         // graphs that captured the old pointers) on the trial's critical path
         const size_t slice = (size_t)op->batch * op->rows * op->cols * 4;
         const size_t tiles = (size_t)op->batch * ((op->rows + 127) / 128) * ((op->cols + 15) / 16);
-        st = ensure_ws(op, slice * 16, tiles * 16 * 4, err, errlen);
+        st = ensure_ws(op, slice * OPEVO_MAX_SPLIT, tiles * 16 * 4, err, errlen);
     }
     if (st) {
         opevo_op_destroy(op);
@@ -1258,7 +1297,27 @@ int opevo_op_upload(opevo_op* op, const void* a_host, const void* b_host, char* 
     g_cu.CtxSetCurrent(ctx->cu);
     if (a_host) CU_TRY(ctx, g_cu.MemcpyHtoDAsync(op->a, a_host, op->a_bytes, ctx->stream), "upload A");
     if (b_host) CU_TRY(ctx, g_cu.MemcpyHtoDAsync(op->b, b_host, op->b_bytes, ctx->stream), "upload B");
-    op->verified.clear();                 // new operands: every instance is verified again
+    if (op->d.kind == OPEVO_CONV2D && (a_host || b_host)) {
+        // the reference convolves the paper's layouts: NHWC -> NCHW is the
+        // generic [n][c][h][w] -> [n][h][w][c] transpose with C' = H*W,
+        // H' = C, W' = 1 (and OHWI -> OIHW with N = O, C' = KH*KW, H' = I)
+        const int32_t* c = op->d.conv;
+        int N = c[0], C = c[1], HW = c[2] * c[3], K = c[4], T = c[5] * c[6], one = 1;
+        int st = OPEVO_OK;
+        if (a_host) {
+            void* a1[] = {&op->a, &op->conv_x, &N, &HW, &C, &one};
+            st = launch_simple(ctx, ctx->k_nchw2nhwc, grid_for(op->a_bytes / 2), 256, a1, err, errlen);
+        }
+        if (!st && b_host) {
+            void* a2[] = {&op->b, &op->conv_w, &K, &T, &C, &one};
+            st = launch_simple(ctx, ctx->k_nchw2nhwc, grid_for(op->b_bytes / 2), 256, a2, err, errlen);
+        }
+        if (st) return st;
+    }
+    if (a_host || b_host) {
+        op->verified.clear();             // new operands: every instance is verified again
+        op->ref_stale = true;             // and against a reference recomputed from them
+    }
     return OPEVO_OK;
 }
 
@@ -1286,6 +1345,7 @@ int opevo_op_reference(opevo_op* op, float* host, size_t count, char* err, size_
     opevo_ctx* ctx = op->ctx;
     g_cu.CtxSetCurrent(ctx->cu);
     size_t n = std::min<size_t>(count, (size_t)op->batch * op->rows * op->cols);
+    if (int st = fresh_reference(op, err, errlen)) return st;
     CU_TRY(ctx, g_cu.StreamSynchronize(ctx->stream), "sync");
     CU_TRY(ctx, g_cu.MemcpyDtoH(host, op->ref, n * 4), "download reference");
     return OPEVO_OK;
@@ -1295,6 +1355,7 @@ int opevo_op_refresh_reference(opevo_op* op, char* err, size_t errlen) {
     if (!op) return OPEVO_ERR_ARG;
     g_cu.CtxSetCurrent(op->ctx->cu);
     op->verified.clear();
+    op->ref_stale = false;
     return compute_reference(op, err, errlen);
 }
 
@@ -1523,12 +1584,7 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
         if (max_split > 1 && !dsm) {
             const size_t slice = (size_t)op->batch * op->rows * op->cols * 4;
             st = ensure_ws(op, slice * max_split, (size_t)tiles * clsz * 4, err, errlen);
-            if (!st && tsplit) {
-                uint64_t wd[3] = {(uint64_t)op->cols, (uint64_t)op->rows, (uint64_t)tsplit};
-                uint64_t wstr[2] = {(uint64_t)op->cols * 4, (uint64_t)op->cols * op->rows * 4};
-                uint32_t wb[3] = {32, 32, 1};
-                st = encode_map(&kr->tma_w, op->ws, 3, wd, wstr, wb, 128, err, errlen, 1);
-            }
+            if (!st && tsplit) st = encode_split_map(kr, tsplit, err, errlen);
             if (st) {
                 delete kr;
                 return st;
@@ -1788,7 +1844,7 @@ int enqueue_warmup_estimate(opevo_kernel* k, int warmup, CUevent e0, CUevent e1,
 // role.  In mode 0 the graph is captured and instantiated while phase A runs
 // on the device.
 int check_and_time(opevo_kernel* k, double tol, double* rel_err, int warmup, int reps, int mode,
-                   double* ms_per_launch, char* err, size_t errlen) {
+                   double* ms_per_launch, char* err, size_t errlen, bool budgeted) {
     opevo_ctx* ctx = k->op->ctx;
     int st = OPEVO_OK;
     CUgraphExec ge = nullptr;
@@ -1815,12 +1871,12 @@ int check_and_time(opevo_kernel* k, double tol, double* rel_err, int warmup, int
         if (ge) g_cu.GraphExecDestroy(ge);
         return st;
     }
-    if (slow_candidate(est)) {
+    if (budgeted && slow_candidate(est)) {
         if (ge) g_cu.GraphExecDestroy(ge);
         *ms_per_launch = est;
         return OPEVO_OK;
     }
-    reps = capped_reps(reps, est);
+    if (budgeted) reps = capped_reps(reps, est);
     for (int i = 0; i + 1 < warmup && !st; ++i) st = launch_kernel(k, err, errlen);
     double total = 0.0;
     if (!st && mode == 0) {
@@ -1850,7 +1906,8 @@ int opevo_kernel_check(opevo_kernel* k, double tol, double* rel_err, char* err, 
     if (!k) return OPEVO_ERR_ARG;
     opevo_ctx* ctx = k->op->ctx;
     g_cu.CtxSetCurrent(ctx->cu);
-    int st = enqueue_check(k, err, errlen);
+    int st = fresh_reference(k->op, err, errlen);
+    if (!st) st = enqueue_check(k, err, errlen);
     if (!st) st = sync_checked(ctx, "check", err, errlen);
     if (!st) st = finish_check(k, tol < 0 ? 0.0 : tol, rel_err, err, errlen);
     return st;
@@ -1860,7 +1917,9 @@ int opevo_kernel_time(opevo_kernel* k, int warmup, int reps, int flush_l2, doubl
                       size_t errlen) {
     if (!k || reps < 1 || !ms_per_launch) return OPEVO_ERR_ARG;
     g_cu.CtxSetCurrent(k->op->ctx->cu);
-    return check_and_time(k, -1.0, nullptr, warmup, reps, flush_l2, ms_per_launch, err, errlen);
+    // an explicit measurement: exactly `reps` launches (the per-trial device
+    // budget applies to the trial paths only)
+    return check_and_time(k, -1.0, nullptr, warmup, reps, flush_l2, ms_per_launch, err, errlen, false);
 }
 
 int opevo_trial(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nknobs, int warmup, int reps,
@@ -1871,7 +1930,8 @@ int opevo_trial(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nknobs, 
     int st = opevo_kernel_get(ctx, op, knobs, nknobs, &k, res, err, errlen);
     if (st) return st;
     double rel = 0.0, ms = 0.0;
-    st = check_and_time(k, tol < 0 ? 0.0 : tol, &rel, warmup, reps, flush_l2, &ms, err, errlen);
+    st = fresh_reference(op, err, errlen);
+    if (!st) st = check_and_time(k, tol < 0 ? 0.0 : tol, &rel, warmup, reps, flush_l2, &ms, err, errlen, true);
     res->rel_err = rel;
     if (!st) {
         res->ms = ms;
@@ -1889,6 +1949,7 @@ int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nk
         return OPEVO_ERR_ARG;
     const int mode = flush_l2;
     g_cu.CtxSetCurrent(ctx->cu);
+    if (int rst = fresh_reference(op, err, errlen)) return rst;
     static const bool prof = getenv("OPEVO_PROFILE_BATCH") != nullptr;
     double tp[8] = {now_ms(), 0, 0, 0, 0, 0, 0, 0};
     std::vector<opevo_kernel*> ks(count, nullptr);

@@ -56,6 +56,7 @@ from .spaces import Discrete, SearchSpace
 
 SMEM_LIMIT = 232448          # 227 KB opt-in per CTA on B200
 B200_SMS = 148
+MAX_SPLIT = 16               # OPEVO_MAX_SPLIT: split-K workspace slices allocated at prepare
 SMEM_EXTRA = 1024 + 256      # alignment slack + barriers
 STAGE_VALUES = (2, 3, 4, 5, 6, 7, 8)
 UNROLL_TO_STAGES = {0: 2, 16: 3, 64: 4, 512: 6, 1500: 8}
@@ -235,6 +236,8 @@ def _gemm_knobs(rows: int, cols: int, depth: int, vals: dict,
     split, bk = k[0], k[2]
     if bm not in (128, 256):
         return None, f"BM={bm} is not a UMMA row tile (128 or 256)"
+    if split > MAX_SPLIT:
+        return None, f"split-K {split} exceeds the {MAX_SPLIT}-slice workspace"
     if bn % 16 or not 16 <= bn <= 256:
         return None, f"BN={bn} is not a UMMA column tile (16..256, step 16)"
     if not _bk_ok(bk):
@@ -266,6 +269,8 @@ def _x3_knobs(rows: int, cols: int, vals: dict, batch: int = 0) -> tuple[Knobs |
     split, bk = k[0], k[2]
     if bm not in (128, 256):
         return None, f"BM={bm} is not a UMMA row tile (128 or 256)"
+    if split > MAX_SPLIT:
+        return None, f"split-K {split} exceeds the {MAX_SPLIT}-slice workspace"
     if bn % 16 or not 16 <= bn <= 256:
         return None, f"BN={bn} is not a UMMA column tile (16..256, step 16)"
     if not _bk_ok(2 * bk):
