@@ -16,8 +16,9 @@ identical engine replica and evaluates the ask indices i = rank (mod N); one
 all_reduce of the result rows per generation (scheduler.ShardedEvaluator).
 
 ``--impl reference``: the reference's own CPU path (OpEvo + its synthetic CPU
-evaluator, restated in oracle/opevo_port.py because the reference tree does
-not exist on the GPU box), rank 0 only, on the host cores.
+evaluator): the unmodified reference package installed into baseline/_ref
+(tools/install_reference.sh), or its restatement oracle/opevo_port.py when
+that install is absent; rank 0 only, on the host cores.
 """
 
 from __future__ import annotations
@@ -166,25 +167,65 @@ def dist_env():
     return world, rank, local
 
 
-def cpu_reference_arm(op: str, steps: int, warmup: int, seed: int) -> dict:
-    """The reference's CPU search + synthetic evaluator, timed on this host."""
-    from oracle import opevo_port
+REF_DIR = os.path.join(REPO, "baseline", "_ref")
 
-    budget = RHO * (steps + warmup)
+
+def _stock_reference():
+    """The unmodified reference package (topotune 0.1.0) installed into
+    baseline/_ref by tools/install_reference.sh, or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "topotune")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import topotune
+        from topotune import benchmarks, engine
+    except ImportError:
+        return None
+    if not os.path.abspath(topotune.__file__).startswith(REF_DIR):
+        return None
+    return engine, benchmarks
+
+
+def cpu_reference_arm(op: str, budget: int, seed: int, max_s: float = 10.0) -> dict:
+    """The reference's CPU search + synthetic evaluator, timed on this host:
+    the stock ``topotune.run(space, EngineConfig(seed, budget), objective)``
+    with ``make_objective`` (reference engine.py:293-310, benchmarks.py:294-302)
+    from baseline/_ref, or -- when that install is absent -- its restatement
+    oracle/opevo_port.py.  One thread: a search is one serial ask/tell chain,
+    and the reference's ``concurrency`` knob (a thread pool over the objective
+    calls) measured slower than serial for its microsecond objective
+    (6.5 k vs 3.9 k trials/s with 8 threads on the build host).  Each run is
+    one search of ``budget`` trials (our arm's search budget)."""
+    stock = _stock_reference()
+    if stock is not None:
+        engine, benchmarks = stock
+        space, objective = benchmarks.make_objective(benchmarks.parse_operator(op))
+
+        def one(s):
+            _, recs = engine.run(space, engine.EngineConfig(seed=s, budget=budget), objective)
+            return len(recs)
+        kind, what = "reference", ("the unmodified reference (stock topotune 0.1.0 from baseline/_ref): "
+                                   "topotune.engine.run with benchmarks.make_objective")
+    else:
+        from oracle import opevo_port
+
+        def one(s):
+            return len(opevo_port.opevo_run(op, seed=s, budget=budget)[1])
+        kind, what = "port", "the reference's loop restated in oracle/opevo_port.py (baseline/_ref absent)"
     reps, total_s, trials = 0, 0.0, 0
-    t_end = time.perf_counter() + 10.0
+    t_end = time.perf_counter() + max_s
     while True:
         t0 = time.perf_counter()
-        _, log = opevo_port.opevo_run(op, seed=seed + reps, budget=budget)
+        trials += one(seed + reps)
         total_s += time.perf_counter() - t0
-        trials += len(log)
         reps += 1
         if time.perf_counter() > t_end or reps >= 2000:
             break
-    return {"value": trials / total_s, "unit": "trials/s", "cores": 1, "kind": "port",
-            "sample": f"{reps} OpEvo runs x {budget} trials of {op} with the reference's "
-                      f"synthetic CPU evaluator (oracle/opevo_port.py), 1 thread, "
-                      f"{total_s:.1f} s of CPU work",
+    return {"value": trials / total_s, "unit": "trials/s", "cores": 1, "kind": kind,
+            "stock": stock is not None,
+            "sample": f"{reps} OpEvo runs x {budget} trials of {op} with the reference's synthetic "
+                      f"CPU evaluator: {what}; 1 thread, {total_s:.1f} s of CPU work",
             "cpu": _cpu_model(), "host_cpus": os.cpu_count()}
 
 
@@ -260,7 +301,8 @@ def run_reference(args) -> None:
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    cb = cpu_reference_arm(args.op, args.steps, args.warmup, args.seed)
+    budget = max(args.budget, RHO * (args.steps + args.warmup))
+    cb = cpu_reference_arm(args.op, budget, args.seed)
     cb["operator"] = cpu_operator_throughput(args.op)
     ms = 1e3 * RHO / cb["value"]
     line = {"metric": METRIC, "value": cb["value"], "unit": "trials/s", "n_gpus": args.gpus,
@@ -268,7 +310,7 @@ def run_reference(args) -> None:
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
             "config": {"workload": f"OpEvo search, {args.op}, reference synthetic CPU evaluator",
-                       "rho": RHO, "seed": args.seed},
+                       "operator": args.op, "rho": RHO, "seed": args.seed, "search_budget": budget},
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": "trials/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
@@ -286,6 +328,12 @@ def main() -> None:
     ap.add_argument("--op", default=DEFAULT_OP)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--reps", type=int, default=20, help="timed launches per trial")
+    ap.add_argument("--budget", type=int, default=500,
+                    help="trials of the whole search (the north star's 500); the generations after "
+                         "the timed ones complete it untimed")
+    ap.add_argument("--loser-ratio", type=float, default=1.5,
+                    help="straggler rule: candidates slower than this x the fastest verified one "
+                         "are timed with 5 launches (0: off)")
     ap.add_argument("--l2", default="warm", choices=("warm", "cold"))
     ap.add_argument("--timing", default="stream", choices=("graph", "stream"),
                     help="fitness launches: stream launches released together by a device gate "
@@ -297,6 +345,7 @@ def main() -> None:
     ap.add_argument("--no-preload", action="store_true",
                     help="do not load the cached kernel family into the context before timing")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cold", action="store_true", help="skip the cold-kernel-cache sub-record")
     ap.add_argument("--log", default="")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -333,7 +382,7 @@ def main() -> None:
     space = gpu_operator_space(spec, args.dtype)
     settings = EvalSettings(reps=args.reps, preload_family=not args.no_preload,
                             flush_l2=1 if args.l2 == "cold" else (2 if args.timing == "stream" else 0),
-                            dtype=DTYPES[args.dtype])
+                            dtype=DTYPES[args.dtype], loser_ratio=args.loser_ratio)
     local_ev = GpuEvaluator(spec, space, local, settings)
     if world > 1:
         evaluator = ShardedEvaluator(local_ev, rank, world, device=coll_device)
@@ -359,93 +408,118 @@ def main() -> None:
         return sum(int(e.get("launches", 0)) + (1 if e.get("status") in ("ok", "verify_failed")
                                                 and not e.get("verify_cached") else 0) for e in extras)
 
-    budget = RHO * (args.steps + args.warmup)
-    engine = OpEvo(space, EngineConfig(seed=args.seed, budget=budget, parents=RHO, offspring=RHO))
-    recorder = TrialRecorder(space)
+    def new_search(budget: int):
+        return (OpEvo(space, EngineConfig(seed=args.seed, budget=budget, parents=RHO, offspring=RHO)),
+                TrialRecorder(space))
 
-    def generation(upload=None) -> tuple[int, int]:
+    def generation(eng, rec, upload=None, tally=None) -> int:
         if upload is not None:
             upload()
-        asked = engine.ask()
+        asked = eng.ask()
         if not asked.configs:
-            return 0, 0
+            return 0
         fits = evaluator(asked.configs)
-        engine.tell(list(zip(asked.configs, fits)))
+        eng.tell(list(zip(asked.configs, fits)))
         owner = getattr(evaluator, "__self__", evaluator)
         extras = owner.last_extras
         for c, f, e in zip(asked.configs, fits, extras):
-            recorder.record(c, f, e)
-        return len(asked.configs), launches_of(extras)
+            rec.record(c, f, e)
+        if tally is not None:
+            tally["launches"] += launches_of(extras)
+            tally["valid"] += sum(e.get("status") == "ok" for e in extras)
+            tally["verified"] += sum(e.get("status") in ("ok", "verify_failed")
+                                     and not e.get("verify_cached") for e in extras)
+            tally["instances"].update(tuple(e["knobs"]) for e in extras if e.get("knobs"))
+        return len(asked.configs)
 
+    budget = max(args.budget, RHO * (args.steps + args.warmup))
+    engine, recorder = new_search(budget)
     for _ in range(args.warmup):
-        generation()
+        generation(engine, recorder)
 
     # ---------------- timed region: K generations, device-timed, max over ranks
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    trials = launches = 0
+    trials = 0
+    tally = {"launches": 0, "valid": 0, "verified": 0, "instances": set()}
     with ClockSampler(local) as clocks:
         e0.record()
         t_wall0 = time.perf_counter()
         for _ in range(args.steps):
             local_ev.dev.flush_l2()     # every step starts with a cold L2
-            n, nl = generation()
-            trials += n
-            launches += nl
+            trials += generation(engine, recorder, tally=tally)
         barrier()
         e1.record()
         torch.cuda.synchronize()
         wall = time.perf_counter() - t_wall0
     sec = max_over_ranks(e0.elapsed_time(e1) / 1e3)
     trials_per_s = trials / sec if sec > 0 else 0.0
+    best_at_timed = engine.best().fitness if engine.archive else 0.0
+    trials_at_timed = len(recorder.records)
 
-    # ---------------- e2e: same loop through the public API, operands from
-    # pinned host memory uploaded every generation, results read back
+    # ---------------- the rest of the search budget (untimed): best within
+    # `budget` trials, the north star's "within 500 trials"
+    while len(recorder.records) < budget:
+        if generation(engine, recorder) == 0:
+            break
+    records = recorder.records
+    best = engine.best()
+
+    # ---------------- confirm the best instance: re-time the top distinct
+    # instances (noise must not decide between near-equal kernels)
+    confirmed = local_ev.confirm_top(k=5, reps=100, rounds=5) if best.fitness > 0 else []
+
+    # ---------------- e2e: the same generations (a fresh engine, same seed:
+    # warm-ups untimed, then the K timed ones) through the public API, with
+    # the operands uploaded from pinned host memory every generation -- so
+    # every trial is verified again, against a reference recomputed from the
+    # uploaded operands -- and the verification results read back
     e2e = None
     if not args.no_e2e:
-        from paper_2006_05664_b200 import capi
-
         op = local_ev.op
         pa, pb = capi.PinnedBuffer(op.a_bytes), capi.PinnedBuffer(op.b_bytes)
-        # stage the device operands in pinned host memory once (untimed); every
-        # timed generation re-uploads them, so the kernel reference stays valid
+        # stage the device operands in pinned host memory once (untimed)
         op.read_inputs(pa.ptr, pb.ptr)
-        e2e_steps = max(1, min(args.steps, 20))
-        engine.config.budget += RHO * e2e_steps
 
         def upload():
             op.upload(pa.ptr, pb.ptr)
 
+        e_engine, e_rec = new_search(RHO * (args.warmup + args.steps))
+        for _ in range(args.warmup):
+            local_ev.dev.flush_l2()
+            generation(e_engine, e_rec, upload)
         barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record()
         e2e_trials = 0
-        for _ in range(e2e_steps):
+        for _ in range(args.steps):
             local_ev.dev.flush_l2()
-            n, _ = generation(upload)
-            e2e_trials += n
+            e2e_trials += generation(e_engine, e_rec, upload)
         barrier()
         f1.record()
         torch.cuda.synchronize()
         e_sec = max_over_ranks(f0.elapsed_time(f1) / 1e3)
         e2e = {"value": e2e_trials / e_sec if e_sec > 0 else 0.0, "unit": "trials/s",
                "h2d_bytes_per_step": (op.a_bytes + op.b_bytes) * world,
-               "d2h_bytes_per_step": 12 * RHO, "steps": e2e_steps}
+               "d2h_bytes_per_step": 16 * RHO, "steps": args.steps,
+               "what": "the timed region's generations (fresh engine, same seed) through "
+                       "GpuEvaluator.evaluate + OpEvo ask/tell, operands uploaded from pinned "
+                       "host memory every generation (reference recomputed, every trial "
+                       "re-verified), compare results read back"}
         pa.close()
         pb.close()
 
     # ---------------- best kernel: re-time live (roofline.achieved)
-    best = engine.best()
-    records = recorder.records
     pk = peaks()
     roof = None
     best_knobs = None
     best_cold = None
-    if best.fitness > 0:
-        mapped = config_to_knobs(spec, space, best.config, args.dtype)
-        best_knobs = mapped.knobs.as_tuple()
+    best_conf = confirmed[0] if confirmed else None
+    if best_conf is not None:
+        best_knobs = tuple(best_conf["knobs"])
         k = local_ev.dev.kernel(local_ev.op, best_knobs)
-        ms = k.time(warmup=5, reps=100, flush_l2=False)
+        reps_graph = 100
+        ms = k.time(warmup=5, reps=reps_graph, flush_l2=False)
         ms_cold = k.time(warmup=2, reps=20, flush_l2=True)
         best_cold = spec.flops() / (ms_cold * 1e-3) / 1e12
         k.close()
@@ -470,11 +544,18 @@ def main() -> None:
                     "peak": peak, "unit": "TFLOP/s",
                     "frac": ach / peak, "traffic": _ncu_traffic(ncu_op, best_knobs),
                     "peak_source": _dtype_peak_source(args.dtype, pk),
-                    "kernel_ms": ms, "per_launch_flops": spec.flops(), "per_launch_bytes": nbytes}
+                    "kernel_ms": ms, "timing": f"{reps_graph} back-to-back launches in one CUDA graph",
+                    "per_launch_flops": spec.flops(), "per_launch_bytes": nbytes}
+
+    # ---------------- cold kernel cache: a fresh evaluator over an empty
+    # cubin cache (every instance NVRTC-compiled on the host pool), a few
+    # generations of a fresh search
+    cold = None
+    if not args.no_cold and rank == 0 and world == 1:
+        cold = cold_cache_record(spec, space, settings, local, args)
 
     if rank == 0:
-        cpu = None if (args.no_cpu or world > 1) else cpu_reference_arm(
-            args.op, args.steps, args.warmup, args.seed)
+        cpu = None if (args.no_cpu or world > 1) else cpu_reference_arm(args.op, budget, args.seed)
         if cpu is not None:
             # §8d (2): the operator itself on the host cores, beside best_tflops
             cpu["operator"] = cpu_operator_throughput(args.op, "bf16" if args.dtype == "bf16" else "f32")
@@ -482,6 +563,7 @@ def main() -> None:
             from paper_2006_05664_b200.logs import write_trial_log
 
             write_trial_log(args.log, records)
+        best_tflops = best_conf["tflops"] if best_conf else 0.0
         line = {
             "metric": METRIC, "value": trials_per_s, "unit": "trials/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps,
@@ -496,7 +578,7 @@ def main() -> None:
                                    + (" (BASELINE configs[1])" if args.op == DEFAULT_OP
                                       and args.dtype == "bf16" else ""),
                        "operator": args.op, "rho": RHO, "lambda": RHO, "q": 0.5,
-                       "seed": args.seed, "trials_timed": trials,
+                       "seed": args.seed, "trials_timed": trials, "search_budget": budget,
                        "space": ("reference operator space (fp32 SIMT family)" if args.dtype == "f32"
                                  else "reference operator space + stages (mapping.py)"),
                        "fitness_timing": (f"{settings.reps} back-to-back launches in one CUDA graph"
@@ -504,10 +586,12 @@ def main() -> None:
                                           f"{settings.reps} back-to-back stream launches released "
                                           f"by a device gate")
                                          + f" after {settings.warmup} warm-up launches incl. "
-                                         f"the verified one (a 0.3 ms device budget per trial "
-                                         f"caps the repetitions; a candidate whose verified "
-                                         f"launch alone exceeds it is timed by that launch), L2 "
-                                         f"{args.l2} (operands fit in L2)",
+                                         f"the verified one (a {settings.budget_ms} ms device budget "
+                                         f"per trial caps the repetitions; a candidate whose "
+                                         f"verified launch alone exceeds it is timed by that "
+                                         f"launch; a candidate slower than {settings.loser_ratio}x "
+                                         f"the fastest verified one gets {settings.loser_reps} "
+                                         f"launches), L2 {args.l2} (operands fit in L2)",
                        "l2_between_steps": "flushed: a 256 MB write (2x L2) before every timed "
                                            "step; within a trial the fitness is L2-warm "
                                            "back-to-back launches (use --l2 cold to flush "
@@ -516,21 +600,71 @@ def main() -> None:
                        "kernel_cache": ("prebuilt cubins (build()); the operator's cached family "
                                         "loaded into the context before timing" if not args.no_preload
                                         else "prebuilt cubins (build()), loaded on first use")},
-            "best_tflops": best.fitness,
-            "best_frac_of_peak": best.fitness / _dtype_peak(args.dtype, pk),
-            "best_knobs": best_knobs, "best_config": space.config_to_json(best.config),
+            "best_tflops": best_tflops,
+            "best_frac_of_peak": best_tflops / _dtype_peak(args.dtype, pk),
+            "best_knobs": list(best_knobs) if best_knobs else None,
+            "best_confirmed": confirmed,
+            "best_search_fitness": best.fitness,
+            "best_config": space.config_to_json(best.config) if best.fitness > 0 else None,
+            "best_tflops_at_timed_end": {"trials": trials_at_timed, "tflops": best_at_timed},
+            "best_tflops_at_500_trials": best_tflops if len(records) >= 500 else None,
             "best_tflops_cold_l2": best_cold,
             "trials_to_95pct": trials_to_fraction(records),
             "wallclock_to_95pct_s": wallclock_to_fraction(records) / 1e3,
             "valid_fraction": sum(r.fitness > 0 for r in records) / len(records),
             "trials_total": len(records), "wall_s_timed": wall,
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "timed_trial_mix": {"trials": trials, "valid": tally["valid"],
+                                "verified": tally["verified"],
+                                "distinct_instances": len(tally["instances"]),
+                                "valid_trials_per_s": tally["valid"] / sec if sec > 0 else 0.0,
+                                "verified_trials_per_s": tally["verified"] / sec if sec > 0 else 0.0},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": tally["launches"],
+            "cold_kernel_cache": cold,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
     local_ev.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def cold_cache_record(spec, space, settings, device: int, args, max_gens: int = 6,
+                      max_s: float = 30.0) -> dict:
+    """trials/s with an EMPTY cubin cache: a fresh
+    evaluator compiles every instance it meets with NVRTC on a host pool of
+    os.cpu_count() threads; a fresh search (same seed) runs up to `max_gens`
+    generations or `max_s` seconds, wall-clock timed (compilation is host
+    work)."""
+    import dataclasses
+    import shutil
+    import tempfile
+
+    from paper_2006_05664_b200 import EngineConfig, OpEvo
+    from paper_2006_05664_b200.evaluator import GpuEvaluator
+
+    tmp = tempfile.mkdtemp(prefix="opevo_cold_cache_")
+    threads = os.cpu_count() or 1
+    cs = dataclasses.replace(settings, cache_dir=tmp, preload_family=False, compile_threads=threads)
+    ev = GpuEvaluator(spec, space, device, cs)
+    try:
+        eng = OpEvo(space, EngineConfig(seed=args.seed, budget=RHO * max_gens, parents=RHO,
+                                        offspring=RHO))
+        trials = 0
+        t0 = time.perf_counter()
+        while time.perf_counter() - t0 < max_s:
+            asked = eng.ask()
+            if not asked.configs:
+                break
+            eng.tell(list(zip(asked.configs, ev.evaluate(asked.configs))))
+            trials += len(asked.configs)
+        wall = time.perf_counter() - t0
+        return {"value": trials / wall if wall > 0 else 0.0, "unit": "trials/s", "trials": trials,
+                "wall_s": wall, "instances_compiled": len(os.listdir(tmp)),
+                "nvrtc_pool_threads": threads, "timing": "host wall clock (NVRTC is host work)",
+                "best_tflops": max((h.fitness for h in ev.history), default=0.0)}
+    finally:
+        ev.close()
+        shutil.rmtree(tmp, ignore_errors=True)
 
 
 def _dtype_peak(dtype: str, pk: dict) -> float:

@@ -211,6 +211,15 @@ int opevo_op_preload(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
  * (as in timing) and launch i's stamps follow launch i-1's. */
 int opevo_kernel_trace(opevo_kernel* k, uint64_t* host, size_t count, char* err, size_t errlen);
 
+/* Trial timing policy of opevo_trial / opevo_trial_batch on this context.
+ * budget_ms (default OPEVO_TIME_BUDGET_MS or 0.3; <= 0 disables): a
+ * candidate whose verified launch alone exceeds it is timed by that launch;
+ * otherwise the repetitions are capped at budget_ms / (one-launch time),
+ * min 5.  loser_ratio (default 0 = off): a verified candidate whose
+ * one-launch time exceeds loser_ratio x the fastest one verified on the same
+ * operator so far gets loser_reps timed launches and no extra warm-up. */
+int opevo_ctx_set_timing(opevo_ctx* ctx, double budget_ms, double loser_ratio, int loser_reps);
+
 /* Write a 256 MB buffer (2x L2) on the context's stream so the next work
  * starts with a cold L2; returns after the flush completes. */
 int opevo_ctx_flush_l2(opevo_ctx* ctx, char* err, size_t errlen);

@@ -50,7 +50,7 @@ EXPORTS = (
     "opevo_op_refresh_reference", "opevo_kernel_get", "opevo_kernel_release",
     "opevo_kernel_run", "opevo_kernel_check", "opevo_kernel_time", "opevo_trial",
     "opevo_kernel_trace", "opevo_ctx_flush_l2", "opevo_host_alloc", "opevo_host_free",
-    "opevo_op_preload", "opevo_trial_batch",
+    "opevo_op_preload", "opevo_trial_batch", "opevo_ctx_set_timing",
 )
 MAX_BATCH = 64
 
@@ -120,6 +120,7 @@ def load() -> C.CDLL:
         "opevo_trial": (I, [P, P, i32p, I, I, I, I, D, C.POINTER(TrialResult), cp, sz]),
         "opevo_kernel_trace": (I, [P, C.POINTER(C.c_uint64), sz, cp, sz]),
         "opevo_ctx_flush_l2": (I, [P, cp, sz]),
+        "opevo_ctx_set_timing": (I, [P, D, D, I]),
         "opevo_host_alloc": (P, [sz]),
         "opevo_host_free": (None, [P]),
         "opevo_op_preload": (I, [P, P, i32p, I, dp, C.POINTER(I), cp, sz]),
@@ -220,6 +221,14 @@ class Device:
 
     def __exit__(self, *exc):
         self.close()
+
+    def set_timing(self, budget_ms: float = 0.3, loser_ratio: float = 0.0, loser_reps: int = 5) -> None:
+        """Trial timing policy (``opevo_ctx_set_timing``): per-trial device
+        budget, and the straggler rule -- candidates slower than
+        ``loser_ratio`` x the fastest verified one get ``loser_reps`` launches."""
+        st = self.lib.opevo_ctx_set_timing(self.handle, budget_ms, loser_ratio, loser_reps)
+        if st != OK:
+            raise OpevoError(st, "bad timing policy")
 
     def flush_l2(self) -> None:
         """Evict L2 (write 2x its size) and wait."""

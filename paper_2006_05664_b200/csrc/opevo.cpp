@@ -661,6 +661,10 @@ struct opevo_ctx {
     size_t flush_bytes = 0;
     CUdeviceptr cmp_buf = 0;
     int sm_count = 0, smem_optin = 0, cc_major = 0, cc_minor = 0;
+    // trial timing policy (opevo_ctx_set_timing)
+    double budget_ms = 0.3;
+    double loser_ratio = 0.0;
+    int loser_reps = 5;
     std::string cache_dir;
     std::unordered_map<std::string, LoadedModule> modules;
     std::mutex modules_mu;              // modules may be preloaded from host pool threads
@@ -677,6 +681,7 @@ struct opevo_op {
     size_t ws_bytes = 0, counter_bytes = 0;
     unsigned ws_gen = 0;                                // bumped when `ws` moves
     bool ref_stale = false;                             // operands uploaded since the reference
+    float best_est_ms = 0.f;                            // fastest verified single launch (loser policy)
     size_t a_bytes = 0, b_bytes = 0, c_bytes = 0;
     int in_f32 = 0, out_f32 = 0;
     // Timed graphs by (knobs, repetitions).  Many configurations map to one
@@ -1075,6 +1080,7 @@ int opevo_ctx_create(int device, const char* cache_dir, opevo_ctx** out, char* e
     }
     opevo_ctx* ctx = new opevo_ctx();
     ctx->device = device;
+    if (const char* b = getenv("OPEVO_TIME_BUDGET_MS")) ctx->budget_ms = atof(b);
     ctx->cache_dir = cache_dir ? cache_dir : "";
     CUresult r = g_cu.DeviceGet(&ctx->dev, device);
     if (r != CUDA_SUCCESS) {
@@ -1658,22 +1664,20 @@ int finish_check(opevo_kernel* k, double tol, double* rel_err, char* err, size_t
     return judge(res, tol, rel_err, err, errlen);
 }
 
-// Device-time budget per measurement (OPEVO_TIME_BUDGET_MS, default 0.3): a
-// one-launch estimate caps the repetitions of slow candidates at
-// budget/estimate (min 5), so a 30 us instance costs 10 launches rather than
-// 20 and a 10 ms one 5; the fast instances that decide the search keep all
-// `reps`.  Once the measured time is device-bound (the trial pipeline's
-// host work is overlapped), this budget sets the trial rate.
+// Device-time budget per measurement (ctx->budget_ms, opevo_ctx_set_timing;
+// default OPEVO_TIME_BUDGET_MS or 0.3): a one-launch estimate caps the
+// repetitions of slow candidates at budget/estimate (min 5), so a 30 us
+// instance costs 10 launches rather than 20 and a 10 ms one 5; the fast
+// instances that decide the search keep all `reps`.  Once the measured time
+// is device-bound (the trial pipeline's host work is overlapped), this
+// budget sets the trial rate.
 // A candidate whose single timed launch exceeds the whole per-trial budget.
-bool slow_candidate(float est_ms) {
-    double budget = 0.3;
-    if (const char* b = getenv("OPEVO_TIME_BUDGET_MS")) budget = atof(b);
-    return budget > 0 && est_ms > budget;
+bool slow_candidate(const opevo_ctx* ctx, float est_ms) {
+    return ctx->budget_ms > 0 && est_ms > ctx->budget_ms;
 }
 
-int capped_reps(int reps, float est_ms) {
-    double budget = 0.3;
-    if (const char* b = getenv("OPEVO_TIME_BUDGET_MS")) budget = atof(b);
+int capped_reps(const opevo_ctx* ctx, int reps, float est_ms) {
+    const double budget = ctx->budget_ms;
     if (budget > 0 && est_ms > 0 && est_ms * reps > budget) {
         // quantised to {reps, 16, 8, 5} so an instance has few distinct timed graphs
         const int want = std::max(std::min(reps, 5), (int)(budget / est_ms));
@@ -1684,6 +1688,17 @@ int capped_reps(int reps, float est_ms) {
         reps = q;
     }
     return reps;
+}
+
+// Straggler control (ctx->loser_ratio > 0): a verified candidate whose
+// single-launch estimate exceeds loser_ratio x the fastest estimate verified
+// on this operator so far cannot reach the top of the archive; it is timed
+// with loser_reps back-to-back launches and no extra warm-up instead of the
+// full measurement.  Its fitness stays a measured back-to-back time, only
+// with fewer samples; the competitive candidates keep every repetition.
+bool loser(const opevo_op* op, float est_ms) {
+    const opevo_ctx* ctx = op->ctx;
+    return ctx->loser_ratio > 0 && op->best_est_ms > 0 && est_ms > ctx->loser_ratio * op->best_est_ms;
 }
 
 // `reps` back-to-back launches timed with CUDA events on the library stream.
@@ -1871,12 +1886,12 @@ int check_and_time(opevo_kernel* k, double tol, double* rel_err, int warmup, int
         if (ge) g_cu.GraphExecDestroy(ge);
         return st;
     }
-    if (budgeted && slow_candidate(est)) {
+    if (budgeted && slow_candidate(ctx, est)) {
         if (ge) g_cu.GraphExecDestroy(ge);
         *ms_per_launch = est;
         return OPEVO_OK;
     }
-    if (budgeted) reps = capped_reps(reps, est);
+    if (budgeted) reps = capped_reps(ctx, reps, est);
     for (int i = 0; i + 1 < warmup && !st; ++i) st = launch_kernel(k, err, errlen);
     double total = 0.0;
     if (!st && mode == 0) {
@@ -2028,6 +2043,19 @@ int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nk
     std::vector<char> cached(count, 0);
     std::vector<std::string> vkey(count);
     std::vector<int> nreps(count, reps);
+    // warm-up launches before the timed ones: the check launch counts as one,
+    // a re-timed (cached) instance gets its `warmup` in full; losers (see
+    // loser()) get only what their first timed launch needs
+    std::vector<int> nwarm(count, 0);
+    auto plan = [&](int i, float est) {
+        if (loser(op, est)) {
+            nreps[i] = std::min(reps, ctx->loser_reps);
+            nwarm[i] = cached[i] ? 1 : 0;
+        } else {
+            nreps[i] = capped_reps(ctx, reps, est);
+            nwarm[i] = std::max(0, warmup - 1 + cached[i]);
+        }
+    };
     // Gated stream timing (mode 2): each trial's warm-ups and timed launches
     // (between its own events) are queued behind a device gate of at most 64
     // launches, so the launch queue never fills while a gate holds the
@@ -2049,7 +2077,7 @@ int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nk
         gate_open = false;
     };
     auto enqueue_timed = [&](int i) -> int {
-        const int need = std::max(0, warmup - 1 + cached[i]) + nreps[i];
+        const int need = nwarm[i] + nreps[i];
         // the first gate holds one trial, so the device starts while the
         // host queues the rest (queueing a trial takes less host time than
         // running it); a trial never straddles two gates
@@ -2059,7 +2087,7 @@ int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nk
             if (gst2) return gst2 < 0 ? gst2 : OPEVO_ERR_CUDA;
         }
         int st2 = OPEVO_OK;
-        for (int w = 0; w + 1 < warmup + cached[i] && !st2; ++w) st2 = launch_kernel(ks[i], msg(i), mlen());
+        for (int w = 0; w < nwarm[i] && !st2; ++w) st2 = launch_kernel(ks[i], msg(i), mlen());
         if (!st2 && g_cu.EventRecord(ev[4 * i + 2], ctx->stream) != CUDA_SUCCESS) st2 = OPEVO_ERR_CUDA;
         for (int r = 0; r < nreps[i] && !st2; ++r) st2 = launch_kernel(ks[i], msg(i), mlen());
         if (!st2 && g_cu.EventRecord(ev[4 * i + 3], ctx->stream) != CUDA_SUCCESS) st2 = OPEVO_ERR_CUDA;
@@ -2097,7 +2125,7 @@ int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nk
             if (status[i] != OPEVO_OK || !cached[i]) continue;
             const opevo_op::Verified& v = op->verified[vkey[i]];
             if (tol >= 0 && !(v.rel_err <= tol)) continue;       // judged (and failed) below
-            nreps[i] = capped_reps(reps, v.est_ms);
+            plan(i, v.est_ms);
             status[i] = enqueue_timed(i);
             early[i] = 1;
             if (status[i] < 0) fatal = status[i];
@@ -2146,14 +2174,15 @@ int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nk
             g_cu.EventElapsedTime(&est, ev[4 * i], ev[4 * i + 1]);
             // slow candidates are timed by their verified launch itself, so
             // only fast ones are remembered (a repeat of a slow one re-checks)
-            if (!slow_candidate(est) && tol >= 0) op->verified[vkey[i]] = opevo_op::Verified{rel, est};
+            if (!slow_candidate(ctx, est) && tol >= 0) op->verified[vkey[i]] = opevo_op::Verified{rel, est};
         }
-        if (slow_candidate(est)) {
+        if (slow_candidate(ctx, est)) {
             res[i].ms = est;
             timed[i] = 1;
             continue;
         }
-        nreps[i] = capped_reps(reps, est);
+        if (op->best_est_ms <= 0.f || est < op->best_est_ms) op->best_est_ms = est;
+        if (!early[i]) plan(i, est);
         if (mode == 0 && nreps[i] != greps[i]) {
             remember(i);                                 // keep the full-length graph too
             greps[i] = nreps[i];
@@ -2174,7 +2203,7 @@ int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nk
         for (int i = 0; i < count; ++i) {
             if (status[i] != OPEVO_OK || timed[i]) continue;
             int wst = OPEVO_OK;
-            for (int w = 0; w + 1 < warmup + cached[i] && !wst; ++w) wst = launch_kernel(ks[i], msg(i), mlen());
+            for (int w = 0; w < nwarm[i] && !wst; ++w) wst = launch_kernel(ks[i], msg(i), mlen());
             if (wst) {
                 status[i] = wst;
                 if (wst < 0) { fatal = wst; break; }
@@ -2231,7 +2260,7 @@ int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nk
     } else if (!fatal) {
         for (int i = 0; i < count && !fatal; ++i) {
             if (status[i] != OPEVO_OK || timed[i]) continue;
-            for (int w = 0; w + 1 < warmup + cached[i] && status[i] == OPEVO_OK; ++w)
+            for (int w = 0; w < nwarm[i] && status[i] == OPEVO_OK; ++w)
                 status[i] = launch_kernel(ks[i], msg(i), mlen());
             if (status[i] != OPEVO_OK) {
                 if (status[i] < 0) fatal = status[i];
@@ -2290,6 +2319,14 @@ int opevo_op_preload(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
     if (compile_ms) *compile_ms = cms;
     if (cache_hit) *cache_hit = hit;
     return st;
+}
+
+int opevo_ctx_set_timing(opevo_ctx* ctx, double budget_ms, double loser_ratio, int loser_reps) {
+    if (!ctx || loser_reps < 1) return OPEVO_ERR_ARG;
+    ctx->budget_ms = budget_ms;
+    ctx->loser_ratio = loser_ratio;
+    ctx->loser_reps = loser_reps;
+    return OPEVO_OK;
 }
 
 int opevo_ctx_flush_l2(opevo_ctx* ctx, char* err, size_t errlen) {
