@@ -476,7 +476,13 @@ def main() -> None:
     # uploaded operands -- and the verification results read back
     e2e = None
     if not args.no_e2e:
-        op = local_ev.op
+        # a freshly prepared operand too: nothing the main search learnt on
+        # the device (verified instances, the straggler rule's fastest
+        # launch) carries over into the replayed generations
+        from paper_2006_05664_b200.evaluator import _op_args
+
+        main_op = local_ev.op
+        op = local_ev.op = local_ev.dev.prepare(dtype=settings.dtype, seed=settings.seed, **_op_args(spec))
         pa, pb = capi.PinnedBuffer(op.a_bytes), capi.PinnedBuffer(op.b_bytes)
         # stage the device operands in pinned host memory once (untimed)
         op.read_inputs(pa.ptr, pb.ptr)
@@ -508,6 +514,8 @@ def main() -> None:
                        "re-verified), compare results read back"}
         pa.close()
         pb.close()
+        local_ev.op = main_op
+        op.close()
 
     # ---------------- best kernel: re-time live (roofline.achieved)
     pk = peaks()
@@ -628,13 +636,14 @@ def main() -> None:
         dist.destroy_process_group()
 
 
-def cold_cache_record(spec, space, settings, device: int, args, max_gens: int = 6,
-                      max_s: float = 30.0) -> dict:
+def cold_cache_record(spec, space, settings, device: int, args, budget: int = 500,
+                      max_s: float = 40.0) -> dict:
     """trials/s with an EMPTY cubin cache: a fresh
     evaluator compiles every instance it meets with NVRTC on a host pool of
-    os.cpu_count() threads; a fresh search (same seed) runs up to `max_gens`
-    generations or `max_s` seconds, wall-clock timed (compilation is host
-    work)."""
+    os.cpu_count() threads; a fresh search (same seed) runs `budget` trials
+    or `max_s` seconds, wall-clock timed (compilation is host work).  The
+    first generations are mostly infeasible configurations (nothing to
+    compile), so a short run would overstate the cold rate."""
     import dataclasses
     import shutil
     import tempfile
@@ -647,8 +656,7 @@ def cold_cache_record(spec, space, settings, device: int, args, max_gens: int = 
     cs = dataclasses.replace(settings, cache_dir=tmp, preload_family=False, compile_threads=threads)
     ev = GpuEvaluator(spec, space, device, cs)
     try:
-        eng = OpEvo(space, EngineConfig(seed=args.seed, budget=RHO * max_gens, parents=RHO,
-                                        offspring=RHO))
+        eng = OpEvo(space, EngineConfig(seed=args.seed, budget=budget, parents=RHO, offspring=RHO))
         trials = 0
         t0 = time.perf_counter()
         while time.perf_counter() - t0 < max_s:
@@ -661,6 +669,7 @@ def cold_cache_record(spec, space, settings, device: int, args, max_gens: int = 
         return {"value": trials / wall if wall > 0 else 0.0, "unit": "trials/s", "trials": trials,
                 "wall_s": wall, "instances_compiled": len(os.listdir(tmp)),
                 "nvrtc_pool_threads": threads, "timing": "host wall clock (NVRTC is host work)",
+                "valid_trials": sum(h.status == "ok" for h in ev.history),
                 "best_tflops": max((h.fitness for h in ev.history), default=0.0)}
     finally:
         ev.close()
