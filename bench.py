@@ -346,6 +346,8 @@ def main() -> None:
                     help="do not load the cached kernel family into the context before timing")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-cold", action="store_true", help="skip the cold-kernel-cache sub-record")
+    ap.add_argument("--python-ask", action="store_true",
+                    help="propose with the Python engine instead of the native core (same proposals)")
     ap.add_argument("--log", default="")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -408,8 +410,14 @@ def main() -> None:
         return sum(int(e.get("launches", 0)) + (1 if e.get("status") in ("ok", "verify_failed")
                                                 and not e.get("verify_cached") else 0) for e in extras)
 
+    from paper_2006_05664_b200.native import NativeOpEvo
+
     def new_search(budget: int):
-        return (OpEvo(space, EngineConfig(seed=args.seed, budget=budget, parents=RHO, offspring=RHO)),
+        # the C++ proposal core (csrc/search.cpp): the reference's proposals,
+        # bit for bit, in microseconds (tests/test_native_search.py)
+        engine_cls = OpEvo if args.python_ask else NativeOpEvo
+        return (engine_cls(space, EngineConfig(seed=args.seed, budget=budget, parents=RHO,
+                                               offspring=RHO)),
                 TrialRecorder(space))
 
     def generation(eng, rec, upload=None, tally=None) -> int:
@@ -587,6 +595,7 @@ def main() -> None:
                                       and args.dtype == "bf16" else ""),
                        "operator": args.op, "rho": RHO, "lambda": RHO, "q": 0.5,
                        "seed": args.seed, "trials_timed": trials, "search_budget": budget,
+                       "ask": "python" if args.python_ask else "native (csrc/search.cpp)",
                        "space": ("reference operator space (fp32 SIMT family)" if args.dtype == "f32"
                                  else "reference operator space + stages (mapping.py)"),
                        "fitness_timing": (f"{settings.reps} back-to-back launches in one CUDA graph"

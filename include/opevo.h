@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define OPEVO_ABI_VERSION 4   /* 4: OPEVO_F32_TF32X3, verification cache; 3: 13-slot knobs, trial batch */
+#define OPEVO_ABI_VERSION 5   /* 5: timing policy, native search core; 4: OPEVO_F32_TF32X3, verification cache */
 
 enum opevo_status {
     OPEVO_OK = 0,
@@ -227,6 +227,56 @@ int opevo_ctx_flush_l2(opevo_ctx* ctx, char* err, size_t errlen);
 /* Pinned host memory for honest end-to-end copies. */
 void* opevo_host_alloc(size_t bytes);
 void opevo_host_free(void* p);
+
+/* ------------------------------------------------------------------------
+ * Native OpEvo proposal core (host only, no device).  Replaces the Python
+ * ask path of the reference -- OpEvo._initial_batch / _offspring_batch,
+ * recombine, mutate / sample_walk, the four neighbour relations and unrank,
+ * the archive ranking (pkg/src/topotune/engine.py:73-261, walk.py:41-59,
+ * spaces.py:71-84, 189-221, 266-289, 334-342, 385-387) -- drawing from
+ * numpy's Generator(PCG64) stream exactly as the reference does, so its
+ * proposals are the reference's bit for bit under the same told fitness.
+ * A configuration crosses the ABI as int64 "slots": a factorization value
+ * is its factor tuple, a permutation value its item indices, a discrete /
+ * categorical value its index in the declared list.
+ * ---------------------------------------------------------------------- */
+enum opevo_param_kind {
+    OPEVO_PARAM_FACTORIZATION = 0,   /* a = product, arity = tuple length   */
+    OPEVO_PARAM_DISCRETE = 1,        /* a = number of values (a path graph)  */
+    OPEVO_PARAM_CATEGORICAL = 2,     /* a = number of labels (complete graph) */
+    OPEVO_PARAM_PERMUTATION = 3      /* a = number of items (<= 20)          */
+};
+#define OPEVO_SEARCH_WALK_LIMIT (-10)   /* a q-walk did not stop within 1e6 steps */
+
+typedef struct opevo_search opevo_search;
+
+int opevo_search_create(int nparams, const int32_t* kinds, const int64_t* a, const int32_t* arity,
+                        int parents, int offspring, double q, int retry_cap, opevo_search** out);
+void opevo_search_destroy(opevo_search* s);
+/* int64 slots per configuration (sum of the parameters' arities) */
+int opevo_search_slots(const opevo_search* s);
+/* numpy PCG64 state: st = {state hi, state lo, inc hi, inc lo}, plus the
+ * buffered upper 32-bit half (has_uint32, uinteger) */
+int opevo_search_set_rng(opevo_search* s, const uint64_t st[4], int has_uint32, uint32_t uinteger);
+int opevo_search_get_rng(const opevo_search* s, uint64_t st[4], int* has_uint32, uint32_t* uinteger);
+/* Up to `want` proposals of the pending batch into out[want][slots]:
+ * initial = 1 for the first batch (uniform draws, deduplicated in-batch),
+ * else offspring of the archive's top `parents` (deduplicated against the
+ * archive and the batch); first = 1 starts a new batch.  Returns how many
+ * were made; *need_fallback = 1 when the next one exhausted the retry cap:
+ * the caller draws it with sample_unvisited from this RNG state (get_rng /
+ * set_rng around it), records it with opevo_search_add_pending and calls
+ * again for the rest. */
+int opevo_search_propose(opevo_search* s, int initial, int first, int want, int64_t* out,
+                         int* need_fallback);
+int opevo_search_add_pending(opevo_search* s, const int64_t* slots);
+/* Insert evaluated configurations in ask order (ranked by fitness, ties by
+ * insertion); ends the pending batch. */
+int opevo_search_tell(opevo_search* s, int n, const int64_t* slots, const double* fitness);
+/* RNG primitives (tests of the stream contract) */
+int opevo_search_uniform_int(opevo_search* s, uint64_t n, uint64_t* out);
+int opevo_search_random(opevo_search* s, double* out);
+double opevo_search_np_sum(const double* a, size_t n);
 
 #ifdef __cplusplus
 }

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libopevo.so")
 DEFAULT_CACHE = os.path.join(HERE, "kernel_cache")
 
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 # status codes (opevo.h)
 OK = 0
