@@ -51,6 +51,10 @@ EXPORTS = (
     "opevo_kernel_run", "opevo_kernel_check", "opevo_kernel_time", "opevo_trial",
     "opevo_kernel_trace", "opevo_ctx_flush_l2", "opevo_host_alloc", "opevo_host_free",
     "opevo_op_preload", "opevo_trial_batch", "opevo_ctx_set_timing",
+    # native OpEvo proposal core (bound in native.py)
+    "opevo_search_create", "opevo_search_destroy", "opevo_search_slots", "opevo_search_set_rng",
+    "opevo_search_get_rng", "opevo_search_propose", "opevo_search_add_pending", "opevo_search_tell",
+    "opevo_search_uniform_int", "opevo_search_random", "opevo_search_np_sum",
 )
 MAX_BATCH = 64
 
