@@ -377,8 +377,12 @@ def main() -> None:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group("gloo")
-    coll_device = torch.device("cuda", local) if backend == "nccl" else None
+    # the per-generation exchange, the barriers and the max over ranks run on
+    # a host (gloo) group: no CUDA context is involved, so a rank whose
+    # context a faulting candidate poisoned still takes part
+    exch = (dist.new_group(backend="gloo") if backend == "nccl" else None) if world > 1 else None
     from paper_2006_05664_b200 import capi
+    from paper_2006_05664_b200.scheduler import ProcessEvaluator
 
     spec = parse_operator(args.op)
     space = gpu_operator_space(spec, args.dtype)
@@ -387,20 +391,31 @@ def main() -> None:
                             dtype=DTYPES[args.dtype], loser_ratio=args.loser_ratio)
     local_ev = GpuEvaluator(spec, space, local, settings)
     if world > 1:
-        evaluator = ShardedEvaluator(local_ev, rank, world, device=coll_device)
+        evaluator = ShardedEvaluator(local_ev, rank, world, group=exch,
+                                     respawn=lambda: ProcessEvaluator(spec, space, local, settings))
     else:
         evaluator = local_ev.evaluate
 
+    def poisoned() -> bool:
+        return bool(getattr(evaluator, "poisoned", False))
+
+    def flush():
+        if world > 1:
+            evaluator.flush_l2()        # the worker process's after a fault
+        else:
+            local_ev.dev.flush_l2()
+
     def barrier():
         if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
+            dist.barrier(group=exch)
+        if not poisoned():
+            torch.cuda.synchronize()
 
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=coll_device or "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=exch)
         return float(t.item())
 
     def launches_of(extras) -> int:
@@ -454,13 +469,23 @@ def main() -> None:
         e0.record()
         t_wall0 = time.perf_counter()
         for _ in range(args.steps):
-            local_ev.dev.flush_l2()     # every step starts with a cold L2
+            flush()                     # every step starts with a cold L2
             trials += generation(engine, recorder, tally=tally)
         barrier()
-        e1.record()
-        torch.cuda.synchronize()
         wall = time.perf_counter() - t_wall0
-    sec = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+        timing = "cuda events (max over ranks)"
+        try:
+            if poisoned():
+                raise RuntimeError("context poisoned")
+            e1.record()
+            torch.cuda.synchronize()
+            local_sec = e0.elapsed_time(e1) / 1e3
+        except RuntimeError:
+            # a faulting candidate poisoned this rank's CUDA context mid-run
+            # (its evaluation moved to a worker process): events are gone
+            local_sec = wall
+            timing = f"host wall clock on rank {rank} (CUDA context poisoned by a faulting candidate)"
+    sec = max_over_ranks(local_sec)
     trials_per_s = trials / sec if sec > 0 else 0.0
     best_at_timed = engine.best().fitness if engine.archive else 0.0
     trials_at_timed = len(recorder.records)
@@ -472,10 +497,11 @@ def main() -> None:
             break
     records = recorder.records
     best = engine.best()
+    healthy = not poisoned()        # the measurements below need this process's context
 
     # ---------------- confirm the best instance: re-time the top distinct
     # instances (noise must not decide between near-equal kernels)
-    confirmed = local_ev.confirm_top(k=5, reps=100, rounds=5) if best.fitness > 0 else []
+    confirmed = local_ev.confirm_top(k=5, reps=100, rounds=5) if best.fitness > 0 and healthy else []
 
     # ---------------- e2e: the same generations (a fresh engine, same seed:
     # warm-ups untimed, then the K timed ones) through the public API, with
@@ -483,7 +509,7 @@ def main() -> None:
     # every trial is verified again, against a reference recomputed from the
     # uploaded operands -- and the verification results read back
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and healthy:
         # a freshly prepared operand too: nothing the main search learnt on
         # the device (verified instances, the straggler rule's fastest
         # launch) carries over into the replayed generations
@@ -500,14 +526,14 @@ def main() -> None:
 
         e_engine, e_rec = new_search(RHO * (args.warmup + args.steps))
         for _ in range(args.warmup):
-            local_ev.dev.flush_l2()
+            flush()
             generation(e_engine, e_rec, upload)
         barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record()
         e2e_trials = 0
         for _ in range(args.steps):
-            local_ev.dev.flush_l2()
+            flush()
             e2e_trials += generation(e_engine, e_rec, upload)
         barrier()
         f1.record()
@@ -567,7 +593,7 @@ def main() -> None:
     # cubin cache (every instance NVRTC-compiled on the host pool), a few
     # generations of a fresh search
     cold = None
-    if not args.no_cold and rank == 0 and world == 1:
+    if not args.no_cold and rank == 0 and world == 1 and healthy:
         cold = cold_cache_record(spec, space, settings, local, args)
 
     if rank == 0:
@@ -637,9 +663,13 @@ def main() -> None:
                                 "verified_trials_per_s": tally["verified"] / sec if sec > 0 else 0.0},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": tally["launches"],
             "cold_kernel_cache": cold,
+            "timing": timing,
+            "faulted_trials": sum(1 for r in records if (r.extra or {}).get("status") == "fault"),
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
+    if world > 1:
+        evaluator.close()
     local_ev.close()
     if world > 1:
         dist.destroy_process_group()

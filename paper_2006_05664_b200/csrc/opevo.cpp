@@ -319,6 +319,26 @@ std::string extra_flags() {
     return v ? v : "";
 }
 
+// Fault injection for the robustness tests (OPEVO_FAULT_KNOBS="bm,bn,bk,..."):
+// an instance whose knob vector starts with these values is compiled with
+// OPEVO_ABLATE=5, a `trap` at kernel entry -- the sticky fault that poisons
+// a CUDA context, as a broken candidate would.  Part of the cache key.
+std::string instance_flags(int family, const Knobs& k) {
+    std::string f = extra_flags();
+    const char* v = getenv("OPEVO_FAULT_KNOBS");
+    if (!v || !*v || family == 2) return f;
+    const int kv[OPEVO_NUM_KNOBS] = {k.bm, k.bn, k.bk, k.stages, k.split, k.cluster, k.tile_h, k.tile_w,
+                                     k.acc, k.cg, k.grid_mode, k.b_res, k.bpu};
+    std::istringstream in(v);
+    std::string tok;
+    int i = 0;
+    while (std::getline(in, tok, ',')) {
+        if (i >= OPEVO_NUM_KNOBS || atoi(tok.c_str()) != kv[i]) return f;
+        ++i;
+    }
+    return i ? f + " -DOPEVO_ABLATE=5" : f;
+}
+
 bool want_pdl() {
     const char* v = getenv("OPEVO_NO_PDL");
     return !(v && v[0] == '1');
@@ -327,7 +347,7 @@ bool want_pdl() {
 std::string make_key(int family, const Knobs& k, int batched, int out_f32) {
     static const uint64_t src_hash = fnv1a(opevo_gemm_source, strlen(opevo_gemm_source));
     static const uint64_t simt_hash = fnv1a(opevo_sgemm_source, strlen(opevo_sgemm_source));
-    const std::string extra = extra_flags();
+    const std::string extra = instance_flags(family, k);
     const uint64_t h = fnv1a(extra.data(), extra.size(), family == 2 ? simt_hash : src_hash);
     char buf[256];
     if (family == 2) {
@@ -537,7 +557,7 @@ int nvrtc_build(int family, const Knobs& k, int batched, int out_f32, std::vecto
         "-DOPEVO_HALO=" + std::to_string(halo_kw(k, family))};
     if (want_lineinfo()) opts.push_back("-lineinfo");
     {
-        std::istringstream extra(extra_flags());
+        std::istringstream extra(instance_flags(family, k));
         std::string tok;
         while (extra >> tok) opts.push_back(tok);
     }

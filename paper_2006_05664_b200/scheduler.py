@@ -15,9 +15,14 @@ Two drivers:
   same asks) and the only exchange is one small ``all_reduce`` of the
   per-trial result rows per generation.
 * :class:`TrialScheduler` -- one controller process with a worker *process*
-  per GPU.  A worker whose CUDA context is poisoned by a faulting candidate
-  (``WorkerFault``) is replaced and the rest of its shard re-submitted; the
-  faulting configuration scores 0, like any invalid configuration.
+  per GPU, each running its whole shard as one trial-batch pipeline.  A
+  worker whose CUDA context is poisoned by a faulting candidate
+  (``WorkerFault``) is replaced and its shard re-run one configuration at a
+  time; the faulting configuration scores 0, like any invalid one.
+
+Both survive a faulting candidate: :class:`ShardedEvaluator` moves a rank
+whose context was poisoned onto a worker process (:class:`ProcessEvaluator`)
+and exchanges results over a host (gloo) group.
 """
 
 from __future__ import annotations
@@ -32,7 +37,7 @@ from .spaces import SearchSpace
 
 # result row layout for the all-reduce
 _COLS = ("fitness", "device_ms", "compile_ms", "rel_err", "status", "cache_hit", "gpu_id", "present",
-         "launches")
+         "launches", "verify_cached", "abort")
 _STATUS = ("ok", "invalid_config", "compile_error", "launch_error", "verify_failed", "fault")
 
 
@@ -45,54 +50,8 @@ def shard_indices(n: int, world: int, rank: int) -> list[int]:
     return list(range(rank, n, world))
 
 
-class ShardedEvaluator:
-    """Batch evaluator for ``run(..., evaluator=...)`` under torch.distributed."""
-
-    def __init__(self, local: GpuEvaluator | None, rank: int, world: int, group=None,
-                 device=None, local_fn=None):
-        self.local = local
-        self.local_fn = local_fn            # testing hook: configs -> list[TrialInfo]
-        self.rank, self.world = rank, world
-        self.group = group
-        self.device = device                # torch device for the collective tensor
-        self.last_extras: list[dict] = []
-
-    def _local_infos(self, configs: list[tuple]) -> list[TrialInfo]:
-        if self.local_fn is not None:
-            return self.local_fn(configs)
-        return self.local.evaluate_infos(configs)
-
-    def __call__(self, configs: list[tuple]) -> list[float]:
-        import torch
-        import torch.distributed as dist
-
-        mine = shard_indices(len(configs), self.world, self.rank)
-        infos = self._local_infos([configs[i] for i in mine]) if mine else []
-        rows = torch.zeros((len(configs), len(_COLS)), dtype=torch.float64)
-        for i, info in zip(mine, infos):
-            rows[i] = torch.tensor([info.fitness, info.ms, info.compile_ms, info.rel_err,
-                                    _status_code(info.status), info.cache_hit, self.rank, 1.0,
-                                    info.launches], dtype=torch.float64)
-        if self.device is not None:
-            rows = rows.to(self.device)
-        dist.all_reduce(rows, group=self.group)
-        rows = rows.cpu()
-        if not bool((rows[:, 7] == 1.0).all()):
-            raise FatalEvaluationError("a trial was evaluated by zero or several ranks")
-        self.last_extras = []
-        fits = []
-        for r in rows.tolist():
-            code = int(r[4])
-            self.last_extras.append({"status": _STATUS[code] if code < len(_STATUS) else "error",
-                                     "device_ms": r[1], "compile_ms": r[2], "rel_err": r[3],
-                                     "cache_hit": int(r[5]), "gpu_id": int(r[6]),
-                                     "launches": int(r[8])})
-            fits.append(r[0])
-        return fits
-
-
 # ----------------------------------------------------------------------------
-# process-pool scheduler
+# worker process: one GpuEvaluator, a whole shard per message
 # ----------------------------------------------------------------------------
 
 def _worker_main(conn, spec, space_json, device, settings_dict):
@@ -107,26 +66,39 @@ def _worker_main(conn, spec, space_json, device, settings_dict):
         msg = conn.recv()
         if msg is None:
             break
-        idx, config = msg
         try:
-            info = ev.evaluate_infos([config])[0]
-            conn.send(("result", idx, asdict(info)))
+            if msg[0] == "batch":
+                conn.send(("infos", [asdict(i) for i in ev.evaluate_infos(list(msg[1]))]))
+            elif msg[0] == "flush":
+                ev.dev.flush_l2()
+                conn.send(("ok",))
+            else:
+                conn.send(("error", f"unknown request {msg[0]!r}"))
         except WorkerFault as err:
-            conn.send(("fault", idx, str(err)))
+            conn.send(("fault", str(err)))
             return
         except FatalEvaluationError as err:
             conn.send(("fatal", str(err)))
             return
         except Exception:   # noqa: BLE001
-            conn.send(("error", idx, traceback.format_exc(limit=3)))
+            conn.send(("error", traceback.format_exc(limit=3)))
     ev.close()
 
 
 class _Worker:
+    """A GPU worker process.  ``evaluate`` sends a whole shard in one message
+    (the process runs it as one ``opevo_trial_batch`` pipeline); when the
+    shard faults -- a candidate poisoned the worker's CUDA context, and the
+    batch does not say which -- the worker is replaced and the shard is
+    re-run one configuration per message, so exactly the faulting
+    candidates score 0 (status "fault", the reference's failure-to-0
+    semantics, engine.py:276-285) and each costs one more respawn."""
+
     def __init__(self, ctx, spec, space, device, settings):
         self.device = device
         self.args = (spec, space.to_json(), device, asdict(settings))
         self.ctx = ctx
+        self.respawns = 0
         self.start()
 
     def start(self):
@@ -138,6 +110,13 @@ class _Worker:
         if msg[0] != "ready":
             raise FatalEvaluationError(f"GPU worker {self.device} failed to start: {msg[1]}")
 
+    def respawn(self):
+        self.proc.join(timeout=10)
+        if self.proc.is_alive():
+            self.proc.kill()
+        self.start()
+        self.respawns += 1
+
     def stop(self):
         try:
             self.conn.send(None)
@@ -147,9 +126,187 @@ class _Worker:
         if self.proc.is_alive():
             self.proc.kill()
 
+    def send_batch(self, configs: list[tuple]) -> None:
+        self.conn.send(("batch", list(configs)))
+
+    def _recv(self):
+        try:
+            return self.conn.recv()
+        except EOFError:
+            return ("fault", "worker died")
+
+    def finish_batch(self, configs: list[tuple]) -> list[TrialInfo]:
+        """Result of the batch sent with ``send_batch`` (isolating faults)."""
+        msg = self._recv()
+        if msg[0] == "infos":
+            return [TrialInfo(**d) for d in msg[1]]
+        if msg[0] == "fatal":
+            raise FatalEvaluationError(f"GPU worker {self.device}: {msg[1]}")
+        if msg[0] == "error":
+            raise FatalEvaluationError(f"GPU worker {self.device}: {msg[1]}")
+        # fault: replace the worker and find the faulting candidate(s)
+        self.respawn()
+        if len(configs) == 1:
+            return [TrialInfo(0.0, "fault", message=str(msg[1])[:200])]
+        out = []
+        for c in configs:
+            self.send_batch([c])
+            out.extend(self.finish_batch([c]))
+        return out
+
+    def evaluate(self, configs: list[tuple]) -> list[TrialInfo]:
+        self.send_batch(configs)
+        return self.finish_batch(configs)
+
+    def flush_l2(self) -> None:
+        self.conn.send(("flush",))
+        msg = self._recv()
+        if msg[0] != "ok":
+            if msg[0] == "fault":
+                self.respawn()
+            else:
+                raise FatalEvaluationError(f"GPU worker {self.device}: {msg[1]}")
+
+
+class ProcessEvaluator:
+    """``GpuEvaluator``'s batch interface served by a worker process (a fresh
+    CUDA context that a faulting candidate cannot take down with the caller)."""
+
+    def __init__(self, spec, space: SearchSpace, device: int = 0,
+                 settings: EvalSettings | None = None):
+        self.device_index = device
+        self.worker = _Worker(mp.get_context("spawn"), spec, space, device, settings or EvalSettings())
+        self.last_extras: list[dict] = []
+        self.history: list[TrialInfo] = []
+
+    def evaluate_infos(self, configs: list[tuple]) -> list[TrialInfo]:
+        infos = self.worker.evaluate(configs) if configs else []
+        self.history.extend(infos)
+        return infos
+
+    def evaluate(self, configs: list[tuple]) -> list[float]:
+        infos = self.evaluate_infos(configs)
+        self.last_extras = [i.as_extra(self.device_index) for i in infos]
+        return [i.fitness for i in infos]
+
+    @property
+    def respawns(self) -> int:
+        return self.worker.respawns
+
+    def flush_l2(self) -> None:
+        self.worker.flush_l2()
+
+    def close(self) -> None:
+        self.worker.stop()
+
+
+# ----------------------------------------------------------------------------
+# one process per GPU (torchrun)
+# ----------------------------------------------------------------------------
+
+class ShardedEvaluator:
+    """Batch evaluator for ``run(..., evaluator=...)`` under torch.distributed.
+
+    The per-generation exchange is one ``all_reduce`` of a small host tensor
+    over ``group`` (a gloo group: no CUDA context is involved, so a rank
+    whose context a faulting candidate poisoned still takes part).  On such
+    a fault (``WorkerFault``) the rank moves its evaluation to a worker
+    process (:class:`ProcessEvaluator`, a fresh context), which re-runs the
+    shard with the faulting candidate isolated and scored 0; the other ranks
+    never notice.  A fatal error on any rank (no device, NVRTC missing) sets
+    the row's abort flag and every rank raises it after the exchange, so no
+    rank is left waiting in the collective."""
+
+    def __init__(self, local: GpuEvaluator | None, rank: int, world: int, group=None,
+                 device=None, local_fn=None, respawn=None):
+        self.local = local
+        self.local_fn = local_fn            # testing hook: configs -> list[TrialInfo]
+        self.rank, self.world = rank, world
+        self.group = group
+        self.device = device                # unused (kept for callers); the exchange is on host
+        # () -> a replacement evaluator after a fault, e.g.
+        # lambda: ProcessEvaluator(spec, space, device, settings)
+        self.respawn = respawn
+        self.fallback = None
+        self.poisoned = False               # this process's CUDA context is unusable
+        self.faults = 0
+        self.last_extras: list[dict] = []
+
+    def _local_infos(self, configs: list[tuple]) -> list[TrialInfo]:
+        if self.fallback is not None:
+            return self.fallback.evaluate_infos(configs)
+        if self.local_fn is not None:
+            return self.local_fn(configs)
+        return self.local.evaluate_infos(configs)
+
+    def flush_l2(self) -> None:
+        if self.fallback is not None:
+            self.fallback.flush_l2()
+        elif self.local is not None and not self.poisoned:
+            self.local.dev.flush_l2()
+
+    def __call__(self, configs: list[tuple]) -> list[float]:
+        import torch
+        import torch.distributed as dist
+
+        mine = shard_indices(len(configs), self.world, self.rank)
+        abort_msg = ""
+        infos: list[TrialInfo] = []
+        try:
+            infos = self._local_infos([configs[i] for i in mine]) if mine else []
+        except WorkerFault as err:
+            self.poisoned = True
+            self.faults += 1
+            if self.respawn is None:
+                abort_msg = str(err)
+            else:
+                try:
+                    self.fallback = self.respawn()
+                    infos = self.fallback.evaluate_infos([configs[i] for i in mine])
+                except FatalEvaluationError as err2:
+                    abort_msg = str(err2)
+        except FatalEvaluationError as err:
+            abort_msg = str(err)
+        rows = torch.zeros((len(configs), len(_COLS)), dtype=torch.float64)
+        for i, info in zip(mine, infos):
+            rows[i] = torch.tensor([info.fitness, info.ms, info.compile_ms, info.rel_err,
+                                    _status_code(info.status), info.cache_hit, self.rank, 1.0,
+                                    info.launches, info.verify_cached, 0.0], dtype=torch.float64)
+        if abort_msg:
+            rows[mine, 7] = 1.0
+            rows[mine, 10] = 1.0 + self.rank
+        dist.all_reduce(rows, group=self.group)
+        if bool((rows[:, 10] > 0).any()):
+            culprit = int(rows[:, 10].max().item()) - 1
+            raise FatalEvaluationError(f"rank {culprit} aborted the generation"
+                                       + (f": {abort_msg}" if abort_msg else ""))
+        if not bool((rows[:, 7] == 1.0).all()):
+            raise FatalEvaluationError("a trial was evaluated by zero or several ranks")
+        self.last_extras = []
+        fits = []
+        for r in rows.tolist():
+            code = int(r[4])
+            self.last_extras.append({"status": _STATUS[code] if code < len(_STATUS) else "error",
+                                     "device_ms": r[1], "compile_ms": r[2], "rel_err": r[3],
+                                     "cache_hit": int(r[5]), "gpu_id": int(r[6]),
+                                     "launches": int(r[8]), "verify_cached": int(r[9])})
+            fits.append(r[0])
+        return fits
+
+    def close(self) -> None:
+        if self.fallback is not None:
+            self.fallback.close()
+
+
+# ----------------------------------------------------------------------------
+# single controller, one worker process per GPU
+# ----------------------------------------------------------------------------
 
 class TrialScheduler:
-    """Evaluate batches over several GPUs with one worker process each."""
+    """Evaluate batches over several GPUs with one worker process each: every
+    worker gets its round-robin shard as one message (one trial-batch
+    pipeline per GPU), all shards run at once, results come back in ask
+    order; a faulting shard is isolated and its worker replaced."""
 
     def __init__(self, spec, space: SearchSpace, devices: list[int],
                  settings: EvalSettings | None = None):
@@ -158,7 +315,10 @@ class TrialScheduler:
         ctx = mp.get_context("spawn")
         self.workers = [_Worker(ctx, spec, space, d, self.settings) for d in devices]
         self.last_extras: list[dict] = []
-        self.respawns = 0
+
+    @property
+    def respawns(self) -> int:
+        return sum(w.respawns for w in self.workers)
 
     def close(self):
         for w in self.workers:
@@ -172,41 +332,18 @@ class TrialScheduler:
 
     def __call__(self, configs: list[tuple]) -> list[float]:
         n = len(configs)
-        results: list[dict | None] = [None] * n
-        queues = [shard_indices(n, len(self.workers), r) for r in range(len(self.workers))]
-        busy = {}
-        for w, q in zip(self.workers, queues):
-            if q:
-                i = q.pop(0)
-                w.conn.send((i, configs[i]))
-                busy[w] = (i, q)
-        while busy:
-            ready = mp.connection.wait([w.conn for w in busy])
-            for w in [w for w in list(busy) if w.conn in ready]:
-                i, q = busy.pop(w)
-                try:
-                    msg = w.conn.recv()
-                except EOFError:
-                    msg = ("fault", i, "worker died")
-                if msg[0] == "result":
-                    results[i] = msg[2]
-                elif msg[0] in ("fault", "error"):
-                    results[i] = asdict(TrialInfo(0.0, "fault", message=str(msg[2])[:200]))
-                    if msg[0] == "fault":
-                        w.proc.join(timeout=10)
-                        w.start()
-                        self.respawns += 1
-                else:
-                    raise FatalEvaluationError(f"GPU worker {w.device}: {msg[1]}")
-                if q:
-                    j = q.pop(0)
-                    w.conn.send((j, configs[j]))
-                    busy[w] = (j, q)
+        shards = [shard_indices(n, len(self.workers), r) for r in range(len(self.workers))]
+        for w, idx in zip(self.workers, shards):
+            if idx:
+                w.send_batch([configs[i] for i in idx])
+        results: list[TrialInfo | None] = [None] * n
+        for w, idx in zip(self.workers, shards):
+            if idx:
+                for i, info in zip(idx, w.finish_batch([configs[i] for i in idx])):
+                    results[i] = info
         self.last_extras = []
         fits = []
-        for i, r in enumerate(results):
-            gpu = self.workers[i % len(self.workers)].device
-            info = TrialInfo(**r)
-            self.last_extras.append(info.as_extra(gpu))
+        for i, info in enumerate(results):
+            self.last_extras.append(info.as_extra(self.workers[i % len(self.workers)].device))
             fits.append(info.fitness)
         return fits

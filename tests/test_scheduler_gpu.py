@@ -73,3 +73,47 @@ def test_trapping_candidates_are_isolated_and_the_worker_respawned():
     assert all(f == 0.0 for f in fits)
     assert any(e["status"] == "fault" for e in extras)
     assert again == [0.0]
+
+
+def test_two_rank_gloo_bench_survives_a_trapping_candidate(tmp_path):
+    """bench.py on two ranks (gloo exchange, both on GPU 0) with one kernel
+    instance built to trap (OPEVO_FAULT_KNOBS, a sticky fault that poisons
+    the evaluating rank's CUDA context): the run completes, the faulting
+    trial scores 0 with status "fault", and the faulted rank carries on in
+    a worker process."""
+    import json
+    import socket
+    import subprocess
+    import sys
+
+    from paper_2006_05664_b200 import EngineConfig
+    from paper_2006_05664_b200.mapping import config_to_knobs, gpu_operator_space
+    from paper_2006_05664_b200.native import NativeOpEvo
+    from paper_2006_05664_b200.operators import MatMulSpec
+
+    spec = MatMulSpec(1024, 1024, 1024)
+    space = gpu_operator_space(spec)
+    # a seed whose first (uniform, fitness-independent) batch holds a valid
+    # configuration: its instance is the one built to trap
+    for seed in range(200):
+        first = NativeOpEvo(space, EngineConfig(seed=seed, budget=64)).ask().configs
+        valid = [config_to_knobs(spec, space, c) for c in first]
+        valid = [m for m in valid if m.valid]
+        if valid:
+            break
+    knobs = ",".join(map(str, valid[0].knobs.as_tuple()))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, OPEVO_DIST_BACKEND="gloo", OPEVO_FAULT_KNOBS=knobs)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={port}", "bench.py", "--gpus", "2",
+           "--steps", "6", "--warmup", "3", "--budget", "96", "--seed", str(seed), "--no-e2e",
+           "--no-cpu", "--no-cold"]
+    out = subprocess.run(cmd, cwd=repo, env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, (out.stdout[-2000:], out.stderr[-4000:])
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["faulted_trials"] >= 1
+    assert line["trials_total"] == 96 and line["value"] > 0
