@@ -462,11 +462,14 @@ def main() -> None:
 
     # ---------------- timed region: K generations, device-timed, max over ranks
     barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     trials = 0
     tally = {"launches": 0, "valid": 0, "verified": 0, "instances": set()}
+    e0 = e1 = None
+    if not poisoned():
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
-        e0.record()
+        if e0 is not None:
+            e0.record()
         t_wall0 = time.perf_counter()
         for _ in range(args.steps):
             flush()                     # every step starts with a cold L2
@@ -475,7 +478,7 @@ def main() -> None:
         wall = time.perf_counter() - t_wall0
         timing = "cuda events (max over ranks)"
         try:
-            if poisoned():
+            if poisoned() or e0 is None:
                 raise RuntimeError("context poisoned")
             e1.record()
             torch.cuda.synchronize()

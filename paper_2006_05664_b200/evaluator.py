@@ -104,15 +104,19 @@ class GpuEvaluator:
     """Objective + batch evaluator bound to one operator on one B200."""
 
     def __init__(self, spec: OperatorSpec, space: SearchSpace | None = None, device: int = 0,
-                 settings: EvalSettings | None = None):
+                 settings: EvalSettings | None = None, dev: "capi.Device | None" = None):
         self.spec = spec
         self.settings = settings or EvalSettings()
         self.dtype = DTYPE_NAMES[self.settings.dtype]
         self.space = space if space is not None else gpu_operator_space(spec, self.dtype)
         self.device_index = device
         self.tol = F32_TOL if self.settings.dtype in capi.FP32_OUT else BF16_TOL
+        # `dev`: share an existing context (its loaded kernel modules); this
+        # evaluator then owns only its operand, verification record and
+        # timing state (the projection tool runs one per simulated rank)
+        self._owns_dev = dev is None
         try:
-            self.dev = capi.Device(device, self.settings.cache_dir)
+            self.dev = dev if dev is not None else capi.Device(device, self.settings.cache_dir)
             self.op = self.dev.prepare(dtype=self.settings.dtype, seed=self.settings.seed,
                                        **_op_args(spec))
             self.dev.set_timing(self.settings.budget_ms, self.settings.loser_ratio,
@@ -134,7 +138,8 @@ class GpuEvaluator:
             self.op.close()
             self.op = None
         if getattr(self, "dev", None) is not None:
-            self.dev.close()
+            if getattr(self, "_owns_dev", True):
+                self.dev.close()
             self.dev = None
 
     # -- the reference objective contract -----------------------------------

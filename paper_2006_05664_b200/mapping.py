@@ -12,9 +12,11 @@ configuration          B200 kernel knob
 ``n[0]``, ``m[0]``     CTA grid; CTA tile ``BM = N / n[0]``, ``BN = M / m[0]``
                        (UMMA shape: BM in {128, 256 = two M=128 atoms},
                        BN multiple of 16 in [16, 256])
-``m[1]``               cluster level: CTAs of a cluster along the column-tile axis
-                       that share one TMA-multicast A tile,
-                       ``cluster = largest c in {4, 2, 1} dividing m[1] and m[0]``
+``m[1]``               with OPEVO_MAP_MULTICAST=1 only: CTAs of a cluster along the
+                       column-tile axis that share one TMA-multicast A tile,
+                       ``cluster = largest c in {4, 2, 1} dividing m[1] and m[0]``;
+                       by default canonicalised away like ``n[2..3]`` (see
+                       ``_multicast_enabled``)
 ``n[1..3]``, ``m[2..3]`` the warp/thread split of the CTA tile: no tcgen05 counterpart
                        (canonicalised away -- many configurations, one kernel)
 ``k[0]``               split-K factor (CTAs along K, in-kernel deterministic reduce)
@@ -200,6 +202,18 @@ def _fit_stages(want: int, bm: int, bn: int, bk: int, cta_group: int = 1, bpu: i
     return s
 
 
+def _multicast_enabled() -> bool:
+    """``m[1]`` -> A-multicast cluster only with OPEVO_MAP_MULTICAST=1.  Off by
+    default: multicast never won on any BASELINE operator (cluster <= 4
+    unicast loads of one tile are deduplicated in L2 anyway), and the extra
+    instance per ``m[1]`` parity made the landscape rugged -- at 1024^3, 6 of
+    8 seeds reached the best instance with it, 8 of 8 without
+    (profiles/round2/seeds/).  The library keeps the knob."""
+    import os
+
+    return os.environ.get("OPEVO_MAP_MULTICAST", "0") == "1"
+
+
 def _largest_pow2_divisor(*vals: int, cap: int = 4) -> int:
     c = cap
     while c > 1 and any(v % c for v in vals):
@@ -251,7 +265,8 @@ def _gemm_knobs(rows: int, cols: int, depth: int, vals: dict,
     stages = _fit_stages(int(vals.get("stages", 4)), bm, bn, bk, cta_group, bpu)
     if stages < 1:
         return None, "one stage does not fit in shared memory"
-    cluster = 1 if (cta_group == 2 or bpu > 1) else _largest_pow2_divisor(m[1], m[0])
+    cluster = (1 if (cta_group == 2 or bpu > 1 or not _multicast_enabled())
+               else _largest_pow2_divisor(m[1], m[0]))
     kn = Knobs(bm, bn, bk, stages, split, cluster, cta_group=cta_group, bpu=bpu,
                batched=int(bool(batch)))
     if kn.tma_split() and (rows // bm) * (cols // bn) * split > B200_SMS:

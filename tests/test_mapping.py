@@ -31,12 +31,16 @@ def test_gpu_space_extends_reference_space_in_json_format():
     assert SearchSpace.from_json(sp.to_json()).to_json() == sp.to_json()
 
 
-def test_matmul_mapping_levels():
+def test_matmul_mapping_levels(monkeypatch):
     spec = MatMulSpec(1024, 1024, 1024)
     sp = gpu_operator_space(spec)
     cfg = ((8, 2, 8, 8), (8, 4, 4, 8), (2, 8, 64), 4)
     m = config_to_knobs(spec, sp, cfg)
     assert m.valid
+    # default: m[1] does not select a multicast cluster
+    assert m.knobs == Knobs(bm=128, bn=128, bk=64, stages=4, split=2, cluster=1)
+    monkeypatch.setenv("OPEVO_MAP_MULTICAST", "1")
+    m = config_to_knobs(spec, sp, cfg)
     assert m.knobs == Knobs(bm=128, bn=128, bk=64, stages=4, split=2, cluster=4)
     # 256-row tile with an even row vthread split -> CTA pair
     pair = config_to_knobs(spec, sp, ((4, 2, 16, 8), (8, 4, 4, 8), (1, 16, 64), 4)).knobs

@@ -113,7 +113,8 @@ def test_two_rank_gloo_bench_survives_a_trapping_candidate(tmp_path):
            "--steps", "6", "--warmup", "3", "--budget", "96", "--seed", str(seed), "--no-e2e",
            "--no-cpu", "--no-cold"]
     out = subprocess.run(cmd, cwd=repo, env=env, capture_output=True, text=True, timeout=900)
-    assert out.returncode == 0, (out.stdout[-2000:], out.stderr[-4000:])
+    if out.returncode != 0:
+        pytest.fail("bench failed:\n" + out.stdout[-2000:] + "\n" + out.stderr[-6000:])
     line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["faulted_trials"] >= 1
     assert line["trials_total"] == 96 and line["value"] > 0

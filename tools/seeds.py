@@ -1,0 +1,53 @@
+"""Search reliability: OpEvo over several seeds on one operator, each run to
+the full budget, the best instance of each run confirmed by re-timing
+(GpuEvaluator.confirm_top).  One evaluator (one kernel-family preload) serves
+every seed; its trial history is reset between seeds.
+Usage: python tools/seeds.py OP SEED0 SEED1 [BUDGET] [--python-ask]"""
+import json
+import sys
+import time
+
+sys.path.insert(0, ".")
+from paper_2006_05664_b200 import EngineConfig, OpEvo, parse_operator  # noqa: E402
+from paper_2006_05664_b200.evaluator import EvalSettings, GpuEvaluator  # noqa: E402
+from paper_2006_05664_b200.mapping import gpu_operator_space  # noqa: E402
+from paper_2006_05664_b200.native import NativeOpEvo  # noqa: E402
+
+
+def main():
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    op, s0, s1 = args[0], int(args[1]), int(args[2])
+    budget = int(args[3]) if len(args) > 3 else 500
+    spec = parse_operator(op)
+    space = gpu_operator_space(spec)
+    ev = GpuEvaluator(spec, space, 0, EvalSettings(preload_family=True))
+    cls = OpEvo if "--python-ask" in sys.argv else NativeOpEvo
+    rows = []
+    for seed in range(s0, s1):
+        ev.history = []
+        eng = cls(space, EngineConfig(seed=seed, budget=budget))
+        t0 = time.perf_counter()
+        n = 0
+        while True:
+            a = eng.ask()
+            if not a.configs:
+                break
+            eng.tell(list(zip(a.configs, ev.evaluate(a.configs))))
+            n += len(a.configs)
+        wall = time.perf_counter() - t0
+        conf = ev.confirm_top(k=5, reps=100, rounds=5)
+        row = {"seed": seed, "trials": n, "wall_s": wall, "search_best": eng.best().fitness,
+               "confirmed_best": conf[0]["tflops"] if conf else 0.0,
+               "best_knobs": conf[0]["knobs"] if conf else None,
+               "top": [(c["knobs"][:10], round(c["tflops"], 1)) for c in conf]}
+        rows.append(row)
+        print(json.dumps(row), flush=True)
+    best = max(r["confirmed_best"] for r in rows)
+    ok = sum(r["confirmed_best"] >= 0.98 * best for r in rows)
+    print(json.dumps({"op": op, "seeds": [s0, s1], "budget": budget, "overall_best": best,
+                      "within_2pct": ok, "runs": len(rows)}))
+    ev.close()
+
+
+if __name__ == "__main__":
+    main()
