@@ -435,13 +435,26 @@ def main() -> None:
                                                offspring=RHO)),
                 TrialRecorder(space))
 
-    def generation(eng, rec, upload=None, tally=None) -> int:
+    history: list[tuple[list, list]] = []      # (asked, told) of every generation of the search
+
+    def generation(eng, rec, upload=None, tally=None, replay=None) -> int:
+        """One generation: ask -> evaluate -> tell.  ``replay`` (the
+        e2e leg): the recorded (asked, told) of the same generation of the
+        search -- the engine is told the recorded fitness, so a fresh engine
+        with the same seed asks exactly the same configurations again, and
+        they are measured again from scratch."""
         if upload is not None:
             upload()
         asked = eng.ask()
         if not asked.configs:
             return 0
         fits = evaluator(asked.configs)
+        if replay is not None:
+            if asked.configs != replay[0]:
+                raise RuntimeError("e2e replay diverged from the recorded search")
+            fits = replay[1]
+        else:
+            history.append((list(asked.configs), list(fits)))
         eng.tell(list(zip(asked.configs, fits)))
         owner = getattr(evaluator, "__self__", evaluator)
         extras = owner.last_extras
@@ -528,16 +541,16 @@ def main() -> None:
             op.upload(pa.ptr, pb.ptr)
 
         e_engine, e_rec = new_search(RHO * (args.warmup + args.steps))
-        for _ in range(args.warmup):
+        for g in range(args.warmup):
             flush()
-            generation(e_engine, e_rec, upload)
+            generation(e_engine, e_rec, upload, replay=history[g])
         barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record()
         e2e_trials = 0
-        for _ in range(args.steps):
+        for g in range(args.warmup, args.warmup + args.steps):
             flush()
-            e2e_trials += generation(e_engine, e_rec, upload)
+            e2e_trials += generation(e_engine, e_rec, upload, replay=history[g])
         barrier()
         f1.record()
         torch.cuda.synchronize()
@@ -545,10 +558,12 @@ def main() -> None:
         e2e = {"value": e2e_trials / e_sec if e_sec > 0 else 0.0, "unit": "trials/s",
                "h2d_bytes_per_step": (op.a_bytes + op.b_bytes) * world,
                "d2h_bytes_per_step": 16 * RHO, "steps": args.steps,
-               "what": "the timed region's generations (fresh engine, same seed) through "
-                       "GpuEvaluator.evaluate + OpEvo ask/tell, operands uploaded from pinned "
-                       "host memory every generation (reference recomputed, every trial "
-                       "re-verified), compare results read back"}
+               "what": "the timed region's generations replayed -- a fresh engine with the same "
+                       "seed told the recorded fitness asks the same configurations, each "
+                       "measured again -- through GpuEvaluator.evaluate + OpEvo ask/tell on a "
+                       "freshly prepared operand, operands uploaded from pinned host memory "
+                       "every generation (reference recomputed, every trial re-verified), "
+                       "compare results read back"}
         pa.close()
         pb.close()
         local_ev.op = main_op

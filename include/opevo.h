@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define OPEVO_ABI_VERSION 5   /* 5: timing policy, native search core; 4: OPEVO_F32_TF32X3, verification cache */
+#define OPEVO_ABI_VERSION 6   /* 6: 14-slot knobs (conv padded lines), conv stride / narrow Cin, conv CTA pairs; 5: timing policy, native search core */
 
 enum opevo_status {
     OPEVO_OK = 0,
@@ -101,7 +101,12 @@ enum opevo_knob {
     OPEVO_KNOB_BPU = 12,      /* BatchMatMul: consecutive batches per CTA
                                  work unit (1, 2, 4), loaded by one TMA box
                                  per operand and stage                    */
-    OPEVO_NUM_KNOBS = 13
+    OPEVO_KNOB_LINE = 13,     /* conv: 16 / 32 = "padded lines": lines of
+                                 TILE_W <= LINE output pixels padded to
+                                 LINE tile rows, one TMA box per filter tap
+                                 (any stride; widths no power of two
+                                 divides); 0 = dense tile or halo lines   */
+    OPEVO_NUM_KNOBS = 14
 };
 
 /* Result of one trial (opevo_trial). */

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libopevo.so")
 DEFAULT_CACHE = os.path.join(HERE, "kernel_cache")
 
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 # status codes (opevo.h)
 OK = 0
@@ -38,7 +38,7 @@ STATUS_NAMES = {OK: "ok", INVALID_CONFIG: "invalid_config", COMPILE_ERROR: "comp
 MATMUL, BATCHMATMUL, CONV2D = 0, 1, 2
 BF16, F32, F32_TF32X3 = 0, 1, 2
 FP32_OUT = (F32, F32_TF32X3)
-NUM_KNOBS = 13
+NUM_KNOBS = 14
 KNOB_NAMES = ("bm", "bn", "bk", "stages", "split", "cluster", "tile_h", "tile_w", "acc",
               "cta_group", "grid")
 
@@ -141,7 +141,7 @@ def load() -> C.CDLL:
     return lib
 
 
-_KNOB_DEFAULTS = (128, 128, 64, 4, 1, 1, 1, 1, 1, 1, 0, 0, 1)
+_KNOB_DEFAULTS = (128, 128, 64, 4, 1, 1, 1, 1, 1, 1, 0, 0, 1, 0)
 
 
 def _knob_array(knobs) -> "C.Array":

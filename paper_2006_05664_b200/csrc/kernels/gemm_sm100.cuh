@@ -24,11 +24,22 @@
 //                 the SW128 pattern is keyed on the absolute shared address, so
 //                 any whole-row shift stays canonical -- tools/swizzle_probe.cu).
 //                 KW times fewer TMA boxes for (16 - TILE_W)/16 more MMA rows.
+//   OPEVO_LINE    16 / 32: conv "padded lines" (any stride, no halo): the tile is
+//                 TILE_N*TILE_H lines of TILE_W <= LINE output pixels, each
+//                 line padded to LINE tile rows, one box per filter tap; the
+//                 junk rows are computed and never stored.  Output widths
+//                 that no power of two divides (27, 55, ...) tile this way.
 //   OPEVO_CTA_GROUP 2: a cluster of two CTAs on neighbouring SMs computes a
 //                 256 x BN tile with tcgen05.mma.cta_group::2 (M=256); each
 //                 CTA stages 128 rows of A and BN/2 rows of B, so per-SM
 //                 operand traffic (TMA ingress and smem reads) drops versus a
 //                 single-CTA 256-row tile.  Only the leader CTA issues MMAs.
+//                 Conv pairs: each CTA holds TILE_N images of the pair's
+//                 2 x TILE_N (its own 128 tile rows).
+//   Conv stride S: the activation tensor map traverses W and H with element
+//                 stride S (box extents LINE*S / TILE_H*S input pixels land
+//                 LINE / TILE_H output pixels' worth), so strided filters need
+//                 no im2col buffer either.
 //   OPEVO_SPLIT_CLUSTER S: split-K whose S slices of one tile run as one
 //                 thread-block cluster.  After the mainloop each CTA stages
 //                 its fp32 partial in shared memory and bulk-copies the row
@@ -96,6 +107,9 @@
 #endif
 #ifndef OPEVO_HALO
 #define OPEVO_HALO 0       // conv: KW taps per halo box (0: one box per tap)
+#endif
+#ifndef OPEVO_LINE
+#define OPEVO_LINE 0       // conv: padded lines of this many tile rows (0: dense tile)
 #endif
 #ifndef OPEVO_TILE_H
 #define OPEVO_TILE_H 1
@@ -190,8 +204,15 @@ constexpr int NUM_THREADS = 192;
 constexpr int SMEM_ALIGN = 1024;
 constexpr int TILE_H = OPEVO_TILE_H;
 constexpr int TILE_W = OPEVO_TILE_W;
-constexpr int LINE_ROWS = HALO ? 16 : TILE_W;            // tile rows per output line
-constexpr int TILE_N = BM / (TILE_H * LINE_ROWS);
+constexpr int LINE = OPEVO_LINE;
+constexpr bool LINES = HALO || LINE > 0;                 // lines padded with junk rows
+constexpr int LINE_ROWS = HALO ? 16 : (LINE > 0 ? LINE : TILE_W);   // tile rows per output line
+constexpr int TILE_N = BM_CTA / (TILE_H * LINE_ROWS);     // images of this CTA's tile
+constexpr int PAIR_TN = CG * TILE_N;                      // images of the (pair) tile
+// padded lines may leave tile rows past TILE_N x TILE_H lines unloaded (junk,
+// never stored): the activation box lands A_ROWS rows
+constexpr int A_ROWS = OPEVO_CONV ? TILE_N * TILE_H * LINE_ROWS : BM_CTA;
+constexpr int TX_STAGE = OPEVO_CONV ? (A_ROWS * BK * 2 + B_TILE) * CG : TX_BYTES;   // expect_tx per stage
 
 static_assert(BM == 64 || BM == 128 || BM == 256, "BM must be 64, 128 or 256");
 static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "BN must be a multiple of 16 in [16, 256]");
@@ -201,12 +222,15 @@ static_assert(TMEM_USED <= 512, "accumulator exceeds TMEM");
 static_assert(ACC == 1 || ACC == 2 || ACC == 4, "ACC must be 1, 2 or 4");
 static_assert((BK / 16) % ACC == 0, "each stage must feed every accumulator");
 static_assert(BM % (8 * CLUSTER) == 0, "multicast slice must be whole 8-row groups");
-static_assert(CG == 1 || (CG == 2 && BM == 256 && CLUSTER == 1 && !OPEVO_CONV && BN % 16 == 0),
-              "CTA pairs: 256-row tiles, no extra multicast, GEMM only");
-static_assert(!HALO || (OPEVO_CONV && TILE_W + HKW - 1 == 16 && SWZ == 128 && CG == 1),
+static_assert(CG == 1 || (CG == 2 && BM == 256 && CLUSTER == 1 && BN % 16 == 0 && OPEVO_B_RES == 0),
+              "CTA pairs: 256-row tiles, no extra multicast or resident weights");
+static_assert(!HALO || (OPEVO_CONV && TILE_W + HKW - 1 == 16 && SWZ == 128 && LINE == 0),
               "halo lines: 3x3-style conv, TILE_W = 17 - KW, 128-byte swizzle");
-static_assert(!OPEVO_CONV || (TILE_N * TILE_H * LINE_ROWS == BM && CLUSTER == 1),
-              "conv tile must cover BM pixels, no multicast");
+static_assert(LINE == 0 || (OPEVO_CONV && !HALO && (LINE == 16 || LINE == 32) && TILE_W <= LINE),
+              "padded lines: conv, 16 or 32 rows per line of TILE_W pixels");
+static_assert(!OPEVO_CONV || ((LINE > 0 ? (TILE_N >= 1 && A_ROWS <= BM_CTA) : A_ROWS == BM_CTA) &&
+                              CLUSTER == 1),
+              "conv tile must cover BM pixels (padded lines: at most BM), no multicast");
 
 // UMMA instruction descriptor, kind::f16: D=f32, A=B=bf16, both K-major
 // (kind::tf32 for X3: A=B=tf32, format code 2).
@@ -271,7 +295,7 @@ static_assert(SPLITT == 0 || ((SPLITT == 2 || SPLITT == 4) && SPLITCL == 0 && CG
                            BM == 128 && ACC == 1 && !OPEVO_BATCHED && !OPEVO_CONV && BN % 32 == 0 &&
                            OPEVO_BPU == 1 && !OPEVO_OUT_F32),
               "TMA split-K: S in {2,4}, single-CTA 128-row bf16 GEMM tiles");
-static_assert(SPLITCL == 0 || ((SPLITCL == 2 || SPLITCL == 4 || SPLITCL == 8) && CG == 1 && CLUSTER == 1 &&
+static_assert(SPLITCL == 0 || ((SPLITCL == 2 || SPLITCL == 4 || SPLITCL == 8) && CG == 1 && CLUSTER == 1 && !LINES &&
                            MATOMS == 1 && BM % (SPLITCL * 8) == 0),
               "DSMEM split-K: S in {2,4,8}, single-CTA 128-row tiles");
 
@@ -294,7 +318,8 @@ struct Sched {
 // Conv geometry (unused by the GEMM instances).
 struct ConvGeom {
     int cin, ho, wo, kw, pad;
-    int taps_cchunks;      // (Cin / BK): K blocks per filter tap
+    int taps_cchunks;      // (Cin / BK): K blocks per filter tap (Cin padded to 16)
+    int stride;
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -571,6 +596,18 @@ __device__ __forceinline__ u32 mapa_cta(u32 addr, u32 rank) {
     u32 r;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
     return r;
+}
+
+// Conv operand loads: plain, or (CTA pair) credited to the leader's barrier.
+__device__ __forceinline__ void conv_load_a(u32 dst, const TmaDesc* d, u32 bar, int c0, int c1, int c2,
+                                            int c3) {
+    if (CG == 2) tma2_load_4d(dst, d, bar, c0, c1, c2, c3);
+    else         tma_load_4d(dst, d, bar, c0, c1, c2, c3);
+}
+
+__device__ __forceinline__ void conv_load_b(u32 dst, const TmaDesc* d, u32 bar, int c0, int c1) {
+    if (CG == 2) tma2_load_2d(dst, d, bar, c0, c1);
+    else         tma_load_2d(dst, d, bar, c0, c1);
 }
 
 __device__ __forceinline__ void umma_commit_mc(u32 bar, u16 mask) {
@@ -948,7 +985,8 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
             const int w_tiles = geom.wo / TILE_W, h_tiles = geom.ho / TILE_H;
             const int w0 = (t.row_tile % w_tiles) * TILE_W;
             const int h0 = ((t.row_tile / w_tiles) % h_tiles) * TILE_H;
-            const int n0 = (t.row_tile / (w_tiles * h_tiles)) * TILE_N;
+            const int n0 = (t.row_tile / (w_tiles * h_tiles)) * PAIR_TN + (int)prank * TILE_N;
+            const int b_row0 = col0 + (int)prank * BN_LOAD;         // first B row here
 #else
             const int row0 = t.row_tile * BM + (int)prank * BM_CTA;   // first A row here
             const int b_row0 = col0 + (int)prank * BN_LOAD;         // first B row here
@@ -963,7 +1001,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                     if (++s == STAGES) { s = 0; ph ^= 1; }
                     continue;
                 }
-                if (prank == 0) mbar_expect_tx(smem_u32(full_bar + s), TX_BYTES);
+                if (prank == 0) mbar_expect_tx(smem_u32(full_bar + s), TX_STAGE);
                 if (first && lane == 0) TRACE(11);
                 const u32 a_dst = smem_u32(smem + s * STAGE_BYTES);
                 const u32 b_dst = a_dst + A_TILE;
@@ -979,22 +1017,24 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                     const int di = tap - geom.pad;
 #pragma unroll
                     for (int ka = 0; ka < KATOMS; ++ka) {
-                        tma_load_4d(a_dst + ka * (BM_CTA * SWZ), &tma_a, fb, cbase + ka * ATOM_K,
+                        conv_load_a(a_dst + ka * (BM_CTA * SWZ), &tma_a, fb, cbase + ka * ATOM_K,
                                     w0 - geom.pad, h0 + di, n0);
                         if (!B_RES)
 #pragma unroll
                             for (int dj = 0; dj < HKW; ++dj)
-                                tma_load_2d(b_dst + dj * B_SUB + ka * (BN_LOAD * SWZ), &tma_b, fb,
-                                            (tap * HKW + dj) * geom.cin + cbase + ka * ATOM_K, col0);
+                                conv_load_b(b_dst + dj * B_SUB + ka * (BN_LOAD * SWZ), &tma_b, fb,
+                                            (tap * HKW + dj) * geom.cin + cbase + ka * ATOM_K, b_row0);
                     }
                 } else {
+                // input pixel of output (h0, w0) under tap (di, dj): the map
+                // traverses W and H with element stride S
                 const int di = tap / geom.kw - geom.pad, dj = tap % geom.kw - geom.pad;
 #pragma unroll
                 for (int ka = 0; ka < KATOMS; ++ka) {
-                    tma_load_4d(a_dst + ka * (BM_CTA * SWZ), &tma_a, fb, cbase + ka * ATOM_K,
-                                w0 + dj, h0 + di, n0);
+                    conv_load_a(a_dst + ka * (BM_CTA * SWZ), &tma_a, fb, cbase + ka * ATOM_K,
+                                w0 * geom.stride + dj, h0 * geom.stride + di, n0);
                     if (!B_RES)
-                        tma_load_2d(b_dst + ka * (BN_LOAD * SWZ), &tma_b, fb, kk + ka * ATOM_K, col0);
+                        conv_load_b(b_dst + ka * (BN_LOAD * SWZ), &tma_b, fb, kk + ka * ATOM_K, b_row0);
                 }
                 }
 #else
@@ -1120,8 +1160,9 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                                 for (int ma = 0; ma < MATOMS; ++ma) {
                                     const u64 adesc = da + (u64)((ka * (BM_CTA * SWZ) + ma * (128 * SWZ) + dj * 128) >> 4);
                                     const u32 accumulate = (kb != 0 || step >= ACC) ? 1u : 0u;
-                                    umma1_atom<ATOM_K / 16>(acc_base + (u32)((acc * MATOMS + ma) * BN), adesc, bdesc,
-                                                            accumulate);
+                                    const u32 d = acc_base + (u32)((acc * MATOMS + ma) * BN);
+                                    if (CG == 2) umma2_atom<ATOM_K / 16>(d, adesc, bdesc, accumulate);
+                                    else         umma1_atom<ATOM_K / 16>(d, adesc, bdesc, accumulate);
                                 }
                             }
                         }
@@ -1255,9 +1296,15 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
             const int w_tiles = geom.wo / TILE_W, h_tiles = geom.ho / TILE_H;
             const int w0 = (t.row_tile % w_tiles) * TILE_W;
             const int h0 = ((t.row_tile / w_tiles) % h_tiles) * TILE_H;
-            const int n0 = (t.row_tile / (w_tiles * h_tiles)) * TILE_N;
-            // tile row -> NHWC output pixel row
+            const int n0 = (t.row_tile / (w_tiles * h_tiles)) * PAIR_TN + (int)prank * TILE_N;
+            // tile row -> NHWC output pixel row (split-K paths); -1 for the
+            // junk rows of padded lines
             auto out_row = [&](int lr) -> int {
+                if (LINES) {
+                    const int line = lr / LINE_ROWS, p = lr % LINE_ROWS;
+                    if (p >= TILE_W || line >= TILE_N * TILE_H) return -1;
+                    return ((n0 + line / TILE_H) * geom.ho + h0 + line % TILE_H) * geom.wo + w0 + p;
+                }
                 const int n = n0 + lr / (TILE_H * TILE_W);
                 const int h = h0 + (lr / TILE_W) % TILE_H;
                 const int w = w0 + lr % TILE_W;
@@ -1312,14 +1359,16 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                         __syncwarp();
                         if (lane == 0 && OPEVO_ABLATE != 6 && OPEVO_ABLATE != 7) {
 #if OPEVO_CONV
-                            if (HALO) {
-                                // the chunk's 32 rows are two 16-row lines: store
-                                // their TILE_W valid pixels, skip the junk rows
-                                // (direct st.global per lane measured no faster)
+                            if (LINES) {
+                                // the chunk's 32 rows are 32 / LINE_ROWS padded
+                                // lines: store their TILE_W valid pixels, skip the
+                                // junk rows (direct st.global per lane measured
+                                // no faster)
 #pragma unroll
-                                for (int q = 0; q < 2; ++q) {
-                                    const int line = lr0 / 16 + q;
-                                    tma_store_4d(&tma_c, buf + (u32)(q * 16 * EPI_ROW_BYTES), col0 + c, w0,
+                                for (int q = 0; q < 32 / LINE_ROWS; ++q) {
+                                    const int line = lr0 / LINE_ROWS + q;
+                                    if (line >= TILE_N * TILE_H) break;   // rows past the tile's lines
+                                    tma_store_4d(&tma_c, buf + (u32)(q * LINE_ROWS * EPI_ROW_BYTES), col0 + c, w0,
                                                  h0 + line % TILE_H, n0 + line / TILE_H);
                                 }
                             } else {
@@ -1454,7 +1503,8 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
 #pragma unroll 1
                     for (int c = 0; c < BN; c += EPI_COLS) {
                         float acc[EPI_COLS];
-                        gather_acc(lane_addr + ma * BN + c, acc);
+                        gather_acc(lane_addr + ma * BN + c, acc);      // warp-collective
+                        if (r < 0) continue;                           // junk row of a padded line
                         float* dst = ws + (u64)t.kz * slice + c_batch + (u64)r * cols + col0 + c;
 #pragma unroll
                         for (int j = 0; j < EPI_COLS; j += 4)
@@ -1483,7 +1533,8 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
 #pragma unroll 1
                         for (int c = 0; c < BN; c += EPI_COLS) {
                             float own[EPI_COLS], acc[EPI_COLS];
-                            gather_acc(lane_addr + ma * BN + c, own);
+                            gather_acc(lane_addr + ma * BN + c, own);  // warp-collective
+                            if (r < 0) continue;                       // junk row of a padded line
 #pragma unroll
                             for (int j = 0; j < EPI_COLS; ++j) acc[j] = 0.0f;
                             const u64 base = c_batch + (u64)r * cols + col0 + c;
@@ -1571,7 +1622,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
         const int w_tiles = geom.wo / TILE_W, h_tiles = geom.ho / TILE_H;
         const int w0 = (t.row_tile % w_tiles) * TILE_W;
         const int h0 = ((t.row_tile / w_tiles) % h_tiles) * TILE_H;
-        const int n0 = (t.row_tile / (w_tiles * h_tiles)) * TILE_N;
+        const int n0 = (t.row_tile / (w_tiles * h_tiles)) * PAIR_TN;
 #endif
         const float* recv = reinterpret_cast<const float*>(smem + RED_OWN_BYTES);
         const int my_row0 = (int)crank * RED_ROWS;

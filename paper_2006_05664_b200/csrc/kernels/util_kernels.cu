@@ -155,6 +155,37 @@ extern "C" __global__ void opevo_nchw_to_nhwc(const u16* __restrict__ src, u16* 
     }
 }
 
+// NCHW -> NHWC with the channels padded with zeros to Cp (dst has N*H*W*Cp
+// elements): the conv kernels' layout, whose pixel rows must be >= 16 bytes
+// and a whole UMMA K step (narrow Cin, e.g. 3 -> 16).  Also OIHW -> O(HW)I.
+extern "C" __global__ void opevo_nchw_to_nhwc_pad(const u16* __restrict__ src, u16* __restrict__ dst,
+                                                  int N, int C, int H, int W, int Cp) {
+    const u64 total = (u64)N * Cp * H * W;
+    for (u64 o = blockIdx.x * (u64)blockDim.x + threadIdx.x; o < total; o += (u64)gridDim.x * blockDim.x) {
+        const int c = (int)(o % Cp);
+        u64 p = o / Cp;
+        const int w = (int)(p % W); p /= W;
+        const int h = (int)(p % H);
+        const int n = (int)(p / H);
+        dst[o] = c < C ? src[(((u64)n * C + c) * H + h) * W + w] : (u16)0;
+    }
+}
+
+// The inverse (padding dropped): an uploaded kernel-layout operand back to
+// the paper layout the reference convolution reads.
+extern "C" __global__ void opevo_nhwc_pad_to_nchw(const u16* __restrict__ src, u16* __restrict__ dst,
+                                                  int N, int C, int H, int W, int Cp) {
+    const u64 total = (u64)N * C * H * W;
+    for (u64 o = blockIdx.x * (u64)blockDim.x + threadIdx.x; o < total; o += (u64)gridDim.x * blockDim.x) {
+        const int w = (int)(o % W);
+        u64 p = o / W;
+        const int h = (int)(p % H); p /= H;
+        const int c = (int)(p % C);
+        const int n = (int)(p / C);
+        dst[o] = src[(((u64)n * H + h) * W + w) * Cp + c];
+    }
+}
+
 // ---------------------------------------------------------------------------
 // out[0] = max |C - R|, out[1] = max |R|, out[2] = count of non-finite C.
 // Non-negative floats compare like their bit patterns, so atomicMax on u32.

@@ -189,13 +189,13 @@ void load_nvrtc() {
 
 // ------------------------------------------------------------- knobs
 struct Knobs {
-    int bm, bn, bk, stages, split, cluster, tile_h, tile_w, acc, cg, grid_mode, b_res, bpu;
+    int bm, bn, bk, stages, split, cluster, tile_h, tile_w, acc, cg, grid_mode, b_res, bpu, line;
 };
 
 Knobs read_knobs(const int32_t* k, int n) {
-    int32_t v[OPEVO_NUM_KNOBS] = {128, 128, 64, 4, 1, 1, 1, 1, 1, 1, 0, 0, 1};
+    int32_t v[OPEVO_NUM_KNOBS] = {128, 128, 64, 4, 1, 1, 1, 1, 1, 1, 0, 0, 1, 0};
     for (int i = 0; i < n && i < OPEVO_NUM_KNOBS; ++i) v[i] = k[i];
-    return Knobs{v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8], v[9], v[10], v[11], v[12]};
+    return Knobs{v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8], v[9], v[10], v[11], v[12], v[13]};
 }
 
 // Family 3 (fp32 GEMM as 3xTF32 on tcgen05) takes BK in fp32 elements at the
@@ -239,7 +239,9 @@ bool b_resident(const Knobs& k, int family) {
 // to 16 tile rows; one TMA box per filter row serves its KW taps.  Returns KW,
 // or 0 for the one-box-per-tap layout.
 int halo_kw(const Knobs& k, int family) {
-    return (family == 1 && k.tile_w >= 1 && k.tile_w < 16 && k.tile_h >= 1 && k.bm % (k.tile_h * k.tile_w) != 0)
+    const int bm_cta = k.cg == 2 ? 128 : k.bm;
+    return (family == 1 && k.line == 0 && k.tile_w >= 1 && k.tile_w < 16 && k.tile_h >= 1 &&
+            bm_cta % (k.tile_h * k.tile_w) != 0)
                ? 17 - k.tile_w : 0;
 }
 
@@ -269,6 +271,7 @@ int tma_split(const Knobs& k, int family, int batched) {
 
 bool dsmem_split(const Knobs& k, int family, int batched = 0) {
     return family != 2 && (k.split == 2 || k.split == 4 || k.split == 8) && k.cg == 1 &&
+           !(family == 1 && k.line) &&   // padded lines reduce through the global path
            k.cluster == 1 && k.bm == 128 && !tma_split(k, family, batched) &&
            (dsmem_red_bytes(k) + 1023) / 1024 * 1024 + epi_stage_bytes(k, family == FAMILY_X3) + 1024 + 256 <=
                232448;
@@ -328,7 +331,7 @@ std::string instance_flags(int family, const Knobs& k) {
     const char* v = getenv("OPEVO_FAULT_KNOBS");
     if (!v || !*v || family == 2) return f;
     const int kv[OPEVO_NUM_KNOBS] = {k.bm, k.bn, k.bk, k.stages, k.split, k.cluster, k.tile_h, k.tile_w,
-                                     k.acc, k.cg, k.grid_mode, k.b_res, k.bpu};
+                                     k.acc, k.cg, k.grid_mode, k.b_res, k.bpu, k.line};
     std::istringstream in(v);
     std::string tok;
     int i = 0;
@@ -357,11 +360,13 @@ std::string make_key(int family, const Knobs& k, int batched, int out_f32) {
                  want_lineinfo() ? "L" : "", (unsigned long long)(h & 0xffffffffffffull));
         return buf;
     }
-    snprintf(buf, sizeof buf, "f%d_m%d_n%d_k%d_s%d_b%d_o%d_c%d_h%d_w%d_a%d_g%d%s_%s%012llx", family,
+    char line[16] = "";
+    if (family == 1 && k.line) snprintf(line, sizeof line, "_l%d", k.line);
+    snprintf(buf, sizeof buf, "f%d_m%d_n%d_k%d_s%d_b%d_o%d_c%d_h%d_w%d_a%d_g%d%s%s_%s%012llx", family,
              k.bm, k.bn, k.bk, k.stages, batched, out_f32, k.cluster, family == 1 ? k.tile_h : 1,
              family == 1 ? k.tile_w : 1, k.acc,
              k.cg * 100 + (dsmem_split(k, family, batched) ? k.split : 0) + 10 * tma_split(k, family, batched),
-             b_resident(k, family) ? "_r" : k.bpu > 1 ? (k.bpu == 2 ? "_u2" : "_u4") : "",
+             b_resident(k, family) ? "_r" : k.bpu > 1 ? (k.bpu == 2 ? "_u2" : "_u4") : "", line,
              want_lineinfo() ? "L" : "",
              (unsigned long long)(h & 0xffffffffffffull));
     return buf;
@@ -435,8 +440,8 @@ bool knobs_compilable(int family, const Knobs& k, char* err, size_t len) {
         return false;
     }
     if (!(k.cg == 1 || k.cg == 2) ||
-        (k.cg == 2 && (k.bm != 256 || k.cluster != 1 || family != 0))) {
-        put_err(err, len, "cta_group=%d needs BM=256, no multicast cluster, GEMM family", k.cg);
+        (k.cg == 2 && (k.bm != 256 || k.cluster != 1 || (family != 0 && family != 1) || b_resident(k, family)))) {
+        put_err(err, len, "cta_group=%d needs BM=256, no multicast cluster or resident weights", k.cg);
         return false;
     }
     if (!(k.bpu == 1 || k.bpu == 2 || k.bpu == 4) ||
@@ -462,20 +467,32 @@ bool knobs_compilable(int family, const Knobs& k, char* err, size_t len) {
         put_err(err, len, "shared memory %zu B exceeds 227 KB", smem_bytes(k, family));
         return false;
     }
+    if (family != 1 && k.line) {
+        put_err(err, len, "padded lines are a conv tiling");
+        return false;
+    }
     if (family == 1) {
+        const int bm_cta = k.cg == 2 ? 128 : k.bm;     // tile rows held by one CTA
         if (k.cluster != 1) {
             put_err(err, len, "conv instances do not multicast");
             return false;
         }
         if (halo_kw(k, family)) {
-            if (k.bm % (16 * k.tile_h) || k.bk % 64 || k.split != 1 || k.cg != 1) {
-                put_err(err, len, "halo lines: BM=%d must hold 16-row lines of %d rows, BK a multiple of 64, "
-                        "no split", k.bm, k.tile_h);
+            if (bm_cta % (16 * k.tile_h) || k.bk % 64 || k.split != 1) {
+                put_err(err, len, "halo lines: %d rows must hold 16-row lines of %d rows, BK a multiple of 64, "
+                        "no split", bm_cta, k.tile_h);
                 return false;
             }
-        } else if (k.tile_h < 1 || k.tile_w < 1 || k.bm % (k.tile_h * k.tile_w) || k.tile_w > 256 ||
-                   k.tile_h > 256 || k.bm / (k.tile_h * k.tile_w) > 256) {
-            put_err(err, len, "conv tile %dx%d does not divide BM=%d", k.tile_h, k.tile_w, k.bm);
+        } else if (k.line) {
+            if (!(k.line == 16 || k.line == 32) || k.tile_w < 1 || k.tile_w > k.line || k.tile_h < 1 ||
+                k.line * k.tile_h > bm_cta) {
+                put_err(err, len, "padded lines: %d rows must hold at least one image of %d lines of %d rows "
+                        "(16/32, >= TILE_W %d)", bm_cta, k.tile_h, k.line, k.tile_w);
+                return false;
+            }
+        } else if (k.tile_h < 1 || k.tile_w < 1 || bm_cta % (k.tile_h * k.tile_w) || k.tile_w > 256 ||
+                   k.tile_h > 256 || bm_cta / (k.tile_h * k.tile_w) > 256) {
+            put_err(err, len, "conv tile %dx%d does not divide %d rows", k.tile_h, k.tile_w, bm_cta);
             return false;
         }
     }
@@ -554,7 +571,8 @@ int nvrtc_build(int family, const Knobs& k, int batched, int out_f32, std::vecto
         "-DOPEVO_B_RES=" + std::to_string(b_resident(k, family) ? 1 : 0),
         "-DOPEVO_BPU=" + std::to_string(family == 0 ? std::max(1, k.bpu) : 1),
         "-DOPEVO_TF32X3=" + std::to_string(family == FAMILY_X3 ? 1 : 0),
-        "-DOPEVO_HALO=" + std::to_string(halo_kw(k, family))};
+        "-DOPEVO_HALO=" + std::to_string(halo_kw(k, family)),
+        "-DOPEVO_LINE=" + std::to_string(family == 1 ? k.line : 0)};
     if (want_lineinfo()) opts.push_back("-lineinfo");
     {
         std::istringstream extra(instance_flags(family, k));
@@ -673,7 +691,7 @@ struct opevo_ctx {
     CUmodule util = nullptr;
     CUfunction k_fill_bf16 = nullptr, k_fill_f32 = nullptr, k_fill_u8 = nullptr, k_ref_gemm = nullptr,
                k_ref_conv = nullptr, k_nchw2nhwc = nullptr, k_compare = nullptr, k_flush = nullptr,
-               k_gate = nullptr;
+               k_gate = nullptr, k_nchw2nhwc_pad = nullptr, k_nhwc_pad2nchw = nullptr;
     volatile uint32_t* gate_host = nullptr;   // mapped pinned flag opening the timing gate
     CUdeviceptr gate_dev = 0;
     uint32_t gate_seq = 0;
@@ -695,6 +713,9 @@ struct opevo_op {
     opevo_ctx* ctx = nullptr;
     opevo_op_desc d{};
     int64_t rows = 0, cols = 0, depth = 0, batch = 1;   // GEMM view
+    int64_t flop_depth = 0;                             // K of the operator (conv: unpadded Cin)
+    int cpad = 0;                                       // conv: Cin in the kernel layout (16-aligned)
+    size_t x_bytes = 0, w_bytes = 0;                    // conv: paper-layout operands
     CUdeviceptr a = 0, b = 0, c = 0, ref = 0;
     CUdeviceptr conv_x = 0, conv_w = 0;                 // paper layouts (NCHW / OIHW)
     CUdeviceptr ws = 0, counters = 0;
@@ -727,14 +748,14 @@ void drop_graphs(opevo_op* op) {
 
 std::string graph_key(const Knobs& k, int reps) {
     char buf[160];
-    snprintf(buf, sizeof buf, "%d_%d_%d_%d_%d_%d_%d_%d_%d_%d_%d_%d_%d_r%d", k.bm, k.bn, k.bk, k.stages, k.split,
-             k.cluster, k.tile_h, k.tile_w, k.acc, k.cg, k.grid_mode, k.b_res, k.bpu, reps);
+    snprintf(buf, sizeof buf, "%d_%d_%d_%d_%d_%d_%d_%d_%d_%d_%d_%d_%d_%d_r%d", k.bm, k.bn, k.bk, k.stages,
+             k.split, k.cluster, k.tile_h, k.tile_w, k.acc, k.cg, k.grid_mode, k.b_res, k.bpu, k.line, reps);
     return buf;
 }
 }  // namespace
 
 struct ConvGeomHost {
-    int cin, ho, wo, kw, pad, taps_cchunks;
+    int cin, ho, wo, kw, pad, taps_cchunks, stride;   // mirrors ConvGeom in gemm_sm100.cuh
 };
 
 // mirrors `Sched` in gemm_sm100.cuh
@@ -856,8 +877,11 @@ CUtensorMapSwizzle swz_enum(int bytes) {
 }
 
 int encode_map(CUtensorMap* map, CUdeviceptr base, int rank, const uint64_t* dims, const uint64_t* strides_b,
-               const uint32_t* box, int swz, char* err, size_t errlen, int f32 = 0) {
+               const uint32_t* box, int swz, char* err, size_t errlen, int f32 = 0,
+               const uint32_t* elem_strides = nullptr) {
     uint32_t es[5] = {1, 1, 1, 1, 1};
+    if (elem_strides)
+        for (int i = 0; i < rank; ++i) es[i] = elem_strides[i];
     CUresult r = g_cu.TensorMapEncodeTiled(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
                                            (cuuint32_t)rank,
                                            (void*)base, (const cuuint64_t*)dims,
@@ -1044,7 +1068,7 @@ int simt_kernel_get(opevo_ctx* ctx, opevo_op* op, const Knobs& k, opevo_kernel**
     kr->grid[0] = (unsigned)(op->cols / g.bn());
     kr->grid[1] = (unsigned)(op->rows / g.bm());
     kr->grid[2] = (unsigned)op->batch;
-    kr->flops = 2.0 * (double)op->batch * (double)op->rows * (double)op->cols * (double)op->depth;
+    kr->flops = 2.0 * (double)op->batch * (double)op->rows * (double)op->cols * (double)op->flop_depth;
     double compile_ms = 0.0;
     int hit = 1;
     int st = get_function(ctx, 2, k, op->d.kind == OPEVO_BATCHMATMUL, 1, "opevo_sgemm", kr->smem, &kr->fn,
@@ -1140,7 +1164,8 @@ int opevo_ctx_create(int device, const char* cache_dir, opevo_ctx** out, char* e
             {&ctx->k_fill_u8, "opevo_fill_u8"},     {&ctx->k_ref_gemm, "opevo_ref_gemm"},
             {&ctx->k_ref_conv, "opevo_ref_conv"},   {&ctx->k_nchw2nhwc, "opevo_nchw_to_nhwc"},
             {&ctx->k_compare, "opevo_compare"},     {&ctx->k_flush, "opevo_flush"},
-            {&ctx->k_gate, "opevo_gate"}};
+            {&ctx->k_gate, "opevo_gate"},           {&ctx->k_nchw2nhwc_pad, "opevo_nchw_to_nhwc_pad"},
+            {&ctx->k_nhwc_pad2nchw, "opevo_nhwc_pad_to_nchw"}};
         for (auto& f : fns) {
             if ((r = g_cu.ModuleGetFunction(f.f, ctx->util, f.n)) != CUDA_SUCCESS) {
                 bail(r, f.n);
@@ -1244,6 +1269,7 @@ int opevo_op_prepare(opevo_ctx* ctx, const opevo_op_desc* desc, opevo_op** out, 
             delete op;
             return OPEVO_ERR_ARG;
         }
+        op->flop_depth = op->depth;
         op->a_bytes = (size_t)op->batch * op->rows * op->depth * esz;
         op->b_bytes = (size_t)op->batch * op->cols * op->depth * esz;
         op->c_bytes = (size_t)op->batch * op->rows * op->cols * (op->out_f32 ? 4 : 2);
@@ -1263,28 +1289,42 @@ int opevo_op_prepare(opevo_ctx* ctx, const opevo_op_desc* desc, opevo_op** out, 
             return OPEVO_ERR_ARG;
         }
         int HO = (H + 2 * P - KH) / S + 1, WO = (W + 2 * P - KW) / S + 1;
+        if (HO < 1 || WO < 1) {
+            put_err(err, errlen, "conv2d output is empty");
+            delete op;
+            return OPEVO_ERR_ARG;
+        }
+        // kernel layouts: X NHWC and W [Cout][Kh][Kw][Cin] with Cin padded
+        // with zeros to a multiple of 16 (one 32-byte UMMA K step; a TMA
+        // row must be >= 16 bytes), e.g. AlexNet conv1's Cin = 3 -> 16
+        int CP = (C + 15) / 16 * 16;
+        op->cpad = CP;
         op->batch = 1;
         op->rows = (int64_t)N * HO * WO;
         op->cols = K;
-        op->depth = (int64_t)KH * KW * C;
-        op->a_bytes = (size_t)N * C * H * W * 2;
-        op->b_bytes = (size_t)K * C * KH * KW * 2;
+        op->depth = (int64_t)KH * KW * CP;
+        op->flop_depth = (int64_t)KH * KW * C;
+        op->x_bytes = (size_t)N * C * H * W * 2;
+        op->w_bytes = (size_t)K * C * KH * KW * 2;
+        op->a_bytes = (size_t)N * H * W * CP * 2;
+        op->b_bytes = (size_t)K * KH * KW * CP * 2;
         op->c_bytes = (size_t)op->rows * op->cols * 2;
-        if (alloc(&op->conv_x, op->a_bytes, "alloc X") && alloc(&op->conv_w, op->b_bytes, "alloc W") &&
+        if (alloc(&op->conv_x, op->x_bytes, "alloc X") && alloc(&op->conv_w, op->w_bytes, "alloc W") &&
             alloc(&op->a, op->a_bytes, "alloc X nhwc") && alloc(&op->b, op->b_bytes, "alloc W ohwi") &&
             alloc(&op->c, op->c_bytes, "alloc C") && alloc(&op->ref, (size_t)op->rows * op->cols * 4, "alloc ref")) {
-            st = fill(ctx, op->conv_x, op->a_bytes / 2, desc->seed, 0, err, errlen);
-            if (!st) st = fill(ctx, op->conv_w, op->b_bytes / 2, desc->seed + 1, 0, err, errlen);
+            st = fill(ctx, op->conv_x, op->x_bytes / 2, desc->seed, 0, err, errlen);
+            if (!st) st = fill(ctx, op->conv_w, op->w_bytes / 2, desc->seed + 1, 0, err, errlen);
             if (!st) {
+                // NCHW -> NHWC (channels padded with zeros to CP)
                 uint64_t n1 = op->a_bytes / 2;
-                void* a1[] = {&op->conv_x, &op->a, &N, &C, &H, &W};
-                st = launch_simple(ctx, ctx->k_nchw2nhwc, grid_for(n1), 256, a1, err, errlen);
+                void* a1[] = {&op->conv_x, &op->a, &N, &C, &H, &W, &CP};
+                st = launch_simple(ctx, ctx->k_nchw2nhwc_pad, grid_for(n1), 256, a1, err, errlen);
             }
             if (!st) {
-                // OIHW viewed as [O][I][KH][KW] -> [O][KH][KW][I]
+                // OIHW viewed as [O][I][KH][KW] -> [O][KH][KW][I padded]
                 uint64_t n2 = op->b_bytes / 2;
-                void* a2[] = {&op->conv_w, &op->b, &K, &C, &KH, &KW};
-                st = launch_simple(ctx, ctx->k_nchw2nhwc, grid_for(n2), 256, a2, err, errlen);
+                void* a2[] = {&op->conv_w, &op->b, &K, &C, &KH, &KW, &CP};
+                st = launch_simple(ctx, ctx->k_nchw2nhwc_pad, grid_for(n2), 256, a2, err, errlen);
             }
         }
     } else {
@@ -1324,19 +1364,18 @@ int opevo_op_upload(opevo_op* op, const void* a_host, const void* b_host, char* 
     if (a_host) CU_TRY(ctx, g_cu.MemcpyHtoDAsync(op->a, a_host, op->a_bytes, ctx->stream), "upload A");
     if (b_host) CU_TRY(ctx, g_cu.MemcpyHtoDAsync(op->b, b_host, op->b_bytes, ctx->stream), "upload B");
     if (op->d.kind == OPEVO_CONV2D && (a_host || b_host)) {
-        // the reference convolves the paper's layouts: NHWC -> NCHW is the
-        // generic [n][c][h][w] -> [n][h][w][c] transpose with C' = H*W,
-        // H' = C, W' = 1 (and OHWI -> OIHW with N = O, C' = KH*KW, H' = I)
+        // the reference convolves the paper's layouts: NHWC (channels padded
+        // to CP) -> NCHW, and [O][KH][KW][I padded] -> OIHW
         const int32_t* c = op->d.conv;
-        int N = c[0], C = c[1], HW = c[2] * c[3], K = c[4], T = c[5] * c[6], one = 1;
+        int N = c[0], C = c[1], H = c[2], W = c[3], K = c[4], KH = c[5], KW = c[6], CP = op->cpad;
         int st = OPEVO_OK;
         if (a_host) {
-            void* a1[] = {&op->a, &op->conv_x, &N, &HW, &C, &one};
-            st = launch_simple(ctx, ctx->k_nchw2nhwc, grid_for(op->a_bytes / 2), 256, a1, err, errlen);
+            void* a1[] = {&op->a, &op->conv_x, &N, &C, &H, &W, &CP};
+            st = launch_simple(ctx, ctx->k_nhwc_pad2nchw, grid_for(op->x_bytes / 2), 256, a1, err, errlen);
         }
         if (!st && b_host) {
-            void* a2[] = {&op->b, &op->conv_w, &K, &T, &C, &one};
-            st = launch_simple(ctx, ctx->k_nchw2nhwc, grid_for(op->b_bytes / 2), 256, a2, err, errlen);
+            void* a2[] = {&op->b, &op->conv_w, &K, &C, &KH, &KW, &CP};
+            st = launch_simple(ctx, ctx->k_nhwc_pad2nchw, grid_for(op->w_bytes / 2), 256, a2, err, errlen);
         }
         if (st) return st;
     }
@@ -1411,7 +1450,7 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
     // operator-dependent feasibility (divisibility: no tail handling by design)
     // (halo-line conv tiles hold 16 * lines rows for TILE_W * lines pixels;
     // the conv branch checks their tiling)
-    if ((op->rows % k.bm && !halo_kw(k, family)) || op->cols % k.bn) {
+    if ((op->rows % k.bm && family != 1) || op->cols % k.bn) {
         put_err(err, errlen, "tile %dx%d does not divide %lldx%lld", k.bm, k.bn, (long long)op->rows,
                 (long long)op->cols);
         return OPEVO_INVALID_CONFIG;
@@ -1432,34 +1471,43 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
     kr->k_per_split = (int)(depth / k.split);
     kr->kdepth = (int)depth;
     kr->smem = smem_bytes(k, family, op->out_f32, batched);
-    kr->flops = 2.0 * (double)op->batch * (double)op->rows * (double)op->cols * (double)op->depth;
+    kr->flops = 2.0 * (double)op->batch * (double)op->rows * (double)op->cols * (double)op->flop_depth;
     int st = OPEVO_OK;
     const int swz = swizzle_bytes(k.bk);
     const uint32_t atom_k = (uint32_t)(swz / 2);
     if (family == 1) {
         const int32_t* c = op->d.conv;
-        int N = c[0], C = c[1], H = c[2], W = c[3], KH = c[5], KW = c[6], S = c[7], P = c[8];
+        int N = c[0], H = c[2], W = c[3], KH = c[5], KW = c[6], S = c[7], P = c[8];
         int HO = (H + 2 * P - KH) / S + 1, WO = (W + 2 * P - KW) / S + 1;
         const int hkw = halo_kw(k, family);
-        const int tile_n = k.bm / (k.tile_h * (hkw ? 16 : k.tile_w));
-        if (hkw && (hkw != KW || k.split != 1 || P >= KW)) {
-            put_err(err, errlen, "halo lines of %d pixels need a %d-wide filter (this one is %d wide)",
-                    k.tile_w, hkw, KW);
+        const int CP = op->cpad;                          // Cin padded to 16 (kernel layout)
+        // per-CTA tile: TILE_N images x TILE_H lines of LINE tile rows; a
+        // CTA pair holds 2 x TILE_N images
+        const int line_rows = hkw ? 16 : k.line ? k.line : k.tile_w;
+        const int bm_cta = k.cg == 2 ? 128 : k.bm;
+        const int tile_n = bm_cta / (k.tile_h * line_rows);
+        const int pair_n = tile_n * k.cg;
+        if (hkw && (hkw != KW || k.split != 1 || P >= KW || S != 1)) {
+            put_err(err, errlen, "halo lines of %d pixels need a %d-wide stride-1 filter (this one is %d wide, "
+                    "stride %d)", k.tile_w, hkw, KW, S);
             delete kr;
             return OPEVO_INVALID_CONFIG;
         }
-        if (S != 1 || C % k.bk || HO % k.tile_h || WO % k.tile_w || N % tile_n) {
-            put_err(err, errlen, "conv tiling (n%d h%d w%d, BK %d, stride %d) does not divide the problem",
-                    tile_n, k.tile_h, k.tile_w, k.bk, S);
+        if (tile_n < 1 || CP % k.bk || HO % k.tile_h || WO % k.tile_w || N % pair_n ||
+            line_rows * S > 256 || k.tile_h * S > 256) {
+            put_err(err, errlen, "conv tiling (n%d h%d w%d line %d, BK %d, stride %d) does not divide the problem",
+                    pair_n, k.tile_h, k.tile_w, line_rows, k.bk, S);
             delete kr;
             return OPEVO_INVALID_CONFIG;
         }
-        kr->geom = ConvGeomHost{C, HO, WO, KW, P, C / k.bk};
-        uint64_t dims[4] = {(uint64_t)C, (uint64_t)W, (uint64_t)H, (uint64_t)N};
-        uint64_t strides[3] = {(uint64_t)C * 2, (uint64_t)C * W * 2, (uint64_t)C * W * H * 2};
-        // halo lines: 16 input pixels per line (TILE_W outputs + KW - 1 halo)
-        uint32_t box[4] = {atom_k, (uint32_t)(hkw ? 16 : k.tile_w), (uint32_t)k.tile_h, (uint32_t)tile_n};
-        st = encode_map(&kr->tma_a, op->a, 4, dims, strides, box, swz, err, errlen);
+        kr->geom = ConvGeomHost{CP, HO, WO, KW, P, CP / k.bk, S};
+        uint64_t dims[4] = {(uint64_t)CP, (uint64_t)W, (uint64_t)H, (uint64_t)N};
+        uint64_t strides[3] = {(uint64_t)CP * 2, (uint64_t)CP * W * 2, (uint64_t)CP * W * H * 2};
+        // halo lines: 16 input pixels per line (TILE_W outputs + KW - 1 halo);
+        // stride S: the box traverses S x the pixels with element stride S
+        uint32_t box[4] = {atom_k, (uint32_t)(line_rows * S), (uint32_t)(k.tile_h * S), (uint32_t)tile_n};
+        uint32_t es[4] = {1, (uint32_t)S, (uint32_t)S, 1};
+        st = encode_map(&kr->tma_a, op->a, 4, dims, strides, box, swz, err, errlen, 0, es);
         if (b_resident(k, family)) {
             // resident weight panel: atom view {64, Cout, K/64}, one box {64, BN, K/64}
             const uint64_t d = (uint64_t)depth;
@@ -1477,19 +1525,20 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
         } else {
             uint64_t bd[2] = {(uint64_t)depth, (uint64_t)op->cols};
             uint64_t bs[1] = {(uint64_t)depth * 2};
-            uint32_t bb[2] = {atom_k, (uint32_t)k.bn};
+            uint32_t bb[2] = {atom_k, (uint32_t)(k.bn / k.cg)};     // a CTA pair splits B's rows
             if (!st) st = encode_map(&kr->tma_b, op->b, 2, bd, bs, bb, swz, err, errlen);
         }
         if (!st) {
             // output NHWC {Cout, Wo, Ho, N}; a 32-pixel epilogue chunk of the
             // TILE_N x TILE_H x TILE_W tile is the box {EPI_COLS, bw, bh, bn}
-            // (halo lines: one box per line, {EPI_COLS, TILE_W, 1, 1}; the
-            // chunk's junk rows are never stored)
+            // (halo / padded lines: one box per line, {EPI_COLS, TILE_W, 1, 1};
+            // the chunk's junk rows are never stored)
+            const bool lines = hkw || k.line;
             const int ob = op->out_f32 ? 4 : 2, ec = epi_cols(k, op->out_f32);
-            const int bw = hkw ? k.tile_w : std::min(k.tile_w, 32);
-            const int bh = hkw ? 1 : k.tile_w >= 32 ? 1 : std::min(k.tile_h, 32 / k.tile_w);
-            const int bn = hkw ? 1 : k.tile_w * k.tile_h >= 32 ? 1 : 32 / (k.tile_w * k.tile_h);
-            if (!hkw && (bw * bh * bn != 32 || k.tile_w % bw || k.tile_h % bh || tile_n % bn)) {
+            const int bw = lines ? k.tile_w : std::min(k.tile_w, 32);
+            const int bh = lines ? 1 : k.tile_w >= 32 ? 1 : std::min(k.tile_h, 32 / k.tile_w);
+            const int bn = lines ? 1 : k.tile_w * k.tile_h >= 32 ? 1 : 32 / (k.tile_w * k.tile_h);
+            if (!lines && (bw * bh * bn != 32 || k.tile_w % bw || k.tile_h % bh || tile_n % bn)) {
                 put_err(err, errlen, "conv tile %dx%d cannot be stored in 32-pixel boxes", k.tile_h, k.tile_w);
                 st = OPEVO_INVALID_CONFIG;
             } else {
@@ -1500,9 +1549,9 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
                 st = encode_map(&kr->tma_c, op->c, 4, cd, cs, cb, ec * ob, err, errlen, op->out_f32);
             }
         }
-        kr->sched = SchedHost{(N / tile_n) * (HO / k.tile_h) * (WO / k.tile_w), (int)col_tiles, 1,
+        kr->sched = SchedHost{(N / pair_n) * (HO / k.tile_h) * (WO / k.tile_w), (int)col_tiles, 1,
                               k.split, 0, 1, 0};
-        if (hkw) kr->kdepth = KH * C;       // the K loop runs over filter rows x channel blocks
+        if (hkw) kr->kdepth = KH * CP;      // the K loop runs over filter rows x channel blocks
     } else {
         const uint32_t a_rows = (uint32_t)((k.cg == 2 ? 128 : k.bm) / k.cluster);
         const uint32_t b_rows = (uint32_t)(k.bn / k.cg);

@@ -86,13 +86,15 @@ class Knobs:
     grid: int = 0
     b_res: int = 0           # conv: weight panel resident in shared memory
     bpu: int = 1             # BatchMatMul: batches per work unit
+    line: int = 0            # conv: padded lines of 16 / 32 tile rows (0: dense tile / halo)
     panel_bytes: int = 0     # size of the resident panel (BN x K x 2; not a code knob)
     family: int = 0          # kernel family / batched operator (set by the mapping; decide
     batched: int = 0         # which split-K reduction is compiled in)
 
     def as_tuple(self) -> tuple[int, ...]:
         return (self.bm, self.bn, self.bk, self.stages, self.split, self.cluster,
-                self.tile_h, self.tile_w, self.acc, self.cta_group, self.grid, self.b_res, self.bpu)
+                self.tile_h, self.tile_w, self.acc, self.cta_group, self.grid, self.b_res, self.bpu,
+                self.line)
 
     def tma_split(self) -> int:
         """Split factor compiled in when the K slices reduce through fp32
@@ -111,7 +113,7 @@ class Knobs:
         ld = self.bn + 4
         red = self.bm * ld * 4 + (s - 1) * (self.bm // max(s, 1)) * ld * 4
         ok = (s in (2, 4, 8) and self.cta_group == 1 and self.cluster == 1 and self.bm == 128
-              and not self.tma_split()
+              and not self.tma_split() and not (self.family == FAMILY_CONV and self.line)
               and _align1k(red) + epi_bytes(self.bn, self.family == FAMILY_TF32X3) + SMEM_EXTRA
               <= SMEM_LIMIT)
         return s if ok else 0
@@ -120,24 +122,30 @@ class Knobs:
         """Conv "halo lines" (mirrors ``halo_kw`` in csrc/opevo.cpp): a tile
         width that does not divide BM marks lines of 17 - KW pixels padded to
         16 rows, one TMA box per filter row; returns KW, else 0."""
-        if (self.family == FAMILY_CONV and 1 <= self.tile_w < 16 and self.tile_h >= 1
-                and self.bm % (self.tile_h * self.tile_w)):
+        if (self.family == FAMILY_CONV and self.line == 0 and 1 <= self.tile_w < 16 and self.tile_h >= 1
+                and self.bm_cta % (self.tile_h * self.tile_w)):
             return 17 - self.tile_w
         return 0
+
+    @property
+    def bm_cta(self) -> int:
+        """Tile rows one CTA holds (a CTA pair splits BM = 256 in two)."""
+        return 128 if self.cta_group == 2 else self.bm
 
     def compile_key(self) -> tuple[int, ...]:
         """Fields that change the generated code (split-K is a launch arg
         except for DSMEM-reduced splits)."""
         return (self.bm, self.bn, self.bk, self.stages, self.cluster, self.tile_h, self.tile_w,
-                self.acc, self.cta_group, self.dsmem_split(), self.tma_split(), self.b_res, self.bpu)
+                self.acc, self.cta_group, self.dsmem_split(), self.tma_split(), self.b_res, self.bpu,
+                self.line)
 
     def smem_bytes(self) -> int:
         """Mirrors ``smem_bytes`` in csrc/opevo.cpp (bf16 output)."""
         if self.b_res:
             return _align1k(self.bm * self.bk * 2 * self.stages) + epi_bytes(self.bn) + 2048 + self.panel_bytes
         if self.halo_kw():
-            return (_align1k((self.bm + self.halo_kw() * self.bn) * self.bk * 2 * self.stages)
-                    + epi_bytes(self.bn) + SMEM_EXTRA)
+            return (_align1k((self.bm_cta + self.halo_kw() * self.bn // self.cta_group) * self.bk * 2
+                             * self.stages) + epi_bytes(self.bn) + SMEM_EXTRA)
         x3 = self.family == FAMILY_TF32X3
         if x3:   # fp32 operands (bf16 pairs) staged twice: hi as landed + lo
             pipe = 2 * stage_bytes(self.bm, self.bn, 2 * self.bk) * self.stages
@@ -316,74 +324,104 @@ def _batches_per_unit(vals: dict, batch: int, bm: int, bn: int, bk: int, split: 
     return u
 
 
+def conv_channels_padded(cin: int) -> int:
+    """Cin in the conv kernels' layout: padded with zeros to a multiple of 16
+    (a pixel row must be >= 16 bytes for TMA and hold whole 32-byte UMMA K
+    steps; AlexNet conv1's Cin = 3 -> 16).  Mirrors op->cpad in csrc/opevo.cpp."""
+    return (cin + 15) // 16 * 16
+
+
 def _conv_knobs(spec: Conv2dSpec, vals: dict) -> tuple[Knobs | None, str]:
     co, ho, wo, ci = vals["co"], vals["ho"], vals["wo"], vals["ci"]
     kh, kw = vals["kh"], vals["kw"]
-    if spec.stride != 1:
-        return None, "strided convolution is not served by the TMA tiled implicit GEMM"
+    s_ = spec.stride
     bn = spec.out_channels // co[0]
     th, tw = spec.out_height // ho[0], spec.out_width // wo[0]
-    bk = spec.in_channels // ci[0]
-    # an even Cout virtual-thread split runs two M=128 atoms per K step:
-    # 256-pixel tiles, so each tap's activation box is twice as large (a TMA
-    # box costs about the same whatever its size, so this halves the boxes)
+    cpad = conv_channels_padded(spec.in_channels)
+    if cpad % ci[0]:
+        return None, f"BK = {cpad} padded channels / {ci[0]} is not whole"
+    bk = cpad // ci[0]
+    # an even Cout virtual-thread split runs 256-pixel tiles (each tap's
+    # activation box twice as large; a TMA box costs about the same whatever
+    # its size, so this halves the boxes): two M=128 atoms in one CTA, or --
+    # with an even H virtual-thread split -- a CTA pair (cta_group::2, each
+    # SM holds 128 pixel rows and half the weight tile)
     bm = 256 if co[1] % 2 == 0 else 128
+    cg = 2 if (bm == 256 and ho[1] % 2 == 0) else 1
+    bm_cta = 128 if cg == 2 else bm
     if bn % 16 or not 16 <= bn <= 256:
         return None, f"BN={bn} is not a UMMA column tile"
-    if bm == 256 and 2 * bn > 512:
+    if bm == 256 and cg == 1 and 2 * bn > 512:
         return None, "accumulator exceeds TMEM"
-    if tw + spec.kernel_w - 1 == 16 and bm % (th * tw):
-        return _conv_halo_knobs(spec, vals, bm, bn, bk, th, tw)
-    if th * tw > bm or bm % (th * tw):
-        return None, f"output tile {th}x{tw} does not divide {bm} pixels"
-    tn = bm // (th * tw)
-    if spec.batch % tn or tn > 256 or th > 256 or tw > 256:
-        return None, f"image tile {tn} does not divide the batch {spec.batch}"
     if not _bk_ok(bk):
         return None, f"BK={bk} channels is not a TMA/UMMA K stage"
+    if s_ == 1 and tw + spec.kernel_w - 1 == 16 and bm_cta % (th * tw):
+        return _conv_halo_knobs(spec, vals, bm, bn, bk, th, tw, cg)
     split = kh[0] * kw[0]
+    line = 0
+    if split > MAX_SPLIT:
+        return None, f"split over {split} filter taps exceeds the {MAX_SPLIT}-slice workspace"
+    if th * tw > bm_cta or bm_cta % (th * tw):
+        # padded lines: TILE_W <= LINE output pixels per line of LINE rows
+        # (TILE_N = floor(rows / (LINE x TILE_H)) images; rows past them are junk)
+        line = 16 if tw <= 16 else 32 if tw <= 32 else 0
+        if not line or line * th > bm_cta:
+            return None, f"output tile {th}x{tw} neither divides {bm_cta} pixels nor packs in lines"
+        tn = bm_cta // (line * th)
+        rows_w = line
+    else:
+        tn = bm_cta // (th * tw)
+        rows_w = tw
+    if spec.batch % (tn * cg) or tn > 256 or th > 256 or tw > 256:
+        return None, f"image tile {tn * cg} does not divide the batch {spec.batch}"
+    if rows_w * s_ > 256 or th * s_ > 256:
+        return None, f"stride {s_}: the activation box would exceed 256 pixels"
     want = UNROLL_TO_STAGES[vals["unroll_step"]]
-    if vals.get("unroll_explicit") == UNROLL_ON:
+    if vals.get("unroll_explicit") == UNROLL_ON and cg == 1:
         stages, panel = _conv_resident_fit(spec, bn, bk, split, want, bm)
         if stages:
-            return Knobs(bm, bn, bk, stages, split, 1, th, tw, b_res=1, panel_bytes=panel,
+            return Knobs(bm, bn, bk, stages, split, 1, th, tw, b_res=1, panel_bytes=panel, line=line,
                          family=FAMILY_CONV), ""
-    stages = _fit_stages(want, bm, bn, bk)
+    stages = _fit_stages(want, bm, bn, bk, cg)
     if stages < 1:
         return None, "one stage does not fit in shared memory"
-    return Knobs(bm, bn, bk, stages, split, 1, th, tw, family=FAMILY_CONV), ""
+    return Knobs(bm, bn, bk, stages, split, 1, th, tw, cta_group=cg, line=line, family=FAMILY_CONV), ""
 
 
 def _conv_halo_knobs(spec: Conv2dSpec, vals: dict, bm: int, bn: int, bk: int, th: int,
-                     tw: int) -> tuple[Knobs | None, str]:
+                     tw: int, cg: int = 1) -> tuple[Knobs | None, str]:
     """Halo lines: output lines of TILE_W = 17 - KW pixels, each padded to 16
     tile rows, so one TMA box {Cin block, 16, TILE_H, TILE_N} per filter row
-    serves all KW taps of that row (mirrors OPEVO_HALO in gemm_sm100.cuh)."""
+    serves all KW taps of that row (mirrors OPEVO_HALO in gemm_sm100.cuh).
+    On a CTA pair each CTA holds TILE_N of the pair's 2 x TILE_N images."""
     kh, kw = vals["kh"], vals["kw"]
-    if bm % (16 * th):
-        return None, f"BM={bm} does not hold 16-row lines x {th} rows"
-    tn = bm // (16 * th)
-    if spec.batch % tn or spec.padding >= spec.kernel_w:
-        return None, f"image tile {tn} does not divide the batch {spec.batch}"
+    bm_cta = 128 if cg == 2 else bm
+    if bm_cta % (16 * th):
+        return None, f"{bm_cta} rows do not hold 16-row lines x {th} rows"
+    tn = bm_cta // (16 * th)
+    if spec.batch % (tn * cg) or spec.padding >= spec.kernel_w:
+        return None, f"image tile {tn * cg} does not divide the batch {spec.batch}"
     if bk % 64 or kh[0] * kw[0] != 1:
         return None, "halo lines need BK a multiple of 64 and no split over taps"
     want = UNROLL_TO_STAGES[vals["unroll_step"]]
-    if vals.get("unroll_explicit") == UNROLL_ON:
+    if vals.get("unroll_explicit") == UNROLL_ON and cg == 1:
         stages, panel = _conv_resident_fit(spec, bn, bk, 1, want, bm)
         if stages:
             return Knobs(bm, bn, bk, stages, 1, 1, th, tw, b_res=1, panel_bytes=panel,
                          family=FAMILY_CONV), ""
-    stages = _fit_halo_stages(want, bm, bn, bk, spec.kernel_w)
+    stages = _fit_halo_stages(want, bm, bn, bk, spec.kernel_w, cg)
     if stages < 1:
         return None, "one stage does not fit in shared memory"
-    return Knobs(bm, bn, bk, stages, 1, 1, th, tw, family=FAMILY_CONV), ""
+    return Knobs(bm, bn, bk, stages, 1, 1, th, tw, cta_group=cg, family=FAMILY_CONV), ""
 
 
-def _fit_halo_stages(want: int, bm: int, bn: int, bk: int, kw: int) -> int:
+def _fit_halo_stages(want: int, bm: int, bn: int, bk: int, kw: int, cg: int = 1) -> int:
     """Stages of a streaming halo-lines conv: each holds the activation box
-    and the KW weight tiles of one filter row."""
+    and the KW weight tiles of one filter row (a CTA pair: 128 rows and half
+    of each weight tile per CTA)."""
+    rows = (128 if cg == 2 else bm) + kw * bn // cg
     s = want
-    while s > 0 and _align1k(s * (bm + kw * bn) * bk * 2) + epi_bytes(bn) + SMEM_EXTRA > SMEM_LIMIT:
+    while s > 0 and _align1k(s * rows * bk * 2) + epi_bytes(bn) + SMEM_EXTRA > SMEM_LIMIT:
         s -= 1
     return s
 
@@ -395,7 +433,7 @@ def _conv_resident_fit(spec: Conv2dSpec, bn: int, bk: int, split: int, want: int
     or (0, 0) when it does not apply (needs BN = Cout, BK a multiple of 64, no
     split over taps, the panel plus two stages within 227 KB).  Mirrors
     ``b_resident`` / the panel check in csrc/opevo.cpp."""
-    depth = spec.kernel_h * spec.kernel_w * spec.in_channels
+    depth = spec.kernel_h * spec.kernel_w * conv_channels_padded(spec.in_channels)
     if bn != spec.out_channels or bk % 64 or split != 1 or depth // 64 > 256:
         return 0, 0
     panel = bn * depth * 2

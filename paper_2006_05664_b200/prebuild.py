@@ -57,6 +57,42 @@ def _x3_instances(spec) -> set[tuple[int, bool, tuple]]:
     return out
 
 
+def _representatives(space, key) -> list:
+    """One value per distinct key(value) of a parameter space."""
+    seen = {}
+    for v in space.enumerate():
+        seen.setdefault(key(v), v)
+    return list(seen.values())
+
+
+def _conv_instances(spec) -> set[tuple[int, bool, tuple]]:
+    """Conv instances reachable from conv2d_space: the mapping itself
+    (mapping._conv_knobs) over one representative configuration per
+    combination of the parameter features it reads -- co[0], co[1] parity,
+    ho[0], ho[1] parity, wo[0], ci[0], kh[0] * kw[0], unroll settings."""
+    from .mapping import _conv_knobs
+    from .operators import conv2d_space
+
+    space = conv2d_space(spec)
+    sp = dict(zip(space.names, space.spaces))
+    reps = {
+        "co": _representatives(sp["co"], lambda v: (v[0], v[1] % 2)),
+        "ho": _representatives(sp["ho"], lambda v: (v[0], v[1] % 2)),
+        "wo": _representatives(sp["wo"], lambda v: v[0]),
+        "ci": _representatives(sp["ci"], lambda v: v[0]),
+        "kh": _representatives(sp["kh"], lambda v: v[0]),
+        "kw": _representatives(sp["kw"], lambda v: v[0]),
+        "unroll_explicit": list(sp["unroll_explicit"].labels),
+        "unroll_step": list(sp["unroll_step"].values),
+    }
+    out = set()
+    for combo in itertools.product(*(reps[n] for n in space.names)):
+        kn, _ = _conv_knobs(spec, dict(zip(space.names, combo)))
+        if kn is not None:
+            out.add((1, False, kn.as_tuple()))
+    return out
+
+
 def family_instances(spec, dtype: str = "bf16") -> set[tuple[int, bool, tuple]]:
     """All (family, batched, knobs) reachable from the operator's space."""
     out = set()
@@ -101,49 +137,7 @@ def family_instances(spec, dtype: str = "bf16") -> set[tuple[int, bool, tuple]]:
                                     if (kn.dsmem_split() or kn.tma_split()) and spec.k % (sp * bk) == 0:
                                         out.add((0, batched, kn.as_tuple()))
     elif isinstance(spec, Conv2dSpec):
-        if spec.stride != 1:
-            return out
-        ths = [t for t in _divisors(spec.out_height) if 128 % t == 0]
-        tws = [t for t in _divisors(spec.out_width) if 128 % t == 0]
-        for bm, th, tw in itertools.product((128, 256), ths, tws):
-            if th * tw > bm or bm % (th * tw) or spec.batch % (bm // (th * tw)):
-                continue
-            for bn in range(16, 257, 16):
-                if spec.out_channels % bn or (bm == 256 and 2 * bn > 512):
-                    continue
-                for bk in _divisors(spec.in_channels):
-                    if not _bk_ok(bk):
-                        continue
-                    for st in set(UNROLL_TO_STAGES.values()):
-                        s = _fit_stages(st, bm, bn, bk)
-                        if s >= 1:
-                            out.add((1, False, Knobs(bm, bn, bk, s, 1, 1, th, tw).as_tuple()))
-                        # weight-resident variant (unroll_explicit = on)
-                        rs, panel = _conv_resident_fit(spec, bn, bk, 1, st, bm)
-                        if rs:
-                            out.add((1, False, Knobs(bm, bn, bk, rs, 1, 1, th, tw, b_res=1,
-                                                     panel_bytes=panel).as_tuple()))
-        # halo lines: 17 - KW output pixels per 16-row line (mapping._conv_halo_knobs)
-        tw = 17 - spec.kernel_w
-        if 1 <= tw < 16 and spec.out_width % tw == 0 and spec.padding < spec.kernel_w:
-            for bm in (128, 256):
-                for th in _divisors(spec.out_height):
-                    if bm % (16 * th) or spec.batch % (bm // (16 * th)) or bm % (th * tw) == 0:
-                        continue
-                    for bn in range(16, 257, 16):
-                        if spec.out_channels % bn or (bm == 256 and 2 * bn > 512):
-                            continue
-                        for bk in _divisors(spec.in_channels):
-                            if bk % 64 or not _bk_ok(bk):
-                                continue
-                            for st in set(UNROLL_TO_STAGES.values()):
-                                s = _fit_halo_stages(st, bm, bn, bk, spec.kernel_w)
-                                if s >= 1:
-                                    out.add((1, False, Knobs(bm, bn, bk, s, 1, 1, th, tw).as_tuple()))
-                                rs, panel = _conv_resident_fit(spec, bn, bk, 1, st, bm)
-                                if rs:
-                                    out.add((1, False, Knobs(bm, bn, bk, rs, 1, 1, th, tw, b_res=1,
-                                                             panel_bytes=panel).as_tuple()))
+        out |= _conv_instances(spec)
     return out
 
 

@@ -111,11 +111,49 @@ def test_conv_halo_lines_mapping():
     bad = config_to_knobs(spec, sp, ((1, 1, 8, 8), (14, 1, 4, 1), (4, 2, 7, 1), (1, 64), (3, 1), (1, 3),
                                      "explicit_unroll_off", 64))
     assert not bad.valid
-    # a 5x5 filter needs 12-pixel lines, so 14-pixel tiles stay invalid for it
+    # a 5x5 filter's halo lines are 12 pixels wide, so 14-pixel tiles are
+    # padded lines for it instead (one box per tap, 16-row lines)
     spec5 = parse_operator("conv2d:32,64,56,56,64,5,5,1,2")
     sp5 = gpu_operator_space(spec5)
     cfg5 = ((1, 1, 8, 8), (14, 1, 4, 1), (4, 2, 7, 1), (1, 64), (1, 5), (1, 5), "explicit_unroll_off", 64)
-    assert not config_to_knobs(spec5, sp5, cfg5).valid
+    k5 = config_to_knobs(spec5, sp5, cfg5).knobs
+    assert k5.line == 16 and k5.halo_kw() == 0 and (k5.tile_h, k5.tile_w) == (4, 14)
+
+
+def test_conv_paper_operators_map():
+    """The paper's AlexNet convolutions: C1 (Cin = 3 padded
+    to 16, 11x11, stride 4) and C2 (5x5 on 27x27 outputs) map through padded
+    lines and strided activation boxes; valid fractions above 1 %."""
+    from paper_2006_05664_b200.mapping import conv_channels_padded, valid_fraction
+
+    c1 = parse_operator("conv2d:512,3,227,227,64,11,11,4,0")
+    sp1 = gpu_operator_space(c1)
+    assert conv_channels_padded(3) == 16 and (c1.out_height, c1.out_width) == (55, 55)
+    m = config_to_knobs(c1, sp1, ((1, 1, 8, 8), (55, 1, 1, 1), (5, 1, 11, 1), (1, 3), (1, 11), (1, 11),
+                                  "explicit_unroll_off", 64))
+    assert m.valid, m.reason
+    assert (m.knobs.bk, m.knobs.tile_h, m.knobs.tile_w, m.knobs.line) == (16, 1, 11, 16)
+    c2 = parse_operator("conv2d:512,64,27,27,192,5,5,1,2")
+    sp2 = gpu_operator_space(c2)
+    m2 = config_to_knobs(c2, sp2, ((3, 2, 4, 8), (27, 1, 1, 1), (1, 3, 3, 3), (1, 64), (1, 5), (1, 5),
+                                   "explicit_unroll_off", 512))
+    assert m2.valid, m2.reason
+    assert (m2.knobs.bn, m2.knobs.tile_w, m2.knobs.line, m2.knobs.bm, m2.knobs.cta_group) == (64, 27, 32, 256, 1)
+    assert valid_fraction(c1, sp1, 4000) > 0.01 and valid_fraction(c2, sp2, 4000) > 0.01
+
+
+def test_conv_cta_pair_mapping():
+    """An even co[1] (256-pixel tiles) with an even ho[1] runs on a CTA pair:
+    each CTA holds 128 pixel rows and half the weight tile."""
+    spec = parse_operator("conv2d:32,64,56,56,64,3,3,1,1")
+    sp = gpu_operator_space(spec)
+    halo = config_to_knobs(spec, sp, ((1, 2, 4, 8), (14, 2, 2, 1), (4, 2, 7, 1), (1, 64), (1, 3), (1, 3),
+                                      "explicit_unroll_off", 64)).knobs
+    assert (halo.bm, halo.cta_group, halo.tile_h, halo.tile_w, halo.halo_kw()) == (256, 2, 4, 14, 3)
+    assert halo.smem_bytes() == halo.stages * (128 + 3 * 32) * 64 * 2 + 32768 + 1280
+    dense = config_to_knobs(spec, sp, ((1, 2, 4, 8), (14, 2, 2, 1), (7, 1, 8, 1), (1, 64), (1, 3), (1, 3),
+                                       "explicit_unroll_on", 64)).knobs
+    assert dense.cta_group == 2 and dense.b_res == 0 and dense.bm == 256
 
 
 def test_bmm_mapping_is_batched():
@@ -151,11 +189,15 @@ def test_tf32x3_mapping():
 def test_every_valid_mapping_is_prebuilt():
     """Uniform samples that map must land in the enumerated (prebuilt) family."""
     for op in ("matmul:1024,1024,1024", "batchmatmul:960,128,64,128",
-               "conv2d:32,64,56,56,64,3,3,1,1"):
+               "conv2d:32,64,56,56,64,3,3,1,1", "conv2d:512,3,227,227,64,11,11,4,0",
+               "conv2d:512,64,27,27,192,5,5,1,2"):
         spec = parse_operator(op)
         sp = gpu_operator_space(spec)
         fam = {(f, b, tuple(k[:4]) + tuple(k[5:])) for f, b, k in family_instances(spec)}
-        assert any(k[9] == 2 for _, _, k in family_instances(spec)) == op.startswith("matmul")
+        # CTA pairs: MatMul 256-row tiles, conv 256-pixel tiles with an even
+        # ho[1] (BMM1 has 128 rows; 55 and 27 output rows have no factor 2)
+        assert any(k[9] == 2 for _, _, k in family_instances(spec)) == (
+            op.startswith("matmul") or op.startswith("conv2d:32"))
         rng = np.random.default_rng(0)
         hits = 0
         for _ in range(4000):
