@@ -20,7 +20,7 @@ from paper_2006_05664_b200 import EngineConfig, MatMulSpec, run
 from paper_2006_05664_b200.engine import FatalEvaluationError
 from paper_2006_05664_b200.evaluator import TrialInfo, WorkerFault
 from paper_2006_05664_b200.mapping import config_to_knobs, gpu_operator_space
-from paper_2006_05664_b200.scheduler import ShardedEvaluator, shard_indices
+from paper_2006_05664_b200.scheduler import ShardedEvaluator, ShmExchange, shard_indices
 
 SPEC = MatMulSpec(1024, 1024, 1024)
 
@@ -47,11 +47,12 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, shm=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     space = gpu_operator_space(SPEC)
-    ev = ShardedEvaluator(None, rank, world, local_fn=fake_infos(space, rank))
+    xchg = ShmExchange.create(rank, world) if shm else None
+    ev = ShardedEvaluator(None, rank, world, local_fn=fake_infos(space, rank), exchange=xchg)
     best, recs = run(space, EngineConfig(seed=5, budget=96), None, evaluator=ev)
     with open(os.path.join(out_dir, f"r{rank}.json"), "w") as fh:
         json.dump({"seq": [[r.config, r.fitness] for r in recs],
@@ -66,13 +67,15 @@ def test_shard_indices_partition():
             assert got == list(range(n))
 
 
-def test_two_rank_gloo_sharding_matches_single_process():
+@pytest.mark.parametrize("shm", [False, True])
+def test_two_rank_gloo_sharding_matches_single_process(shm):
+    """Through a gloo all-reduce and through the shared-memory exchange."""
     space = gpu_operator_space(SPEC)
     # single-process reference trajectory with the same fitness function
     local = fake_infos(space, 0)
     _, single = run(space, EngineConfig(seed=5, budget=96), lambda c: local([c])[0].fitness)
     with tempfile.TemporaryDirectory() as d:
-        tmp.start_processes(_worker, args=(2, _free_port(), d), nprocs=2, start_method="spawn")
+        tmp.start_processes(_worker, args=(2, _free_port(), d, shm), nprocs=2, start_method="spawn")
         r0 = json.load(open(os.path.join(d, "r0.json")))
         r1 = json.load(open(os.path.join(d, "r1.json")))
     want = [[r.config, r.fitness] for r in single]
@@ -110,7 +113,7 @@ def _fault_worker(rank, world, port, out_dir, mode):
         return inner(cfgs)
 
     repl = {}
-    ev = ShardedEvaluator(None, rank, world, local_fn=local,
+    ev = ShardedEvaluator(None, rank, world, local_fn=local, exchange=ShmExchange.create(rank, world),
                           respawn=lambda: repl.setdefault("r", _Replacement(space, rank, state["bad"])))
     result = {}
     try:
@@ -150,3 +153,36 @@ def test_two_rank_fatal_error_aborts_every_rank_together():
         r1 = json.load(open(os.path.join(d, "r1.json")))
     assert not r0["ok"] and not r1["ok"]
     assert "rank 1" in r0["error"] and "no NVRTC" in r1["error"]
+
+
+def _xchg_worker(rank, world, port, out_dir):
+    import numpy as np
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ex = ShmExchange.create(rank, world)
+    res = []
+    for g in range(200):                       # generations of different sizes
+        n = 1 + (g % 8)
+        rows = np.zeros((n, ex.cols))
+        rows[rank::world] = g + rank + 0.5
+        res.append(ex.allreduce(rows)[:, 0].tolist())
+    res.append([ex.max(float(rank * 3))])
+    with open(os.path.join(out_dir, f"x{rank}.json"), "w") as fh:
+        json.dump(res, fh)
+    ex.close()
+    dist.destroy_process_group()
+
+
+def test_shm_exchange_four_ranks():
+    """Every rank sees every rank's rows summed, generation after generation
+    (double buffering by parity), and the max over ranks."""
+    world = 4
+    with tempfile.TemporaryDirectory() as d:
+        tmp.start_processes(_xchg_worker, args=(world, _free_port(), d), nprocs=world, start_method="spawn")
+        got = [json.load(open(os.path.join(d, f"x{r}.json"))) for r in range(world)]
+    assert got[0] == got[1] == got[2] == got[3]
+    for g, row in enumerate(got[0][:-1]):
+        n = 1 + (g % 8)
+        assert row == [g + (i % world) + 0.5 for i in range(n)]
+    assert got[0][-1] == [9.0]
