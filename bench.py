@@ -777,7 +777,13 @@ def _ncu_traffic(op: str, knobs) -> float | None:
             d = json.load(fh)
     except (OSError, ValueError):
         return None
-    entry = d.get("kernels", {}).get(op + "|" + ",".join(map(str, knobs)))
+    kernels = d.get("kernels", {})
+    knobs = list(knobs)
+    entry = kernels.get(op + "|" + ",".join(map(str, knobs)))
+    if entry is None and len(knobs) == 14 and knobs[13] == 0:
+        # captures taken before the conv `line` slot (ABI 6) carry 13 knobs;
+        # line = 0 is the same kernel
+        entry = kernels.get(op + "|" + ",".join(map(str, knobs[:13])))
     return entry.get("dram_bytes") if entry else None
 
 

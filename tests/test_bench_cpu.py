@@ -36,3 +36,11 @@ def test_ncu_traffic_is_keyed_by_operator():
     kn = (128, 64, 128, 4, 1, 1, 1, 1, 1, 1, 0, 0, 1)
     assert bench._ncu_traffic("matmul:1024,1024,1024", kn) is not None
     assert bench._ncu_traffic("matmul:2048,2048,2048", kn) is None
+
+
+def test_ncu_traffic_accepts_the_14_slot_knobs():
+    # bench lines carry 14 knobs since the conv `line` slot (ABI 6); a capture
+    # keyed by the 13-slot tuple is the same kernel when line = 0
+    kn = (128, 64, 128, 4, 1, 1, 1, 1, 1, 1, 0, 0, 1, 0)
+    assert bench._ncu_traffic("matmul:1024,1024,1024", kn) is not None
+    assert bench._ncu_traffic("matmul:1024,1024,1024", kn[:13] + (16,)) is None
