@@ -1486,6 +1486,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                         *reinterpret_cast<float4*>(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
                 }
                 release();
+                if (epi_tid == 0) TRACE(12);
                 // generic-proxy smem writes -> visible to the bulk-copy (async) proxy
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 epi_bar();
@@ -1598,6 +1599,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
         // ---- DSMEM split-K reduction (one unit per cluster; slice kz == rank)
         // 2. every slice has staged its partial and finished its mainloop
         cluster_sync();
+        if (threadIdx.x == 0) TRACE(13);
         const float* own = reinterpret_cast<const float*>(smem);
         if (threadIdx.x == 0) {
             // push the row block each peer owns into that peer's RECV slot
@@ -1615,6 +1617,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
         }
         // 3. the peers' blocks of my rows have landed: sum in z order, write
         mbar_wait(smem_u32(red_bar), 0);
+        if (threadIdx.x == 0) TRACE(14);
         const Unit t = decode(u_first);
         const int col0 = t.col_tile * BN;
         const u64 c_batch = (u64)t.batch * (u64)rows * (u64)cols;
@@ -1661,6 +1664,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                   pack_bf16(acc[4], acc[5]), pack_bf16(acc[6], acc[7]));
 #endif
         }
+        if (threadIdx.x == 0) TRACE(7);
         // 4. my outgoing copies have finished reading `own`
         if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncthreads();
@@ -1668,6 +1672,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
 #endif
     if (threadIdx.x == 0) TRACE(8);
     if (CLSZ > 1) cluster_sync();
+    if (threadIdx.x == 0) TRACE(15);
     if (warp == 1) {
         __syncwarp();
         tc_fence_after();

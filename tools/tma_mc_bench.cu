@@ -35,6 +35,9 @@ __device__ __forceinline__ void wait_bar(u32 bar, u32 par) {
 __global__ void __launch_bounds__(64, 1) tma_mc(const __grid_constant__ CUtensorMap ma,
                                                 const __grid_constant__ CUtensorMap mb, int mode, int a_rows,
                                                 int b_rows, int K, int bk, int stages, int csz, u64* out) {
+    // (slot release: relaxed remote arrives -- nothing is read from the
+    // slots here; a real pipeline releases with tcgen05.commit's multicast
+    // arrive, which needs no cluster-scope fence either)
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     __shared__ __align__(8) u64 full[16];
     __shared__ __align__(8) u64 empty[16];
@@ -100,7 +103,7 @@ __global__ void __launch_bounds__(64, 1) tma_mc(const __grid_constant__ CUtensor
                 for (int r = 0; r < cl; ++r) {
                     u32 remote;
                     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(&empty[s])), "r"(r));
-                    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" :: "r"(remote) : "memory");
+                    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" :: "r"(remote) : "memory");
                 }
             } else {
                 asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&empty[s])) : "memory");
@@ -158,12 +161,14 @@ int main() {
     CK(cudaFuncSetAttribute(tma_mc, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     struct Cfg { int a_rows, b_rows, bk, stages; } cfgs[] = {
         {128, 64, 128, 4}, {128, 64, 64, 6}, {128, 64, 256, 2}, {128, 32, 128, 4}, {128, 128, 128, 3}};
-    for (auto c : cfgs) {
+    for (auto& c : cfgs) {
         for (int mode = 0; mode < 3; ++mode) {
-            for (int csz : {1, 2, 4, 8}) {
+            for (int gc : {1001, 1032, 1064, 1128, 1148, 2, 4, 8}) {
+                const int csz = gc > 1000 ? 1 : gc;
+                const int grid = gc > 1000 ? gc - 1000 : 128;
                 if ((mode < 2) != (csz == 1)) continue;
+                if (mode < 2 && grid != 128 && &c != &cfgs[0]) continue;
                 if (mode == 2 && (c.a_rows / csz) % 8) continue;
-                const int grid = 128;
                 CUtensorMap ma = mode == 0 ? map3(a, N, K, c.a_rows, c.bk / 64)
                                            : map4(a, N, K, mode == 2 ? c.a_rows / csz : c.a_rows, c.bk / 64);
                 CUtensorMap mb = mode == 0 ? map3(b, N, K, c.b_rows, c.bk / 64) : map4(b, N, K, c.b_rows, c.bk / 64);
@@ -189,8 +194,8 @@ int main() {
                 cyc /= grid; ns /= grid;
                 const double bytes = (double)(c.a_rows + c.b_rows) * K * 2;     // received per CTA
                 const double issued = (double)((mode == 2 ? c.a_rows / csz : c.a_rows) + c.b_rows) * K * 2;
-                printf("%-12s csz %d  A%3d+B%3d BK%3d st%d: recv %6.1f B/clk/SM (issued %6.1f)  loop %.2f us (slowest %.2f)  chip recv %.1f TB/s\n",
-                       mode == 0 ? "atom-major" : mode == 1 ? "group-major" : "group+mc", csz, c.a_rows, c.b_rows,
+                printf("%-12s grid %3d csz %d  A%3d+B%3d BK%3d st%d: recv %6.1f B/clk/SM (issued %6.1f)  loop %.2f us (slowest %.2f)  chip recv %.1f TB/s\n",
+                       mode == 0 ? "atom-major" : mode == 1 ? "group-major" : "group+mc", grid, csz, c.a_rows, c.b_rows,
                        c.bk, c.stages, bytes / cyc, issued / cyc, ns / 1e3, mx / 1e3, grid * bytes / mx / 1e3);
             }
         }

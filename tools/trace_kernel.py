@@ -20,7 +20,11 @@ PHASES = [("launch skew", None, 1), ("setup", 1, 2), ("pdl wait", 2, 9),
           ("  wait->empty ok", 9, 10), ("  ->expect_tx", 10, 11), ("  ->TMAs issued", 11, 3),
           ("  epi: first LDTM", 6, 12), ("  epi: first stores", 12, 13), ("first TMA issue", 9, 3),
           ("first stage landed", 3, 4), ("mainloop", 4, 5), ("accum->epi", 5, 6),
-          ("epilogue", 6, 7), ("exit sync", 7, 8), ("CTA total", 1, 8)]
+          ("epilogue", 6, 7), ("exit sync", 7, 8), ("CTA total", 1, 8),
+          # DSMEM split-K reduction (OPEVO_SPLIT_CLUSTER): stage own partial,
+          # cluster sync, peers' blocks landed, sum + store; then exit sync
+          ("dsmem: stage own", 6, 12), ("dsmem: cluster sync", 12, 13), ("dsmem: recv wait", 13, 14),
+          ("dsmem: sum+store", 14, 7), ("final cluster sync", 8, 15)]
 
 
 def main():
