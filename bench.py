@@ -589,15 +589,21 @@ def main() -> None:
         ncu_op = ("" if args.dtype == "bf16" else args.dtype + ":") + args.op
         if args.dtype == "bf16" and spec.flops() / nbytes < pk["tflops"] * 1e3 / pk["hbm_gbs"]:
             # below the ridge (BMM 960x128x64x128: AI 32): HBM-bound roofline,
-            # measured with the operands coming from HBM (L2 flushed before
-            # every launch, each launch timed alone); the L2-warm figure the
-            # fitness uses is reported beside it
-            gbs = nbytes / (ms_cold * 1e-3) / 1e9
+            # measured with the operands coming from HBM -- back-to-back
+            # launches cycling over operand copies that together span more
+            # than 2x the L2 (every launch's operands were evicted since their
+            # last use); the single-launch cold figure (L2 flushed before each
+            # launch) and the L2-warm figure the fitness uses ride along
+            ms_rot, ncopies = hbm_fed_time(local_ev, spec, settings, best_knobs, nbytes)
+            gbs = nbytes / (ms_rot * 1e-3) / 1e9
             roof = {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
                     "frac": gbs / pk["hbm_gbs"], "traffic": _ncu_traffic(ncu_op, best_knobs),
                     "peak_source": f"{pk['source']} HBM copy bandwidth (MEASURED_PEAKS.json)",
-                    "kernel_ms": ms_cold, "timing": "cold L2, single launches",
+                    "kernel_ms": ms_rot,
+                    "timing": (f"HBM-fed: {16 * ncopies} back-to-back launches in one CUDA graph cycling "
+                               f"over {ncopies} operand copies ({ncopies * nbytes / 1e6:.0f} MB > 2x L2)"),
                     "per_launch_bytes": nbytes,
+                    "single_launch_cold_l2": {"kernel_ms": ms_cold, "gbs": nbytes / (ms_cold * 1e-3) / 1e9},
                     "l2_warm": {"kernel_ms": ms, "gbs": nbytes / (ms * 1e-3) / 1e9, "tflops": ach}}
         else:
             roof = {"bound": "fp32-fma" if args.dtype == "f32" else "tensor", "achieved": ach,
@@ -653,7 +659,7 @@ def main() -> None:
                                          f"launch; a candidate slower than {settings.loser_ratio}x "
                                          f"the fastest verified one gets {settings.loser_reps} "
                                          f"launches), L2 {args.l2} (operands fit in L2)",
-                       "l2_between_steps": "flushed: a 256 MB write (2x L2) before every timed "
+                       "l2_between_steps": "flushed: a 256 MB read pass (2x L2, leaves only clean lines) before every timed "
                                            "step; within a trial the fitness is L2-warm "
                                            "back-to-back launches (use --l2 cold to flush "
                                            "before every timed launch)",
@@ -732,6 +738,28 @@ def cold_cache_record(spec, space, settings, device: int, args, budget: int = 50
     finally:
         ev.close()
         shutil.rmtree(tmp, ignore_errors=True)
+
+
+def hbm_fed_time(ev, spec, settings, knobs, nbytes: int, l2_bytes: int = 126 << 20) -> tuple[float, int]:
+    """ms per launch of `knobs` with its operands streamed from HBM: the
+    instance bound to n freshly prepared operand copies (n x bytes > 2x L2,
+    n >= 3) and launched back to back, cycling over them
+    (capi.time_rotating)."""
+    from paper_2006_05664_b200 import capi
+    from paper_2006_05664_b200.evaluator import _op_args
+
+    n = max(3, -(-2 * l2_bytes // nbytes) + 1)
+    ops = [ev.dev.prepare(dtype=settings.dtype, seed=settings.seed + 1 + i, **_op_args(spec)) for i in range(n)]
+    ks = []
+    try:
+        ks = [ev.dev.kernel(o, knobs) for o in ops]
+        ms = min(capi.time_rotating(ks, warmup=1, reps=16 * n) for _ in range(3))
+    finally:
+        for k in ks:
+            k.close()
+        for o in ops:
+            o.close()
+    return ms, n
 
 
 def _dtype_peak(dtype: str, pk: dict) -> float:

@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define OPEVO_ABI_VERSION 6   /* 6: 14-slot knobs (conv padded lines), conv stride / narrow Cin, conv CTA pairs; 5: timing policy, native search core */
+#define OPEVO_ABI_VERSION 7   /* 7: opevo_kernels_time_rotating; 6: 14-slot knobs (conv padded lines), conv stride / narrow Cin, conv CTA pairs; 5: timing policy, native search core */
 
 enum opevo_status {
     OPEVO_OK = 0,
@@ -185,6 +185,17 @@ int opevo_kernel_check(opevo_kernel* k, double tol, double* rel_err, char* err, 
 int opevo_kernel_time(opevo_kernel* k, int warmup, int reps, int flush_l2, double* ms_per_launch,
                       char* err, size_t errlen);
 
+/* HBM-fed back-to-back timing for operators below the ridge: `reps` launches
+ * cycling through `n` kernels of the same instance bound to n distinct
+ * operand copies (one opevo_op each, prepared alike) in one CUDA graph, PDL
+ * between launches as in every other mode.  With n copies spanning more than
+ * twice the L2, each launch's operands were evicted since their last use, so
+ * the kernel streams them from HBM while its prologue still overlaps the
+ * previous launch -- the steady state of a tuned kernel in a pipeline whose
+ * working set does not fit in L2.  All kernels must belong to one context. */
+int opevo_kernels_time_rotating(opevo_kernel* const* ks, int n, int warmup, int reps,
+                                double* ms_per_launch, char* err, size_t errlen);
+
 /* One complete trial: get + check (tol) + time, with one host synchronisation
  * before the timed launches.  Fitness in res->tflops. */
 int opevo_trial(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nknobs, int warmup,
@@ -225,8 +236,9 @@ int opevo_kernel_trace(opevo_kernel* k, uint64_t* host, size_t count, char* err,
  * operator so far gets loser_reps timed launches and no extra warm-up. */
 int opevo_ctx_set_timing(opevo_ctx* ctx, double budget_ms, double loser_ratio, int loser_reps);
 
-/* Write a 256 MB buffer (2x L2) on the context's stream so the next work
- * starts with a cold L2; returns after the flush completes. */
+/* Read a 256 MB buffer (2x L2) on the context's stream so the next work
+ * starts with a cold L2 holding only clean lines (no write-backs land on the
+ * next work); returns after the flush completes. */
 int opevo_ctx_flush_l2(opevo_ctx* ctx, char* err, size_t errlen);
 
 /* Pinned host memory for honest end-to-end copies. */

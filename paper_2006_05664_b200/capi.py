@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libopevo.so")
 DEFAULT_CACHE = os.path.join(HERE, "kernel_cache")
 
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 # status codes (opevo.h)
 OK = 0
@@ -48,7 +48,8 @@ EXPORTS = (
     "opevo_op_sizes", "opevo_op_upload", "opevo_op_download", "opevo_op_read_inputs",
     "opevo_op_reference",
     "opevo_op_refresh_reference", "opevo_kernel_get", "opevo_kernel_release",
-    "opevo_kernel_run", "opevo_kernel_check", "opevo_kernel_time", "opevo_trial",
+    "opevo_kernel_run", "opevo_kernel_check", "opevo_kernel_time", "opevo_kernels_time_rotating",
+    "opevo_trial",
     "opevo_kernel_trace", "opevo_ctx_flush_l2", "opevo_host_alloc", "opevo_host_free",
     "opevo_op_preload", "opevo_trial_batch", "opevo_ctx_set_timing",
     # native OpEvo proposal core (bound in native.py)
@@ -121,6 +122,7 @@ def load() -> C.CDLL:
         "opevo_kernel_run": (I, [P, cp, sz]),
         "opevo_kernel_check": (I, [P, D, dp, cp, sz]),
         "opevo_kernel_time": (I, [P, I, I, I, dp, cp, sz]),
+        "opevo_kernels_time_rotating": (I, [C.POINTER(P), I, I, I, dp, cp, sz]),
         "opevo_trial": (I, [P, P, i32p, I, I, I, I, D, C.POINTER(TrialResult), cp, sz]),
         "opevo_kernel_trace": (I, [P, C.POINTER(C.c_uint64), sz, cp, sz]),
         "opevo_ctx_flush_l2": (I, [P, cp, sz]),
@@ -404,6 +406,20 @@ class Kernel:
         _check(self.dev.lib.opevo_kernel_time(self.handle, warmup, reps, int(flush_l2),
                                               C.byref(ms), err, len(err)), err)
         return ms.value
+
+
+def time_rotating(kernels: "list[Kernel]", warmup: int = 1, reps: int = 64) -> float:
+    """ms per launch of `reps` back-to-back launches cycling through kernels
+    of one instance bound to distinct operand copies (HBM-fed steady state;
+    ``opevo_kernels_time_rotating``)."""
+    if not kernels:
+        raise ValueError("no kernels")
+    arr = (C.c_void_p * len(kernels))(*[k.handle for k in kernels])
+    ms = C.c_double()
+    err = _errbuf()
+    lib = kernels[0].dev.lib
+    _check(lib.opevo_kernels_time_rotating(arr, len(kernels), warmup, reps, C.byref(ms), err, len(err)), err)
+    return ms.value
 
 
 class PinnedBuffer:

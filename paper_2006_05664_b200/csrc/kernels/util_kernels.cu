@@ -213,9 +213,20 @@ extern "C" __global__ void opevo_compare(const void* __restrict__ C, const float
 }
 
 // Streams a buffer larger than L2 so the next timed launch starts cold.
+// A READ pass over a 2x-L2 buffer: every resident line is evicted (dirty
+// ones -- the previous launch's output -- are written back now, during the
+// flush) and L2 is left holding clean lines of this buffer, so the timed
+// launch's misses cost no write-backs.  (A write pass would leave 126 MB of
+// dirty lines whose write-back then shares HBM with the timed launch's
+// reads: measured as half the HBM bandwidth for an HBM-bound operator.)
 extern "C" __global__ void opevo_flush(uint4* buf, u64 n16, u32 salt) {
-    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n16; i += (u64)gridDim.x * blockDim.x)
-        buf[i] = make_uint4(salt, (u32)i, salt, (u32)(i >> 32));
+    uint4 acc = make_uint4(0u, 0u, 0u, 0u);
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n16; i += (u64)gridDim.x * blockDim.x) {
+        const uint4 v = __ldcg(buf + i);
+        acc.x ^= v.x; acc.y ^= v.y; acc.z ^= v.z; acc.w ^= v.w;
+    }
+    // keeps the loads (never true in practice; the buffer is scratch anyway)
+    if (acc.x == salt && acc.y == 0x9E3779B9u && acc.z == ~salt && acc.w == 0x7F4A7C15u) buf[0] = acc;
 }
 
 // Launch gate for timing: the stream stalls here while the host enqueues the

@@ -1863,7 +1863,8 @@ int time_graph(opevo_kernel* k, CUgraphExec ge, double* total_ms, char* err, siz
     return OPEVO_OK;
 }
 
-// Cold-L2 timing: a 2x-L2 write before every launch, each launch timed alone.
+// Cold-L2 timing: a 2x-L2 read pass (opevo_flush: clean lines only, so the
+// timed launch pays no write-backs) before every launch, each timed alone.
 int time_flushed(opevo_kernel* k, int reps, double* total_ms, char* err, size_t errlen) {
     opevo_ctx* ctx = k->op->ctx;
     if (!ctx->flush_buf) {
@@ -1995,6 +1996,40 @@ int opevo_kernel_check(opevo_kernel* k, double tol, double* rel_err, char* err, 
     if (!st) st = sync_checked(ctx, "check", err, errlen);
     if (!st) st = finish_check(k, tol < 0 ? 0.0 : tol, rel_err, err, errlen);
     return st;
+}
+
+int opevo_kernels_time_rotating(opevo_kernel* const* ks, int n, int warmup, int reps, double* ms_per_launch,
+                                char* err, size_t errlen) {
+    if (!ks || n < 1 || reps < 1 || warmup < 0 || !ms_per_launch) return OPEVO_ERR_ARG;
+    for (int i = 0; i < n; ++i)
+        if (!ks[i] || ks[i]->op->ctx != ks[0]->op->ctx) return OPEVO_ERR_ARG;
+    opevo_ctx* ctx = ks[0]->op->ctx;
+    g_cu.CtxSetCurrent(ctx->cu);
+    CUgraph g = nullptr;
+    CUgraphExec ge = nullptr;
+    CU_TRY(ctx, g_cu.StreamBeginCapture(ctx->cap_stream, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL), "capture");
+    int st = OPEVO_OK;
+    for (int i = 0; i < reps && !st; ++i) st = launch_kernel(ks[i % n], err, errlen, ctx->cap_stream);
+    CUresult r = g_cu.StreamEndCapture(ctx->cap_stream, &g);
+    if (!st && r == CUDA_SUCCESS) r = g_cu.GraphInstantiate(&ge, g, 0);
+    if (g) g_cu.GraphDestroy(g);
+    if (st) return st;
+    if (r != CUDA_SUCCESS) return fail_cu(ctx, r, "graph", err, errlen);
+    double total = 0.0;
+    // warm-up passes of the whole cycle (module, instruction caches, TLBs);
+    // they do not warm the L2 for the timed pass: every copy is evicted again
+    // before the cycle comes back to it
+    for (int w = 0; w < warmup && !st; ++w) {
+        r = g_cu.GraphLaunch(ge, ctx->stream);
+        if (r != CUDA_SUCCESS) st = fail_cu(ctx, r, "graph", err, errlen);
+    }
+    if (!st) st = time_graph(ks[0], ge, &total, err, errlen);
+    if (!st) st = sync_checked(ctx, "rotating timing", err, errlen);
+    g_cu.GraphExecDestroy(ge);
+    if (st) return st;
+    for (int i = 0; i < reps; ++i) ks[i % n]->launches += warmup + 1;
+    *ms_per_launch = total / reps;
+    return OPEVO_OK;
 }
 
 int opevo_kernel_time(opevo_kernel* k, int warmup, int reps, int flush_l2, double* ms_per_launch, char* err,

@@ -319,3 +319,41 @@ def test_kernel_time_runs_requested_reps(dev, mm1024):
         assert 0 < ms < 1.0
     finally:
         k.close()
+
+
+def test_rotating_timing_streams_from_hbm(dev, bmm1):
+    """opevo_kernels_time_rotating (bench.py's HBM-fed roofline for BMM1):
+    cycling over operand copies spanning > 2x L2 must read from HBM -- no
+    faster than the L2-warm chain, and the implied bandwidth no higher than
+    HBM can deliver -- and every copy's output must still verify."""
+    import json
+    import os
+
+    from paper_2006_05664_b200 import capi
+
+    op, ref = bmm1
+    knobs = (128, 64, 64, 6, 1, 1, 1, 1, 1, 1, 0, 0, 1)
+    b, n, m, k = BMM1
+    nbytes = 2 * b * (n * k + m * k + n * m)
+    copies = [dev.prepare(capi.BATCHMATMUL, batch=b, rows=n, cols=m, depth=k, seed=SEED) for _ in range(5)]
+    ks = [dev.kernel(o, knobs) for o in copies]
+    try:
+        warm = dev.kernel(op, knobs)
+        ms_warm = warm.time(warmup=3, reps=80)
+        warm.close()
+        ms_rot = capi.time_rotating(ks, warmup=1, reps=80)
+        for kk in ks:
+            assert kk.check() < BF16_TOL
+        gbs = nbytes / (ms_rot * 1e-3) / 1e9
+        peak = 8000.0
+        path = os.path.join(os.path.dirname(os.path.dirname(__file__)), "MEASURED_PEAKS.json")
+        if os.path.exists(path):
+            with open(path) as fh:
+                peak = json.load(fh).get("hbm_gbs", peak)
+        assert ms_rot >= 0.95 * ms_warm, (ms_rot, ms_warm)
+        assert gbs <= 1.1 * peak, (gbs, peak)
+    finally:
+        for kk in ks:
+            kk.close()
+        for o in copies:
+            o.close()
