@@ -334,7 +334,9 @@ def main() -> None:
     ap.add_argument("--loser-ratio", type=float, default=1.5,
                     help="straggler rule: candidates slower than this x the fastest verified one "
                          "are timed with 5 launches (0: off)")
-    ap.add_argument("--l2", default="warm", choices=("warm", "cold"))
+    ap.add_argument("--l2", default="auto", choices=("auto", "warm", "cold"),
+                    help="fitness launches with a warm L2, or each after an L2 flush (cold); auto: "
+                         "cold for bf16 operators below the ridge (HBM-bound: BMM1), warm otherwise")
     ap.add_argument("--timing", default="stream", choices=("graph", "stream"),
                     help="fitness launches: stream launches released together by a device gate "
                          "(default) or one CUDA graph")
@@ -390,6 +392,13 @@ def main() -> None:
 
     spec = parse_operator(args.op)
     space = gpu_operator_space(spec, args.dtype)
+    if args.l2 == "auto":
+        # tune in the regime the operator's roofline describes: an HBM-bound
+        # operator's fitness is its launch with the operands coming from HBM
+        pk0 = peaks()
+        below = (args.dtype == "bf16"
+                 and spec.flops() / algo_bytes(spec, 2) < pk0["tflops"] * 1e3 / pk0["hbm_gbs"])
+        args.l2 = "cold" if below else "warm"
     settings = EvalSettings(reps=args.reps, preload_family=not args.no_preload,
                             flush_l2=1 if args.l2 == "cold" else (2 if args.timing == "stream" else 0),
                             dtype=DTYPES[args.dtype], loser_ratio=args.loser_ratio)
@@ -648,7 +657,9 @@ def main() -> None:
                        "ask": "python" if args.python_ask else "native (csrc/search.cpp)",
                        "space": ("reference operator space (fp32 SIMT family)" if args.dtype == "f32"
                                  else "reference operator space + stages (mapping.py)"),
-                       "fitness_timing": (f"{settings.reps} back-to-back launches in one CUDA graph"
+                       "fitness_timing": (f"{settings.reps} launches, each after a 2x-L2 read pass and "
+                                          f"timed alone" if args.l2 == "cold" else
+                                          f"{settings.reps} back-to-back launches in one CUDA graph"
                                           if args.timing == "graph" else
                                           f"{settings.reps} back-to-back stream launches released "
                                           f"by a device gate")
@@ -658,7 +669,9 @@ def main() -> None:
                                          f"verified launch alone exceeds it is timed by that "
                                          f"launch; a candidate slower than {settings.loser_ratio}x "
                                          f"the fastest verified one gets {settings.loser_reps} "
-                                         f"launches), L2 {args.l2} (operands fit in L2)",
+                                         (f"launches), L2 warm (operands fit in L2)" if args.l2 == "warm" else
+                                            "launches), L2 cold: every timed launch after a 2x-L2 "
+                                            "read pass, timed alone (HBM-bound operator)"),
                        "l2_between_steps": "flushed: a 256 MB read pass (2x L2, leaves only clean lines) before every timed "
                                            "step; within a trial the fitness is L2-warm "
                                            "back-to-back launches (use --l2 cold to flush "

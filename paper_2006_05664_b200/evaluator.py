@@ -242,7 +242,12 @@ class GpuEvaluator:
         top = sorted(best.items(), key=lambda kv: -kv[1])[:k]
         if not top:
             return []
-        mode = int(self.settings.flush_l2 if mode is None else mode)
+        if mode is None:
+            # the gated-stream fitness (mode 2) is confirmed as one CUDA graph
+            # of back-to-back launches (mode 0): the kernel's own rate without
+            # stream-launch gaps (~6 % at 1024^3, profiles/round2/
+            # timing_modes.txt); a cold-L2 fitness (mode 1) is confirmed cold
+            mode = 0 if int(self.settings.flush_l2) == 2 else int(self.settings.flush_l2)
         kernels = [self.dev.kernel(self.op, kn) for kn, _ in top]
         times: list[list[float]] = [[] for _ in top]
         try:
