@@ -526,7 +526,7 @@ def main() -> None:
 
     # ---------------- confirm the best instance: re-time the top distinct
     # instances (noise must not decide between near-equal kernels)
-    confirmed = local_ev.confirm_top(k=5, reps=100, rounds=5) if best.fitness > 0 and healthy else []
+    confirmed = local_ev.confirm_top(k=10, reps=100, rounds=5) if best.fitness > 0 and healthy else []
 
     # ---------------- e2e: the same generations (a fresh engine, same seed:
     # warm-ups untimed, then the K timed ones) through the public API, with

@@ -16,6 +16,10 @@ from paper_2006_05664_b200.native import NativeOpEvo  # noqa: E402
 
 def main():
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    # --target=KNOBS: report whether each run visited that instance (e.g. the
+    # family optimum from tools/sweep_family.py) and its best search fitness
+    target = next((tuple(int(x) for x in a.split("=", 1)[1].split(",")) for a in sys.argv[1:]
+                   if a.startswith("--target=")), None)
     op, s0, s1 = args[0], int(args[1]), int(args[2])
     budget = int(args[3]) if len(args) > 3 else 500
     spec = parse_operator(op)
@@ -35,11 +39,16 @@ def main():
             eng.tell(list(zip(a.configs, ev.evaluate(a.configs))))
             n += len(a.configs)
         wall = time.perf_counter() - t0
-        conf = ev.confirm_top(k=5, reps=100, rounds=5)
+        conf = ev.confirm_top(k=10, reps=100, rounds=5)
         row = {"seed": seed, "trials": n, "wall_s": wall, "search_best": eng.best().fitness,
                "confirmed_best": conf[0]["tflops"] if conf else 0.0,
                "best_knobs": conf[0]["knobs"] if conf else None,
-               "top": [(c["knobs"][:10], round(c["tflops"], 1)) for c in conf]}
+               "top": [(c["knobs"][:10], round(c["tflops"], 1)) for c in conf[:5]]}
+        if target is not None:
+            fits = [h.fitness for h in ev.history
+                    if h.knobs is not None and tuple(h.knobs)[:len(target)] == target]
+            row["target_visits"] = len(fits)
+            row["target_best_search_fitness"] = max(fits, default=0.0)
         rows.append(row)
         print(json.dumps(row), flush=True)
     best = max(r["confirmed_best"] for r in rows)
