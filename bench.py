@@ -657,25 +657,9 @@ def main() -> None:
                        "ask": "python" if args.python_ask else "native (csrc/search.cpp)",
                        "space": ("reference operator space (fp32 SIMT family)" if args.dtype == "f32"
                                  else "reference operator space + stages (mapping.py)"),
-                       "fitness_timing": (f"{settings.reps} launches, each after a 2x-L2 read pass and "
-                                          f"timed alone" if args.l2 == "cold" else
-                                          f"{settings.reps} back-to-back launches in one CUDA graph"
-                                          if args.timing == "graph" else
-                                          f"{settings.reps} back-to-back stream launches released "
-                                          f"by a device gate")
-                                         + f" after {settings.warmup} warm-up launches incl. "
-                                         f"the verified one (a {settings.budget_ms} ms device budget "
-                                         f"per trial caps the repetitions; a candidate whose "
-                                         f"verified launch alone exceeds it is timed by that "
-                                         f"launch; a candidate slower than {settings.loser_ratio}x "
-                                         f"the fastest verified one gets {settings.loser_reps} "
-                                         (f"launches), L2 warm (operands fit in L2)" if args.l2 == "warm" else
-                                            "launches), L2 cold: every timed launch after a 2x-L2 "
-                                            "read pass, timed alone (HBM-bound operator)"),
-                       "l2_between_steps": "flushed: a 256 MB read pass (2x L2, leaves only clean lines) before every timed "
-                                           "step; within a trial the fitness is L2-warm "
-                                           "back-to-back launches (use --l2 cold to flush "
-                                           "before every timed launch)",
+                       "fitness_timing": fitness_timing(args, settings),
+                       "l2_between_steps": "flushed: a 256 MB read pass (2x L2, leaves only clean "
+                                           "lines) before every timed step",
                        "parallelism": f"trial sharding x{world}",
                        "kernel_cache": ("prebuilt cubins (build()); the operator's cached family "
                                         "loaded into the context before timing" if not args.no_preload
@@ -751,6 +735,22 @@ def cold_cache_record(spec, space, settings, device: int, args, budget: int = 50
     finally:
         ev.close()
         shutil.rmtree(tmp, ignore_errors=True)
+
+
+def fitness_timing(args, settings) -> str:
+    """How the search's fitness launches are timed (the bench line's config)."""
+    if args.l2 == "cold":
+        how = (f"{settings.reps} launches, each after a 2x-L2 read pass and timed alone (HBM-bound "
+               f"operator: the fitness is its launch with the operands coming from HBM)")
+    elif args.timing == "graph":
+        how = f"{settings.reps} back-to-back launches in one CUDA graph, L2 warm (operands fit in L2)"
+    else:
+        how = (f"{settings.reps} back-to-back stream launches released by a device gate, L2 warm "
+               f"(operands fit in L2)")
+    return (how + f"; {settings.warmup} warm-up launches incl. the verified one; a "
+            f"{settings.budget_ms} ms device budget per trial caps the repetitions, a candidate whose "
+            f"verified launch alone exceeds it is timed by that launch, and one slower than "
+            f"{settings.loser_ratio}x the fastest verified one gets {settings.loser_reps} launches")
 
 
 def hbm_fed_time(ev, spec, settings, knobs, nbytes: int, l2_bytes: int = 126 << 20) -> tuple[float, int]:

@@ -189,23 +189,60 @@ extern "C" __global__ void opevo_nhwc_pad_to_nchw(const u16* __restrict__ src, u
 // ---------------------------------------------------------------------------
 // out[0] = max |C - R|, out[1] = max |R|, out[2] = count of non-finite C.
 // Non-negative floats compare like their bit patterns, so atomicMax on u32.
-extern "C" __global__ void opevo_compare(const void* __restrict__ C, const float* __restrict__ R,
-                                         u64 n, int c_f32, u32* __restrict__ out) {
+// Four outputs per step (16-byte R loads, 8- or 16-byte C loads), reduced in
+// the warp, then in the block through shared memory: ONE set of atomics per
+// block.  (One set per warp -- 32 K warps on the same two words for a
+// 1024^2 output -- serialised at one L2 slice and cost ~0.1 ms per check.)
+__device__ __forceinline__ void cmp_one(float c, float r, float& md, float& mr, u32& bad) {
+    if (!isfinite(c)) { ++bad; return; }
+    md = fmaxf(md, fabsf(c - r));
+    mr = fmaxf(mr, fabsf(r));
+}
+
+extern "C" __global__ void __launch_bounds__(256) opevo_compare(const void* __restrict__ C,
+                                                                const float* __restrict__ R, u64 n,
+                                                                int c_f32, u32* __restrict__ out) {
     float md = 0.0f, mr = 0.0f;
     u32 bad = 0;
-    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    const u64 tid = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    const u64 n4 = n / 4;
+    for (u64 q = tid; q < n4; q += stride) {
+        const float4 r = reinterpret_cast<const float4*>(R)[q];
+        float c0, c1, c2, c3;
+        if (c_f32) {
+            const float4 c = reinterpret_cast<const float4*>(C)[q];
+            c0 = c.x; c1 = c.y; c2 = c.z; c3 = c.w;
+        } else {
+            const uint2 u = reinterpret_cast<const uint2*>(C)[q];
+            c0 = __uint_as_float(u.x << 16); c1 = __uint_as_float(u.x & 0xFFFF0000u);
+            c2 = __uint_as_float(u.y << 16); c3 = __uint_as_float(u.y & 0xFFFF0000u);
+        }
+        cmp_one(c0, r.x, md, mr, bad);
+        cmp_one(c1, r.y, md, mr, bad);
+        cmp_one(c2, r.z, md, mr, bad);
+        cmp_one(c3, r.w, md, mr, bad);
+    }
+    for (u64 i = 4 * n4 + tid; i < n; i += stride) {
         const float c = c_f32 ? ((const float*)C)[i] : bf16_to_f32(((const u16*)C)[i]);
-        const float r = R[i];
-        if (!isfinite(c)) { ++bad; continue; }
-        md = fmaxf(md, fabsf(c - r));
-        mr = fmaxf(mr, fabsf(r));
+        cmp_one(c, R[i], md, mr, bad);
     }
     for (int o = 16; o > 0; o >>= 1) {
         md = fmaxf(md, __shfl_xor_sync(0xffffffffu, md, o));
         mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, o));
         bad += __shfl_xor_sync(0xffffffffu, bad, o);
     }
-    if ((threadIdx.x & 31) == 0) {
+    __shared__ float s_md[8], s_mr[8];
+    __shared__ u32 s_bad[8];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) { s_md[warp] = md; s_mr[warp] = mr; s_bad[warp] = bad; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+            md = fmaxf(md, s_md[w]);
+            mr = fmaxf(mr, s_mr[w]);
+            bad += s_bad[w];
+        }
         atomicMax(out + 0, __float_as_uint(md));
         atomicMax(out + 1, __float_as_uint(mr));
         if (bad) atomicAdd(out + 2, bad);

@@ -1708,7 +1708,10 @@ int enqueue_check(opevo_kernel* k, char* err, size_t errlen, int slot = 0, CUeve
     uint64_t n = (uint64_t)op->batch * op->rows * op->cols;
     int c_f32 = op->out_f32;
     void* args[] = {&op->c, &op->ref, &n, &c_f32, &out};
-    return launch_simple(ctx, ctx->k_compare, grid_for(n), 256, args, err, errlen);
+    // four outputs per thread-step, a few steps per thread, one atomic set per block
+    const unsigned cgrid = (unsigned)std::min<uint64_t>((uint64_t)ctx->sm_count * 4,
+                                                        std::max<uint64_t>(1, (n / 4 + 255) / 256));
+    return launch_simple(ctx, ctx->k_compare, cgrid, 256, args, err, errlen);
 }
 
 // Judge one compare slot {max|C-R|, max|R|, non-finite count}.

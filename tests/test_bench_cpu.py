@@ -44,3 +44,29 @@ def test_ncu_traffic_accepts_the_14_slot_knobs():
     kn = (128, 64, 128, 4, 1, 1, 1, 1, 1, 1, 0, 0, 1, 0)
     assert bench._ncu_traffic("matmul:1024,1024,1024", kn) is not None
     assert bench._ncu_traffic("matmul:1024,1024,1024", kn[:13] + (16,)) is None
+
+
+def test_bench_compiles_without_warnings():
+    # a SyntaxWarning here (e.g. two adjacent string literals read as a call)
+    # is a TypeError at the end of a GPU run
+    import os
+    import warnings
+
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "bench.py")
+    with open(path) as fh:
+        src = fh.read()
+    with warnings.catch_warnings():
+        warnings.simplefilter("error")
+        compile(src, path, "exec")
+
+
+def test_fitness_timing_names_the_mode():
+    import types
+
+    from paper_2006_05664_b200.evaluator import EvalSettings
+
+    s = EvalSettings()
+    cold = bench.fitness_timing(types.SimpleNamespace(l2="cold", timing="stream"), s)
+    warm = bench.fitness_timing(types.SimpleNamespace(l2="warm", timing="stream"), s)
+    graph = bench.fitness_timing(types.SimpleNamespace(l2="warm", timing="graph"), s)
+    assert "read pass" in cold and "gate" in warm and "CUDA graph" in graph
