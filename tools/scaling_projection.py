@@ -36,6 +36,8 @@ def main():
     ap.add_argument("generations", nargs="?", type=int, default=40)
     ap.add_argument("--allreduce-us", type=float, default=30.0)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--timing", default="stream", choices=("stream", "graph"),
+                    help="fitness launches: gated stream (bench default) or one CUDA graph per trial")
     args = ap.parse_args()
 
     from paper_2006_05664_b200 import EngineConfig, parse_operator
@@ -46,7 +48,8 @@ def main():
 
     spec = parse_operator(args.op)
     space = gpu_operator_space(spec)
-    ev = GpuEvaluator(spec, space, 0, EvalSettings(preload_family=True))
+    mode = 2 if args.timing == "stream" else 0
+    ev = GpuEvaluator(spec, space, 0, EvalSettings(preload_family=True, flush_l2=mode))
     warm = 3
     budget = 8 * (args.generations + warm)
 
@@ -63,9 +66,10 @@ def main():
         eng.tell(list(zip(a.configs, fits)))
 
     out = {"op": args.op, "generations": args.generations, "allreduce_us": args.allreduce_us,
+           "timing": args.timing,
            "seed": args.seed, "per_n": {}}
     for n in (1, 2, 4, 8):
-        ranks = [GpuEvaluator(spec, space, 0, EvalSettings(), dev=ev.dev) for _ in range(n)]
+        ranks = [GpuEvaluator(spec, space, 0, EvalSettings(flush_l2=mode), dev=ev.dev) for _ in range(n)]
         eng = NativeOpEvo(space, EngineConfig(seed=args.seed, budget=budget))
         gen_ms, rank_ms = [], []
         trials = 0
