@@ -32,3 +32,14 @@ run x3_bmm             batchmatmul:8,128,64,128      128,64,32,3                
 run conv_halo          conv2d:4,64,28,28,64,3,3,1,1  128,64,64,4,1,1,4,14
 run conv_halo_resident conv2d:4,64,28,28,64,3,3,1,1  256,64,64,3,1,1,4,14,1,1,0,1
 run bmm_nbuf4          batchmatmul:64,128,64,128     128,64,64,4,1,1
+# round 2: conv widening (stride 4 + Cin padded to 16, padded lines, tap split with lines, CTA pairs),
+# the rotating-copy timing and the per-block compare ride along in every run
+run conv_c1_stride4_lines  conv2d:8,3,227,227,64,11,11,4,0   256,64,16,8,1,1,11,11,1,1,0,0,1,16
+run conv_c1_lines_split    conv2d:8,3,227,227,64,11,11,4,0   256,64,16,8,11,1,11,5,1,1,0,0,1,16
+run conv_c2_lines          conv2d:8,64,27,27,192,5,5,1,2     256,16,32,2,1,1,9,9,1,1,0,0,1,16
+run conv_c2_lines_split    conv2d:8,64,27,27,192,5,5,1,2     256,192,32,6,5,1,9,3,1,1,0,0,1,16
+run conv_pair              conv2d:4,64,56,56,64,3,3,1,1      256,16,16,3,1,1,8,8,1,2,0,0,1,0
+run conv_pair_split        conv2d:4,64,56,56,64,3,3,1,1      256,64,16,2,3,1,8,8,1,2,0,0,1,0
+run conv_pair_halo         conv2d:4,64,56,56,64,3,3,1,1      256,32,64,6,1,1,4,14,1,2,0,0,1,0
+run conv_pair_lines_split  conv2d:4,64,56,56,64,3,3,1,1      256,32,16,6,9,1,8,7,1,2,0,0,1,16
+run conv_lines_resident    conv2d:4,64,56,56,64,3,3,1,1      256,64,64,3,1,1,8,28,1,1,0,1,1,32
