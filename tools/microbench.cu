@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(256, 1) mma_issue_bench(u64* out, int iters, i
     __shared__ u32 tslot;
     __shared__ volatile int done;
     const int warp = threadIdx.x >> 5;
-    for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) ((u32*)smem)[i] = 0x3c003c00u;
+    for (int i = threadIdx.x; i < 128 * 1024 / 4; i += blockDim.x) ((u32*)smem)[i] = 0x3c003c00u;
     if (threadIdx.x == 0) {
         done = 0;
         mbar_init(smem_u32(&never), 1);
@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(256, 1) mma_issue_bench(u64* out, int iters, i
     constexpr u32 IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((u32)(64 >> 3) << 17) | ((u32)(128 >> 4) << 24);
     constexpr u64 HI = ((u64)1 << 16) | ((u64)(1024 >> 4) << 32) | ((u64)1 << 46) | ((u64)2 << 61);
     const u32 alo = (u32)(HI | (u64)((smem_u32(smem) >> 4) & 0x3FFF));
-    const u32 blo = (u32)(HI | (u64)(((smem_u32(smem) + 24 * 1024) >> 4) & 0x3FFF));
+    const u32 blo = (u32)(HI | (u64)(((smem_u32(smem) + 16 * 1024) >> 4) & 0x3FFF));
     const u32 dhi = (u32)(HI >> 32);
     const u64 ad = ((u64)dhi << 32) | alo, bd = ((u64)dhi << 32) | blo;
     if ((v == 2 && warp == 4) || (v == 3 && warp == 5)) {
@@ -379,9 +379,28 @@ __global__ void __launch_bounds__(256, 1) mma_issue_bench(u64* out, int iters, i
                 }
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const u32 acc = (i | rep) ? 1u : 0u;
-                if (v != 1) {
+                // v = 5: the K blocks cycle through 4 stage slots 24 KB apart
+                // (fresh shared memory for every K block, as in the kernel's ring)
+                const u64 soff = (v == 5) ? (u64)((i & 3) * (24 * 1024 / 16)) : 0ull;
+                if (v == 6) {
+                    // one thread issues (no elect / predicate per MMA)
+                    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+                        for (int dj = 0; dj < 3; ++dj) {
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const u64 a = ad + (u64)(dj * 8 + k * 2), b = bd + (u64)(dj * 512 + k * 2);
+                                const u32 accd = (dj | k) ? 1u : acc;
+                                asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0; "
+                                             "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }"
+                                             :: "r"(tmem), "l"(a), "l"(b), "r"(IDESC), "r"(accd));
+                            }
+                        }
+                    }
+                    __syncwarp();
+                } else if (v != 1) {
                     for (int dj = 0; dj < 3; ++dj) {
-                        const u64 a = ad + (u64)(dj * 8), b = bd + (u64)(dj * 512);
+                        const u64 a = ad + soff + (u64)(dj * 8), b = bd + soff + (u64)(dj * 512);
                         asm volatile("{ .reg .pred e, p, t; .reg .b64 a1, b1, a2, b2, a3, b3; elect.sync _|e, 0xffffffff; "
                                      "setp.ne.b32 p, %4, 0; setp.eq.b32 t, 0, 0; "
                                      "add.s64 a1, %1, 2; add.s64 b1, %2, 2; add.s64 a2, %1, 4; add.s64 b2, %2, 4; "
@@ -405,9 +424,16 @@ __global__ void __launch_bounds__(256, 1) mma_issue_bench(u64* out, int iters, i
                                  :: "r"(tmem), "r"(alo), "r"(blo), "r"(IDESC), "r"(acc), "r"(dhi));
 #undef MI_ONE
                 }
-                asm volatile("{ .reg .pred e; elect.sync _|e, 0xffffffff; "
-                             "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0]; }"
-                             :: "r"(smem_u32(&cbar)) : "memory");
+                if (v == 6) {
+                    if ((threadIdx.x & 31) == 0)
+                        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                                     :: "r"(smem_u32(&cbar)) : "memory");
+                    __syncwarp();
+                } else {
+                    asm volatile("{ .reg .pred e; elect.sync _|e, 0xffffffff; "
+                                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0]; }"
+                                 :: "r"(smem_u32(&cbar)) : "memory");
+                }
             }
             asm volatile("{ .reg .pred e; elect.sync _|e, 0xffffffff; "
                          "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0]; }"
@@ -522,9 +548,9 @@ int main() {
         printf("mma 12 per asm block N=64: %.1f cyc/MMA\n", (double)h[0] / (iters * 12));
     }
     {
-        const int smem = 64 * 1024 + 1024;
+        const int smem = 128 * 1024 + 1024;
         CK(cudaFuncSetAttribute(mma_issue_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        for (int v : {0, 1, 4}) {
+        for (int v : {0, 6}) {
             const int iters = 128;
             mma_issue_bench<<<1, 256, smem>>>(d_out, iters, v);
             CK(cudaDeviceSynchronize());
@@ -533,7 +559,8 @@ int main() {
             printf("mma issue v%d (%s): %.1f cyc/MMA\n", v,
                    v == 0 ? "per-tap asm blocks, 64-bit adds" : v == 1 ? "one asm block per K block, 32-bit adds"
                    : v == 2 ? "v0 + a spinning warp on the MMA warp's sub-partition"
-                   : v == 3 ? "v0 + a spinning warp elsewhere" : "v0 with the kernel's watchdog wait",
+                   : v == 3 ? "v0 + a spinning warp elsewhere" : v == 4 ? "v0 with the kernel's watchdog wait"
+                   : v == 5 ? "v0 with the K blocks cycling through 4 stage slots" : "one thread issues, no elect",
                    (double)h[0] / (iters * 12));
         }
     }
