@@ -406,6 +406,11 @@ __device__ __forceinline__ u32 sm_id() {
 #else
 #define UTRACE(slot) do { } while (0)
 #endif
+#if OPEVO_TRACE == 3
+#define UTRACE3(slot) do { trace[(slot)] = global_ns(); } while (0)
+#else
+#define UTRACE3(slot) do { } while (0)
+#endif
 
 __device__ __forceinline__ void tma_prefetch(const TmaDesc* d) {
     asm volatile("prefetch.tensormap [%0];" :: "l"(d) : "memory");
@@ -1124,9 +1129,11 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                 // the epilogue must have drained this accumulator buffer
                 mbar_wait(smem_u32(tempty_bar + buf), bph ^ 1);
                 tc_fence_after();
+                if (lane == 0 && mu < 5) UTRACE3(1 + 3 * mu);
                 const u32 acc_base = tmem_base + (u32)(buf * TMEM_USED);
                 for (int kb = 0; kb < num_kb; ++kb) {
                     mbar_wait(smem_u32(full_bar + s), ph);
+                    if (kb == 0 && lane == 0 && mu < 5) UTRACE3(2 + 3 * mu);
                     if (X3) mbar_wait(smem_u32(lo_bar + s), ph);
                     tc_fence_after();
                     if (first && lane == 0) { TRACE(4); first = false; }
@@ -1232,6 +1239,7 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                 if (CG == 2) umma2_commit_mc(smem_u32(tfull_bar + buf), (u16)3);   // both halves
                 else         umma_commit(smem_u32(tfull_bar + buf));
                 if (lane == 0 && mu < 5) UTRACE(1 + 3 * mu);
+                if (lane == 0 && mu < 5) UTRACE3(3 + 3 * mu);
                 ++mu;
                 if (++buf == NBUF) { buf = 0; bph ^= 1; }
             }

@@ -7,7 +7,8 @@ Usage: python tools/trace_units.py batchmatmul:960,128,64,128 128,64,64,6,1,1"""
 import os
 import sys
 
-os.environ["OPEVO_EXTRA_FLAGS"] = ("-DOPEVO_TRACE=2 " + os.environ.get("OPEVO_ABLATE_FLAG", "")).strip()
+MODE = int(os.environ.get("OPEVO_TRACE_MODE", "2"))
+os.environ["OPEVO_EXTRA_FLAGS"] = (f"-DOPEVO_TRACE={MODE} " + os.environ.get("OPEVO_ABLATE_FLAG", "")).strip()
 sys.path.insert(0, ".")
 import numpy as np  # noqa: E402
 
@@ -27,6 +28,22 @@ def main():
         k.trace(ctas)
     tr = k.trace(ctas).astype(np.int64)
     print(f"{spec.id()} knobs={knobs} ctas={ctas} {os.environ['OPEVO_EXTRA_FLAGS']}")
+    if MODE == 3:
+        # MMA warp per unit: accumulator free (start), first stage ready, commit issued
+        print("  unit   start   first-stage-ready   commit-issued   (us; wait-for-data, issue, gap-to-next-start)")
+        prev = None
+        for u in range(5):
+            a, b, c = tr[:, 1 + 3 * u], tr[:, 2 + 3 * u], tr[:, 3 + 3 * u]
+            ok = (a > 0) & (b > 0) & (c > 0)
+            if not ok.any():
+                break
+            t0 = tr[ok, 1].min()
+            ma, mb, mc = (np.median(x[ok] - t0) / 1e3 for x in (a, b, c))
+            gap = "" if prev is None else f", gap {ma - prev:.2f}"
+            print(f"  {u:4d}   {ma:5.2f}   {mb:17.2f}   {mc:13.2f}   (data {mb - ma:.2f}, issue {mc - mb:.2f}{gap})")
+            prev = mc
+        k.close()
+        return
     print("  unit   commit-issued   epilogue-saw   epilogue-done   (us, median over CTAs; "
           "saw-commit, done-saw)")
     rows = []
