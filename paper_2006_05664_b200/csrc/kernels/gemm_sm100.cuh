@@ -1123,6 +1123,13 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
             const u64 desc_b0 = desc_a0 + (u64)(A_TILE >> 4);
             const u64 desc_bres = DESC_HI | (u64)((smem_u32(smem + BRES_OFF) >> 4) & 0x3FFF);
             if (B_RES) mbar_wait(smem_u32(bres_bar), 0);     // the resident weight panel
+            // halo + resident weights: descriptor steps through the panel
+            // (atom = (BN x 128 B) >> 4 per 64 channels; C/64 atoms per tap
+            // column; (KW - 1) columns skipped when a filter row is done)
+            constexpr int bres_atom = (BN * SWZ) >> 4;
+            const u64 bres_dj = (HALO && B_RES) ? (u64)(geom.cin / 64) * (u64)bres_atom : 0ull;
+            const u64 bres_wrap = (u64)(HKW > 0 ? HKW - 1 : 0) * bres_dj;
+            (void)bres_wrap;
             for (UnitWalk w = digits(u_first); w.u < sched.units; walk_next(w)) {
                 const Unit tu = unit_of(w);
                 const int num_kb = tu.num_kb;
@@ -1131,6 +1138,10 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                 tc_fence_after();
                 if (lane == 0 && mu < 5) UTRACE3(1 + 3 * mu);
                 const u32 acc_base = tmem_base + (u32)(buf * TMEM_USED);
+                u64 bres_kb = desc_bres;       // halo + resident weights: this K block's panel atom
+                int bres_cch = 0;              // ... and its channel block within the filter row
+                (void)bres_kb;
+                (void)bres_cch;
                 for (int kb = 0; kb < num_kb; ++kb) {
                     mbar_wait(smem_u32(full_bar + s), ph);
                     if (kb == 0 && lane == 0 && mu < 5) UTRACE3(2 + 3 * mu);
@@ -1149,16 +1160,18 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                                          : desc_b0 + sdesc;
                     if (HALO) {
                         // filter row `tap` of this K block: tap dj reads the
-                        // halo box dj rows further on
-                        const int kblk = tu.k0 / BK + kb;
-                        const int tap = kblk / geom.taps_cchunks;
-                        const int cbase = (kblk - tap * geom.taps_cchunks) * BK;
+                        // halo box dj rows further on.  Resident weights: the
+                        // panel atom of (row, channel block, dj, ka) is
+                        // row*KW*C/64 + dj*C/64 + chunk*KATOMS + ka, walked
+                        // incrementally (bres_kb) -- no division or multiply
+                        // by runtime values in the MMA warp's loop, whose
+                        // instruction count paces the N = 64 MMAs
 #pragma unroll
                         for (int dj = 0; dj < HKW; ++dj) {
 #pragma unroll
                             for (int ka = 0; ka < KATOMS; ++ka) {
                                 const u64 bdesc = B_RES
-                                    ? desc_bres + (u64)(((((tap * HKW + dj) * geom.cin + cbase) / 64 + ka) * (BN * SWZ)) >> 4)
+                                    ? bres_kb + (u64)dj * bres_dj + (u64)(ka * bres_atom)
                                     : db + (u64)((dj * B_SUB + ka * (BN_LOAD * SWZ)) >> 4);
                                 // (tap, atom) steps round-robin over ACC accumulators
                                 const int step = dj * KATOMS + ka;
@@ -1234,6 +1247,10 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
 #else
                     umma_commit(smem_u32(empty_bar + s));
 #endif
+                    if (HALO && B_RES) {
+                        bres_kb += (u64)(KATOMS * bres_atom);
+                        if (++bres_cch == geom.taps_cchunks) { bres_cch = 0; bres_kb += bres_wrap; }
+                    }
                     if (++s == STAGES) { s = 0; ph ^= 1; }
                 }
                 if (CG == 2) umma2_commit_mc(smem_u32(tfull_bar + buf), (u16)3);   // both halves
