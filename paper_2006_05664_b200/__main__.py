@@ -4,10 +4,12 @@
         --budget 500 --seed 0 --out out/
     python -m paper_2006_05664_b200 compare --operator matmul:1024,1024,1024 \\
         --algo opevo,random,sa,gbfs --seeds 0,1,2 --budget 300 --out out/
+    python -m paper_2006_05664_b200 sweep --operator matmul:1024,1024,1024 \\
+        --q-grid 0.25,0.5,0.75 --lambda-grid 4,8,16 --seeds 0,1,2 --out out/
 
-Mirrors the reference CLI's ``tune`` / ``bench`` subcommands
-(``pkg/src/topotune/cli.py:164-233``): same trial-log schema and
-summary/curve CSVs, with ``--evaluator gpu`` (default) measuring TFLOP/s on
+Mirrors the reference CLI's ``tune`` / ``bench`` / ``sweep`` subcommands
+(``pkg/src/topotune/cli.py:164-270``): same trial-log schema, summary/curve
+CSVs and per-cell layout of the hyper-parameter sweep, with ``--evaluator gpu`` (default) measuring TFLOP/s on
 the device and ``--evaluator synthetic`` using the reference's CPU model.
 Exit codes: 0 ok, 2 usage error, 3 evaluator unavailable.
 """
@@ -58,10 +60,11 @@ def _peak_tflops() -> float:
         return 1590.0
 
 
-def _run(algo, space, objective, seed, budget):
+def _run(algo, space, objective, seed, budget, parents: int = 8, mutation_rate: float = 0.5):
     if algo == "opevo":
         evaluator = getattr(objective, "evaluate", None)
-        return run(space, EngineConfig(seed=seed, budget=budget), objective, evaluator=evaluator)
+        cfg = EngineConfig(seed=seed, budget=budget, parents=parents, mutation_rate=mutation_rate)
+        return run(space, cfg, objective, evaluator=evaluator)
     if algo == "random":
         return random_search(space, budget, seed, objective)
     if algo == "sa":
@@ -107,10 +110,42 @@ def cmd_compare(args) -> int:
     return 0
 
 
+def cmd_sweep(args) -> int:
+    """OpEvo's hyper-parameters -- mutation rate q and parent count lambda --
+    over a grid (reference ``cli.py:237-270``, the paper's sensitivity study):
+    one directory ``q{q}_lambda{lambda}`` of trial logs per cell and one
+    ``sweep_summary.csv`` row per cell (the reference's column layout: q,
+    parents, then the summary columns)."""
+    space, objective = _objective(args)
+    qs = [float(x) for x in args.q_grid.split(",") if x]
+    lams = [int(x) for x in args.lambda_grid.split(",") if x]
+    seeds = [int(s) for s in args.seeds.split(",") if s]
+    if not qs or not lams or not seeds:
+        raise ValueError("empty --q-grid, --lambda-grid or --seeds")
+    if args.budget < max(lams):
+        raise ValueError(f"--budget {args.budget} is below the parent count {max(lams)}")
+    os.makedirs(args.out, exist_ok=True)
+    rows = []
+    for q in qs:
+        for lam in lams:
+            cell = os.path.join(args.out, f"q{q}_lambda{lam}")
+            os.makedirs(cell, exist_ok=True)
+            logs = []
+            for seed in seeds:
+                _, recs = _run("opevo", space, objective, seed, args.budget, parents=lam, mutation_rate=q)
+                write_trial_log(os.path.join(cell, f"trials_opevo_seed{seed}.jsonl"), recs)
+                logs.append(recs)
+            row = summary_row_dict(summarize("opevo", args.operator, logs), q=q, parents=lam)
+            rows.append(row)
+            print(json.dumps(row), flush=True)
+    write_summary_csv(os.path.join(args.out, "sweep_summary.csv"), rows)
+    return 0
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="paper_2006_05664_b200")
     sub = ap.add_subparsers(dest="cmd", required=True)
-    for name in ("tune", "compare"):
+    for name in ("tune", "compare", "sweep"):
         p = sub.add_parser(name)
         p.add_argument("--operator", required=True)
         p.add_argument("--evaluator", default="gpu", choices=("gpu", "synthetic"))
@@ -122,12 +157,16 @@ def main(argv=None) -> int:
         if name == "tune":
             p.add_argument("--algo", default="opevo", choices=ALGORITHMS)
             p.add_argument("--seed", type=int, default=int(os.environ.get("TOPO_TUNE_SEED", 0)))
-        else:
+        elif name == "compare":
             p.add_argument("--algo", default=",".join(ALGORITHMS))
+            p.add_argument("--seeds", default="0,1,2")
+        else:
+            p.add_argument("--q-grid", default="0.5", help="comma-separated mutation rates")
+            p.add_argument("--lambda-grid", default="8", help="comma-separated parent counts")
             p.add_argument("--seeds", default="0,1,2")
     args = ap.parse_args(argv)
     try:
-        return cmd_tune(args) if args.cmd == "tune" else cmd_compare(args)
+        return {"tune": cmd_tune, "compare": cmd_compare, "sweep": cmd_sweep}[args.cmd](args)
     except FatalEvaluationError as err:
         print(f"evaluator unavailable: {err}", file=sys.stderr)
         return 3

@@ -221,3 +221,36 @@ def test_wallclock_to_fraction_is_elapsed_of_trials_to_fraction(reference_topotu
     t = ours.trials_to_fraction(recs)
     assert ours.wallclock_to_fraction(recs) == next(r.elapsed_ms for r in recs if r.trial == t)
     assert t == reference_topotune.reporting.trials_to_fraction(_gpu_log_records(reference_topotune.logs))
+
+
+def test_sweep_matches_the_reference_cli(reference_topotune, tmp_path):
+    """``sweep`` (OpEvo's q / lambda grid, reference ``cli.py:237-270``) with the
+    reference's synthetic evaluator: the same cell directories, the same trial
+    logs (configs and fitness, trial by trial) and the same sweep_summary.csv
+    apart from the wall-clock column."""
+    import csv
+
+    args = ["--q-grid", "0.25,0.75", "--lambda-grid", "4,8", "--seeds", "0,3", "--budget", "60"]
+    env = dict(os.environ, PYTHONPATH=os.path.dirname(os.path.dirname(reference_topotune.__file__)))
+    ref = subprocess.run([sys.executable, "-m", "topotune", "sweep", "--operator", "matmul:512,1024,1024",
+                          *args, "--out", str(tmp_path / "ref")], capture_output=True, text=True, env=env,
+                         timeout=300)
+    assert ref.returncode == 0, ref.stderr
+    ours = subprocess.run([sys.executable, "-m", "paper_2006_05664_b200", "sweep", "--operator",
+                           "matmul:512,1024,1024", "--evaluator", "synthetic", *args, "--out",
+                           str(tmp_path / "ours")], capture_output=True, text=True, cwd=REPO, timeout=300)
+    assert ours.returncode == 0, ours.stderr
+    cells = sorted(p.name for p in (tmp_path / "ref").iterdir() if p.is_dir())
+    assert cells == sorted(p.name for p in (tmp_path / "ours").iterdir() if p.is_dir()) and len(cells) == 4
+    for cell in cells:
+        for seed in (0, 3):
+            name = f"trials_opevo_seed{seed}.jsonl"
+            a = [json.loads(x) for x in (tmp_path / "ref" / cell / name).read_text().splitlines()]
+            b = [json.loads(x) for x in (tmp_path / "ours" / cell / name).read_text().splitlines()]
+            assert [(r["config"], r["fitness"]) for r in a] == [(r["config"], r["fitness"]) for r in b]
+
+    def rows(path):
+        with open(path) as fh:
+            return [{k: v for k, v in r.items() if k != "mean_elapsed_ms"} for r in csv.DictReader(fh)]
+
+    assert rows(tmp_path / "ref" / "sweep_summary.csv") == rows(tmp_path / "ours" / "sweep_summary.csv")
