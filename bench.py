@@ -483,6 +483,12 @@ def main() -> None:
         generation(engine, recorder)
 
     # ---------------- timed region: K generations, device-timed, max over ranks
+    # (the Python garbage collector is paused inside it: a collection pass is
+    # host jitter of a few ms against a ~70 ms region)
+    import gc
+
+    gc.collect()
+    gc.disable()
     barrier()
     trials = 0
     tally = {"launches": 0, "valid": 0, "verified": 0, "instances": set()}
@@ -510,6 +516,7 @@ def main() -> None:
             # (its evaluation moved to a worker process): events are gone
             local_sec = wall
             timing = f"host wall clock on rank {rank} (CUDA context poisoned by a faulting candidate)"
+    gc.enable()
     sec = max_over_ranks(local_sec)
     trials_per_s = trials / sec if sec > 0 else 0.0
     best_at_timed = engine.best().fitness if engine.archive else 0.0
@@ -553,6 +560,8 @@ def main() -> None:
         for g in range(args.warmup):
             flush()
             generation(e_engine, e_rec, upload, replay=history[g])
+        gc.collect()
+        gc.disable()
         barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record()
@@ -563,6 +572,7 @@ def main() -> None:
         barrier()
         f1.record()
         torch.cuda.synchronize()
+        gc.enable()
         e_sec = max_over_ranks(f0.elapsed_time(f1) / 1e3)
         e2e = {"value": e2e_trials / e_sec if e_sec > 0 else 0.0, "unit": "trials/s",
                "h2d_bytes_per_step": (op.a_bytes + op.b_bytes) * world,
