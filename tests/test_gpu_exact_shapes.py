@@ -357,3 +357,42 @@ def test_rotating_timing_streams_from_hbm(dev, bmm1):
             kk.close()
         for o in copies:
             o.close()
+
+
+_WRONG_KERNEL = r"""
+import json, sys
+sys.path.insert(0, ".")
+from paper_2006_05664_b200 import capi
+dev = capi.Device(0, sys.argv[1])
+op = dev.prepare(capi.MATMUL, rows=256, cols=512, depth=512, seed=7)
+out = []
+for batch in ([(128, 64, 128, 3)], [(128, 64, 128, 3), (128, 128, 64, 4)]):
+    out.append([t.status for t in dev.trial_batch(op, batch, warmup=1, reps=3, flush_l2=2)])
+t = dev.trial(op, (128, 64, 128, 3), warmup=1, reps=3)
+out.append([t.status])
+print(json.dumps(out))
+"""
+
+
+@pytest.mark.parametrize("ablate,what", [(2, "no mainloop: C is an unwritten accumulator"),
+                                         (6, "no C stores: C keeps its NaN poison")])
+def test_verification_rejects_wrong_kernels(tmp_path, ablate, what):
+    """The in-library check (poisoned C, the per-block compare kernel) must
+    fail a kernel that computes the wrong output or never writes it -- single
+    trials and batches alike.  Debug builds of the real instance: -DOPEVO_ABLATE
+    removes the mainloop (the epilogue stores an accumulator no MMA wrote) or
+    the C stores (the output keeps its NaN poison)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    from paper_2006_05664_b200 import capi
+
+    env = dict(os.environ, OPEVO_EXTRA_FLAGS=f"-DOPEVO_ABLATE={ablate}")
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    done = subprocess.run([sys.executable, "-c", _WRONG_KERNEL, str(tmp_path / "cache")], cwd=repo, env=env,
+                          capture_output=True, text=True, timeout=300)
+    assert done.returncode == 0, done.stderr[-2000:]
+    statuses = json.loads(done.stdout.strip().splitlines()[-1])
+    assert all(s == capi.VERIFY_FAILED for group in statuses for s in group), (what, statuses)
