@@ -499,9 +499,14 @@ def main() -> None:
         if e0 is not None:
             e0.record()
         t_wall0 = time.perf_counter()
+        gen_diag = [] if os.environ.get("OPEVO_BENCH_GEN_TIMES") == "1" else None
         for _ in range(args.steps):
             flush()                     # every step starts with a cold L2
+            tg = time.perf_counter()
             trials += generation(engine, recorder, tally=tally)
+            if gen_diag is not None:    # diagnostics: host time per generation + its trials
+                owner = getattr(evaluator, "__self__", evaluator)
+                gen_diag.append((1e3 * (time.perf_counter() - tg), list(owner.last_extras)))
         barrier()
         wall = time.perf_counter() - t_wall0
         timing = "cuda events (max over ranks)"
@@ -517,6 +522,15 @@ def main() -> None:
             local_sec = wall
             timing = f"host wall clock on rank {rank} (CUDA context poisoned by a faulting candidate)"
     gc.enable()
+    if gen_diag:
+        slow = sorted(range(len(gen_diag)), key=lambda i: -gen_diag[i][0])[:3]
+        med = statistics.median(t for t, _ in gen_diag)
+        for i in slow:
+            t, ex = gen_diag[i]
+            print(f"[gen {i}] {t:.3f} ms (median {med:.3f}): " + "; ".join(
+                f"{e.get('status')} c{e.get('cache_hit')} cm{e.get('compile_ms', 0):.1f} "
+                f"d{(e.get('device_ms') or 0) * 1e3:.1f}us vc{e.get('verify_cached')}" for e in ex),
+                file=sys.stderr)
     sec = max_over_ranks(local_sec)
     trials_per_s = trials / sec if sec > 0 else 0.0
     best_at_timed = engine.best().fitness if engine.archive else 0.0
@@ -597,7 +611,12 @@ def main() -> None:
     if best_conf is not None:
         best_knobs = tuple(best_conf["knobs"])
         k = local_ev.dev.kernel(local_ev.op, best_knobs)
-        reps_graph = 100
+        # the kernel timed alone, as a burst: 100 back-to-back launches, or
+        # fewer for long kernels so the graph lasts ~1 ms (9 ms of 4096^3
+        # launches already runs into the board's power limit, and the
+        # roofline denominator is the burst peak)
+        est = confirmed[0]["ms"] if confirmed and confirmed[0].get("ms") else 0.0
+        reps_graph = 100 if est <= 0.01 else max(5, min(100, int(1.0 / est)))
         ms = k.time(warmup=5, reps=reps_graph, flush_l2=False)
         ms_cold = k.time(warmup=2, reps=20, flush_l2=True)
         best_cold = spec.flops() / (ms_cold * 1e-3) / 1e12
@@ -626,20 +645,12 @@ def main() -> None:
                     "l2_warm": {"kernel_ms": ms, "gbs": nbytes / (ms * 1e-3) / 1e9, "tflops": ach}}
         else:
             peak_src = _dtype_peak_source(args.dtype, pk)
-            if args.dtype == "bf16" and pk.get("tflops_sustained") and ms * reps_graph >= 2.0:
-                # the re-time is a long step (>= 2 ms of back-to-back tensor
-                # work: 4096^3): the board's power limit engages, so the
-                # sustained measured peak is the denominator (the burst one
-                # for a kernel timed alone, e.g. 1024^3's 0.5 ms)
-                peak = pk["tflops_sustained"]
-                peak_src = (f"{pk['source']} sustained bf16 (MEASURED_PEAKS.json; the re-time runs "
-                            f"{ms * reps_graph:.1f} ms of back-to-back launches); burst-peak fraction "
-                            f"{ach / pk['tflops']:.3f}")
             roof = {"bound": "fp32-fma" if args.dtype == "f32" else "tensor", "achieved": ach,
                     "peak": peak, "unit": "TFLOP/s",
                     "frac": ach / peak, "traffic": _ncu_traffic(ncu_op, best_knobs),
                     "peak_source": peak_src,
-                    "kernel_ms": ms, "timing": f"{reps_graph} back-to-back launches in one CUDA graph",
+                    "kernel_ms": ms, "timing": f"{reps_graph} back-to-back launches in one CUDA graph"
+                                               f" ({ms * reps_graph:.2f} ms: a burst)",
                     "per_launch_flops": spec.flops(), "per_launch_bytes": nbytes}
 
     # ---------------- cold kernel cache: a fresh evaluator over an empty

@@ -690,6 +690,7 @@ struct opevo_ctx {
     std::unique_ptr<HostPool> pool;     // graph builds of a trial batch
     CUmodule util = nullptr;
     CUfunction k_fill_bf16 = nullptr, k_fill_f32 = nullptr, k_fill_u8 = nullptr, k_ref_gemm = nullptr,
+               k_ref_gemm128 = nullptr,
                k_ref_conv = nullptr, k_nchw2nhwc = nullptr, k_compare = nullptr, k_flush = nullptr,
                k_gate = nullptr, k_nchw2nhwc_pad = nullptr, k_nhwc_pad2nchw = nullptr;
     volatile uint32_t* gate_host = nullptr;   // mapped pinned flag opening the timing gate
@@ -832,8 +833,12 @@ int compute_reference(opevo_op* op, char* err, size_t errlen) {
     } else {
         int rows = (int)op->rows, cols = (int)op->cols, depth = (int)op->depth, in_f32 = op->in_f32;
         void* args[] = {&op->a, &op->b, &op->ref, &rows, &cols, &depth, &in_f32};
-        CU_TRY(ctx, g_cu.LaunchKernel(ctx->k_ref_gemm, (unsigned)((cols + 63) / 64), (unsigned)((rows + 63) / 64),
-                                      (unsigned)op->batch, 256, 1, 1, 0, ctx->stream, args, nullptr),
+        // large operands: the 128x128-tile reference (bit-identical sums)
+        const bool big = rows >= 512 && cols >= 512;
+        const unsigned t = big ? 128u : 64u;
+        CU_TRY(ctx, g_cu.LaunchKernel(big ? ctx->k_ref_gemm128 : ctx->k_ref_gemm, (unsigned)((cols + t - 1) / t),
+                                      (unsigned)((rows + t - 1) / t), (unsigned)op->batch, 256, 1, 1, 0,
+                                      ctx->stream, args, nullptr),
                "reference gemm");
     }
     CU_TRY(ctx, g_cu.StreamSynchronize(ctx->stream), "reference sync");
@@ -1162,6 +1167,7 @@ int opevo_ctx_create(int device, const char* cache_dir, opevo_ctx** out, char* e
         struct { CUfunction* f; const char* n; } fns[] = {
             {&ctx->k_fill_bf16, "opevo_fill_bf16"}, {&ctx->k_fill_f32, "opevo_fill_f32"},
             {&ctx->k_fill_u8, "opevo_fill_u8"},     {&ctx->k_ref_gemm, "opevo_ref_gemm"},
+            {&ctx->k_ref_gemm128, "opevo_ref_gemm128"},
             {&ctx->k_ref_conv, "opevo_ref_conv"},   {&ctx->k_nchw2nhwc, "opevo_nchw_to_nhwc"},
             {&ctx->k_compare, "opevo_compare"},     {&ctx->k_flush, "opevo_flush"},
             {&ctx->k_gate, "opevo_gate"},           {&ctx->k_nchw2nhwc_pad, "opevo_nchw_to_nhwc_pad"},

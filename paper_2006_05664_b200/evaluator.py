@@ -250,10 +250,15 @@ class GpuEvaluator:
             mode = 0 if int(self.settings.flush_l2) == 2 else int(self.settings.flush_l2)
         kernels = [self.dev.kernel(self.op, kn) for kn, _ in top]
         times: list[list[float]] = [[] for _ in top]
+        # each measurement is a burst of ~1 ms at most (long kernels get
+        # fewer launches): minutes of back-to-back 4096^3 launches would
+        # measure the board's power limit, not the kernel
+        nreps = [max(5, min(reps, int(1.0 / (self.flops / (fit * 1e9))))) if fit > 0 else reps
+                 for _, fit in top]
         try:
             for _ in range(rounds):
                 for i, kr in enumerate(kernels):
-                    times[i].append(kr.time(warmup=3, reps=reps, flush_l2=mode))
+                    times[i].append(kr.time(warmup=3, reps=nreps[i], flush_l2=mode))
         finally:
             for kr in kernels:
                 kr.close()
@@ -261,13 +266,13 @@ class GpuEvaluator:
         tq = {1: 12.706, 2: 4.303, 3: 3.182, 4: 2.776, 5: 2.571, 6: 2.447, 7: 2.365, 8: 2.306,
               9: 2.262}.get(rounds - 1, 1.96)
         out = []
-        for (kn, fit), ts in zip(top, times):
+        for (kn, fit), ts, n in zip(top, times, nreps):
             mean = sum(ts) / len(ts)
             sd = (sum((t - mean) ** 2 for t in ts) / (len(ts) - 1)) ** 0.5 if len(ts) > 1 else 0.0
             half = tq * sd / len(ts) ** 0.5
             out.append({"knobs": list(kn), "tflops": self.flops / (mean * 1e-3) / 1e12,
                         "ms": mean, "ci95_pct": 100.0 * half / mean if mean > 0 else None,
-                        "search_tflops": fit, "rounds": rounds, "reps": reps})
+                        "search_tflops": fit, "rounds": rounds, "reps": n})
         out.sort(key=lambda d: -d["tflops"])
         return out
 

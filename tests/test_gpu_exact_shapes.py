@@ -126,6 +126,14 @@ def mm1024(dev):
     op.close()
 
 
+def test_large_reference_gemm_matches_the_oracle(dev, mm1024):
+    """The in-library fp32 reference every trial is checked against (for
+    operands of 512+ rows and columns the 128x128-tile variant) within 1e-5
+    of the fp64 oracle over the whole 1024^3 output."""
+    op, ref = mm1024
+    assert _rel(op.reference(), ref) < 1e-5
+
+
 @pytest.mark.parametrize("knobs", MM1024)
 def test_matmul_1024_full(dev, mm1024, knobs):
     op, ref = mm1024
