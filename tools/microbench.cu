@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(256, 1) mma_issue_bench(u64* out, int iters, i
     __shared__ u32 tslot;
     __shared__ volatile int done;
     const int warp = threadIdx.x >> 5;
-    for (int i = threadIdx.x; i < 128 * 1024 / 4; i += blockDim.x) ((u32*)smem)[i] = 0x3c003c00u;
+    for (int i = threadIdx.x; i < 96 * 1024 / 4; i += blockDim.x) ((u32*)smem)[i] = 0x3c003c00u;
     if (threadIdx.x == 0) {
         done = 0;
         mbar_init(smem_u32(&never), 1);
@@ -356,6 +356,40 @@ __global__ void __launch_bounds__(256, 1) mma_issue_bench(u64* out, int iters, i
     const u32 blo = (u32)(HI | (u64)(((smem_u32(smem) + 16 * 1024) >> 4) & 0x3FFF));
     const u32 dhi = (u32)(HI >> 32);
     const u64 ad = ((u64)dhi << 32) | alo, bd = ((u64)dhi << 32) | blo;
+    if (v == 7 && warp == 4) {
+        // a TMA-like writer: bulk copies (L2 -> this CTA's shared memory, 6 x 8 KB
+        // in flight) into a scratch area while the MMA warp runs; the bytes
+        // it landed are reported in out[600 + block]
+        __shared__ __align__(8) u64 wb[6];
+        const int lane = threadIdx.x & 31;
+        if (lane == 0) {
+            for (int q = 0; q < 6; ++q) mbar_init(smem_u32(&wb[q]), 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        u64 landed = 0;
+        int it = 0;
+        const char* src = reinterpret_cast<const char*>(out) + 8192;
+        if (lane == 0) {
+            for (int q = 0; q < 6; ++q) {
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(&wb[q])), "r"(8192) : "memory");
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                             :: "r"(smem_u32(smem + 48 * 1024 + q * 8192)), "l"(src), "r"(8192), "r"(smem_u32(&wb[q])) : "memory");
+            }
+            while (!done) {
+                const int q = it % 6;
+                mbar_wait(smem_u32(&wb[q]), (it / 6) & 1);
+                landed += 8192;
+                ++it;
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(&wb[q])), "r"(8192) : "memory");
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                             :: "r"(smem_u32(smem + 48 * 1024 + q * 8192)), "l"(src), "r"(8192), "r"(smem_u32(&wb[q])) : "memory");
+            }
+            for (int r = 0; r < 6; ++r, ++it) mbar_wait(smem_u32(&wb[it % 6]), (it / 6) & 1);
+            out[600 + blockIdx.x] = landed;
+        }
+        __syncwarp();
+    }
     if ((v == 2 && warp == 4) || (v == 3 && warp == 5)) {
         while (!done) {
             u32 ok;
@@ -441,7 +475,7 @@ __global__ void __launch_bounds__(256, 1) mma_issue_bench(u64* out, int iters, i
             mbar_wait(smem_u32(&bar), rep & 1);
             c1 = clock64();
         }
-        if (threadIdx.x == 0) { out[0] = c1 - c0; done = 1; }
+        if (threadIdx.x == 0) { out[blockIdx.x] = c1 - c0; done = 1; }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -548,7 +582,31 @@ int main() {
         printf("mma 12 per asm block N=64: %.1f cyc/MMA\n", (double)h[0] / (iters * 12));
     }
     {
-        const int smem = 128 * 1024 + 1024;
+        // two CTAs per SM, each with its own MMA-issuing warp: does the SM's
+        // tensor pipe take more N = 64 MMAs than one issuing warp feeds?
+        const int smem = 100 * 1024;
+        CK(cudaFuncSetAttribute(mma_issue_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        for (int v : {0, 7})
+        for (int grid : {1, 148, 296}) {
+            const int iters = 256;
+            mma_issue_bench<<<grid, 256, smem>>>(d_out, iters, v);
+            CK(cudaDeviceSynchronize());
+            u64 h[1024];
+            CK(cudaMemcpy(h, d_out, sizeof(u64) * 1024, cudaMemcpyDeviceToHost));
+            double cyc = 0, bytes = 0;
+            for (int i = 0; i < grid; ++i) { cyc += (double)h[i]; bytes += (double)h[600 + i]; }
+            cyc /= grid;
+            bytes /= grid;
+            printf("mma issue v%d, %d CTAs (%s): %.1f cyc/MMA per CTA -> %.1f cyc/MMA per SM%s", v, grid,
+                   grid == 296 ? "2 per SM" : "1 per SM", cyc / (iters * 12),
+                   cyc / (iters * 12) / (grid == 296 ? 2.0 : 1.0), v == 7 ? "" : "\n");
+            if (v == 7)
+                printf("; concurrent bulk writes %.1f B/clk per CTA (%.1f per SM)\n", bytes / cyc,
+                       bytes / cyc * (grid == 296 ? 2.0 : 1.0));
+        }
+    }
+    {
+        const int smem = 100 * 1024;
         CK(cudaFuncSetAttribute(mma_issue_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         for (int v : {0, 6}) {
             const int iters = 128;
