@@ -71,6 +71,7 @@ struct Driver {
     X(ModuleGetFunction, cuModuleGetFunction)                     \
     X(FuncLoad, cuFuncLoad)                                       \
     X(FuncSetAttribute, cuFuncSetAttribute)                       \
+    X(FuncGetAttribute, cuFuncGetAttribute)                       \
     X(LaunchKernel, cuLaunchKernel)                               \
     X(LaunchKernelEx, cuLaunchKernelEx)                           \
     X(MemAlloc, cuMemAlloc_v2)                                    \
@@ -700,6 +701,7 @@ struct opevo_ctx {
     size_t flush_bytes = 0;
     CUdeviceptr cmp_buf = 0;
     int sm_count = 0, smem_optin = 0, cc_major = 0, cc_minor = 0;
+    int smem_per_sm = 0, regs_per_sm = 0;
     // trial timing policy (opevo_ctx_set_timing)
     double budget_ms = 0.3;
     double loser_ratio = 0.0;
@@ -1145,6 +1147,8 @@ int opevo_ctx_create(int device, const char* cache_dir, opevo_ctx** out, char* e
     }
     g_cu.DeviceGetAttribute(&ctx->sm_count, CU_DEVICE_ATTRIBUTE_MULTIPROCESSOR_COUNT, ctx->dev);
     g_cu.DeviceGetAttribute(&ctx->smem_optin, CU_DEVICE_ATTRIBUTE_MAX_SHARED_MEMORY_PER_BLOCK_OPTIN, ctx->dev);
+    g_cu.DeviceGetAttribute(&ctx->smem_per_sm, CU_DEVICE_ATTRIBUTE_MAX_SHARED_MEMORY_PER_MULTIPROCESSOR, ctx->dev);
+    g_cu.DeviceGetAttribute(&ctx->regs_per_sm, CU_DEVICE_ATTRIBUTE_MAX_REGISTERS_PER_MULTIPROCESSOR, ctx->dev);
     g_cu.DeviceGetAttribute(&ctx->cc_major, CU_DEVICE_ATTRIBUTE_COMPUTE_CAPABILITY_MAJOR, ctx->dev);
     g_cu.DeviceGetAttribute(&ctx->cc_minor, CU_DEVICE_ATTRIBUTE_COMPUTE_CAPABILITY_MINOR, ctx->dev);
     if (ctx->cc_major != 10) {
@@ -1629,6 +1633,29 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
     {
         int per_sm = 1;
         if (g_cu.OccupancyMaxBlocks(&per_sm, kr->fn, 192, kr->smem) != CUDA_SUCCESS || per_sm < 1) per_sm = 1;
+        // The occupancy API answers 1 CTA per SM for every tcgen05 kernel (it
+        // does so for a 64-thread register-light one too), yet two
+        // single-CTA instances whose shared memory fits twice do run side by
+        // side (BMM1 128x64 BK 64, 2 stages: 262 -> 296 TFLOP/s with the
+        // persistent grid at 296; profiles/round2/two_ctas_per_sm.txt).  For
+        // single-CTA launches the residency is therefore counted from the
+        // resources themselves: shared memory (+ static + the 1 KB per-CTA
+        // reservation), registers (per-warp allocation in 256-register units),
+        // threads, and below the TMEM columns.
+        if (clsz == 1 && ctx->smem_per_sm > 0 && ctx->regs_per_sm > 0) {
+            int regs = 0, static_smem = 0;
+            g_cu.FuncGetAttribute(&regs, CU_FUNC_ATTRIBUTE_NUM_REGS, kr->fn);
+            g_cu.FuncGetAttribute(&static_smem, CU_FUNC_ATTRIBUTE_SHARED_SIZE_BYTES, kr->fn);
+            const long per_cta_smem = (long)kr->smem + static_smem + 1024;
+            const int warps = 192 / 32;
+            const long per_warp_regs = ((long)std::max(regs, 1) * 32 + 255) / 256 * 256;
+            const int by_smem = (int)(ctx->smem_per_sm / per_cta_smem);
+            const int by_regs = (int)(ctx->regs_per_sm / (per_warp_regs * warps));
+            const int by_threads = 2048 / 192;
+            per_sm = std::max(per_sm, std::min(std::min(by_smem, by_regs), std::min(by_threads, 32)));
+        }
+        static const int force_per_sm = getenv("OPEVO_FORCE_PER_SM") ? atoi(getenv("OPEVO_FORCE_PER_SM")) : 0;
+        if (force_per_sm > 0) per_sm = force_per_sm;      // experiments only
         per_sm = std::min(per_sm, 512 / tmem_alloc_cols(k));
         const int capacity = std::max(1, (ctx->sm_count / clsz) * per_sm);
         SchedHost& sc = kr->sched;
