@@ -111,6 +111,9 @@
 #ifndef OPEVO_LINE
 #define OPEVO_LINE 0       // conv: padded lines of this many tile rows (0: dense tile)
 #endif
+#ifndef OPEVO_NARROW_EPI
+#define OPEVO_NARROW_EPI 0 // 32-column epilogue staging (host rule: two CTAs per SM)
+#endif
 #ifndef OPEVO_TILE_H
 #define OPEVO_TILE_H 1
 #endif
@@ -199,7 +202,9 @@ constexpr u32 LAYOUT = SWZ == 128 ? 2u : SWZ == 64 ? 4u : 6u;
 constexpr int EPI_COLS = (BN % 32 == 0) ? 32 : 16;    // split-K / DSMEM reduction chunks
 // TMA-store epilogue chunk: 64 bf16 columns (one 128-byte swizzle row) when
 // BN allows, so each chunk is one TMEM load, one proxy fence and one store
-constexpr int STORE_COLS = (!OPEVO_OUT_F32 && BN % 64 == 0 && OPEVO_ACC == 1) ? 64 : EPI_COLS;
+// (32 columns instead when the host's two-CTAs-per-SM rule asks for the
+// smaller staging: OPEVO_NARROW_EPI, narrow_epi in opevo.cpp)
+constexpr int STORE_COLS = (!OPEVO_OUT_F32 && BN % 64 == 0 && OPEVO_ACC == 1 && !OPEVO_NARROW_EPI) ? 64 : EPI_COLS;
 constexpr int NUM_THREADS = 192;
 constexpr int SMEM_ALIGN = 1024;
 constexpr int TILE_H = OPEVO_TILE_H;

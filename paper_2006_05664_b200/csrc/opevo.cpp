@@ -257,7 +257,7 @@ size_t dsmem_red_bytes(const Knobs& k) {
     return (size_t)k.bm * ld * 4 + (size_t)(s - 1) * (k.bm / s) * ld * 4;
 }
 
-size_t epi_stage_bytes(const Knobs& k, int out_f32);
+size_t wide_epi_stage_bytes(const Knobs& k, int out_f32);
 
 // TMA split-K (split 2 or 4 on single-CTA 128-row bf16 GEMM tiles): the
 // slices of a tile reduce through fp32 partials in global memory written
@@ -274,24 +274,24 @@ bool dsmem_split(const Knobs& k, int family, int batched = 0) {
     return family != 2 && (k.split == 2 || k.split == 4 || k.split == 8) && k.cg == 1 &&
            !(family == 1 && k.line) &&   // padded lines reduce through the global path
            k.cluster == 1 && k.bm == 128 && !tma_split(k, family, batched) &&
-           (dsmem_red_bytes(k) + 1023) / 1024 * 1024 + epi_stage_bytes(k, family == FAMILY_X3) + 1024 + 256 <=
+           (dsmem_red_bytes(k) + 1023) / 1024 * 1024 + wide_epi_stage_bytes(k, family == FAMILY_X3) + 1024 + 256 <=
                232448;
 }
 
-// TMA-store epilogue chunk width (mirrors STORE_COLS in gemm_sm100.cuh).
-int epi_cols(const Knobs& k, int out_f32 = 0) {
+// TMA-store epilogue chunk width before the two-CTAs-per-SM rule below.
+int wide_epi_cols(const Knobs& k, int out_f32) {
     return (!out_f32 && k.bn % 64 == 0 && k.acc == 1) ? 64 : k.bn % 32 == 0 ? 32 : 16;
 }
 
 // TMA-store staging: 4 epilogue warps x 2 buffers x 32 rows x STORE_COLS outputs.
-size_t epi_stage_bytes(const Knobs& k, int out_f32) {
-    return (size_t)4 * 2 * 32 * epi_cols(k, out_f32) * (out_f32 ? 4 : 2);
+size_t epi_stage_bytes_cols(int cols, int out_f32) { return (size_t)4 * 2 * 32 * cols * (out_f32 ? 4 : 2); }
+size_t wide_epi_stage_bytes(const Knobs& k, int out_f32) {
+    return epi_stage_bytes_cols(wide_epi_cols(k, out_f32), out_f32);
 }
 
-// per-CTA: a CTA pair stages 128 rows of A and BN/2 rows of B each; then the
-// epilogue staging (1024-aligned) and the barriers (mirrors EPI_OFF/BAR_OFF)
-size_t smem_bytes(const Knobs& k, int family = 0, int out_f32 = 0, int batched = 0) {
-    if (family == 2) return 0;
+// Pipeline (operand stages or split-K reduction buffer) of one CTA, 1 KB aligned:
+// a CTA pair stages 128 rows of A and BN/2 rows of B each (mirrors PIPE_BYTES).
+size_t pipe_bytes(const Knobs& k, int family, int batched) {
     const int a_rows = k.cg == 2 ? 128 : k.bm;
     const int b_rows = b_resident(k, family) ? 0 : k.bn / (k.cg == 2 ? 2 : 1) * std::max(1, halo_kw(k, family));
     size_t pipe = (size_t)k.stages * (size_t)(a_rows + b_rows) * (size_t)k.bk * 2 * (size_t)std::max(1, k.bpu);
@@ -299,8 +299,39 @@ size_t smem_bytes(const Knobs& k, int family = 0, int out_f32 = 0, int batched =
     if (dsmem_split(k, family, batched)) pipe = std::max(pipe, dsmem_red_bytes(k));
     if (const int ts = tma_split(k, family, batched))
         pipe = std::max(pipe, (size_t)std::max(ts - 1, 1) * 128 * k.bn * 4);   // SPLITT_BYTES
-    pipe = (pipe + 1023) / 1024 * 1024;
-    return pipe + epi_stage_bytes(k, out_f32) + 1024 + 256;
+    return (pipe + 1023) / 1024 * 1024;
+}
+
+// Two CTAs per SM need 2 x (dynamic smem + the 1 KB per-CTA reservation) within
+// the SM's 228 KB.  A single-CTA bf16 instance that misses this only by its
+// 64-column epilogue staging (32 KB) stages 32 columns instead (16 KB): one
+// more TMEM load / fence / store per 64 columns, in exchange for a second CTA
+// -- i.e. a second MMA-issuing warp -- on every SM (conv halo tiles with 2
+// stages; profiles/round2/two_ctas_per_sm.txt).  Not for resident weight
+// panels (the panel alone keeps them at one CTA).  OPEVO_NARROW_EPI=0 disables
+// the rule (A/B experiments).  Mirrors Knobs.narrow_epi in mapping.py.
+constexpr size_t SM_SMEM_BYTES = 233472, CTA_RESERVED_SMEM = 1024;
+bool narrow_epi(const Knobs& k, int family, int out_f32, int batched) {
+    static const bool enabled = !(getenv("OPEVO_NARROW_EPI") && getenv("OPEVO_NARROW_EPI")[0] == '0');
+    if (!enabled || (family != 0 && family != 1) || out_f32 || wide_epi_cols(k, out_f32) != 64 ||
+        k.cluster != 1 || k.cg != 1 || dsmem_split(k, family, batched) || b_resident(k, family))
+        return false;
+    const size_t base = pipe_bytes(k, family, batched) + 1024 + 256 + CTA_RESERVED_SMEM;
+    return 2 * (base + epi_stage_bytes_cols(64, 0)) > SM_SMEM_BYTES &&
+           2 * (base + epi_stage_bytes_cols(32, 0)) <= SM_SMEM_BYTES;
+}
+
+// TMA-store epilogue chunk width (mirrors STORE_COLS in gemm_sm100.cuh).
+int epi_cols(const Knobs& k, int family, int out_f32, int batched) {
+    return narrow_epi(k, family, out_f32, batched) ? 32 : wide_epi_cols(k, out_f32);
+}
+
+// per-CTA: the pipeline, then the epilogue staging (1024-aligned) and the
+// barriers (mirrors EPI_OFF/BAR_OFF)
+size_t smem_bytes(const Knobs& k, int family = 0, int out_f32 = 0, int batched = 0) {
+    if (family == 2) return 0;
+    return pipe_bytes(k, family, batched) + epi_stage_bytes_cols(epi_cols(k, family, out_f32, batched), out_f32) +
+           1024 + 256;
 }
 
 uint64_t fnv1a(const char* s, size_t n, uint64_t h = 1469598103934665603ull) {
@@ -363,11 +394,12 @@ std::string make_key(int family, const Knobs& k, int batched, int out_f32) {
     }
     char line[16] = "";
     if (family == 1 && k.line) snprintf(line, sizeof line, "_l%d", k.line);
-    snprintf(buf, sizeof buf, "f%d_m%d_n%d_k%d_s%d_b%d_o%d_c%d_h%d_w%d_a%d_g%d%s%s_%s%012llx", family,
+    snprintf(buf, sizeof buf, "f%d_m%d_n%d_k%d_s%d_b%d_o%d_c%d_h%d_w%d_a%d_g%d%s%s%s_%s%012llx", family,
              k.bm, k.bn, k.bk, k.stages, batched, out_f32, k.cluster, family == 1 ? k.tile_h : 1,
              family == 1 ? k.tile_w : 1, k.acc,
              k.cg * 100 + (dsmem_split(k, family, batched) ? k.split : 0) + 10 * tma_split(k, family, batched),
              b_resident(k, family) ? "_r" : k.bpu > 1 ? (k.bpu == 2 ? "_u2" : "_u4") : "", line,
+             narrow_epi(k, family, out_f32, batched) ? "_e32" : "",
              want_lineinfo() ? "L" : "",
              (unsigned long long)(h & 0xffffffffffffull));
     return buf;
@@ -573,7 +605,8 @@ int nvrtc_build(int family, const Knobs& k, int batched, int out_f32, std::vecto
         "-DOPEVO_BPU=" + std::to_string(family == 0 ? std::max(1, k.bpu) : 1),
         "-DOPEVO_TF32X3=" + std::to_string(family == FAMILY_X3 ? 1 : 0),
         "-DOPEVO_HALO=" + std::to_string(halo_kw(k, family)),
-        "-DOPEVO_LINE=" + std::to_string(family == 1 ? k.line : 0)};
+        "-DOPEVO_LINE=" + std::to_string(family == 1 ? k.line : 0),
+        "-DOPEVO_NARROW_EPI=" + std::to_string(narrow_epi(k, family, out_f32, batched) ? 1 : 0)};
     if (want_lineinfo()) opts.push_back("-lineinfo");
     {
         std::istringstream extra(instance_flags(family, k));
@@ -1544,7 +1577,7 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
             // (halo / padded lines: one box per line, {EPI_COLS, TILE_W, 1, 1};
             // the chunk's junk rows are never stored)
             const bool lines = hkw || k.line;
-            const int ob = op->out_f32 ? 4 : 2, ec = epi_cols(k, op->out_f32);
+            const int ob = op->out_f32 ? 4 : 2, ec = epi_cols(k, family, op->out_f32, batched);
             const int bw = lines ? k.tile_w : std::min(k.tile_w, 32);
             const int bh = lines ? 1 : k.tile_w >= 32 ? 1 : std::min(k.tile_h, 32 / k.tile_w);
             const int bn = lines ? 1 : k.tile_w * k.tile_h >= 32 ? 1 : 32 / (k.tile_w * k.tile_h);
@@ -1598,7 +1631,7 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
         }
         const int rank = batched ? 3 : 2;
         if (!st) {
-            const int ob = op->out_f32 ? 4 : 2, ec = epi_cols(k, op->out_f32);
+            const int ob = op->out_f32 ? 4 : 2, ec = epi_cols(k, family, op->out_f32, batched);
             uint64_t cd[3] = {(uint64_t)op->cols, (uint64_t)op->rows, (uint64_t)op->batch};
             uint64_t cs[2] = {(uint64_t)op->cols * ob, (uint64_t)op->cols * op->rows * ob};
             uint32_t cb[3] = {(uint32_t)ec, 32, 1};

@@ -60,6 +60,8 @@ SMEM_LIMIT = 232448          # 227 KB opt-in per CTA on B200
 B200_SMS = 148
 MAX_SPLIT = 16               # OPEVO_MAX_SPLIT: split-K workspace slices allocated at prepare
 SMEM_EXTRA = 1024 + 256      # alignment slack + barriers
+SM_SMEM_BYTES = 233472       # B200 shared memory per SM
+CTA_RESERVED_SMEM = 1024     # reserved per resident CTA
 STAGE_VALUES = (2, 3, 4, 5, 6, 7, 8)
 UNROLL_TO_STAGES = {0: 2, 16: 3, 64: 4, 512: 6, 1500: 8}
 
@@ -139,13 +141,22 @@ class Knobs:
                 self.acc, self.cta_group, self.dsmem_split(), self.tma_split(), self.b_res, self.bpu,
                 self.line)
 
-    def smem_bytes(self) -> int:
-        """Mirrors ``smem_bytes`` in csrc/opevo.cpp (bf16 output)."""
-        if self.b_res:
-            return _align1k(self.bm * self.bk * 2 * self.stages) + epi_bytes(self.bn) + 2048 + self.panel_bytes
+    def narrow_epi(self) -> bool:
+        """Two-CTAs-per-SM rule (mirrors ``narrow_epi`` in csrc/opevo.cpp): a
+        single-CTA bf16 instance that fits twice on an SM only with 32-column
+        epilogue staging (16 KB instead of 32 KB) uses it."""
+        if (self.family not in (FAMILY_GEMM, FAMILY_CONV) or self.bn % 64 or self.acc != 1
+                or self.cluster != 1 or self.cta_group != 1 or self.dsmem_split() or self.b_res):
+            return False
+        base = self._pipe_bytes() + SMEM_EXTRA + CTA_RESERVED_SMEM
+        return 2 * (base + epi_bytes(64)) > SM_SMEM_BYTES and 2 * (base + epi_bytes(32)) <= SM_SMEM_BYTES
+
+    def _epi(self) -> int:
+        return epi_bytes(32 if self.narrow_epi() else self.bn)
+
+    def _pipe_bytes(self) -> int:
         if self.halo_kw():
-            return (_align1k((self.bm_cta + self.halo_kw() * self.bn // self.cta_group) * self.bk * 2
-                             * self.stages) + epi_bytes(self.bn) + SMEM_EXTRA)
+            return _align1k((self.bm_cta + self.halo_kw() * self.bn // self.cta_group) * self.bk * 2 * self.stages)
         x3 = self.family == FAMILY_TF32X3
         if x3:   # fp32 operands (bf16 pairs) staged twice: hi as landed + lo
             pipe = 2 * stage_bytes(self.bm, self.bn, 2 * self.bk) * self.stages
@@ -156,7 +167,14 @@ class Knobs:
             pipe = max(pipe, self.bm * ld * 4 + (self.split - 1) * (self.bm // self.split) * ld * 4)
         if self.tma_split():
             pipe = max(pipe, max(self.split - 1, 1) * 128 * self.bn * 4)
-        return _align1k(pipe) + epi_bytes(self.bn, x3) + SMEM_EXTRA
+        return _align1k(pipe)
+
+    def smem_bytes(self) -> int:
+        """Mirrors ``smem_bytes`` in csrc/opevo.cpp (bf16 output)."""
+        if self.b_res:
+            return _align1k(self.bm * self.bk * 2 * self.stages) + epi_bytes(self.bn) + 2048 + self.panel_bytes
+        x3 = self.family == FAMILY_TF32X3
+        return self._pipe_bytes() + (epi_bytes(self.bn, True) if x3 else self._epi()) + SMEM_EXTRA
 
 
 @dataclass(frozen=True)

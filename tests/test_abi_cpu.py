@@ -114,3 +114,24 @@ def test_gpu_evaluator_raises_fatal_without_device():
 
     with pytest.raises(FatalEvaluationError):
         GpuEvaluator(MatMulSpec(256, 256, 256))
+
+
+def test_narrow_epilogue_rule_matches_the_mapping():
+    """The two-CTAs-per-SM rule (32-column epilogue staging, key suffix
+    ``_e32``) is decided the same way by the library and by mapping.py, over
+    every instance of the conv cfg4, BMM1 and 1024^3 families."""
+    from paper_2006_05664_b200.mapping import Knobs
+    from paper_2006_05664_b200.operators import parse_operator
+    from paper_2006_05664_b200.prebuild import family_instances
+
+    seen = 0
+    for opid in ("conv2d:32,64,56,56,64,3,3,1,1", "batchmatmul:960,128,64,128", "matmul:1024,1024,1024"):
+        for fam, batched, kn in family_instances(parse_operator(opid)):
+            narrow = Knobs(*kn, family=fam, batched=int(batched)).narrow_epi()
+            assert ("_e32" in capi.kernel_key(fam, kn, batched, False)) == narrow, kn
+            seen += narrow
+    assert seen > 100
+    # a 2-stage halo conv tile: 114 KB with 64-column staging, 98 KB with 32
+    halo2 = Knobs(128, 64, 64, 2, 1, 1, 1, 14, family=1)
+    assert halo2.narrow_epi() and halo2.smem_bytes() == 80 * 1024 + 16 * 1024 + 1280
+    assert not Knobs(128, 64, 64, 3, 1, 1, 1, 14, family=1).narrow_epi()

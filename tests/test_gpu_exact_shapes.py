@@ -66,6 +66,9 @@ MM4096 = [
     # K-interleaved accumulators; global split-K reduction
     (128, 128, 128, 3, 1, 1, 1, 1, 2, 1, 0, 0, 1),
     (128, 256, 64, 4, 8, 1, 1, 1, 1, 1, 0, 0, 1),
+    # 32-column epilogue staging so two CTAs share an SM (narrow_epi)
+    (256, 64, 64, 2, 1, 1, 1, 1, 1, 1, 0, 0, 1),
+    (128, 128, 32, 5, 2, 1, 1, 1, 1, 1, 0, 0, 1),
 ]
 
 
@@ -174,6 +177,8 @@ BMM_KNOBS = [
     (128, 64, 64, 4, 2, 1, 1, 1, 1, 1, 0, 0, 1),
     (128, 64, 32, 4, 4, 1, 1, 1, 1, 1, 0, 0, 1),
     (128, 64, 64, 3, 1, 1, 1, 1, 2, 1, 0, 0, 1),
+    # 32-column epilogue staging so two CTAs share an SM (narrow_epi)
+    (128, 64, 32, 7, 1, 1, 1, 1, 1, 1, 0, 0, 1),
 ]
 
 
@@ -237,6 +242,9 @@ CONV_KNOBS = [
     (128, 64, 64, 4, 3, 1, 2, 8, 1, 1, 0, 0, 1),
     (128, 64, 32, 6, 1, 1, 4, 8, 1, 1, 1, 0, 1),
     (128, 32, 16, 8, 1, 1, 2, 8, 1, 1, 0, 0, 1),
+    # 32-column epilogue staging so two CTAs share an SM (narrow_epi)
+    (128, 64, 64, 2, 1, 1, 1, 14, 1, 1, 0, 0, 1),
+    (256, 64, 64, 2, 3, 1, 4, 2, 1, 1, 0, 0, 1),
 ]
 
 

@@ -22,7 +22,7 @@ __device__ __forceinline__ void mbar_wait(u32 bar, u32 parity) {
                  :: "r"(bar), "r"(parity) : "memory");
 }
 
-template <int N>
+template <int N, int M = 128>
 __global__ void __launch_bounds__(128, 1) mma_bench(u64* out, int iters, int a_shift_rows, int b_off) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = (unsigned char*)(((u64)smem_raw + 1023) & ~1023ull);
@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(128, 1) mma_bench(u64* out, int iters, int a_s
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const u32 tmem = tslot;
-    constexpr u32 IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((u32)(N >> 3) << 17) | ((u32)(128 >> 4) << 24);
+    constexpr u32 IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((u32)(N >> 3) << 17) | ((u32)(M >> 4) << 24);
     constexpr u64 HI = ((u64)1 << 16) | ((u64)(1024 >> 4) << 32) | ((u64)1 << 46) | ((u64)2 << 61);
     // a_shift_rows: the A descriptor starts that many 128-byte rows into the
     // tile (the conv halo-line taps' shifted operands; 8 = one whole group)
@@ -521,12 +521,12 @@ __global__ void __launch_bounds__(32, 1) bulk_bench(const char* src, size_t per_
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); exit(1); } } while (0)
 
-template <int N>
+template <int N, int M = 128>
 void run_mma(u64* d_out, int grid, int shift = 0, int b_off = 160 * 128) {
     const int smem = b_off + 256 * 64 * 2 + 1024;
-    CK(cudaFuncSetAttribute(mma_bench<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaFuncSetAttribute(mma_bench<N, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int iters = 256;
-    mma_bench<N><<<grid, 128, smem>>>(d_out, iters, shift, b_off);
+    mma_bench<N, M><<<grid, 128, smem>>>(d_out, iters, shift, b_off);
     CK(cudaDeviceSynchronize());
     u64 h[2 * 148];
     CK(cudaMemcpy(h, d_out, sizeof(u64) * 2 * grid, cudaMemcpyDeviceToHost));
@@ -534,14 +534,25 @@ void run_mma(u64* d_out, int grid, int shift = 0, int b_off = 160 * 128) {
     for (int i = 0; i < grid; ++i) { cyc += h[2 * i]; ns += h[2 * i + 1]; }
     cyc /= grid; ns /= grid;
     const int mmas = iters * 4;
-    const double flop = 2.0 * 128 * N * 16 * mmas;
-    printf("mma M=128 N=%3d grid=%3d A shift %d rows B at +%6d: %.1f cyc/MMA (ideal %d), %.2f GHz, %.2f TFLOP/s/SM -> %.0f TFLOP/s x148\n",
-           N, grid, shift, b_off, cyc / mmas, 128 * N / 256, cyc / ns, flop / ns / 1e3, 148 * flop / ns / 1e3);
+    const double flop = 2.0 * M * N * 16 * mmas;
+    printf("mma M=%d N=%3d grid=%3d A shift %d rows B at +%6d: %.1f cyc/MMA (ideal %d), %.2f GHz, %.2f TFLOP/s/SM -> %.0f TFLOP/s x148\n",
+           M, N, grid, shift, b_off, cyc / mmas, M * N / 256, cyc / ns, flop / ns / 1e3, 148 * flop / ns / 1e3);
 }
 
 int main() {
     u64* d_out;
     CK(cudaMalloc(&d_out, sizeof(u64) * 2 * 1024));
+    if (getenv("MMA_M64")) {      // M = 64 (e.g. conv with Cout as M and pixels as N)
+        for (int g : {1, 148}) {
+            run_mma<64, 64>(d_out, g);
+            run_mma<128, 64>(d_out, g);
+            run_mma<256, 64>(d_out, g);
+            run_mma<64, 128>(d_out, g);
+            run_mma<256, 128>(d_out, g);
+        }
+        for (int sh : {0, 1, 2, 8}) run_mma<256, 64>(d_out, 1, 0, 160 * 128 + 128 * sh);   // B (pixels) shifted
+        return 0;
+    }
     for (int g : {1, 148}) {
         run_mma<64>(d_out, g);
         run_mma<128>(d_out, g);
