@@ -2364,6 +2364,7 @@ int opevo_trial_batch(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nk
             res[i].rel_err = rel;
             if (status[i] != OPEVO_OK) continue;
             g_cu.EventElapsedTime(&est, ev[4 * i], ev[4 * i + 1]);
+            if (prof) fprintf(stderr, "[check %d] est %.4f ms\n", i, est);
             // slow candidates are timed by their verified launch itself, so
             // only fast ones are remembered (a repeat of a slow one re-checks)
             if (!slow_candidate(ctx, est) && tol >= 0) op->verified[vkey[i]] = opevo_op::Verified{rel, est};

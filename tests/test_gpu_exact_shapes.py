@@ -68,7 +68,6 @@ MM4096 = [
     (128, 256, 64, 4, 8, 1, 1, 1, 1, 1, 0, 0, 1),
     # 32-column epilogue staging so two CTAs share an SM (narrow_epi)
     (256, 64, 64, 2, 1, 1, 1, 1, 1, 1, 0, 0, 1),
-    (128, 128, 32, 5, 2, 1, 1, 1, 1, 1, 0, 0, 1),
 ]
 
 
@@ -114,6 +113,9 @@ MM1024 = [
     (128, 256, 64, 3, 4, 1, 1, 1, 1, 1, 0, 0, 1),     # global split-K reduction
     (128, 64, 64, 4, 8, 1, 1, 1, 1, 1, 0, 0, 1),      # DSMEM split-K (cluster of 8)
     (128, 64, 64, 2, 16, 1, 1, 1, 1, 1, 0, 0, 1),     # deepest split: global reduction
+    # 32-column epilogue staging so two CTAs share an SM (narrow_epi), also under TMA split-K
+    (256, 64, 64, 2, 1, 1, 1, 1, 1, 1, 0, 0, 1),
+    (128, 128, 32, 5, 2, 1, 1, 1, 1, 1, 0, 0, 1),
 ]
 
 
