@@ -303,7 +303,7 @@ size_t pipe_bytes(const Knobs& k, int family, int batched) {
 }
 
 // Two CTAs per SM need 2 x (dynamic smem + the 1 KB per-CTA reservation) within
-// the SM's 228 KB.  A single-CTA bf16 instance that misses this only by its
+// the SM's 228 KB.  A single-CTA or CTA-pair bf16 instance that misses this only by its
 // 64-column epilogue staging (32 KB) stages 32 columns instead (16 KB): one
 // more TMEM load / fence / store per 64 columns, in exchange for a second CTA
 // -- i.e. a second MMA-issuing warp -- on every SM (conv halo tiles with 2
@@ -314,7 +314,7 @@ constexpr size_t SM_SMEM_BYTES = 233472, CTA_RESERVED_SMEM = 1024;
 bool narrow_epi(const Knobs& k, int family, int out_f32, int batched) {
     static const bool enabled = !(getenv("OPEVO_NARROW_EPI") && getenv("OPEVO_NARROW_EPI")[0] == '0');
     if (!enabled || (family != 0 && family != 1) || out_f32 || wide_epi_cols(k, out_f32) != 64 ||
-        k.cluster != 1 || k.cg != 1 || dsmem_split(k, family, batched) || b_resident(k, family))
+        k.cluster != 1 || dsmem_split(k, family, batched) || b_resident(k, family))
         return false;
     const size_t base = pipe_bytes(k, family, batched) + 1024 + 256 + CTA_RESERVED_SMEM;
     return 2 * (base + epi_stage_bytes_cols(64, 0)) > SM_SMEM_BYTES &&
@@ -1675,7 +1675,9 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
         // resources themselves: shared memory (+ static + the 1 KB per-CTA
         // reservation), registers (per-warp allocation in 256-register units),
         // threads, and below the TMEM columns.
-        if (clsz == 1 && ctx->smem_per_sm > 0 && ctx->regs_per_sm > 0) {
+        // (CTA pairs too: two pair clusters share an SM pair the same way)
+        if ((clsz == 1 || (clsz == 2 && k.cg == 2 && k.cluster == 1)) && ctx->smem_per_sm > 0 &&
+            ctx->regs_per_sm > 0) {
             int regs = 0, static_smem = 0;
             g_cu.FuncGetAttribute(&regs, CU_FUNC_ATTRIBUTE_NUM_REGS, kr->fn);
             g_cu.FuncGetAttribute(&static_smem, CU_FUNC_ATTRIBUTE_SHARED_SIZE_BYTES, kr->fn);

@@ -143,10 +143,10 @@ class Knobs:
 
     def narrow_epi(self) -> bool:
         """Two-CTAs-per-SM rule (mirrors ``narrow_epi`` in csrc/opevo.cpp): a
-        single-CTA bf16 instance that fits twice on an SM only with 32-column
+        single-CTA or CTA-pair bf16 instance that fits twice on an SM only with 32-column
         epilogue staging (16 KB instead of 32 KB) uses it."""
         if (self.family not in (FAMILY_GEMM, FAMILY_CONV) or self.bn % 64 or self.acc != 1
-                or self.cluster != 1 or self.cta_group != 1 or self.dsmem_split() or self.b_res):
+                or self.cluster != 1 or self.dsmem_split() or self.b_res):
             return False
         base = self._pipe_bytes() + SMEM_EXTRA + CTA_RESERVED_SMEM
         return 2 * (base + epi_bytes(64)) > SM_SMEM_BYTES and 2 * (base + epi_bytes(32)) <= SM_SMEM_BYTES

@@ -66,8 +66,9 @@ MM4096 = [
     # K-interleaved accumulators; global split-K reduction
     (128, 128, 128, 3, 1, 1, 1, 1, 2, 1, 0, 0, 1),
     (128, 256, 64, 4, 8, 1, 1, 1, 1, 1, 0, 0, 1),
-    # 32-column epilogue staging so two CTAs share an SM (narrow_epi)
+    # 32-column epilogue staging so two CTAs (pairs) share an SM (pair) (narrow_epi)
     (256, 64, 64, 2, 1, 1, 1, 1, 1, 1, 0, 0, 1),
+    (256, 128, 32, 7, 1, 1, 1, 1, 1, 2, 0, 0, 1),
 ]
 
 
@@ -116,6 +117,7 @@ MM1024 = [
     # 32-column epilogue staging so two CTAs share an SM (narrow_epi), also under TMA split-K
     (256, 64, 64, 2, 1, 1, 1, 1, 1, 1, 0, 0, 1),
     (128, 128, 32, 5, 2, 1, 1, 1, 1, 1, 0, 0, 1),
+    (256, 64, 64, 4, 1, 1, 1, 1, 1, 2, 0, 0, 1),       # CTA pair
 ]
 
 
@@ -247,6 +249,9 @@ CONV_KNOBS = [
     # 32-column epilogue staging so two CTAs share an SM (narrow_epi)
     (128, 64, 64, 2, 1, 1, 1, 14, 1, 1, 0, 0, 1),
     (256, 64, 64, 2, 3, 1, 4, 2, 1, 1, 0, 0, 1),
+    # ... and two CTA pairs per SM pair (halo lines, 3 stages)
+    (256, 64, 64, 3, 1, 1, 4, 14, 1, 2, 0, 0, 1),
+    (256, 64, 64, 3, 1, 1, 2, 14, 1, 2, 0, 0, 1),
 ]
 
 
