@@ -4,6 +4,7 @@
         --budget 500 --seed 0 --out out/
     python -m paper_2006_05664_b200 compare --operator matmul:1024,1024,1024 \\
         --algo opevo,random,sa,gbfs --seeds 0,1,2 --budget 300 --out out/
+        (``bench`` is the same command under the reference CLI's name)
     python -m paper_2006_05664_b200 sweep --operator matmul:1024,1024,1024 \\
         --q-grid 0.25,0.5,0.75 --lambda-grid 4,8,16 --seeds 0,1,2 --out out/
 
@@ -77,7 +78,7 @@ def _run(algo, space, objective, seed, budget, parents: int = 8, mutation_rate: 
 def cmd_tune(args) -> int:
     space, objective = _objective(args)
     t0 = time.perf_counter()
-    best, recs = _run(args.algo, space, objective, args.seed, args.budget)
+    best, recs = _run(args.algo, space, objective, args.seed, args.budget, args.parents, args.q)
     wall = time.perf_counter() - t0
     os.makedirs(args.out, exist_ok=True)
     path = os.path.join(args.out, f"trials_{args.algo}_seed{args.seed}.jsonl")
@@ -98,7 +99,7 @@ def cmd_compare(args) -> int:
     for algo in algos:
         logs = []
         for seed in seeds:
-            _, recs = _run(algo, space, objective, seed, args.budget)
+            _, recs = _run(algo, space, objective, seed, args.budget, args.parents, args.q)
             write_trial_log(os.path.join(args.out, f"trials_{algo}_seed{seed}.jsonl"), recs)
             logs.append(recs)
         row = summarize(algo, args.operator, logs)
@@ -145,7 +146,7 @@ def cmd_sweep(args) -> int:
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="paper_2006_05664_b200")
     sub = ap.add_subparsers(dest="cmd", required=True)
-    for name in ("tune", "compare", "sweep"):
+    for name in ("tune", "compare", "bench", "sweep"):
         p = sub.add_parser(name)
         p.add_argument("--operator", required=True)
         p.add_argument("--evaluator", default="gpu", choices=("gpu", "synthetic"))
@@ -154,10 +155,13 @@ def main(argv=None) -> int:
         p.add_argument("--reps", type=int, default=20)
         p.add_argument("--budget", type=int, default=500)
         p.add_argument("--out", default="out")
+        if name != "sweep":   # OpEvo's mutation rate and parent count (reference _add_algo_flags)
+            p.add_argument("--q", type=float, default=0.5)
+            p.add_argument("--lambda", dest="parents", type=int, default=8)
         if name == "tune":
             p.add_argument("--algo", default="opevo", choices=ALGORITHMS)
             p.add_argument("--seed", type=int, default=int(os.environ.get("TOPO_TUNE_SEED", 0)))
-        elif name == "compare":
+        elif name in ("compare", "bench"):
             p.add_argument("--algo", default=",".join(ALGORITHMS))
             p.add_argument("--seeds", default="0,1,2")
         else:
@@ -166,7 +170,8 @@ def main(argv=None) -> int:
             p.add_argument("--seeds", default="0,1,2")
     args = ap.parse_args(argv)
     try:
-        return {"tune": cmd_tune, "compare": cmd_compare, "sweep": cmd_sweep}[args.cmd](args)
+        return {"tune": cmd_tune, "compare": cmd_compare, "bench": cmd_compare,
+                "sweep": cmd_sweep}[args.cmd](args)
     except FatalEvaluationError as err:
         print(f"evaluator unavailable: {err}", file=sys.stderr)
         return 3

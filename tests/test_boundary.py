@@ -254,3 +254,36 @@ def test_sweep_matches_the_reference_cli(reference_topotune, tmp_path):
             return [{k: v for k, v in r.items() if k != "mean_elapsed_ms"} for r in csv.DictReader(fh)]
 
     assert rows(tmp_path / "ref" / "sweep_summary.csv") == rows(tmp_path / "ours" / "sweep_summary.csv")
+
+
+def test_bench_matches_the_reference_cli(reference_topotune, tmp_path):
+    """``bench`` (the reference CLI's name for comparing algorithms over seeds,
+    ``cli.py:189-233``; ``compare`` here) with the reference's synthetic
+    evaluator and non-default q / lambda: the same trial logs and the same
+    summary.csv (apart from wall clock) and curves.csv."""
+    import csv
+
+    args = ["--algo", "opevo,random,sa,gbfs", "--seeds", "0,5", "--budget", "48", "--q", "0.3",
+            "--lambda", "4"]
+    env = dict(os.environ, PYTHONPATH=os.path.dirname(os.path.dirname(reference_topotune.__file__)))
+    ref = subprocess.run([sys.executable, "-m", "topotune", "bench", "--operator", "matmul:512,1024,1024",
+                          *args, "--out", str(tmp_path / "ref")], capture_output=True, text=True, env=env,
+                         timeout=300)
+    assert ref.returncode == 0, ref.stderr
+    ours = subprocess.run([sys.executable, "-m", "paper_2006_05664_b200", "bench", "--operator",
+                           "matmul:512,1024,1024", "--evaluator", "synthetic", *args, "--out",
+                           str(tmp_path / "ours")], capture_output=True, text=True, cwd=REPO, timeout=300)
+    assert ours.returncode == 0, ours.stderr
+    for algo in ("opevo", "random", "sa", "gbfs"):
+        for seed in (0, 5):
+            name = f"trials_{algo}_seed{seed}.jsonl"
+            a = [json.loads(x) for x in (tmp_path / "ref" / name).read_text().splitlines()]
+            b = [json.loads(x) for x in (tmp_path / "ours" / name).read_text().splitlines()]
+            assert [(r["config"], r["fitness"]) for r in a] == [(r["config"], r["fitness"]) for r in b]
+
+    def rows(path, drop=("mean_elapsed_ms",)):
+        with open(path) as fh:
+            return [{k: v for k, v in r.items() if k not in drop} for r in csv.DictReader(fh)]
+
+    assert rows(tmp_path / "ref" / "summary.csv") == rows(tmp_path / "ours" / "summary.csv")
+    assert rows(tmp_path / "ref" / "curves.csv") == rows(tmp_path / "ours" / "curves.csv")
