@@ -620,6 +620,16 @@ __device__ __forceinline__ void conv_load_b(u32 dst, const TmaDesc* d, u32 bar, 
     else         tma_load_2d(dst, d, bar, c0, c1);
 }
 
+// Halo lines: all KW weight tiles of one filter row (and every 64-channel atom
+// of the K block) in ONE box {64, BN_LOAD, KATOMS, KW} of the weight view
+// {64, Cout, Cin/64, KH*KW}; it lands [tap][atom][row][128 B], the layout the
+// MMA descriptors walk (tap stride B_SUB).
+__device__ __forceinline__ void conv_load_b_row(u32 dst, const TmaDesc* d, u32 bar, int row0, int atom0,
+                                                int tap0) {
+    if (CG == 2) tma2_load_4d(dst, d, bar, 0, row0, atom0, tap0);
+    else         tma_load_4d(dst, d, bar, 0, row0, atom0, tap0);
+}
+
 __device__ __forceinline__ void umma_commit_mc(u32 bar, u16 mask) {
     asm volatile("{ .reg .pred e; elect.sync _|e, 0xffffffff; "
                  "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster"
@@ -1026,15 +1036,10 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                     // weight tiles of that filter row
                     const int di = tap - geom.pad;
 #pragma unroll
-                    for (int ka = 0; ka < KATOMS; ++ka) {
+                    for (int ka = 0; ka < KATOMS; ++ka)
                         conv_load_a(a_dst + ka * (BM_CTA * SWZ), &tma_a, fb, cbase + ka * ATOM_K,
                                     w0 - geom.pad, h0 + di, n0);
-                        if (!B_RES)
-#pragma unroll
-                            for (int dj = 0; dj < HKW; ++dj)
-                                conv_load_b(b_dst + dj * B_SUB + ka * (BN_LOAD * SWZ), &tma_b, fb,
-                                            (tap * HKW + dj) * geom.cin + cbase + ka * ATOM_K, b_row0);
-                    }
+                    if (!B_RES) conv_load_b_row(b_dst, &tma_b, fb, b_row0, cbase / ATOM_K, tap * HKW);
                 } else {
                 // input pixel of output (h0, w0) under tap (di, dj): the map
                 // traverses W and H with element stride S

@@ -1565,6 +1565,14 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
             uint32_t bb[3] = {64, (uint32_t)k.bn, (uint32_t)(d / 64)};
             if (!st) st = encode_map(&kr->tma_b, op->b, 3, bd, bs, bb, 128, err, errlen);
             kr->smem += 768 + panel;    // 1 KB barrier block before the panel (BRES_OFF)
+        } else if (hkw) {
+            // halo lines: one box per filter row holds its KW weight tiles,
+            // every 64-channel atom of the K block -- view {64, Cout, Cin/64,
+            // KH*KW} (W is [Cout][KH][KW][Cin]), box {64, BN/cg, BK/64, KW}
+            uint64_t bd[4] = {64, (uint64_t)op->cols, (uint64_t)(CP / 64), (uint64_t)(KH * KW)};
+            uint64_t bs[3] = {(uint64_t)depth * 2, 128, (uint64_t)CP * 2};
+            uint32_t bb[4] = {64, (uint32_t)(k.bn / k.cg), (uint32_t)(k.bk / 64), (uint32_t)hkw};
+            if (!st) st = encode_map(&kr->tma_b, op->b, 4, bd, bs, bb, 128, err, errlen);
         } else {
             uint64_t bd[2] = {(uint64_t)depth, (uint64_t)op->cols};
             uint64_t bs[1] = {(uint64_t)depth * 2};
