@@ -169,9 +169,9 @@ constexpr int CG = OPEVO_CTA_GROUP;
 constexpr int SWZ = (BK * 2 >= 128) ? 128 : BK * 2;     // swizzle span in bytes
 constexpr int ATOM_K = SWZ / 2;                          // K elements per swizzle row
 constexpr int KATOMS = BK / ATOM_K;                      // swizzle atoms along K
-constexpr int BM_CTA = (CG == 2) ? 128 : BM;             // A rows resident in this CTA
+constexpr int BM_CTA = (CG == 2) ? BM / 2 : BM;          // A rows resident in this CTA
 constexpr int BN_LOAD = BN / CG;                          // B rows this CTA stages
-constexpr int MATOMS = (CG == 1 && BM == 256) ? 2 : 1;    // M=128 MMAs per k-step
+constexpr int MATOMS = (BM_CTA == 256) ? 2 : 1;          // MMAs per k-step (M=128, or M=256 per pair)
 constexpr int UMMA_M = (CG == 2) ? 256 : ((BM == 256) ? 128 : BM);
 constexpr int BPU = OPEVO_BPU;
 constexpr int A_SUB = BM_CTA * BK * 2;                    // one batch's A tile of a stage
@@ -219,7 +219,8 @@ constexpr int PAIR_TN = CG * TILE_N;                      // images of the (pair
 constexpr int A_ROWS = OPEVO_CONV ? TILE_N * TILE_H * LINE_ROWS : BM_CTA;
 constexpr int TX_STAGE = OPEVO_CONV ? (A_ROWS * BK * 2 + B_TILE) * CG : TX_BYTES;   // expect_tx per stage
 
-static_assert(BM == 64 || BM == 128 || BM == 256, "BM must be 64, 128 or 256");
+static_assert(BM == 64 || BM == 128 || BM == 256 || (BM == 512 && CG == 2 && HKW > 0),
+              "BM must be 64, 128 or 256 (512: a halo-line conv CTA pair, 256 rows per CTA)");
 static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "BN must be a multiple of 16 in [16, 256]");
 static_assert(BK % 16 == 0 && BK >= 16 && BK <= 256, "BK must be a multiple of 16 in [16, 256]");
 static_assert(BK % ATOM_K == 0, "BK must tile the swizzle atom");
@@ -227,8 +228,9 @@ static_assert(TMEM_USED <= 512, "accumulator exceeds TMEM");
 static_assert(ACC == 1 || ACC == 2 || ACC == 4, "ACC must be 1, 2 or 4");
 static_assert((BK / 16) % ACC == 0, "each stage must feed every accumulator");
 static_assert(BM % (8 * CLUSTER) == 0, "multicast slice must be whole 8-row groups");
-static_assert(CG == 1 || (CG == 2 && BM == 256 && CLUSTER == 1 && BN % 16 == 0 && OPEVO_B_RES == 0),
-              "CTA pairs: 256-row tiles, no extra multicast or resident weights");
+static_assert(CG == 1 || (CG == 2 && (BM == 256 || BM == 512) && CLUSTER == 1 && BN % 16 == 0 &&
+                           OPEVO_B_RES == 0),
+              "CTA pairs: 256- (or halo 512-) row tiles, no extra multicast or resident weights");
 static_assert(!HALO || (OPEVO_CONV && TILE_W + HKW - 1 == 16 && SWZ == 128 && LINE == 0),
               "halo lines: 3x3-style conv, TILE_W = 17 - KW, 128-byte swizzle");
 static_assert(LINE == 0 || (OPEVO_CONV && !HALO && (LINE == 16 || LINE == 32) && TILE_W <= LINE),

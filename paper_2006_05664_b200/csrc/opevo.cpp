@@ -216,9 +216,14 @@ int family_of(const opevo_op_desc& d) {
     return d.dtype == OPEVO_F32 ? 2 : d.dtype == OPEVO_F32_TF32X3 ? FAMILY_X3 : 0;
 }
 
+// Tile rows one CTA holds (a CTA pair splits BM in two) and the MMA atoms
+// per K step (mirror BM_CTA / MATOMS in gemm_sm100.cuh).
+int bm_cta_of(const Knobs& k) { return k.cg == 2 ? k.bm / 2 : k.bm; }
+int matoms_of(const Knobs& k) { return bm_cta_of(k) == 256 ? 2 : 1; }
+
 // TMEM columns the kernel allocates (two accumulator buffers when they fit).
 int tmem_alloc_cols(const Knobs& k) {
-    const int used = (k.cg == 1 && k.bm == 256 ? 2 : 1) * k.bn * k.acc * std::max(1, k.bpu);
+    const int used = matoms_of(k) * k.bn * k.acc * std::max(1, k.bpu);
     const int want = (4 * used <= 256 ? 4 : 2 * used <= 512 ? 2 : 1) * used;   // mirrors NBUF
     int cols = 32;
     while (cols < want) cols *= 2;
@@ -240,7 +245,7 @@ bool b_resident(const Knobs& k, int family) {
 // to 16 tile rows; one TMA box per filter row serves its KW taps.  Returns KW,
 // or 0 for the one-box-per-tap layout.
 int halo_kw(const Knobs& k, int family) {
-    const int bm_cta = k.cg == 2 ? 128 : k.bm;
+    const int bm_cta = bm_cta_of(k);
     return (family == 1 && k.line == 0 && k.tile_w >= 1 && k.tile_w < 16 && k.tile_h >= 1 &&
             bm_cta % (k.tile_h * k.tile_w) != 0)
                ? 17 - k.tile_w : 0;
@@ -292,7 +297,7 @@ size_t wide_epi_stage_bytes(const Knobs& k, int out_f32) {
 // Pipeline (operand stages or split-K reduction buffer) of one CTA, 1 KB aligned:
 // a CTA pair stages 128 rows of A and BN/2 rows of B each (mirrors PIPE_BYTES).
 size_t pipe_bytes(const Knobs& k, int family, int batched) {
-    const int a_rows = k.cg == 2 ? 128 : k.bm;
+    const int a_rows = bm_cta_of(k);
     const int b_rows = b_resident(k, family) ? 0 : k.bn / (k.cg == 2 ? 2 : 1) * std::max(1, halo_kw(k, family));
     size_t pipe = (size_t)k.stages * (size_t)(a_rows + b_rows) * (size_t)k.bk * 2 * (size_t)std::max(1, k.bpu);
     if (family == FAMILY_X3) pipe *= 2;       // hi (as landed) + lo parts per stage
@@ -444,8 +449,8 @@ bool knobs_compilable(int family, const Knobs& k, char* err, size_t len) {
         }
         return true;
     }
-    if (!(k.bm == 128 || k.bm == 256)) {
-        put_err(err, len, "BM=%d unsupported (128 or 256)", k.bm);
+    if (!(k.bm == 128 || k.bm == 256 || (k.bm == 512 && k.cg == 2 && halo_kw(k, family)))) {
+        put_err(err, len, "BM=%d unsupported (128 or 256; 512 for a halo-line conv CTA pair)", k.bm);
         return false;
     }
     if (k.bn < 16 || k.bn > 256 || k.bn % 16) {
@@ -473,8 +478,8 @@ bool knobs_compilable(int family, const Knobs& k, char* err, size_t len) {
         return false;
     }
     if (!(k.cg == 1 || k.cg == 2) ||
-        (k.cg == 2 && (k.bm != 256 || k.cluster != 1 || (family != 0 && family != 1) || b_resident(k, family)))) {
-        put_err(err, len, "cta_group=%d needs BM=256, no multicast cluster or resident weights", k.cg);
+        (k.cg == 2 && (k.bm < 256 || k.cluster != 1 || (family != 0 && family != 1) || b_resident(k, family)))) {
+        put_err(err, len, "cta_group=%d needs BM=256 (or 512), no multicast cluster or resident weights", k.cg);
         return false;
     }
     if (!(k.bpu == 1 || k.bpu == 2 || k.bpu == 4) ||
@@ -487,7 +492,7 @@ bool knobs_compilable(int family, const Knobs& k, char* err, size_t len) {
         put_err(err, len, "3xTF32: single-CTA tiles without multicast, bpu or acc");
         return false;
     }
-    if ((k.cg == 1 && k.bm == 256 ? 2 : 1) * k.bn * k.acc * std::max(1, k.bpu) > 512) {
+    if (matoms_of(k) * k.bn * k.acc * std::max(1, k.bpu) > 512) {
         put_err(err, len, "accumulators %dx%d x%d exceed 512 TMEM columns", k.bm, k.bn, k.acc);
         return false;
     }
@@ -505,7 +510,7 @@ bool knobs_compilable(int family, const Knobs& k, char* err, size_t len) {
         return false;
     }
     if (family == 1) {
-        const int bm_cta = k.cg == 2 ? 128 : k.bm;     // tile rows held by one CTA
+        const int bm_cta = bm_cta_of(k);               // tile rows held by one CTA
         if (k.cluster != 1) {
             put_err(err, len, "conv instances do not multicast");
             return false;
@@ -1527,7 +1532,7 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
         // per-CTA tile: TILE_N images x TILE_H lines of LINE tile rows; a
         // CTA pair holds 2 x TILE_N images
         const int line_rows = hkw ? 16 : k.line ? k.line : k.tile_w;
-        const int bm_cta = k.cg == 2 ? 128 : k.bm;
+        const int bm_cta = bm_cta_of(k);
         const int tile_n = bm_cta / (k.tile_h * line_rows);
         const int pair_n = tile_n * k.cg;
         if (hkw && (hkw != KW || k.split != 1 || P >= KW || S != 1)) {
@@ -1604,7 +1609,7 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
                               k.split, 0, 1, 0};
         if (hkw) kr->kdepth = KH * CP;      // the K loop runs over filter rows x channel blocks
     } else {
-        const uint32_t a_rows = (uint32_t)((k.cg == 2 ? 128 : k.bm) / k.cluster);
+        const uint32_t a_rows = (uint32_t)(bm_cta_of(k) / k.cluster);
         const uint32_t b_rows = (uint32_t)(k.bn / k.cg);
         const uint32_t bpu = (uint32_t)std::max(1, k.bpu);     // batches per work unit
         if (bpu > 1 && (!batched || op->batch % bpu)) {

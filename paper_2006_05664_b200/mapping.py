@@ -132,7 +132,7 @@ class Knobs:
     @property
     def bm_cta(self) -> int:
         """Tile rows one CTA holds (a CTA pair splits BM = 256 in two)."""
-        return 128 if self.cta_group == 2 else self.bm
+        return self.bm // 2 if self.cta_group == 2 else self.bm
 
     def compile_key(self) -> tuple[int, ...]:
         """Fields that change the generated code (split-K is a launch arg
@@ -205,10 +205,10 @@ def epi_bytes(bn: int, out_f32: bool = False) -> int:
 
 
 def stage_bytes(bm: int, bn: int, bk: int, cta_group: int = 1) -> int:
-    """Shared memory per pipeline stage of one CTA (a CTA pair stages 128 rows
+    """Shared memory per pipeline stage of one CTA (a CTA pair stages BM/2 rows
     of A and BN/2 rows of B in each CTA)."""
     if cta_group == 2:
-        return (128 + bn // 2) * bk * 2
+        return (bm // 2 + bn // 2) * bk * 2
     return (bm + bn) * bk * 2
 
 
@@ -366,7 +366,12 @@ def _conv_knobs(spec: Conv2dSpec, vals: dict) -> tuple[Knobs | None, str]:
     # SM holds 128 pixel rows and half the weight tile)
     bm = 256 if co[1] % 2 == 0 else 128
     cg = 2 if (bm == 256 and ho[1] % 2 == 0) else 1
-    bm_cta = 128 if cg == 2 else bm
+    # a Cout split by four on a CTA pair of halo lines: 256 rows per CTA (two
+    # M=256 atoms per K step, one 32 KB activation box per filter row)
+    if (cg == 2 and co[1] % 4 == 0 and s_ == 1 and tw + spec.kernel_w - 1 == 16
+            and kh[0] * kw[0] == 1 and (cpad // ci[0]) % 64 == 0):
+        bm = 512
+    bm_cta = bm // 2 if cg == 2 else bm
     if bn % 16 or not 16 <= bn <= 256:
         return None, f"BN={bn} is not a UMMA column tile"
     if bm == 256 and cg == 1 and 2 * bn > 512:
@@ -413,7 +418,7 @@ def _conv_halo_knobs(spec: Conv2dSpec, vals: dict, bm: int, bn: int, bk: int, th
     serves all KW taps of that row (mirrors OPEVO_HALO in gemm_sm100.cuh).
     On a CTA pair each CTA holds TILE_N of the pair's 2 x TILE_N images."""
     kh, kw = vals["kh"], vals["kw"]
-    bm_cta = 128 if cg == 2 else bm
+    bm_cta = bm // 2 if cg == 2 else bm
     if bm_cta % (16 * th):
         return None, f"{bm_cta} rows do not hold 16-row lines x {th} rows"
     tn = bm_cta // (16 * th)
@@ -437,7 +442,7 @@ def _fit_halo_stages(want: int, bm: int, bn: int, bk: int, kw: int, cg: int = 1)
     """Stages of a streaming halo-lines conv: each holds the activation box
     and the KW weight tiles of one filter row (a CTA pair: 128 rows and half
     of each weight tile per CTA)."""
-    rows = (128 if cg == 2 else bm) + kw * bn // cg
+    rows = (bm // 2 if cg == 2 else bm) + kw * bn // cg
     s = want
     while s > 0 and _align1k(s * rows * bk * 2) + epi_bytes(bn) + SMEM_EXTRA > SMEM_LIMIT:
         s -= 1

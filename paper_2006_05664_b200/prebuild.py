@@ -68,7 +68,7 @@ def _representatives(space, key) -> list:
 def _conv_instances(spec) -> set[tuple[int, bool, tuple]]:
     """Conv instances reachable from conv2d_space: the mapping itself
     (mapping._conv_knobs) over one representative configuration per
-    combination of the parameter features it reads -- co[0], co[1] parity,
+    combination of the parameter features it reads -- co[0], co[1] mod 4,
     ho[0], ho[1] parity, wo[0], ci[0], kh[0] * kw[0], unroll settings."""
     from .mapping import _conv_knobs
     from .operators import conv2d_space
@@ -76,7 +76,7 @@ def _conv_instances(spec) -> set[tuple[int, bool, tuple]]:
     space = conv2d_space(spec)
     sp = dict(zip(space.names, space.spaces))
     reps = {
-        "co": _representatives(sp["co"], lambda v: (v[0], v[1] % 2)),
+        "co": _representatives(sp["co"], lambda v: (v[0], v[1] % 4)),
         "ho": _representatives(sp["ho"], lambda v: (v[0], v[1] % 2)),
         "wo": _representatives(sp["wo"], lambda v: v[0]),
         "ci": _representatives(sp["ci"], lambda v: v[0]),

@@ -252,6 +252,11 @@ CONV_KNOBS = [
     # ... and two CTA pairs per SM pair (halo lines, 3 stages)
     (256, 64, 64, 3, 1, 1, 4, 14, 1, 2, 0, 0, 1),
     (256, 64, 64, 3, 1, 1, 2, 14, 1, 2, 0, 0, 1),
+    # 512-row halo CTA pairs: 256 rows (two M=256 MMA atoms) per CTA
+    (512, 64, 64, 4, 1, 1, 4, 14, 1, 2, 0, 0, 1),
+    (512, 64, 64, 2, 1, 1, 8, 14, 1, 2, 0, 0, 1),
+    (512, 64, 64, 3, 1, 1, 2, 14, 1, 2, 0, 0, 1),
+    (512, 64, 64, 4, 1, 1, 8, 14, 1, 2, 0, 0, 1),
 ]
 
 
