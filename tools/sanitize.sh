@@ -43,3 +43,11 @@ run conv_pair_split        conv2d:4,64,56,56,64,3,3,1,1      256,64,16,2,3,1,8,8
 run conv_pair_halo         conv2d:4,64,56,56,64,3,3,1,1      256,32,64,6,1,1,4,14,1,2,0,0,1,0
 run conv_pair_lines_split  conv2d:4,64,56,56,64,3,3,1,1      256,32,16,6,9,1,8,7,1,2,0,0,1,16
 run conv_lines_resident    conv2d:4,64,56,56,64,3,3,1,1      256,64,64,3,1,1,8,28,1,1,0,1,1,32
+# late round 2: 512-row halo CTA pairs, one weight box per filter row, 32-column epilogue staging with two
+# CTAs (pairs) per SM (pair)
+run conv_pair512_halo      conv2d:8,64,56,56,64,3,3,1,1      512,64,64,3,1,1,4,14,1,2,0,0,1,0
+run conv_pair512_halo_2st  conv2d:4,64,56,56,64,3,3,1,1      512,64,64,2,1,1,8,14,1,2,0,0,1,0
+run conv_pair_halo_narrow  conv2d:8,64,56,56,64,3,3,1,1      256,64,64,3,1,1,2,14,1,2,0,0,1,0
+run conv_halo_narrow       conv2d:8,64,28,28,64,3,3,1,1      128,64,64,2,1,1,1,14,1,1,0,0,1,0
+run gemm_narrow_2cta       matmul:1024,1024,1024             256,64,64,2,1,1,1,1,1,1,0,0,1,0
+run gemm_pair_narrow       matmul:1024,1024,1024             256,64,64,4,1,1,1,1,1,2,0,0,1,0
