@@ -90,7 +90,9 @@ enum opevo_knob {
                                  lines": 16-row lines, one TMA box per
                                  filter row serving its KW taps           */
     OPEVO_KNOB_ACC = 8,       /* K-interleaved TMEM accumulators (1,2,4)  */
-    OPEVO_KNOB_CTA_GROUP = 9, /* 2: CTA-pair MMA (cta_group::2), BM=256   */
+    OPEVO_KNOB_CTA_GROUP = 9, /* 2: CTA-pair MMA (cta_group::2), BM=256;
+                                 BM=512 (256 rows per CTA, two M=256
+                                 atoms) for halo-line conv tiles          */
     OPEVO_KNOB_GRID = 10,     /* 0: persistent when work > residency
                                  1: one CTA (cluster) per tile
                                  2: persistent, partial last wave split
