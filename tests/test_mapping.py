@@ -156,6 +156,25 @@ def test_conv_cta_pair_mapping():
     assert dense.cta_group == 2 and dense.b_res == 0 and dense.bm == 256
 
 
+def test_conv_512_row_pair_mapping():
+    """A Cout split divisible by four (co[1] % 4 == 0) on a pair of halo tiles
+    selects 512-row pairs: 256 rows (two M=256 atoms) per CTA, TILE_N twice
+    the 256-row pair's; the same config off the halo path, or with
+    co[1] = 2 mod 4, keeps 256 rows."""
+    spec = parse_operator("conv2d:32,64,56,56,64,3,3,1,1")
+    sp = gpu_operator_space(spec)
+    big = config_to_knobs(spec, sp, ((1, 4, 2, 8), (14, 2, 2, 1), (4, 2, 7, 1), (1, 64), (1, 3), (1, 3),
+                                     "explicit_unroll_off", 16)).knobs
+    assert (big.bm, big.cta_group, big.bm_cta, big.tile_h, big.tile_w, big.halo_kw()) == (512, 2, 256, 4, 14, 3)
+    assert big.smem_bytes() == big.stages * (256 + 3 * 32) * 64 * 2 + 32768 + 1280
+    small = config_to_knobs(spec, sp, ((1, 2, 4, 8), (14, 2, 2, 1), (4, 2, 7, 1), (1, 64), (1, 3), (1, 3),
+                                       "explicit_unroll_off", 16)).knobs
+    assert (small.bm, small.cta_group) == (256, 2)
+    dense = config_to_knobs(spec, sp, ((1, 4, 2, 8), (14, 2, 2, 1), (7, 1, 8, 1), (1, 64), (1, 3), (1, 3),
+                                       "explicit_unroll_off", 16)).knobs
+    assert (dense.bm, dense.cta_group) == (256, 2)
+
+
 def test_bmm_mapping_is_batched():
     spec = BatchMatMulSpec(960, 128, 64, 128)
     sp = gpu_operator_space(spec)
