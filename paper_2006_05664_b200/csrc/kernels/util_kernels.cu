@@ -116,51 +116,67 @@ opevo_ref_gemm(const void* __restrict__ A, const void* __restrict__ B, float* __
 // output is the same sequential fp32 FMA chain over k as opevo_ref_gemm's,
 // so the two agree bit for bit; ~2.5x the throughput (the reference is
 // recomputed whenever operands are uploaded, i.e. every end-to-end step).
-extern "C" __global__ void __launch_bounds__(256)
-opevo_ref_gemm128(const void* __restrict__ A, const void* __restrict__ B, float* __restrict__ R,
-                  int rows, int cols, int depth, int in_f32) {
+template <int NT>   // 128 rows x NT columns per block, 8 x NT/16 outputs per thread
+__device__ __forceinline__ void ref_gemm_tile(const void* __restrict__ A, const void* __restrict__ B,
+                                              float* __restrict__ R, int rows, int cols, int depth, int in_f32) {
+    constexpr int CJ = NT / 16;
     __shared__ float sa[16][128 + 4];
-    __shared__ float sb[16][128 + 4];
+    __shared__ float sb[16][NT + 4];
     const int b = blockIdx.z;
-    const int r0 = blockIdx.y * 128, c0 = blockIdx.x * 128;
+    const int r0 = blockIdx.y * 128, c0 = blockIdx.x * NT;
     const int tr = threadIdx.x / 16, tc = threadIdx.x % 16;
     const u64 a_off = (u64)b * rows * depth, b_off = (u64)b * cols * depth;
-    float acc[8][8];
+    float acc[8][CJ];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
-    for (int k0 = 0; k0 < depth; k0 += 16) {
-        // 128 rows x 16 k per operand: 8 elements per thread, k fastest
+        for (int j = 0; j < CJ; ++j) acc[i][j] = 0.0f;
+    // 128 rows (NT columns) x 16 k per operand, k fastest; the next chunk's
+    // global loads are issued into registers before the current chunk's FMAs
+    float ra[8], rb[CJ];
+    auto fetch = [&](int k0) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             const int t = threadIdx.x + q * 256;
-            const int rr = t / 16, kk = t % 16;
-            const int gr = r0 + rr, gc = c0 + rr, gk = k0 + kk;
-            float va = 0.0f, vb = 0.0f;
+            const int gr = r0 + t / 16, gk = k0 + t % 16;
+            float va = 0.0f;
             if (gr < rows && gk < depth) {
                 const u64 idx = a_off + (u64)gr * depth + gk;
                 va = in_f32 ? ((const float*)A)[idx] : bf16_to_f32(((const u16*)A)[idx]);
             }
+            ra[q] = va;
+        }
+#pragma unroll
+        for (int q = 0; q < CJ; ++q) {
+            const int t = threadIdx.x + q * 256;
+            const int gc = c0 + t / 16, gk = k0 + t % 16;
+            float vb = 0.0f;
             if (gc < cols && gk < depth) {
                 const u64 idx = b_off + (u64)gc * depth + gk;
                 vb = in_f32 ? ((const float*)B)[idx] : bf16_to_f32(((const u16*)B)[idx]);
             }
-            sa[kk][rr] = va;
-            sb[kk][rr] = vb;
+            rb[q] = vb;
         }
+    };
+    fetch(0);
+    for (int k0 = 0; k0 < depth; k0 += 16) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) sa[(threadIdx.x + q * 256) % 16][(threadIdx.x + q * 256) / 16] = ra[q];
+#pragma unroll
+        for (int q = 0; q < CJ; ++q) sb[(threadIdx.x + q * 256) % 16][(threadIdx.x + q * 256) / 16] = rb[q];
         __syncthreads();
+        if (k0 + 16 < depth) fetch(k0 + 16);
 #pragma unroll
         for (int kk = 0; kk < 16; ++kk) {
-            float av[8], bv[8];
+            float av[8], bv[CJ];
 #pragma unroll
             for (int i = 0; i < 8; ++i) av[i] = sa[kk][tr + 16 * i];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) bv[j] = sb[kk][tc + 16 * j];
+            for (int j = 0; j < CJ; ++j) bv[j] = sb[kk][tc + 16 * j];
 #pragma unroll
             for (int i = 0; i < 8; ++i)
 #pragma unroll
-                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+                for (int j = 0; j < CJ; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
         }
         __syncthreads();
     }
@@ -169,11 +185,25 @@ opevo_ref_gemm128(const void* __restrict__ A, const void* __restrict__ B, float*
         const int gr = r0 + tr + 16 * i;
         if (gr >= rows) continue;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < CJ; ++j) {
             const int gc = c0 + tc + 16 * j;
             if (gc < cols) R[(u64)b * rows * cols + (u64)gr * cols + gc] = acc[i][j];
         }
     }
+}
+
+extern "C" __global__ void __launch_bounds__(256)
+opevo_ref_gemm128(const void* __restrict__ A, const void* __restrict__ B, float* __restrict__ R,
+                  int rows, int cols, int depth, int in_f32) {
+    ref_gemm_tile<128>(A, B, R, rows, cols, depth, in_f32);
+}
+
+// 128 x 64 tiles: twice the blocks, for outputs whose 128 x 128 grid would
+// leave most SMs idle (1024^2: 64 blocks on 148 SMs)
+extern "C" __global__ void __launch_bounds__(256)
+opevo_ref_gemm128x64(const void* __restrict__ A, const void* __restrict__ B, float* __restrict__ R,
+                     int rows, int cols, int depth, int in_f32) {
+    ref_gemm_tile<64>(A, B, R, rows, cols, depth, in_f32);
 }
 
 // Reference direct convolution on the paper's layouts:
@@ -203,6 +233,86 @@ extern "C" __global__ void opevo_ref_conv(const u16* __restrict__ X, const u16* 
                 }
             }
         R[o] = acc;
+    }
+}
+
+// The same convolution as a tiled SIMT implicit GEMM: 128 output pixels x
+// 64 output channels per block, 8 x 4 per thread, the reduction index
+// q = (c, i, j) ascending in chunks of 16 staged through shared memory (the
+// activation gather applies the padding), so every output is the same fmaf
+// chain over (ci, kh, kw) as opevo_ref_conv's (a padded tap contributes
+// fmaf(0, w, acc) = acc).  ~100x faster than one thread per output, which
+// matters when new operands are uploaded every generation (bench.py e2e).
+extern "C" __global__ void __launch_bounds__(256)
+opevo_ref_conv_tiled(const u16* __restrict__ X, const u16* __restrict__ W, float* __restrict__ R, int N,
+                     int C, int H, int Wd, int K, int KH, int KW, int stride, int pad, int HO, int WO) {
+    __shared__ float sx[16][128 + 4];
+    __shared__ float sw[16][64 + 4];
+    const int P = N * HO * WO, Q = C * KH * KW;
+    const int p0 = blockIdx.x * 128, k0 = blockIdx.y * 64;
+    const int tr = threadIdx.x / 16, tc = threadIdx.x % 16;
+    float acc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+    // 128 pixels x 16 reduction steps (the activation gather applies the
+    // padding) and 64 output channels x 16 steps (W rows are q-contiguous);
+    // the next chunk is fetched into registers before the current one's FMAs
+    float rx[8], rw[4];
+    auto fetch = [&](int q0) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int t = threadIdx.x + u * 256;
+            const int p = p0 + t / 16, q = q0 + t % 16;
+            float v = 0.0f;
+            if (p < P && q < Q) {
+                const int wo = p % WO, ho = (p / WO) % HO, n = p / (WO * HO);
+                const int j = q % KW, i = (q / KW) % KH, c = q / (KW * KH);
+                const int h = ho * stride - pad + i, w = wo * stride - pad + j;
+                if (h >= 0 && h < H && w >= 0 && w < Wd)
+                    v = bf16_to_f32(X[(((u64)n * C + c) * H + h) * Wd + w]);
+            }
+            rx[u] = v;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int t = threadIdx.x + u * 256;
+            const int k = k0 + t / 16, q = q0 + t % 16;
+            rw[u] = (k < K && q < Q) ? bf16_to_f32(W[(u64)k * Q + q]) : 0.0f;
+        }
+    };
+    fetch(0);
+    for (int q0 = 0; q0 < Q; q0 += 16) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sx[(threadIdx.x + u * 256) % 16][(threadIdx.x + u * 256) / 16] = rx[u];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) sw[(threadIdx.x + u * 256) % 16][(threadIdx.x + u * 256) / 16] = rw[u];
+        __syncthreads();
+        if (q0 + 16 < Q) fetch(q0 + 16);
+#pragma unroll
+        for (int qq = 0; qq < 16; ++qq) {
+            float xv[8], wv[4];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) xv[i] = sx[qq][tr + 16 * i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) wv[j] = sw[qq][tc + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(xv[i], wv[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int p = p0 + tr + 16 * i;
+        if (p >= P) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int k = k0 + tc + 16 * j;
+            if (k < K) R[(u64)p * K + k] = acc[i][j];
+        }
     }
 }
 

@@ -729,8 +729,8 @@ struct opevo_ctx {
     std::unique_ptr<HostPool> pool;     // graph builds of a trial batch
     CUmodule util = nullptr;
     CUfunction k_fill_bf16 = nullptr, k_fill_f32 = nullptr, k_fill_u8 = nullptr, k_ref_gemm = nullptr,
-               k_ref_gemm128 = nullptr,
-               k_ref_conv = nullptr, k_nchw2nhwc = nullptr, k_compare = nullptr, k_flush = nullptr,
+               k_ref_gemm128 = nullptr, k_ref_gemm128x64 = nullptr,
+               k_ref_conv = nullptr, k_ref_conv_tiled = nullptr, k_nchw2nhwc = nullptr, k_compare = nullptr, k_flush = nullptr,
                k_gate = nullptr, k_nchw2nhwc_pad = nullptr, k_nhwc_pad2nchw = nullptr;
     volatile uint32_t* gate_host = nullptr;   // mapped pinned flag opening the timing gate
     CUdeviceptr gate_dev = 0;
@@ -867,17 +867,24 @@ int compute_reference(opevo_op* op, char* err, size_t errlen) {
         int N = c[0], C = c[1], H = c[2], W = c[3], K = c[4], KH = c[5], KW = c[6], S = c[7], P = c[8];
         int HO = (H + 2 * P - KH) / S + 1, WO = (W + 2 * P - KW) / S + 1;
         void* args[] = {&op->conv_x, &op->conv_w, &op->ref, &N, &C, &H, &W, &K, &KH, &KW, &S, &P, &HO, &WO};
-        uint64_t total = (uint64_t)N * HO * WO * K;
-        int st = launch_simple(ctx, ctx->k_ref_conv, grid_for(total), 256, args, err, errlen);
-        if (st) return st;
+        // tiled SIMT implicit GEMM (same fmaf chain per output as the
+        // one-thread-per-output opevo_ref_conv, which remains as its check)
+        const uint64_t pixels = (uint64_t)N * HO * WO;
+        CU_TRY(ctx, g_cu.LaunchKernel(ctx->k_ref_conv_tiled, (unsigned)((pixels + 127) / 128),
+                                      (unsigned)((K + 63) / 64), 1, 256, 1, 1, 0, ctx->stream, args, nullptr),
+               "reference conv");
     } else {
         int rows = (int)op->rows, cols = (int)op->cols, depth = (int)op->depth, in_f32 = op->in_f32;
         void* args[] = {&op->a, &op->b, &op->ref, &rows, &cols, &depth, &in_f32};
-        // large operands: the 128x128-tile reference (bit-identical sums)
+        // large operands: the 128-row-tile references (bit-identical sums),
+        // 128 x 64 tiles when 128 x 128 ones would not fill the SMs twice
         const bool big = rows >= 512 && cols >= 512;
-        const unsigned t = big ? 128u : 64u;
-        CU_TRY(ctx, g_cu.LaunchKernel(big ? ctx->k_ref_gemm128 : ctx->k_ref_gemm, (unsigned)((cols + t - 1) / t),
-                                      (unsigned)((rows + t - 1) / t), (unsigned)op->batch, 256, 1, 1, 0,
+        const bool narrow = big && (uint64_t)((rows + 127) / 128) * ((cols + 127) / 128) * op->batch <
+                                       (uint64_t)ctx->sm_count * 2;
+        const unsigned tr = big ? 128u : 64u, tc = big && !narrow ? 128u : 64u;
+        CUfunction fn = !big ? ctx->k_ref_gemm : narrow ? ctx->k_ref_gemm128x64 : ctx->k_ref_gemm128;
+        CU_TRY(ctx, g_cu.LaunchKernel(fn, (unsigned)((cols + tc - 1) / tc),
+                                      (unsigned)((rows + tr - 1) / tr), (unsigned)op->batch, 256, 1, 1, 0,
                                       ctx->stream, args, nullptr),
                "reference gemm");
     }
@@ -1209,8 +1216,8 @@ int opevo_ctx_create(int device, const char* cache_dir, opevo_ctx** out, char* e
         struct { CUfunction* f; const char* n; } fns[] = {
             {&ctx->k_fill_bf16, "opevo_fill_bf16"}, {&ctx->k_fill_f32, "opevo_fill_f32"},
             {&ctx->k_fill_u8, "opevo_fill_u8"},     {&ctx->k_ref_gemm, "opevo_ref_gemm"},
-            {&ctx->k_ref_gemm128, "opevo_ref_gemm128"},
-            {&ctx->k_ref_conv, "opevo_ref_conv"},   {&ctx->k_nchw2nhwc, "opevo_nchw_to_nhwc"},
+            {&ctx->k_ref_gemm128, "opevo_ref_gemm128"},   {&ctx->k_ref_gemm128x64, "opevo_ref_gemm128x64"},
+            {&ctx->k_ref_conv, "opevo_ref_conv"},   {&ctx->k_ref_conv_tiled, "opevo_ref_conv_tiled"},   {&ctx->k_nchw2nhwc, "opevo_nchw_to_nhwc"},
             {&ctx->k_compare, "opevo_compare"},     {&ctx->k_flush, "opevo_flush"},
             {&ctx->k_gate, "opevo_gate"},           {&ctx->k_nchw2nhwc_pad, "opevo_nchw_to_nhwc_pad"},
             {&ctx->k_nhwc_pad2nchw, "opevo_nhwc_pad_to_nchw"}};

@@ -274,6 +274,14 @@ def conv4(dev):
     op.close()
 
 
+def test_conv_reference_matches_the_oracle(dev, conv4):
+    """The in-library fp32 conv reference every conv trial is checked against
+    (the tiled SIMT implicit GEMM, opevo_ref_conv_tiled) within 1e-5 of the
+    fp64 oracle over the whole cfg4 output."""
+    op, ref = conv4
+    assert _rel(op.reference(), ref) < 1e-5
+
+
 @pytest.mark.parametrize("knobs", CONV_KNOBS)
 def test_conv4_full(dev, conv4, knobs):
     op, ref = conv4
