@@ -120,8 +120,12 @@ template <int NT>   // 128 rows x NT columns per block, 8 x NT/16 outputs per th
 __device__ __forceinline__ void ref_gemm_tile(const void* __restrict__ A, const void* __restrict__ B,
                                               float* __restrict__ R, int rows, int cols, int depth, int in_f32) {
     constexpr int CJ = NT / 16;
-    __shared__ float sa[16][128 + 4];
-    __shared__ float sb[16][NT + 4];
+    // k-major staging; a thread's 8 rows (and CJ columns) are contiguous, so
+    // its operands of one k step are 16-byte shared loads
+    // (rows padded by 4 floats: the transposing stores spread over banks,
+    // and every row still starts 16-byte aligned)
+    __shared__ __align__(16) float sa[16][128 + 4];
+    __shared__ __align__(16) float sb[16][NT + 4];
     const int b = blockIdx.z;
     const int r0 = blockIdx.y * 128, c0 = blockIdx.x * NT;
     const int tr = threadIdx.x / 16, tc = threadIdx.x % 16;
@@ -169,10 +173,16 @@ __device__ __forceinline__ void ref_gemm_tile(const void* __restrict__ A, const 
 #pragma unroll
         for (int kk = 0; kk < 16; ++kk) {
             float av[8], bv[CJ];
+            const float4* pa = reinterpret_cast<const float4*>(&sa[kk][tr * 8]);
+            const float4 a0 = pa[0], a1 = pa[1];
+            av[0] = a0.x; av[1] = a0.y; av[2] = a0.z; av[3] = a0.w;
+            av[4] = a1.x; av[5] = a1.y; av[6] = a1.z; av[7] = a1.w;
+            const float4* pb = reinterpret_cast<const float4*>(&sb[kk][tc * CJ]);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) av[i] = sa[kk][tr + 16 * i];
-#pragma unroll
-            for (int j = 0; j < CJ; ++j) bv[j] = sb[kk][tc + 16 * j];
+            for (int j = 0; j < CJ / 4; ++j) {
+                const float4 v = pb[j];
+                bv[4 * j] = v.x; bv[4 * j + 1] = v.y; bv[4 * j + 2] = v.z; bv[4 * j + 3] = v.w;
+            }
 #pragma unroll
             for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -182,11 +192,11 @@ __device__ __forceinline__ void ref_gemm_tile(const void* __restrict__ A, const 
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const int gr = r0 + tr + 16 * i;
+        const int gr = r0 + tr * 8 + i;
         if (gr >= rows) continue;
 #pragma unroll
         for (int j = 0; j < CJ; ++j) {
-            const int gc = c0 + tc + 16 * j;
+            const int gc = c0 + tc * CJ + j;
             if (gc < cols) R[(u64)b * rows * cols + (u64)gr * cols + gc] = acc[i][j];
         }
     }
