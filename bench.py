@@ -331,7 +331,7 @@ def main() -> None:
     ap.add_argument("--budget", type=int, default=500,
                     help="trials of the whole search (the north star's 500); the generations after "
                          "the timed ones complete it untimed")
-    ap.add_argument("--loser-ratio", type=float, default=1.5,
+    ap.add_argument("--loser-ratio", type=float, default=1.2,
                     help="straggler rule: candidates slower than this x the fastest verified one "
                          "are timed with 5 launches (0: off)")
     ap.add_argument("--l2", default="auto", choices=("auto", "warm", "cold"),

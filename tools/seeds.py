@@ -2,7 +2,7 @@
 the full budget, the best instance of each run confirmed by re-timing
 (GpuEvaluator.confirm_top).  One evaluator (one kernel-family preload) serves
 every seed; its trial history is reset between seeds.
-Usage: python tools/seeds.py OP SEED0 SEED1 [BUDGET] [--python-ask] [--reps=R] [--target=KNOBS]"""
+Usage: python tools/seeds.py OP SEED0 SEED1 [BUDGET] [--python-ask] [--reps=R] [--loser-ratio=X] [--target=KNOBS]"""
 import json
 import sys
 import time
@@ -25,7 +25,8 @@ def main():
     spec = parse_operator(op)
     space = gpu_operator_space(spec)
     reps = next((int(a.split("=", 1)[1]) for a in sys.argv[1:] if a.startswith("--reps=")), 20)
-    ev = GpuEvaluator(spec, space, 0, EvalSettings(preload_family=True, reps=reps))
+    loser = next((float(a.split("=", 1)[1]) for a in sys.argv[1:] if a.startswith("--loser-ratio=")), 1.2)
+    ev = GpuEvaluator(spec, space, 0, EvalSettings(preload_family=True, reps=reps, loser_ratio=loser))
     cls = OpEvo if "--python-ask" in sys.argv else NativeOpEvo
     rows = []
     for seed in range(s0, s1):
