@@ -295,7 +295,7 @@ size_t wide_epi_stage_bytes(const Knobs& k, int out_f32) {
 }
 
 // Pipeline (operand stages or split-K reduction buffer) of one CTA, 1 KB aligned:
-// a CTA pair stages 128 rows of A and BN/2 rows of B each (mirrors PIPE_BYTES).
+// a CTA pair stages BM/2 rows of A and BN/2 rows of B each (mirrors PIPE_BYTES).
 size_t pipe_bytes(const Knobs& k, int family, int batched) {
     const int a_rows = bm_cta_of(k);
     const int b_rows = b_resident(k, family) ? 0 : k.bn / (k.cg == 2 ? 2 : 1) * std::max(1, halo_kw(k, family));
@@ -313,13 +313,14 @@ size_t pipe_bytes(const Knobs& k, int family, int batched) {
 // more TMEM load / fence / store per 64 columns, in exchange for a second CTA
 // -- i.e. a second MMA-issuing warp -- on every SM (conv halo tiles with 2
 // stages; profiles/round2/two_ctas_per_sm.txt).  Not for resident weight
-// panels (the panel alone keeps them at one CTA).  OPEVO_NARROW_EPI=0 disables
+// panels (the panel alone keeps them at one CTA) nor for accumulators that
+// take more than half of TMEM.  OPEVO_NARROW_EPI=0 disables
 // the rule (A/B experiments).  Mirrors Knobs.narrow_epi in mapping.py.
 constexpr size_t SM_SMEM_BYTES = 233472, CTA_RESERVED_SMEM = 1024;
 bool narrow_epi(const Knobs& k, int family, int out_f32, int batched) {
     static const bool enabled = !(getenv("OPEVO_NARROW_EPI") && getenv("OPEVO_NARROW_EPI")[0] == '0');
     if (!enabled || (family != 0 && family != 1) || out_f32 || wide_epi_cols(k, out_f32) != 64 ||
-        k.cluster != 1 || dsmem_split(k, family, batched) || b_resident(k, family))
+        k.cluster != 1 || dsmem_split(k, family, batched) || b_resident(k, family) || tmem_alloc_cols(k) > 256)
         return false;
     const size_t base = pipe_bytes(k, family, batched) + 1024 + 256 + CTA_RESERVED_SMEM;
     return 2 * (base + epi_stage_bytes_cols(64, 0)) > SM_SMEM_BYTES &&

@@ -146,10 +146,21 @@ class Knobs:
         single-CTA or CTA-pair bf16 instance that fits twice on an SM only with 32-column
         epilogue staging (16 KB instead of 32 KB) uses it."""
         if (self.family not in (FAMILY_GEMM, FAMILY_CONV) or self.bn % 64 or self.acc != 1
-                or self.cluster != 1 or self.dsmem_split() or self.b_res):
+                or self.cluster != 1 or self.dsmem_split() or self.b_res or self.tmem_alloc_cols() > 256):
             return False
         base = self._pipe_bytes() + SMEM_EXTRA + CTA_RESERVED_SMEM
         return 2 * (base + epi_bytes(64)) > SM_SMEM_BYTES and 2 * (base + epi_bytes(32)) <= SM_SMEM_BYTES
+
+    def tmem_alloc_cols(self) -> int:
+        """TMEM columns the kernel allocates (mirrors ``tmem_alloc_cols`` in
+        csrc/opevo.cpp: four accumulator buffers when they fit in half of
+        TMEM, else two, else one; rounded up to a power of two >= 32)."""
+        used = (2 if self.bm_cta == 256 else 1) * self.bn * self.acc * max(1, self.bpu)
+        want = (4 if 4 * used <= 256 else 2 if 2 * used <= 512 else 1) * used
+        cols = 32
+        while cols < want:
+            cols *= 2
+        return cols
 
     def _epi(self) -> int:
         return epi_bytes(32 if self.narrow_epi() else self.bn)
