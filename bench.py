@@ -500,15 +500,22 @@ def main() -> None:
             e0.record()
         t_wall0 = time.perf_counter()
         gen_diag = [] if os.environ.get("OPEVO_BENCH_GEN_TIMES") == "1" else None
+        flush_ms = []
         for _ in range(args.steps):
+            tf = time.perf_counter()
             flush()                     # every step starts with a cold L2
             tg = time.perf_counter()
             trials += generation(engine, recorder, tally=tally)
             if gen_diag is not None:    # diagnostics: host time per generation + its trials
                 owner = getattr(evaluator, "__self__", evaluator)
                 gen_diag.append((1e3 * (time.perf_counter() - tg), list(owner.last_extras)))
+                flush_ms.append(1e3 * (tg - tf))
+        t_loop = time.perf_counter()
         barrier()
         wall = time.perf_counter() - t_wall0
+        if gen_diag is not None:
+            print(f"[timed region] loop {1e3 * (t_loop - t_wall0):.1f} ms, final barrier "
+                  f"{1e3 * (time.perf_counter() - t_loop):.1f} ms", file=sys.stderr)
         timing = "cuda events (max over ranks)"
         try:
             if poisoned() or e0 is None:
@@ -525,6 +532,9 @@ def main() -> None:
     if gen_diag:
         slow = sorted(range(len(gen_diag)), key=lambda i: -gen_diag[i][0])[:3]
         med = statistics.median(t for t, _ in gen_diag)
+        print(f"[flush] median {statistics.median(flush_ms):.3f} ms, max {max(flush_ms):.3f} ms, "
+              f"total {sum(flush_ms):.1f} ms; generations total {sum(t for t, _ in gen_diag):.1f} ms",
+              file=sys.stderr)
         for i in slow:
             t, ex = gen_diag[i]
             print(f"[gen {i}] {t:.3f} ms (median {med:.3f}): " + "; ".join(
