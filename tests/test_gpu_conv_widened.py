@@ -173,3 +173,19 @@ def test_narrow_cin_upload_round_trip(dev):
         assert _rel(op.output(), ref) < BF16_TOL
     finally:
         op.close()
+
+
+R3 = "conv2d:32,128,28,28,128,3,3,1,1"
+
+
+def test_halo_pairs_on_a_wider_conv(dev):
+    """Halo-line CTA pairs away from cfg4: Cin = Cout = 128 on 28 x 28, where
+    the 512-row pairs (256 rows, two M=256 atoms per CTA) run with BK = 128
+    (two 64-channel atoms per K block, so the one-box weight load spans two
+    atoms x three taps) and BK = 64, next to a 256-row pair with BK = 128."""
+    cfgs = [((2, 4, 4, 4), (7, 2, 2, 1), (2, 2, 7, 1), (1, 128), (1, 3), (1, 3), "explicit_unroll_off", 64),
+            ((2, 4, 4, 4), (7, 2, 2, 1), (2, 2, 7, 1), (2, 64), (1, 3), (1, 3), "explicit_unroll_off", 64),
+            ((2, 2, 4, 8), (7, 2, 2, 1), (2, 2, 7, 1), (1, 128), (1, 3), (1, 3), "explicit_unroll_off", 64),
+            ((2, 4, 4, 4), (14, 2, 1, 1), (2, 2, 7, 1), (2, 64), (1, 3), (1, 3), "explicit_unroll_off", 512)]
+    assert [_knobs(R3, c)[0] for c in cfgs] == [512, 512, 256, 512]
+    _check_images(dev, R3, cfgs, images=(0, 13, 31))
