@@ -135,3 +135,16 @@ def test_narrow_epilogue_rule_matches_the_mapping():
     halo2 = Knobs(128, 64, 64, 2, 1, 1, 1, 14, family=1)
     assert halo2.narrow_epi() and halo2.smem_bytes() == 80 * 1024 + 16 * 1024 + 1280
     assert not Knobs(128, 64, 64, 3, 1, 1, 1, 14, family=1).narrow_epi()
+
+
+def test_512_row_pairs_only_for_halo_conv(tmp_path):
+    """BM = 512 (256 rows per CTA of a pair) exists only as a halo-line conv
+    CTA pair; the library rejects it for GEMM tiles, single CTAs and dense
+    conv tiles before NVRTC, and compiles the halo pair."""
+    cache = str(tmp_path)
+    assert capi.compile_kernel(1, (512, 64, 64, 3, 1, 1, 4, 14, 1, 2, 0, 0, 1, 0), False, False, cache) > 0
+    for fam, bad in [(0, (512, 64, 64, 3, 1, 1, 1, 1, 1, 2)), (1, (512, 64, 64, 3, 1, 1, 4, 14, 1, 1)),
+                     (1, (512, 64, 64, 3, 1, 1, 8, 8, 1, 2))]:
+        with pytest.raises(capi.OpevoError) as e:
+            capi.compile_kernel(fam, bad, False, False, cache)
+        assert e.value.status == capi.INVALID_CONFIG, bad
