@@ -111,6 +111,10 @@
 #ifndef OPEVO_LINE
 #define OPEVO_LINE 0       // conv: padded lines of this many tile rows (0: dense tile)
 #endif
+#ifndef OPEVO_WBOX
+#define OPEVO_WBOX 1       // halo lines: one 4-D weight box per filter row (0: per-tap 2-D boxes;
+                           // experiments, with OPEVO_WBOX=0 in the host's environment too)
+#endif
 #ifndef OPEVO_NARROW_EPI
 #define OPEVO_NARROW_EPI 0 // 32-column epilogue staging (host rule: two CTAs per SM)
 #endif
@@ -1041,7 +1045,18 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                     for (int ka = 0; ka < KATOMS; ++ka)
                         conv_load_a(a_dst + ka * (BM_CTA * SWZ), &tma_a, fb, cbase + ka * ATOM_K,
                                     w0 - geom.pad, h0 + di, n0);
-                    if (!B_RES) conv_load_b_row(b_dst, &tma_b, fb, b_row0, cbase / ATOM_K, tap * HKW);
+                    if (!B_RES) {
+                        if (OPEVO_WBOX) {
+                            conv_load_b_row(b_dst, &tma_b, fb, b_row0, cbase / ATOM_K, tap * HKW);
+                        } else {    // experiment: one 2-D box per (tap, atom)
+#pragma unroll
+                            for (int ka = 0; ka < KATOMS; ++ka)
+#pragma unroll
+                                for (int dj = 0; dj < HKW; ++dj)
+                                    conv_load_b(b_dst + dj * B_SUB + ka * (BN_LOAD * SWZ), &tma_b, fb,
+                                                (tap * HKW + dj) * geom.cin + cbase + ka * ATOM_K, b_row0);
+                        }
+                    }
                 } else {
                 // input pixel of output (h0, w0) under tap (di, dj): the map
                 // traverses W and H with element stride S

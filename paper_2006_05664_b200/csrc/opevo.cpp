@@ -1578,7 +1578,7 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
             uint32_t bb[3] = {64, (uint32_t)k.bn, (uint32_t)(d / 64)};
             if (!st) st = encode_map(&kr->tma_b, op->b, 3, bd, bs, bb, 128, err, errlen);
             kr->smem += 768 + panel;    // 1 KB barrier block before the panel (BRES_OFF)
-        } else if (hkw) {
+        } else if (hkw && !(getenv("OPEVO_WBOX") && getenv("OPEVO_WBOX")[0] == '0')) {
             // halo lines: one box per filter row holds its KW weight tiles,
             // every 64-channel atom of the K block -- view {64, Cout, Cin/64,
             // KH*KW} (W is [Cout][KH][KW][Cin]), box {64, BN/cg, BK/64, KW}
