@@ -413,10 +413,12 @@ def main() -> None:
         return bool(getattr(evaluator, "poisoned", False))
 
     def flush():
+        # enqueued ahead of the step's kernels on the library's stream; the
+        # host goes on with the step's ask meanwhile
         if world > 1:
             evaluator.flush_l2()        # the worker process's after a fault
         else:
-            local_ev.dev.flush_l2()
+            local_ev.dev.flush_l2(wait=False)
 
     def barrier():
         if not poisoned():

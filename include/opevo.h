@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define OPEVO_ABI_VERSION 7   /* 7: opevo_kernels_time_rotating; 6: 14-slot knobs (conv padded lines), conv stride / narrow Cin, conv CTA pairs; 5: timing policy, native search core */
+#define OPEVO_ABI_VERSION 8   /* 8: opevo_ctx_flush_l2_async; 7: opevo_kernels_time_rotating; 6: 14-slot knobs (conv padded lines), conv stride / narrow Cin, conv CTA pairs; 5: timing policy, native search core */
 
 enum opevo_status {
     OPEVO_OK = 0,
@@ -242,6 +242,11 @@ int opevo_ctx_set_timing(opevo_ctx* ctx, double budget_ms, double loser_ratio, i
  * starts with a cold L2 holding only clean lines (no write-backs land on the
  * next work); returns after the flush completes. */
 int opevo_ctx_flush_l2(opevo_ctx* ctx, char* err, size_t errlen);
+
+/* The same read pass, enqueued without waiting: the context's later work
+ * (same stream) still starts after it, while the host goes on (e.g. with the
+ * next generation's ask) -- bench.py's per-step flush. */
+int opevo_ctx_flush_l2_async(opevo_ctx* ctx, char* err, size_t errlen);
 
 /* Pinned host memory for honest end-to-end copies. */
 void* opevo_host_alloc(size_t bytes);

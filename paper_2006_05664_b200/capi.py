@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libopevo.so")
 DEFAULT_CACHE = os.path.join(HERE, "kernel_cache")
 
-ABI_VERSION = 7
+ABI_VERSION = 8
 
 # status codes (opevo.h)
 OK = 0
@@ -50,7 +50,7 @@ EXPORTS = (
     "opevo_op_refresh_reference", "opevo_kernel_get", "opevo_kernel_release",
     "opevo_kernel_run", "opevo_kernel_check", "opevo_kernel_time", "opevo_kernels_time_rotating",
     "opevo_trial",
-    "opevo_kernel_trace", "opevo_ctx_flush_l2", "opevo_host_alloc", "opevo_host_free",
+    "opevo_kernel_trace", "opevo_ctx_flush_l2", "opevo_ctx_flush_l2_async", "opevo_host_alloc", "opevo_host_free",
     "opevo_op_preload", "opevo_trial_batch", "opevo_ctx_set_timing",
     # native OpEvo proposal core (bound in native.py)
     "opevo_search_create", "opevo_search_destroy", "opevo_search_slots", "opevo_search_set_rng",
@@ -126,6 +126,7 @@ def load() -> C.CDLL:
         "opevo_trial": (I, [P, P, i32p, I, I, I, I, D, C.POINTER(TrialResult), cp, sz]),
         "opevo_kernel_trace": (I, [P, C.POINTER(C.c_uint64), sz, cp, sz]),
         "opevo_ctx_flush_l2": (I, [P, cp, sz]),
+        "opevo_ctx_flush_l2_async": (I, [P, cp, sz]),
         "opevo_ctx_set_timing": (I, [P, D, D, I]),
         "opevo_host_alloc": (P, [sz]),
         "opevo_host_free": (None, [P]),
@@ -236,10 +237,12 @@ class Device:
         if st != OK:
             raise OpevoError(st, "bad timing policy")
 
-    def flush_l2(self) -> None:
-        """Evict L2 (write 2x its size) and wait."""
+    def flush_l2(self, wait: bool = True) -> None:
+        """Evict L2 (read 2x its size); wait for it, or (wait=False) only
+        enqueue it ahead of this context's later work."""
         err = _errbuf()
-        _check(self.lib.opevo_ctx_flush_l2(self.handle, err, len(err)), err)
+        fn = self.lib.opevo_ctx_flush_l2 if wait else self.lib.opevo_ctx_flush_l2_async
+        _check(fn(self.handle, err, len(err)), err)
 
     def prepare(self, kind: int, dtype: int = BF16, batch: int = 1, rows: int = 0, cols: int = 0,
                 depth: int = 0, conv=None, seed: int = 1234) -> "Operand":

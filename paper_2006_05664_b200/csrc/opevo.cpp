@@ -2545,8 +2545,21 @@ int opevo_ctx_set_timing(opevo_ctx* ctx, double budget_ms, double loser_ratio, i
     return OPEVO_OK;
 }
 
+static int flush_l2_enqueue(opevo_ctx* ctx, char* err, size_t errlen);
+
 int opevo_ctx_flush_l2(opevo_ctx* ctx, char* err, size_t errlen) {
     if (!ctx) return OPEVO_ERR_ARG;
+    const int st = flush_l2_enqueue(ctx, err, errlen);
+    if (st) return st;
+    return sync_checked(ctx, "flush", err, errlen);
+}
+
+int opevo_ctx_flush_l2_async(opevo_ctx* ctx, char* err, size_t errlen) {
+    if (!ctx) return OPEVO_ERR_ARG;
+    return flush_l2_enqueue(ctx, err, errlen);
+}
+
+static int flush_l2_enqueue(opevo_ctx* ctx, char* err, size_t errlen) {
     g_cu.CtxSetCurrent(ctx->cu);
     if (!ctx->flush_buf) {
         ctx->flush_bytes = (size_t)256 << 20;
@@ -2555,9 +2568,7 @@ int opevo_ctx_flush_l2(opevo_ctx* ctx, char* err, size_t errlen) {
     uint64_t n16 = ctx->flush_bytes / 16;
     unsigned salt = 0x5eed;
     void* fa[] = {&ctx->flush_buf, &n16, &salt};
-    int st = launch_simple(ctx, ctx->k_flush, (unsigned)ctx->sm_count * 4, 512, fa, err, errlen);
-    if (st) return st;
-    return sync_checked(ctx, "flush", err, errlen);
+    return launch_simple(ctx, ctx->k_flush, (unsigned)ctx->sm_count * 4, 512, fa, err, errlen);
 }
 
 int opevo_kernel_trace(opevo_kernel* k, uint64_t* host, size_t count, char* err, size_t errlen) {
