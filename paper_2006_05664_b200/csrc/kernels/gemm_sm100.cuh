@@ -115,6 +115,9 @@
 #define OPEVO_WBOX 1       // halo lines: one 4-D weight box per filter row (0: per-tap 2-D boxes;
                            // experiments, with OPEVO_WBOX=0 in the host's environment too)
 #endif
+#ifndef OPEVO_X3_SMEM_ALO
+#define OPEVO_X3_SMEM_ALO 0 // 1: 3xTF32 keeps A_lo in shared memory (the pre-X3T path; A/B)
+#endif
 #ifndef OPEVO_NARROW_EPI
 #define OPEVO_NARROW_EPI 0 // 32-column epilogue staging (host rule: two CTAs per SM)
 #endif
@@ -264,8 +267,19 @@ constexpr u64 DESC_HI = ((u64)1 << 16)                          // LBO (unused f
 // trails the MMA by up to three units (the commit -> epilogue -> release
 // round trip is long next to a small unit's mainloop).
 constexpr int NBUF = (4 * TMEM_USED <= 256) ? 4 : (2 * TMEM_USED <= 512) ? 2 : 1;
-constexpr int TMEM_ALLOC = (NBUF * TMEM_USED <= 32) ? 32 : (NBUF * TMEM_USED <= 64) ? 64 :
-                           (NBUF * TMEM_USED <= 128) ? 128 : (NBUF * TMEM_USED <= 256) ? 256 : 512;
+// 3xTF32 with A's lo part in TMEM (X3T): the epilogue warps write each landed
+// stage's A_lo rows into a TMEM ring after the accumulators (one fp32 per
+// column, row = lane) and the A_lo x B MMA reads A from TMEM -- A_lo never
+// touches shared memory (its store and its MMA read were a third of the
+// stage's shared-memory traffic).  Single-CTA 128-row tiles, 128-byte
+// swizzle, when the ring fits next to the accumulators.
+constexpr int ALO_COLS = X3 ? BK / 2 : 0;                  // fp32 A elements per row per stage
+constexpr bool X3T = X3 && SWZ == 128 && MATOMS == 1 && CG == 1 && BM == 128 && !OPEVO_X3_SMEM_ALO &&
+                     NBUF * TMEM_USED + STAGES * ALO_COLS <= 512;
+constexpr int ALO_BASE = NBUF * TMEM_USED;                 // first column of the A_lo ring
+constexpr int TMEM_NEED = NBUF * TMEM_USED + (X3T ? STAGES * ALO_COLS : 0);
+constexpr int TMEM_ALLOC = (TMEM_NEED <= 32) ? 32 : (TMEM_NEED <= 64) ? 64 :
+                           (TMEM_NEED <= 128) ? 128 : (TMEM_NEED <= 256) ? 256 : 512;
 constexpr int SPLITCL = OPEVO_SPLIT_CLUSTER;   // DSMEM split-K cluster size (0: off)
 static_assert(BPU == 1 || (OPEVO_BATCHED && CG == 1 && CLUSTER == 1 && MATOMS == 1 && ACC == 1 &&
                            SPLITCL == 0 && (FUSED_K || KATOMS == 1)),
@@ -521,6 +535,16 @@ __device__ __forceinline__ void umma_bf16(u32 tmem_d, u64 adesc, u64 bdesc, u32 
 // exact remainders lo = x - hi at +LO_OFF, so the
 // three products are hi*lo, lo*hi and hi*hi and only lo*lo (~2^-22
 // relative) and the tf32 truncation of the lo parts are lost.
+// The same three MMAs with A_lo read from TMEM (column address alo_t).
+__device__ __forceinline__ void umma_x3t(u32 d, u64 a, u64 b, u32 alo_t, u64 blo, u32 accumulate) {
+    asm volatile("{ .reg .pred e, p, t; elect.sync _|e, 0xffffffff; setp.ne.b32 p, %5, 0; "
+                 "setp.eq.b32 t, 0, 0; "
+                 "@e tcgen05.mma.cta_group::1.kind::tf32.collector::a::fill [%0], %1, %4, %6, p; "
+                 "@e tcgen05.mma.cta_group::1.kind::tf32.collector::a::lastuse [%0], %1, %2, %6, t; "
+                 "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%3], %2, %6, t; }"
+                 :: "r"(d), "l"(a), "l"(b), "r"(alo_t), "l"(blo), "r"(accumulate), "r"(IDESC));
+}
+
 __device__ __forceinline__ void umma_x3(u32 d, u64 a, u64 b, u64 alo, u64 blo, u32 accumulate) {
     asm volatile("{ .reg .pred e, p, t; elect.sync _|e, 0xffffffff; setp.ne.b32 p, %5, 0; "
                  "setp.eq.b32 t, 0, 0; "
@@ -1224,8 +1248,13 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
                                 for (int ma = 0; ma < MATOMS; ++ma) {
                                     const u64 adesc = da + (u64)((ka * (BM_CTA * SWZ) + ma * (128 * SWZ) + koff) >> 4);
                                     const u32 accumulate = (kb != 0 || ka != 0 || k16 != 0) ? 1u : 0u;
-                                    umma_x3(acc_base + (u32)(ma * BN), adesc, bdesc, adesc + (u64)(LO_OFF >> 4),
-                                            bdesc + (u64)(LO_OFF >> 4), accumulate);
+                                    if (X3T)
+                                        umma_x3t(acc_base + (u32)(ma * BN), adesc, bdesc,
+                                                 tmem_base + (u32)(ALO_BASE + s * ALO_COLS + ka * 32 + k16 * 8),
+                                                 bdesc + (u64)(LO_OFF >> 4), accumulate);
+                                    else
+                                        umma_x3(acc_base + (u32)(ma * BN), adesc, bdesc, adesc + (u64)(LO_OFF >> 4),
+                                                bdesc + (u64)(LO_OFF >> 4), accumulate);
                                 }
                             }
                         }
@@ -1322,8 +1351,43 @@ opevo_gemm(const __grid_constant__ TmaDesc tma_a,
             for (int kb = 0; kb < t.num_kb; ++kb) {
                 mbar_wait(smem_u32(full_bar + xs), xph);
                 const u32 base = smem_u32(smem + xs * STAGE_BYTES);
+                if (X3T) {
+                    // A_lo -> TMEM: this thread's row (its TMEM lane), one
+                    // 128-byte swizzle atom (32 fp32) at a time
+                    const int row = quarter * 32 + lane;
+#pragma unroll 1
+                    for (int ka = 0; ka < KATOMS; ++ka) {
+                        const u32 rbase = base + (u32)(ka * (BM_CTA * SWZ) + row * 128);
+                        u32 l[32];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const u32 at = rbase + (u32)(((j ^ (row & 7)) & 7) * 16);
+                            u32 x[4];
+                            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                         : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]) : "r"(at) : "memory");
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                l[4 * j + q] = __float_as_uint(__uint_as_float(x[q]) -
+                                                               __uint_as_float(x[q] & 0xffffe000u));
+                        }
+                        const u32 taddr = tmem_base + ((u32)(quarter * 32) << 16) +
+                                          (u32)(ALO_BASE + xs * ALO_COLS + ka * 32);
+                        asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+                                     "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+                                     "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+                                     :: "r"(taddr), "r"(l[0]), "r"(l[1]), "r"(l[2]), "r"(l[3]), "r"(l[4]),
+                                        "r"(l[5]), "r"(l[6]), "r"(l[7]), "r"(l[8]), "r"(l[9]), "r"(l[10]),
+                                        "r"(l[11]), "r"(l[12]), "r"(l[13]), "r"(l[14]), "r"(l[15]),
+                                        "r"(l[16]), "r"(l[17]), "r"(l[18]), "r"(l[19]), "r"(l[20]),
+                                        "r"(l[21]), "r"(l[22]), "r"(l[23]), "r"(l[24]), "r"(l[25]),
+                                        "r"(l[26]), "r"(l[27]), "r"(l[28]), "r"(l[29]), "r"(l[30]), "r"(l[31])
+                                     : "memory");
+                    }
+                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                    tc_fence_before();
+                }
 #pragma unroll 4
-                for (int v = epi_tid; v < LOAD_BYTES / 16; v += 128) {
+                for (int v = epi_tid + (X3T ? A_TILE / 16 : 0); v < LOAD_BYTES / 16; v += 128) {
                     const u32 at = base + (u32)v * 16u;
                     u32 x[4], h[4], l[4];
                     asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"

@@ -221,10 +221,17 @@ int family_of(const opevo_op_desc& d) {
 int bm_cta_of(const Knobs& k) { return k.cg == 2 ? k.bm / 2 : k.bm; }
 int matoms_of(const Knobs& k) { return bm_cta_of(k) == 256 ? 2 : 1; }
 
-// TMEM columns the kernel allocates (two accumulator buffers when they fit).
-int tmem_alloc_cols(const Knobs& k) {
+// TMEM columns the kernel allocates (two accumulator buffers when they fit;
+// 3xTF32 single-CTA 128-row tiles with 128-byte swizzle add the A_lo ring,
+// mirrors X3T / TMEM_NEED).
+int tmem_alloc_cols(const Knobs& k, int family = 0) {
     const int used = matoms_of(k) * k.bn * k.acc * std::max(1, k.bpu);
-    const int want = (4 * used <= 256 ? 4 : 2 * used <= 512 ? 2 : 1) * used;   // mirrors NBUF
+    const int nbuf = 4 * used <= 256 ? 4 : 2 * used <= 512 ? 2 : 1;   // mirrors NBUF
+    int want = nbuf * used;
+    const int alo = k.bk / 2 * k.stages;                                 // k.bk in bf16 units here
+    if (family == FAMILY_X3 && k.cg == 1 && k.bm == 128 && k.bk >= 64 && want + alo <= 512 &&
+        !(getenv("OPEVO_EXTRA_FLAGS") && strstr(getenv("OPEVO_EXTRA_FLAGS"), "OPEVO_X3_SMEM_ALO=1")))
+        want += alo;
     int cols = 32;
     while (cols < want) cols *= 2;
     return cols;
@@ -1712,7 +1719,7 @@ int opevo_kernel_get(opevo_ctx* ctx, opevo_op* op, const int32_t* knobs, int nkn
         }
         static const int force_per_sm = getenv("OPEVO_FORCE_PER_SM") ? atoi(getenv("OPEVO_FORCE_PER_SM")) : 0;
         if (force_per_sm > 0) per_sm = force_per_sm;      // experiments only
-        per_sm = std::min(per_sm, 512 / tmem_alloc_cols(k));
+        per_sm = std::min(per_sm, 512 / tmem_alloc_cols(k, family));
         const int capacity = std::max(1, (ctx->sm_count / clsz) * per_sm);
         SchedHost& sc = kr->sched;
         const int tiles = sc.row_tiles * sc.col_groups * sc.batches;
