@@ -534,6 +534,7 @@ def main() -> None:
     if gen_diag:
         slow = sorted(range(len(gen_diag)), key=lambda i: -gen_diag[i][0])[:3]
         med = statistics.median(t for t, _ in gen_diag)
+        print("[gen ms] " + " ".join(f"{t:.2f}" for t, _ in gen_diag), file=sys.stderr)
         print(f"[flush] median {statistics.median(flush_ms):.3f} ms, max {max(flush_ms):.3f} ms, "
               f"total {sum(flush_ms):.1f} ms; generations total {sum(t for t, _ in gen_diag):.1f} ms",
               file=sys.stderr)
