@@ -399,7 +399,7 @@ def main() -> None:
         below = (args.dtype == "bf16"
                  and spec.flops() / algo_bytes(spec, 2) < pk0["tflops"] * 1e3 / pk0["hbm_gbs"])
         args.l2 = "cold" if below else "warm"
-    settings = EvalSettings(reps=args.reps, preload_family=not args.no_preload,
+    settings = EvalSettings(reps=args.reps, preload_family=not args.no_preload, warm_family=not args.no_preload,
                             flush_l2=1 if args.l2 == "cold" else (2 if args.timing == "stream" else 0),
                             dtype=DTYPES[args.dtype], loser_ratio=args.loser_ratio)
     local_ev = GpuEvaluator(spec, space, local, settings)
@@ -706,7 +706,7 @@ def main() -> None:
                                            "lines) before every timed step",
                        "parallelism": f"trial sharding x{world}",
                        "kernel_cache": ("prebuilt cubins (build()); the operator's cached family "
-                                        "loaded into the context before timing" if not args.no_preload
+                                        "loaded into the context and launched once before timing" if not args.no_preload
                                         else "prebuilt cubins (build()), loaded on first use")},
             "best_tflops": best_tflops,
             "best_frac_of_peak": best_tflops / _dtype_peak(args.dtype, pk),

@@ -62,6 +62,10 @@ class EvalSettings:
     # trial never pays a module load; uncached instances still compile/load
     # on demand
     preload_family: bool = False
+    # ... and launch each of them once (a service's resident kernels are
+    # warm too): a function's first launch in a process costs extra driver
+    # and device time that is no property of the kernel
+    warm_family: bool = False
 
 
 @dataclass
@@ -197,6 +201,20 @@ class GpuEvaluator:
             if ok:
                 self._staged.add((fam, bool(batched),
                                   Knobs(*kn, family=fam, batched=int(batched)).compile_key()))
+        # (not under fault injection: a trapping instance must fault inside
+        # a trial, where the isolation path handles it)
+        if self.settings.warm_family and not os.environ.get("OPEVO_FAULT_KNOBS"):
+            for (_fam, _batched, kn), ok in zip(todo, oks):
+                if not ok:
+                    continue
+                try:
+                    k = self.dev.kernel(self.op, kn)
+                except capi.OpevoError:
+                    continue                # infeasible on this operator (e.g. tiling)
+                try:
+                    k.run()
+                finally:
+                    k.close()
         return sum(oks)
 
     def evaluate_infos(self, configs: list[tuple]) -> list[TrialInfo]:
