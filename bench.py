@@ -593,14 +593,20 @@ def main() -> None:
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record()
         e2e_trials = 0
+        e_diag = [] if os.environ.get("OPEVO_BENCH_GEN_TIMES") == "1" else None
         for g in range(args.warmup, args.warmup + args.steps):
             flush()
+            tg = time.perf_counter()
             e2e_trials += generation(e_engine, e_rec, upload, replay=history[g])
+            if e_diag is not None:
+                e_diag.append(1e3 * (time.perf_counter() - tg))
         barrier()
         f1.record()
         torch.cuda.synchronize()
         gc.enable()
         e_sec = max_over_ranks(f0.elapsed_time(f1) / 1e3)
+        if e_diag is not None:
+            print("[e2e gen ms] " + " ".join(f"{t:.2f}" for t in e_diag), file=sys.stderr)
         e2e = {"value": e2e_trials / e_sec if e_sec > 0 else 0.0, "unit": "trials/s",
                "h2d_bytes_per_step": (op.a_bytes + op.b_bytes) * world,
                "d2h_bytes_per_step": 16 * RHO, "steps": args.steps,
