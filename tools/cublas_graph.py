@@ -1,19 +1,26 @@
-"""cuBLAS reference point: torch.matmul / bmm of an operator's shape, bf16,
-R back-to-back launches captured in one CUDA graph (the same timing the
-roofline re-time of bench.py uses).  Usage: python tools/cublas_graph.py OP [R]"""
+"""cuBLAS / cuDNN reference point: torch.matmul / bmm / conv2d (channels-last)
+of an operator's shape, bf16, R back-to-back launches captured in one CUDA
+graph (the same timing the roofline re-time of bench.py uses).
+Usage: python tools/cublas_graph.py OP [R]"""
 import sys
 
 import torch
 
 sys.path.insert(0, ".")
-from paper_2006_05664_b200.operators import BatchMatMulSpec, parse_operator  # noqa: E402
+from paper_2006_05664_b200.operators import BatchMatMulSpec, Conv2dSpec, parse_operator  # noqa: E402
 
 
 def main():
     spec = parse_operator(sys.argv[1])
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 100
     dev = torch.device("cuda", 0)
-    if isinstance(spec, BatchMatMulSpec):
+    if isinstance(spec, Conv2dSpec):
+        x = torch.randn(spec.batch, spec.in_channels, spec.in_height, spec.in_width, device=dev,
+                        dtype=torch.bfloat16).to(memory_format=torch.channels_last)
+        w = torch.randn(spec.out_channels, spec.in_channels, spec.kernel_h, spec.kernel_w, device=dev,
+                        dtype=torch.bfloat16).to(memory_format=torch.channels_last)
+        fn = lambda: torch.nn.functional.conv2d(x, w, stride=spec.stride, padding=spec.padding)  # noqa: E731
+    elif isinstance(spec, BatchMatMulSpec):
         a = torch.randn(spec.b, spec.n, spec.k, device=dev, dtype=torch.bfloat16)
         b = torch.randn(spec.b, spec.m, spec.k, device=dev, dtype=torch.bfloat16)
         fn = lambda: torch.bmm(a, b.transpose(1, 2))  # noqa: E731
